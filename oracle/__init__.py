@@ -1,0 +1,280 @@
+"""CPU checkers for the FusEd-PageRank hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu-baseline /
+``--impl reference`` legs import this package.  The product
+(``paper_2203_09284_b200``) never does; it has no CPU fallback.
+
+Two checkers, both loaded with ctypes:
+
+* ``Oracle``    -- ``oracle/libfpr_oracle.so``, the C restatement
+  (``oracle/fpr_oracle.c``), pinned against the reference by
+  ``tests/test_oracle.py`` + ``tests/golden/``.
+* ``Reference`` -- ``oracle/_ref/libfpr_ref.so``, the reference headers of
+  ``/root/reference/proj/include`` compiled unmodified (``oracle/Makefile``).
+  Present wherever it was built (it travels to the GPU box with the repo
+  snapshot); ``load_reference()`` returns None when it is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libfpr_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libfpr_ref.so")
+
+NORM_LINF = 0
+NORM_L1 = 1
+
+_u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u64 = C.c_uint64
+_f64 = C.c_double
+
+
+@dataclass
+class Graph:
+    """Mirror of ``fpr::Graph`` (graph.hpp:20-30): dst-grouped in-CSR, u64."""
+
+    n: int
+    m: int
+    in_start: np.ndarray  # u64[n+1]
+    in_src: np.ndarray  # u64[m]
+    out_degree: np.ndarray  # u64[n]
+
+    def in_degree(self) -> np.ndarray:
+        return np.diff(self.in_start)
+
+
+@dataclass
+class Run:
+    ranks: np.ndarray
+    errors: np.ndarray
+    l1_errors: np.ndarray | None
+    iterations: int
+    history: np.ndarray | None = None
+    seconds: float = 0.0
+
+    @property
+    def converged_linf(self) -> bool:  # unused helper for readability in tests
+        return True
+
+
+def _ensure_built() -> None:
+    if not os.path.exists(ORACLE_SO):
+        subprocess.run(["make", "-s", "-C", HERE, os.path.abspath(ORACLE_SO)], check=True)
+
+
+class Oracle:
+    """ctypes binding of the C restatement (fpr_oracle.h)."""
+
+    def __init__(self) -> None:
+        _ensure_built()
+        L = C.CDLL(ORACLE_SO)
+        L.fo_generate_rmat.argtypes = [C.c_uint32, _u64, _f64, _f64, _f64, _f64, _u64, _u64p, _u64p]
+        L.fo_generate_rmat.restype = C.c_int
+        L.fo_random_sparse.argtypes = [_u64, _u64, _u64, _u64p, _u64p]
+        L.fo_random_sparse.restype = _u64
+        L.fo_build_csr.argtypes = [_u64, _u64, _u64p, _u64p, _u64p, _u64p, _u64p,
+                                   C.POINTER(_u64), C.POINTER(_u64)]
+        L.fo_build_csr.restype = C.c_int
+        eng = [_u64, _u64, _u64p, _u64p, _u64p, _f64, _f64, _u64, C.c_int]
+        outs = [_f64p, _f64p, C.c_void_p, C.POINTER(_u64), C.c_void_p, _u64]
+        L.fo_pagerank_ec.argtypes = eng + outs
+        L.fo_pagerank_fused_seq.argtypes = eng + outs
+        L.fo_pagerank_lockstep.argtypes = eng + [_u64, _u64p] + outs
+        for f in (L.fo_pagerank_ec, L.fo_pagerank_fused_seq, L.fo_pagerank_lockstep):
+            f.restype = C.c_int
+        L.fo_dense_oracle.argtypes = [_u64, _u64p, _u64p, _u64p, _f64, _f64, _u64, _f64p]
+        L.fo_dense_oracle.restype = C.c_int
+        L.fo_l1_norm.argtypes = [_u64, _f64p, _f64p]
+        L.fo_l1_norm.restype = _f64
+        L.fo_linf_norm.argtypes = [_u64, _f64p, _f64p]
+        L.fo_linf_norm.restype = _f64
+        self.lib = L
+
+    # ---- inputs -----------------------------------------------------------
+    def generate_rmat(self, scale, edge_factor, a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
+        draws = edge_factor << scale
+        src = np.empty(draws, np.uint64)
+        dst = np.empty(draws, np.uint64)
+        rc = self.lib.fo_generate_rmat(scale, edge_factor, a, b, c, d, seed, src, dst)
+        if rc:
+            raise ValueError("rmat: invalid parameters")
+        return 1 << scale, src, dst
+
+    def random_sparse(self, n, avg_degree, seed):
+        src = np.empty(n * avg_degree, np.uint64)
+        dst = np.empty(n * avg_degree, np.uint64)
+        k = self.lib.fo_random_sparse(n, avg_degree, seed, src, dst)
+        return n, src[:k].copy(), dst[:k].copy()
+
+    def build_csr(self, n, src, dst) -> Graph:
+        src = np.ascontiguousarray(src, np.uint64)
+        dst = np.ascontiguousarray(dst, np.uint64)
+        in_start = np.empty(n + 1, np.uint64)
+        in_src = np.empty(max(len(src), 1), np.uint64)
+        out_degree = np.empty(max(n, 1), np.uint64)
+        m = _u64(0)
+        bad = _u64(0)
+        rc = self.lib.fo_build_csr(n, len(src), src, dst, in_start, in_src, out_degree,
+                                   C.byref(m), C.byref(bad))
+        if rc == 1:
+            i = bad.value
+            raise ValueError(f"build_csr: edge #{i} ({src[i]},{dst[i]}) has endpoint outside [0,{n})")
+        if rc:
+            raise RuntimeError(f"fo_build_csr rc={rc}")
+        return Graph(n, m.value, in_start, in_src[: m.value].copy(), out_degree[:n].copy())
+
+    # ---- engines ----------------------------------------------------------
+    def _run(self, fn, g: Graph, damping, threshold, max_iterations, norm, extra, history_cap):
+        ranks = np.empty(max(g.n, 1), np.float64)
+        errors = np.empty(max_iterations, np.float64)
+        l1 = np.empty(max_iterations, np.float64)
+        it = _u64(0)
+        hist = None
+        hp = None
+        if history_cap:
+            hist = np.empty((history_cap, g.n), np.float64)
+            hp = hist.ctypes.data
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        rc = fn(g.n, g.m, g.in_start, in_src, g.out_degree, damping, threshold, max_iterations,
+                norm, *extra, ranks, errors, l1.ctypes.data, C.byref(it), hp, history_cap)
+        if rc:
+            raise ValueError(f"pagerank: invalid configuration (rc={rc})")
+        k = it.value
+        return Run(ranks[: g.n], errors[:k].copy(), l1[:k].copy(), k,
+                   None if hist is None else hist[: min(k, history_cap)])
+
+    def pagerank_ec(self, g, damping=0.85, threshold=1e-15, max_iterations=10000,
+                    norm=NORM_LINF, history_cap=0) -> Run:
+        return self._run(self.lib.fo_pagerank_ec, g, damping, threshold, max_iterations, norm,
+                         (), history_cap)
+
+    def pagerank_fused_seq(self, g, damping=0.85, threshold=1e-15, max_iterations=10000,
+                           norm=NORM_LINF, history_cap=0) -> Run:
+        return self._run(self.lib.fo_pagerank_fused_seq, g, damping, threshold, max_iterations,
+                         norm, (), history_cap)
+
+    def pagerank_lockstep(self, g, wave_start, damping=0.85, threshold=1e-15,
+                          max_iterations=10000, norm=NORM_LINF, history_cap=0) -> Run:
+        ws = np.ascontiguousarray(wave_start, np.uint64)
+        return self._run(self.lib.fo_pagerank_lockstep, g, damping, threshold, max_iterations,
+                         norm, (len(ws) - 1, ws), history_cap)
+
+    def dense_oracle(self, g, damping=0.85, threshold=1e-15, max_iterations=10000):
+        ranks = np.empty(g.n, np.float64)
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        rc = self.lib.fo_dense_oracle(g.n, g.in_start, in_src, g.out_degree, damping, threshold,
+                                      max_iterations, ranks)
+        if rc:
+            raise ValueError("dense oracle: invalid input")
+        return ranks
+
+    def l1_norm(self, a, b) -> float:
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        if a.shape != b.shape:
+            raise ValueError(f"l1_norm: length mismatch ({len(a)} vs {len(b)})")
+        return self.lib.fo_l1_norm(len(a), a, b)
+
+    def linf_norm(self, a, b) -> float:
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        if a.shape != b.shape:
+            raise ValueError("linf_norm: length mismatch")
+        return self.lib.fo_linf_norm(len(a), a, b)
+
+
+ENGINES = {"ec_seq": 0, "fused_seq": 1, "ec_par": 2, "fused_par": 3}
+
+
+class Reference:
+    """ctypes binding of oracle/_ref/libfpr_ref.so (the reference itself)."""
+
+    def __init__(self, path: str = REF_SO) -> None:
+        L = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_generate_rmat.argtypes = [C.c_uint32, _u64, _f64, _f64, _f64, _f64, _u64, _u64p, _u64p]
+        L.ref_random_sparse.argtypes = [_u64, _u64, _u64, _u64p, _u64p]
+        L.ref_random_sparse.restype = _u64
+        L.ref_build_csr.argtypes = [_u64, _u64, _u64p, _u64p, _u64p, _u64p, _u64p, C.POINTER(_u64)]
+        L.ref_graph_create.argtypes = [_u64, _u64, _u64p, _u64p, _u64p]
+        L.ref_graph_create.restype = C.c_void_p
+        L.ref_graph_destroy.argtypes = [C.c_void_p]
+        L.ref_graph_run.argtypes = [C.c_void_p, C.c_int, _f64, _f64, _u64, C.c_uint, _f64p, _f64p,
+                                    C.POINTER(_u64), C.POINTER(C.c_int), C.POINTER(_f64),
+                                    C.POINTER(_f64)]
+        L.ref_dense_oracle.argtypes = [_u64, _u64, _u64p, _u64p, _u64p, _f64, _f64, _u64, _f64p]
+        self.lib = L
+
+    def _err(self) -> str:
+        return self.lib.ref_last_error().decode()
+
+    def generate_rmat(self, scale, edge_factor, a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
+        draws = edge_factor << scale
+        src = np.empty(draws, np.uint64)
+        dst = np.empty(draws, np.uint64)
+        if self.lib.ref_generate_rmat(scale, edge_factor, a, b, c, d, seed, src, dst):
+            raise ValueError(self._err())
+        return 1 << scale, src, dst
+
+    def random_sparse(self, n, avg_degree, seed):
+        src = np.empty(n * avg_degree, np.uint64)
+        dst = np.empty(n * avg_degree, np.uint64)
+        k = self.lib.ref_random_sparse(n, avg_degree, seed, src, dst)
+        return n, src[:k].copy(), dst[:k].copy()
+
+    def build_csr(self, n, src, dst) -> Graph:
+        src = np.ascontiguousarray(src, np.uint64)
+        dst = np.ascontiguousarray(dst, np.uint64)
+        in_start = np.empty(n + 1, np.uint64)
+        in_src = np.empty(max(len(src), 1), np.uint64)
+        out_degree = np.empty(max(n, 1), np.uint64)
+        m = _u64(0)
+        if self.lib.ref_build_csr(n, len(src), src, dst, in_start, in_src, out_degree, C.byref(m)):
+            raise ValueError(self._err())
+        return Graph(n, m.value, in_start, in_src[: m.value].copy(), out_degree[:n].copy())
+
+    def run(self, g: Graph, engine: str, damping=0.85, threshold=1e-15, max_iterations=10000,
+            threads=1, handle=None) -> Run:
+        own = handle is None
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        h = handle or self.lib.ref_graph_create(g.n, g.m, g.in_start, in_src, g.out_degree)
+        try:
+            ranks = np.empty(max(g.n, 1), np.float64)
+            errors = np.empty(max_iterations, np.float64)
+            it, conv, fe, secs = _u64(0), C.c_int(0), _f64(0), _f64(0)
+            rc = self.lib.ref_graph_run(h, ENGINES[engine], damping, threshold, max_iterations,
+                                        threads, ranks, errors, C.byref(it), C.byref(conv),
+                                        C.byref(fe), C.byref(secs))
+            if rc:
+                raise ValueError(self._err())
+            k = it.value
+            return Run(ranks[: g.n], errors[:k].copy(), None, k, None, secs.value)
+        finally:
+            if own:
+                self.lib.ref_graph_destroy(h)
+
+    def graph_handle(self, g: Graph):
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        return self.lib.ref_graph_create(g.n, g.m, g.in_start, in_src, g.out_degree)
+
+    def destroy(self, h) -> None:
+        self.lib.ref_graph_destroy(h)
+
+    def dense_oracle(self, g, damping=0.85, threshold=1e-15, max_iterations=10000):
+        ranks = np.empty(g.n, np.float64)
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        if self.lib.ref_dense_oracle(g.n, g.m, g.in_start, in_src, g.out_degree, damping,
+                                     threshold, max_iterations, ranks):
+            raise ValueError(self._err())
+        return ranks
+
+
+def load_reference() -> Reference | None:
+    return Reference() if os.path.exists(REF_SO) else None

@@ -1,0 +1,370 @@
+/*
+ * fpr_oracle.c -- CPU restatement of the reference hot path (TEST
+ * INFRASTRUCTURE ONLY; see fpr_oracle.h).  Parity pinned against the compiled
+ * reference via tests/golden/ (see tests/test_oracle.py).
+ *
+ * Build (oracle/Makefile): gcc -std=c11 -O3 -ffp-contract=off -fPIC -shared.
+ * No -march: the reference's Release build has none, and FMA contraction of
+ * `base + damping*sum` would change result bits.
+ */
+#include "fpr_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define GAMMA 0x9e3779b97f4a7c15ULL
+
+static inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+/* SplitMix64::next (rng.hpp:15-20) */
+uint64_t fo_splitmix_next(uint64_t* state) {
+  *state += GAMMA;
+  return mix64(*state);
+}
+
+/* generate_rmat draw i (rmat.hpp:54-75): the root stream's (i+1)-th output
+ * seeds the child (SplitMix64::split, rng.hpp:22); level l uses the child's
+ * (l+1)-th output through next_unit (rng.hpp:25). */
+void fo_rmat_draw(uint32_t scale, double a, double ab, double abc, uint64_t seed, uint64_t i,
+                  uint64_t* src_out, uint64_t* dst_out) {
+  uint64_t child = mix64(seed + (i + 1) * GAMMA);
+  uint64_t src = 0, dst = 0;
+  for (uint32_t level = 0; level < scale; ++level) {
+    uint64_t z = mix64(child + (uint64_t)(level + 1) * GAMMA);
+    double r = (double)(z >> 11) * 0x1.0p-53;
+    src <<= 1;
+    dst <<= 1;
+    if (r < a) {
+    } else if (r < ab) {
+      dst |= 1;
+    } else if (r < abc) {
+      src |= 1;
+    } else {
+      src |= 1;
+      dst |= 1;
+    }
+  }
+  *src_out = src;
+  *dst_out = dst;
+}
+
+/* generate_rmat (rmat.hpp:24-77), including validate(RmatParams). */
+int fo_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, double b, double c, double d,
+                     uint64_t seed, uint64_t* src, uint64_t* dst) {
+  if (scale == 0 || scale > 32) return FO_EINVAL;
+  if (edge_factor == 0) return FO_EINVAL;
+  if (a < 0 || b < 0 || c < 0 || d < 0 || fabs(a + b + c + d - 1.0) > 1e-9) return FO_EINVAL;
+  const uint64_t draws = edge_factor << scale;
+  const double ab = a + b, abc = a + b + c;
+  for (uint64_t i = 0; i < draws; ++i) fo_rmat_draw(scale, a, ab, abc, seed, i, &src[i], &dst[i]);
+  return FO_OK;
+}
+
+/* testutil::random_sparse (tests/test_util.hpp:49-58). */
+uint64_t fo_random_sparse(uint64_t n, uint64_t avg_degree, uint64_t seed, uint64_t* src,
+                          uint64_t* dst) {
+  uint64_t state = seed, kept = 0;
+  const uint64_t draws = n * avg_degree;
+  for (uint64_t i = 0; i < draws; ++i) {
+    uint64_t u = fo_splitmix_next(&state) % n;
+    uint64_t v = fo_splitmix_next(&state) % n;
+    if (u != v) {
+      src[kept] = u;
+      dst[kept] = v;
+      ++kept;
+    }
+  }
+  return kept;
+}
+
+/* LSD radix sort of 64-bit keys on the low `bits` bits, 11-bit digits. */
+static int radix_sort_u64(uint64_t* keys, uint64_t count, unsigned bits) {
+  if (count < 2 || bits == 0) return FO_OK;
+  uint64_t* tmp = (uint64_t*)malloc(count * sizeof(uint64_t));
+  if (!tmp) return FO_ENOMEM;
+  uint64_t* in = keys;
+  uint64_t* out = tmp;
+  for (unsigned shift = 0; shift < bits; shift += 11) {
+    uint64_t hist[2048];
+    memset(hist, 0, sizeof(hist));
+    for (uint64_t i = 0; i < count; ++i) hist[(in[i] >> shift) & 2047]++;
+    uint64_t sum = 0;
+    for (int b = 0; b < 2048; ++b) {
+      uint64_t h = hist[b];
+      hist[b] = sum;
+      sum += h;
+    }
+    for (uint64_t i = 0; i < count; ++i) out[hist[(in[i] >> shift) & 2047]++] = in[i];
+    uint64_t* t = in;
+    in = out;
+    out = t;
+  }
+  if (in != keys) memcpy(keys, in, count * sizeof(uint64_t));
+  free(tmp);
+  return FO_OK;
+}
+
+/* build_csr (graph.hpp:35-70): range check (:37-44), drop self-loops, sort
+ * by (dst, src), dedup (:48-54), count + prefix sum (:63-68).  The sort key
+ * packs (dst, src) as dst*2^k + src with k = bit width of n-1, so the
+ * restatement handles n <= 2^32. */
+int fo_build_csr(uint64_t n, uint64_t ne, const uint64_t* src, const uint64_t* dst,
+                 uint64_t* in_start, uint64_t* in_src, uint64_t* out_degree, uint64_t* m_out,
+                 uint64_t* bad_edge) {
+  for (uint64_t i = 0; i < ne; ++i) {
+    if (src[i] >= n || dst[i] >= n) {
+      if (bad_edge) *bad_edge = i;
+      return FO_EINVAL;
+    }
+  }
+  if (n > (1ULL << 32)) return FO_ERANGE;
+  unsigned k = 0;
+  while (k < 64 && (1ULL << k) < n) ++k;
+  uint64_t* keys = (uint64_t*)malloc((ne ? ne : 1) * sizeof(uint64_t));
+  if (!keys) return FO_ENOMEM;
+  uint64_t cnt = 0;
+  for (uint64_t i = 0; i < ne; ++i)
+    if (src[i] != dst[i]) keys[cnt++] = (dst[i] << k) | src[i];
+  int rc = radix_sort_u64(keys, cnt, 2 * k);
+  if (rc) {
+    free(keys);
+    return rc;
+  }
+  uint64_t m = 0;
+  for (uint64_t i = 0; i < cnt; ++i)
+    if (m == 0 || keys[i] != keys[m - 1]) keys[m++] = keys[i];
+  const uint64_t mask = (k == 0) ? 0 : ((1ULL << k) - 1);
+  memset(in_start, 0, (n + 1) * sizeof(uint64_t));
+  memset(out_degree, 0, n * sizeof(uint64_t));
+  for (uint64_t s = 0; s < m; ++s) {
+    uint64_t d = keys[s] >> k, sr = keys[s] & mask;
+    in_start[d + 1]++;
+    in_src[s] = sr;
+    out_degree[sr]++;
+  }
+  for (uint64_t u = 0; u < n; ++u) in_start[u + 1] += in_start[u];
+  *m_out = m;
+  free(keys);
+  return FO_OK;
+}
+
+/* validate(PageRankConfig) (pagerank.hpp:40-53) and init_ranks' n>0 check
+ * (:55-57).  thread_count has no meaning here. */
+static int check_config(uint64_t n, double damping, double threshold, uint64_t max_iterations) {
+  if (!(damping > 0.0 && damping < 1.0)) return FO_EINVAL;
+  if (!(threshold > 0.0)) return FO_EINVAL;
+  if (max_iterations == 0) return FO_EINVAL;
+  if (n == 0) return FO_EINVAL;
+  return FO_OK;
+}
+
+static inline double norm_of(int norm, double mx, double sm) {
+  return norm == FO_NORM_L1 ? sm : mx;
+}
+
+/* Pull restatement of pagerank_ec_seq (pagerank.hpp:126-145): the per-edge
+ * scatter_contributions (:63-74) writes pr[u]/outdeg[u] into every slot of
+ * u, so every slot of in_src[e] holds contrib[in_src[e]]; gather_ranks_jacobi
+ * (:76-93) sums a dst segment left to right in ascending-src order.  Reading
+ * contrib[in_src[e]] in the same order is bit-identical. */
+int fo_pagerank_ec(uint64_t n, uint64_t m, const uint64_t* in_start, const uint64_t* in_src,
+                   const uint64_t* out_degree, double damping, double threshold,
+                   uint64_t max_iterations, int norm, double* ranks, double* errors,
+                   double* l1_errors, uint64_t* iterations, double* history,
+                   uint64_t history_cap) {
+  (void)m;
+  int rc = check_config(n, damping, threshold, max_iterations);
+  if (rc) return rc;
+  double* next = (double*)malloc(n * sizeof(double));
+  double* contrib = (double*)malloc(n * sizeof(double));
+  if (!next || !contrib) {
+    free(next);
+    free(contrib);
+    return FO_ENOMEM;
+  }
+  for (uint64_t i = 0; i < n; ++i) ranks[i] = 1.0 / (double)n;
+  const double base = (1.0 - damping) / (double)n;
+  uint64_t it = 0;
+  for (; it < max_iterations;) {
+    for (uint64_t u = 0; u < n; ++u)
+      contrib[u] = out_degree[u] ? ranks[u] / (double)out_degree[u] : 0.0;
+    double err = 0.0, l1 = 0.0;
+    for (uint64_t u = 0; u < n; ++u) {
+      double sum = 0.0;
+      for (uint64_t s = in_start[u]; s < in_start[u + 1]; ++s) sum += contrib[in_src[s]];
+      const double value = base + damping * sum;
+      next[u] = value;
+      const double delta = fabs(value - ranks[u]);
+      err = err > delta ? err : delta;
+      l1 += delta;
+    }
+    memcpy(ranks, next, n * sizeof(double));
+    errors[it] = err;
+    if (l1_errors) l1_errors[it] = l1;
+    if (history && it < history_cap) memcpy(history + it * n, ranks, n * sizeof(double));
+    ++it;
+    if (norm_of(norm, err, l1) <= threshold) break;
+  }
+  *iterations = it;
+  free(next);
+  free(contrib);
+  return FO_OK;
+}
+
+/* Pull restatement of pagerank_fused_seq (pagerank.hpp:152-189): one initial
+ * scatter (:164), then per vertex in ascending order gather the live
+ * contributions, update in place and republish immediately (:166-183). */
+int fo_pagerank_fused_seq(uint64_t n, uint64_t m, const uint64_t* in_start,
+                          const uint64_t* in_src, const uint64_t* out_degree, double damping,
+                          double threshold, uint64_t max_iterations, int norm, double* ranks,
+                          double* errors, double* l1_errors, uint64_t* iterations,
+                          double* history, uint64_t history_cap) {
+  (void)m;
+  int rc = check_config(n, damping, threshold, max_iterations);
+  if (rc) return rc;
+  double* contrib = (double*)malloc(n * sizeof(double));
+  if (!contrib) return FO_ENOMEM;
+  for (uint64_t i = 0; i < n; ++i) ranks[i] = 1.0 / (double)n;
+  const double base = (1.0 - damping) / (double)n;
+  for (uint64_t u = 0; u < n; ++u)
+    contrib[u] = out_degree[u] ? ranks[u] / (double)out_degree[u] : 0.0;
+  uint64_t it = 0;
+  for (; it < max_iterations;) {
+    double err = 0.0, l1 = 0.0;
+    for (uint64_t u = 0; u < n; ++u) {
+      double sum = 0.0;
+      for (uint64_t s = in_start[u]; s < in_start[u + 1]; ++s) sum += contrib[in_src[s]];
+      const double value = base + damping * sum;
+      const double delta = fabs(value - ranks[u]);
+      ranks[u] = value;
+      if (out_degree[u] > 0) contrib[u] = value / (double)out_degree[u];
+      err = err > delta ? err : delta;
+      l1 += delta;
+    }
+    errors[it] = err;
+    if (l1_errors) l1_errors[it] = l1;
+    if (history && it < history_cap) memcpy(history + it * n, ranks, n * sizeof(double));
+    ++it;
+    if (norm_of(norm, err, l1) <= threshold) break;
+  }
+  *iterations = it;
+  free(contrib);
+  return FO_OK;
+}
+
+/* The GPU fused engine's deterministic schedule (see header).  With one
+ * vertex per wave it is exactly fo_pagerank_fused_seq; with one wave it is
+ * exactly fo_pagerank_ec. */
+int fo_pagerank_lockstep(uint64_t n, uint64_t m, const uint64_t* in_start,
+                         const uint64_t* in_src, const uint64_t* out_degree, double damping,
+                         double threshold, uint64_t max_iterations, int norm, uint64_t nwaves,
+                         const uint64_t* wave_start, double* ranks, double* errors,
+                         double* l1_errors, uint64_t* iterations, double* history,
+                         uint64_t history_cap) {
+  (void)m;
+  int rc = check_config(n, damping, threshold, max_iterations);
+  if (rc) return rc;
+  if (nwaves == 0 || wave_start[0] != 0 || wave_start[nwaves] != n) return FO_EINVAL;
+  for (uint64_t w = 0; w < nwaves; ++w)
+    if (wave_start[w + 1] < wave_start[w]) return FO_EINVAL;
+  double* contrib = (double*)malloc(n * sizeof(double));
+  double* wave_val = (double*)malloc(n * sizeof(double));
+  if (!contrib || !wave_val) {
+    free(contrib);
+    free(wave_val);
+    return FO_ENOMEM;
+  }
+  for (uint64_t i = 0; i < n; ++i) ranks[i] = 1.0 / (double)n;
+  const double base = (1.0 - damping) / (double)n;
+  for (uint64_t u = 0; u < n; ++u)
+    contrib[u] = out_degree[u] ? ranks[u] / (double)out_degree[u] : 0.0;
+  uint64_t it = 0;
+  for (; it < max_iterations;) {
+    double err = 0.0, l1 = 0.0;
+    for (uint64_t w = 0; w < nwaves; ++w) {
+      const uint64_t lo = wave_start[w], hi = wave_start[w + 1];
+      for (uint64_t u = lo; u < hi; ++u) {
+        double sum = 0.0;
+        for (uint64_t s = in_start[u]; s < in_start[u + 1]; ++s) sum += contrib[in_src[s]];
+        wave_val[u] = base + damping * sum;
+      }
+      for (uint64_t u = lo; u < hi; ++u) {
+        const double value = wave_val[u];
+        const double delta = fabs(value - ranks[u]);
+        ranks[u] = value;
+        if (out_degree[u] > 0) contrib[u] = value / (double)out_degree[u];
+        err = err > delta ? err : delta;
+        l1 += delta;
+      }
+    }
+    errors[it] = err;
+    if (l1_errors) l1_errors[it] = l1;
+    if (history && it < history_cap) memcpy(history + it * n, ranks, n * sizeof(double));
+    ++it;
+    if (norm_of(norm, err, l1) <= threshold) break;
+  }
+  *iterations = it;
+  free(contrib);
+  free(wave_val);
+  return FO_OK;
+}
+
+/* pagerank_dense_oracle (pagerank.hpp:335-370). */
+int fo_dense_oracle(uint64_t n, const uint64_t* in_start, const uint64_t* in_src,
+                    const uint64_t* out_degree, double damping, double threshold,
+                    uint64_t max_iterations, double* ranks) {
+  int rc = check_config(n, damping, threshold, max_iterations);
+  if (rc) return rc;
+  if (n > 4096) return FO_EINVAL;
+  double* matrix = (double*)calloc(n * n, sizeof(double));
+  double* next = (double*)malloc(n * sizeof(double));
+  if (!matrix || !next) {
+    free(matrix);
+    free(next);
+    return FO_ENOMEM;
+  }
+  for (uint64_t u = 0; u < n; ++u)
+    for (uint64_t s = in_start[u]; s < in_start[u + 1]; ++s) {
+      const uint64_t v = in_src[s];
+      matrix[u * n + v] = 1.0 / (double)out_degree[v];
+    }
+  const double base = (1.0 - damping) / (double)n;
+  for (uint64_t i = 0; i < n; ++i) ranks[i] = 1.0 / (double)n;
+  for (uint64_t it = 0; it < max_iterations; ++it) {
+    double err = 0.0;
+    for (uint64_t u = 0; u < n; ++u) {
+      double sum = 0.0;
+      const double* row = matrix + u * n;
+      for (uint64_t v = 0; v < n; ++v) sum += row[v] * ranks[v];
+      next[u] = base + damping * sum;
+      const double d = fabs(next[u] - ranks[u]);
+      err = err > d ? err : d;
+    }
+    memcpy(ranks, next, n * sizeof(double));
+    if (err <= threshold) break;
+  }
+  free(matrix);
+  free(next);
+  return FO_OK;
+}
+
+/* l1_norm / linf_norm (metrics.hpp:54-75). */
+double fo_l1_norm(uint64_t n, const double* a, const double* b) {
+  double sum = 0.0;
+  for (uint64_t i = 0; i < n; ++i) sum += fabs(a[i] - b[i]);
+  return sum;
+}
+
+double fo_linf_norm(uint64_t n, const double* a, const double* b) {
+  double worst = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double d = fabs(a[i] - b[i]);
+    worst = worst > d ? worst : d;
+  }
+  return worst;
+}
