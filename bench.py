@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""FusEd-PageRank B200 benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "config 2"): uniform G(n,m), n = 2^22,
+2^26 draws of testutil::random_sparse(seed 2) semantics, normalised by
+build_csr -> m = 67,108,723; fp64 ranks, d = 0.85, threshold 1e-10 on the
+reference's L-inf delta.  The graph is generated ON THE DEVICE (K5 + K4,
+bit-identical to the reference's CSR; untimed setup).
+
+One step = one full ec_b200 solve to convergence (time-to-converge; 7
+iterations).  value = GTEPS = m * iterations / step time, with the graph
+resident in HBM.  e2e = the same metric through the reference-facing C-ABI
+call fpr_b200_pagerank() on PINNED HOST u64 CSR arrays (fpr::Graph layout):
+H2D + narrowing + partition + solve + D2H of ranks and error trace, all timed.
+
+--impl reference: the reference's own CPU engine (oracle/_ref, compiled from
+the unmodified headers), pagerank_ec_par with every host thread, one
+iteration per step (a bounded sample of the same workload).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CFG2 = 1 << 22
+DEG_CFG2 = 16
+SEED_CFG2 = 2
+THRESHOLD = 1e-10
+DAMPING = 0.85
+WORKLOAD = "config2: uniform G(n=4194304, 2^26 draws, seed 2) -> build_csr, EC to L-inf 1e-10"
+
+
+def algorithmic_bytes(n: int, m: int) -> int:
+    """Per iteration: 12 B/edge (int32 in_src + fp64 contrib gather) +
+    36 B/vertex (int64 row_ptr, pr read+write, int32 outdeg, contrib write)."""
+    return 12 * m + 36 * n
+
+
+def peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reference_graph(ref):
+    """Config-2 graph built by the reference's own functions."""
+    n, s, d = ref.random_sparse(N_CFG2, DEG_CFG2, SEED_CFG2)
+    return ref.build_csr(n, s, d)
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import Oracle, load_reference
+
+    ref = load_reference()
+    threads = os.cpu_count() or 1
+    if ref is not None:
+        kind = "reference"
+        g = reference_graph(ref)
+        h = ref.graph_handle(g)
+        one = lambda: ref.run(g, "ec_par", DAMPING, THRESHOLD, 1, threads, handle=h).seconds  # noqa: E731
+        engine = "fpr::pagerank_ec_par (oracle/_ref, unmodified reference headers)"
+    else:  # reference not compiled on this box: the C restatement (single thread)
+        kind = "port"
+        o = Oracle()
+        n, s, d = o.random_sparse(N_CFG2, DEG_CFG2, SEED_CFG2)
+        g = o.build_csr(n, s, d)
+        threads = 1
+
+        def one():
+            t0 = time.perf_counter()
+            o.pagerank_ec(g, DAMPING, THRESHOLD, 1)
+            return time.perf_counter() - t0
+        engine = "oracle/fpr_oracle.c fo_pagerank_ec (C restatement, 1 thread)"
+    for _ in range(args.warmup):
+        one()
+    secs = [one() for _ in range(args.steps)]
+    t = float(sum(secs))
+    gteps = g.m * args.steps / t / 1e9
+    line = {"metric": "GTEPS/iter (EC PageRank, config 2)", "value": gteps, "unit": "GTEPS",
+            "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_sparse seed 2)",
+            "config": {"workload": WORKLOAD, "n": g.n, "m": g.m, "step": "1 EC iteration",
+                       "engine": engine},
+            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
+                             "sample": f"{args.steps} single-iteration ec_par calls on config 2"},
+            "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if ref is not None:
+        ref.destroy(h)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(g_host) -> dict:
+    """Rank 0, N=1: the reference's ec_par, all host threads, one full solve."""
+    from oracle import Graph as OGraph
+    from oracle import Oracle, load_reference
+
+    ref = load_reference()
+    og = OGraph(g_host.n, g_host.m, g_host.in_start, g_host.in_src, g_host.out_degree)
+    if ref is not None:
+        threads = os.cpu_count() or 1
+        h = ref.graph_handle(og)
+        try:
+            r = ref.run(og, "ec_par", DAMPING, THRESHOLD, 10000, threads, handle=h)
+        finally:
+            ref.destroy(h)
+        return {"value": og.m * r.iterations / r.seconds / 1e9, "unit": "GTEPS", "cores": threads,
+                "kind": "reference", "iterations": r.iterations, "seconds": r.seconds,
+                "sample": "1 full pagerank_ec_par solve of config 2 (oracle/_ref, -O3, T=nproc)"}
+    o = Oracle()
+    t0 = time.perf_counter()
+    r = o.pagerank_ec(og, DAMPING, THRESHOLD, 2)
+    dt = time.perf_counter() - t0
+    return {"value": og.m * r.iterations / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
+            "iterations": r.iterations, "seconds": dt,
+            "sample": "2 EC iterations of config 2 with the C restatement (1 thread)"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    import paper_2203_09284_b200 as fb
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    dg = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
+    n, m = dg.n, dg.m
+    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
+
+    def step():
+        return dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
+
+    for _ in range(args.warmup):
+        r = step()
+    iters = r.trace.iterations
+    launches_per_step = r.kernel_launches
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+            kernel_ms.append(r.solve_ms)
+            assert r.trace.iterations == iters
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * m * iters / (ms_step * 1e-3) / 1e9
+    kms = float(np.mean(kernel_ms))
+    peak, peak_kind = peaks()
+    achieved = algorithmic_bytes(n, m) * iters / (kms * 1e-3) / 1e9
+
+    # Per-iteration device times of the persistent kernel (globaltimer).
+    tr = dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=True)
+    it_us = (tr.trace.iter_ns.astype(np.float64) / 1e3).tolist()
+
+    # FusEd (block-async) on the same resident graph.
+    fused = {}
+    fr = [dg.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False) for _ in range(max(3, args.steps // 4))]
+    fused = {"engine": "fused_b200", "iterations": fr[-1].trace.iterations,
+             "iterations_min_max": [min(x.trace.iterations for x in fr), max(x.trace.iterations for x in fr)],
+             "ms_per_solve": float(np.mean([x.solve_ms for x in fr])),
+             "gteps": float(np.mean([m * x.trace.iterations / x.solve_ms / 1e6 for x in fr]))}
+    lr = dg.run(fb.ENGINE_FUSED_LOCKSTEP, cfg, copy_ranks=False, copy_trace=False)
+    fused["lockstep"] = {"iterations": lr.trace.iterations, "ms_per_solve": lr.solve_ms,
+                         "waves": int(len(dg.wave_starts()) - 1)}
+
+    g_host = None
+    e2e = None
+    if not args.no_e2e:
+        g_host = dg.download()
+        e2e = e2e_leg(fb, g_host, local, args, iters)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        if g_host is None:
+            g_host = dg.download()
+        cpu = cpu_baseline_leg(g_host)
+
+    if rank == 0:
+        line = {
+            "metric": "GTEPS/iter (ec_b200 time-to-converge, config 2)", "value": value, "unit": "GTEPS",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
+            "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
+                       "norm": "linf", "step": "1 full EC solve (time-to-converge)",
+                       "parallelism": "replicas" if ws > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (in_src 268 MB + contrib 33.5 MB + row_ptr 33.5 MB); no flush"},
+            "time_to_converge_ms": ms_step,
+            "iteration_us": it_us,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "solve_kernel<false> (persistent EC, all iterations)",
+                         "kernel_ms": kms,
+                         "algorithmic_bytes_per_launch": algorithmic_bytes(n, m) * iters},
+            "fused": fused,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dg.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_leg(fb, g, device, args, iters) -> dict:
+    """fpr_b200_pagerank() on pinned host fpr::Graph arrays; H2D + solve + D2H timed."""
+    import torch
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
+        v = t.numpy().view(np.uint64)
+        v[:] = a
+        return t, v
+
+    keep = [pinned(g.in_start), pinned(g.in_src), pinned(g.out_degree)]
+    ins, src, od = (k[1] for k in keep)
+    ranks_t = torch.empty(g.n, dtype=torch.float64, pin_memory=True)
+    errs_t = torch.empty(10000, dtype=torch.float64, pin_memory=True)
+    view = fb._GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data, od.ctypes.data)
+    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)._c()
+    opts = fb._options(device=device)
+    res = fb._Result()
+    L = fb.lib()
+
+    def call():
+        fb._check(L.fpr_b200_pagerank(C.byref(view), fb.ENGINE_EC, C.byref(cfg), C.byref(opts),
+                                      ranks_t.data_ptr(), errs_t.data_ptr(), 10000, C.byref(res)))
+
+    for _ in range(2):
+        call()
+    steps = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    dt = (time.perf_counter() - t0) / steps
+    assert res.iterations == iters
+    h2d = 8 * (g.n + 1) + 8 * g.m + 8 * g.n
+    d2h = 8 * g.n + 8 * int(res.iterations)
+    return {"value": g.m * res.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "api": "fpr_b200_pagerank (C ABI, pinned host u64 CSR)"}
+
+
+if __name__ == "__main__":
+    main()

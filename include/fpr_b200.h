@@ -1,0 +1,151 @@
+/*
+ * fpr_b200.h -- C ABI of the B200-native FusEd-PageRank engines
+ * (libfpr_b200.so, built from paper_2203_09284_b200/csrc/).
+ *
+ * The reference (/root/reference/proj/include/fpr) is a header-only C++20
+ * library with no C ABI.  This header is what a foreign caller (ctypes, JNI,
+ * cgo, or the C++ drop-in wrapper include/fpr/pagerank_b200.hpp) binds.  No
+ * std:: or torch types cross it: plain pointers, sizes and PODs only.
+ *
+ * Entry point -> reference interface it replaces:
+ *   fpr_b200_pagerank(view, FPR_B200_ENGINE_EC, ...)
+ *        -> fpr::pagerank_ec_seq / pagerank_ec_par    (pagerank.hpp:128,147,195)
+ *   fpr_b200_pagerank(view, FPR_B200_ENGINE_FUSED, ...)
+ *        -> fpr::pagerank_fused_par                   (pagerank.hpp:261)
+ *   fpr_b200_pagerank(view, FPR_B200_ENGINE_FUSED_LOCKSTEP, ...)
+ *        -> fpr::pagerank_fused_seq-style deterministic schedule (pagerank.hpp:156)
+ *   fpr_graph_view          -> fpr::Graph               (graph.hpp:20-30)
+ *   fpr_config              -> fpr::PageRankConfig      (pagerank.hpp:17-22)
+ *   fpr_b200_result + ranks/errors buffers
+ *                           -> fpr::PageRankResult      (pagerank.hpp:24-38)
+ *   fpr_b200_graph_generate -> fpr::generate_rmat + fpr::build_csr
+ *                              (rmat.hpp:42, graph.hpp:35) and
+ *                              testutil::random_sparse (tests/test_util.hpp:49)
+ *   fpr_b200_graph_download_csr -> the fpr::Graph arrays of build_csr
+ *
+ * Errors: every function returns a status code; fpr_b200_last_error() gives
+ * the thread-local message.  FPR_B200_EINVAL carries the reference's exact
+ * std::invalid_argument text (pagerank.hpp:42-51,56,100; graph.hpp:39-43).
+ * Non-convergence is not an error (converged = 0), as in the reference.
+ *
+ * Threading: calls are synchronous and blocking.  A graph handle is not
+ * re-entrant; distinct handles are independent.  fpr_config.thread_count is
+ * validated (must be > 0, as the reference requires) and otherwise ignored.
+ */
+#ifndef FPR_B200_H
+#define FPR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPR_B200_OK 0
+#define FPR_B200_EINVAL 1 /* bad argument; message = reference's text */
+#define FPR_B200_ECUDA 2  /* CUDA runtime error or no usable device */
+#define FPR_B200_ENCCL 3  /* collective error (multi-GPU path) */
+#define FPR_B200_ENOMEM 4 /* device/host allocation failed */
+#define FPR_B200_ERANGE 5 /* n >= 2^31 (int32 vertex ids) */
+
+#define FPR_B200_ENGINE_EC 0             /* Jacobi, bit-deterministic */
+#define FPR_B200_ENGINE_FUSED 1          /* block-asynchronous Gauss-Seidel */
+#define FPR_B200_ENGINE_FUSED_LOCKSTEP 2 /* deterministic wave-lockstep GS */
+
+#define FPR_B200_NORM_LINF 0 /* reference stop rule: max |delta| <= threshold */
+#define FPR_B200_NORM_L1 1   /* sum |delta| <= threshold (BASELINE wording) */
+
+#define FPR_B200_GEN_RMAT 0    /* fpr::generate_rmat (rmat.hpp:42-77) */
+#define FPR_B200_GEN_UNIFORM 1 /* testutil::random_sparse (test_util.hpp:49-58) */
+
+/* Borrowed view of an fpr::Graph (graph.hpp:20-30); host or pinned memory. */
+typedef struct fpr_graph_view {
+  uint64_t n;
+  uint64_t m;
+  const uint64_t* in_start;   /* n + 1 */
+  const uint64_t* in_src;     /* m */
+  const uint64_t* out_degree; /* n */
+} fpr_graph_view;
+
+/* fpr::PageRankConfig (pagerank.hpp:17-22). */
+typedef struct fpr_config {
+  double damping;          /* reference default 0.85 */
+  double threshold;        /* reference default 1e-15 */
+  uint64_t max_iterations; /* reference default 10000 */
+  uint32_t thread_count;   /* validated, ignored on the GPU */
+} fpr_config;
+
+typedef struct fpr_b200_options {
+  int32_t device;       /* CUDA ordinal; -1 = current device */
+  int32_t norm;         /* FPR_B200_NORM_* stop rule */
+  uint32_t wave_count;  /* lockstep engine: waves per sweep (0 = auto) */
+  uint32_t reserved0;
+  void* stream;         /* cudaStream_t to run on; NULL = library stream */
+} fpr_b200_options;
+
+typedef struct fpr_b200_result {
+  uint64_t iterations;      /* == errors written (trace.iterations) */
+  int32_t converged;        /* last error <= threshold (detail::finish) */
+  int32_t reserved0;
+  double final_error;       /* last error, 1.0 if none (RankVector::final_error) */
+  double solve_ms;          /* device time of the convergence loop (CUDA events) */
+  double setup_ms;          /* rank/contribution initialisation kernel time */
+  uint64_t kernel_launches; /* library kernels launched by this call */
+} fpr_b200_result;
+
+typedef struct fpr_gen_params {
+  int32_t kind;          /* FPR_B200_GEN_* */
+  uint32_t scale;        /* rmat: n = 2^scale */
+  uint64_t edge_factor;  /* rmat: draws = edge_factor * n */
+  double a, b, c, d;     /* rmat quadrant probabilities */
+  uint64_t n;            /* uniform: vertices */
+  uint64_t avg_degree;   /* uniform: draws = n * avg_degree */
+  uint64_t seed;
+} fpr_gen_params;
+
+typedef struct fpr_b200_graph fpr_b200_graph;
+
+void fpr_b200_options_init(fpr_b200_options* opts);
+void fpr_b200_config_init(fpr_config* cfg); /* reference defaults */
+const char* fpr_b200_last_error(void);
+int fpr_b200_version(void);
+
+/* Copies + narrows a host fpr::Graph to the device (u64 -> int64 offsets,
+ * int32 ids, range-checked) and builds the merge-path task partition. */
+int fpr_b200_graph_create(const fpr_graph_view* view, const fpr_b200_options* opts,
+                          fpr_b200_graph** out);
+/* Generates + normalises a graph on the device, bit-identical to
+ * build_csr(generate_rmat(p)) / build_csr(random_sparse(...)). */
+int fpr_b200_graph_generate(const fpr_gen_params* params, const fpr_b200_options* opts,
+                            fpr_b200_graph** out);
+void fpr_b200_graph_destroy(fpr_b200_graph* g);
+int fpr_b200_graph_info(const fpr_b200_graph* g, uint64_t* n, uint64_t* m, uint64_t* ntasks);
+/* Downloads the CSR as fpr::Graph arrays (u64). */
+int fpr_b200_graph_download_csr(const fpr_b200_graph* g, uint64_t* in_start, uint64_t* in_src,
+                                uint64_t* out_degree);
+/* Vertex boundaries of the lockstep engine's waves for wave_count (0 = auto):
+ * writes *nwaves and wave_start[0..*nwaves] (capacity cap). */
+int fpr_b200_graph_wave_starts(fpr_b200_graph* g, uint32_t wave_count, uint64_t* wave_start,
+                               uint64_t cap, uint64_t* nwaves);
+
+/* Runs one engine to convergence on a resident graph.  ranks_out (n doubles),
+ * errors_out / l1_errors_out (errors_cap doubles, per-iteration max / sum of
+ * |delta|) and iter_ns_out (per-iteration device ns) are host buffers or NULL
+ * (results stay on the device).  Returns FPR_B200_EINVAL if errors_out is
+ * non-NULL and errors_cap < iterations actually run. */
+int fpr_b200_run(fpr_b200_graph* g, int engine, const fpr_config* cfg, double* ranks_out,
+                 double* errors_out, double* l1_errors_out, uint64_t* iter_ns_out,
+                 uint64_t errors_cap, fpr_b200_result* result);
+/* Device pointer of the rank vector left by the last run (n doubles). */
+const double* fpr_b200_graph_ranks_device(const fpr_b200_graph* g);
+
+/* One-shot drop-in: create from host view, run, copy results, destroy. */
+int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* cfg,
+                      const fpr_b200_options* opts, double* ranks_out, double* errors_out,
+                      uint64_t errors_cap, fpr_b200_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

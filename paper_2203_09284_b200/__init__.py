@@ -1,0 +1,379 @@
+"""B200-native FusEd-PageRank (arXiv 2203.09284) -- Python host mirror.
+
+Mirrors the reference's engine interface (``/root/reference/proj/include/fpr``):
+``PageRankConfig`` (pagerank.hpp:17-22), ``PageRankResult`` = ``RankVector`` +
+``ConvergenceTrace`` (:24-38), ``Graph`` (graph.hpp:20-30), ``RmatParams``
+(rmat.hpp:14-22), ``EngineKind`` tags (metrics.hpp:14-35) and ``l1_norm`` /
+``linf_norm`` (metrics.hpp:54-75).  The engines are the GPU ones:
+
+    pagerank_ec_b200(g, cfg)              ~ pagerank_ec_seq / pagerank_ec_par
+    pagerank_fused_b200(g, cfg)           ~ pagerank_fused_par (block-async GS)
+    pagerank_fused_lockstep_b200(g, cfg)  ~ deterministic wave-lockstep GS
+
+Every call goes through the C ABI of ``libfpr_b200.so`` (include/fpr_b200.h).
+There is no CPU fallback: if the library is missing or no B200 is present the
+call raises.  Argument errors raise ``ValueError`` carrying the reference's
+``std::invalid_argument`` text.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "PageRankConfig", "RankVector", "ConvergenceTrace", "PageRankResult", "Graph", "RmatParams",
+    "EngineKind", "DeviceGraph", "B200Error", "pagerank_ec_b200", "pagerank_fused_b200",
+    "pagerank_fused_lockstep_b200", "run_engine", "l1_norm", "linf_norm", "to_string",
+    "parse_engine", "lib", "LIB_PATH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfpr_b200.so")
+
+OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 5
+ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2
+NORM_LINF, NORM_L1 = 0, 1
+GEN_RMAT, GEN_UNIFORM = 0, 1
+
+
+class B200Error(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+# ----------------------------------------------------------------- C structs
+class _GraphView(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("m", C.c_uint64), ("in_start", C.c_void_p),
+                ("in_src", C.c_void_p), ("out_degree", C.c_void_p)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("damping", C.c_double), ("threshold", C.c_double),
+                ("max_iterations", C.c_uint64), ("thread_count", C.c_uint32)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("norm", C.c_int32), ("wave_count", C.c_uint32),
+                ("reserved0", C.c_uint32), ("stream", C.c_void_p)]
+
+
+class _Result(C.Structure):
+    _fields_ = [("iterations", C.c_uint64), ("converged", C.c_int32), ("reserved0", C.c_int32),
+                ("final_error", C.c_double), ("solve_ms", C.c_double), ("setup_ms", C.c_double),
+                ("kernel_launches", C.c_uint64)]
+
+
+class _GenParams(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("scale", C.c_uint32), ("edge_factor", C.c_uint64),
+                ("a", C.c_double), ("b", C.c_double), ("c", C.c_double), ("d", C.c_double),
+                ("n", C.c_uint64), ("avg_degree", C.c_uint64), ("seed", C.c_uint64)]
+
+
+EXPORTS = [
+    "fpr_b200_options_init", "fpr_b200_config_init", "fpr_b200_last_error", "fpr_b200_version",
+    "fpr_b200_graph_create", "fpr_b200_graph_generate", "fpr_b200_graph_destroy",
+    "fpr_b200_graph_info", "fpr_b200_graph_download_csr", "fpr_b200_graph_wave_starts",
+    "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank",
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libfpr_b200.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise B200Error(ECUDA, f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                                   "(make -C paper_2203_09284_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        vp, u64, i32 = C.c_void_p, C.c_uint64, C.c_int
+        L.fpr_b200_last_error.restype = C.c_char_p
+        L.fpr_b200_options_init.argtypes = [C.POINTER(_Options)]
+        L.fpr_b200_config_init.argtypes = [C.POINTER(_Config)]
+        L.fpr_b200_graph_create.argtypes = [C.POINTER(_GraphView), C.POINTER(_Options), C.POINTER(vp)]
+        L.fpr_b200_graph_generate.argtypes = [C.POINTER(_GenParams), C.POINTER(_Options), C.POINTER(vp)]
+        L.fpr_b200_graph_destroy.argtypes = [vp]
+        L.fpr_b200_graph_destroy.restype = None
+        L.fpr_b200_graph_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
+        L.fpr_b200_graph_download_csr.argtypes = [vp, vp, vp, vp]
+        L.fpr_b200_graph_wave_starts.argtypes = [vp, C.c_uint32, vp, u64, C.POINTER(u64)]
+        L.fpr_b200_run.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, vp, u64, C.POINTER(_Result)]
+        L.fpr_b200_graph_ranks_device.argtypes = [vp]
+        L.fpr_b200_graph_ranks_device.restype = vp
+        L.fpr_b200_pagerank.argtypes = [C.POINTER(_GraphView), i32, C.POINTER(_Config),
+                                        C.POINTER(_Options), vp, vp, u64, C.POINTER(_Result)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().fpr_b200_last_error().decode()
+        if rc in (EINVAL, ERANGE):
+            raise ValueError(msg)
+        raise B200Error(rc, msg)
+
+
+# ------------------------------------------------------- reference mirrors
+@dataclass
+class PageRankConfig:
+    """fpr::PageRankConfig (pagerank.hpp:17-22)."""
+
+    damping: float = 0.85
+    threshold: float = 1e-15
+    max_iterations: int = 10000
+    thread_count: int = 1  # validated; the GPU engines ignore it
+
+    def _c(self) -> _Config:
+        return _Config(self.damping, self.threshold, self.max_iterations, self.thread_count)
+
+
+@dataclass
+class RankVector:
+    values: np.ndarray
+    final_error: float = 1.0
+
+
+@dataclass
+class ConvergenceTrace:
+    errors: np.ndarray
+    iterations: int = 0
+    converged: bool = False
+    l1_errors: np.ndarray | None = None  # extension: sum |delta| per iteration
+    iter_ns: np.ndarray | None = None    # extension: device ns per iteration
+
+
+@dataclass
+class PageRankResult:
+    ranks: RankVector
+    trace: ConvergenceTrace
+    solve_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+@dataclass
+class Graph:
+    """fpr::Graph (graph.hpp:20-30): in-CSR with u64 arrays."""
+
+    n: int
+    m: int
+    in_start: np.ndarray
+    in_src: np.ndarray
+    out_degree: np.ndarray
+
+    def in_degree(self, u=None):
+        d = np.diff(self.in_start)
+        return d if u is None else int(d[u])
+
+
+@dataclass
+class RmatParams:
+    """fpr::RmatParams (rmat.hpp:14-22)."""
+
+    scale: int = 10
+    edge_factor: int = 20
+    a: float = 0.57
+    b: float = 0.19
+    c: float = 0.19
+    d: float = 0.05
+    seed: int = 0
+
+
+class EngineKind(enum.Enum):
+    """metrics.hpp:14 EngineKind + the B200 engines."""
+
+    EcSeq = "ec_seq"
+    FusedSeq = "fused_seq"
+    EcPar = "ec_par"
+    FusedPar = "fused_par"
+    EcB200 = "ec_b200"
+    FusedB200 = "fused_b200"
+    FusedLockstepB200 = "fused_lockstep_b200"
+
+
+def to_string(kind: EngineKind) -> str:
+    return kind.value
+
+
+def parse_engine(name: str) -> EngineKind:
+    for k in EngineKind:
+        if k.value == name:
+            return k
+    raise ValueError(f"unknown engine tag '{name}' (expected "
+                     + "|".join(k.value for k in EngineKind) + ")")
+
+
+_B200_ENGINE = {EngineKind.EcB200: ENGINE_EC, EngineKind.FusedB200: ENGINE_FUSED,
+                EngineKind.FusedLockstepB200: ENGINE_FUSED_LOCKSTEP}
+
+
+def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None) -> _Options:
+    o = _Options()
+    lib().fpr_b200_options_init(C.byref(o))
+    o.device = device
+    o.norm = norm
+    o.wave_count = wave_count
+    o.stream = stream
+    return o
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+class DeviceGraph:
+    """A graph resident in HBM (int64 offsets, int32 ids) + its task partition."""
+
+    def __init__(self, handle: int, device=-1, norm=NORM_LINF, wave_count=0):
+        self._h = C.c_void_p(handle)
+        self.norm = norm
+        n, m, nt = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().fpr_b200_graph_info(self._h, C.byref(n), C.byref(m), C.byref(nt)))
+        self.n, self.m, self.ntasks = n.value, m.value, nt.value
+
+    # -- construction ---------------------------------------------------
+    @classmethod
+    def from_graph(cls, g: Graph, device=-1, norm=NORM_LINF, wave_count=0, stream=None):
+        ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
+        v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
+        h = C.c_void_p()
+        _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream)),
+                                           C.byref(h)))
+        return cls(h.value, device, norm, wave_count)
+
+    @classmethod
+    def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None):
+        gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed)
+        h = C.c_void_p()
+        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream)),
+                                             C.byref(h)))
+        return cls(h.value, device, norm, wave_count)
+
+    @classmethod
+    def generate_uniform(cls, n: int, avg_degree: int, seed: int, device=-1, norm=NORM_LINF,
+                         wave_count=0, stream=None):
+        gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, n, avg_degree, seed)
+        h = C.c_void_p()
+        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream)),
+                                             C.byref(h)))
+        return cls(h.value, device, norm, wave_count)
+
+    def close(self) -> None:
+        if self._h:
+            lib().fpr_b200_graph_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- queries ----------------------------------------------------------
+    def download(self) -> Graph:
+        ins = np.empty(self.n + 1, np.uint64)
+        src = np.empty(max(self.m, 1), np.uint64)
+        od = np.empty(max(self.n, 1), np.uint64)
+        _check(lib().fpr_b200_graph_download_csr(self._h, ins.ctypes.data, src.ctypes.data, od.ctypes.data))
+        return Graph(self.n, self.m, ins, src[: self.m], od[: self.n])
+
+    def wave_starts(self, wave_count: int = 0) -> np.ndarray:
+        nw = C.c_uint64()
+        _check(lib().fpr_b200_graph_wave_starts(self._h, wave_count, None, 0, C.byref(nw)))
+        out = np.empty(nw.value + 1, np.uint64)
+        _check(lib().fpr_b200_graph_wave_starts(self._h, wave_count, out.ctypes.data, len(out), C.byref(nw)))
+        return out
+
+    def ranks_device_ptr(self) -> int:
+        return lib().fpr_b200_graph_ranks_device(self._h) or 0
+
+    # -- engines ----------------------------------------------------------
+    def run(self, engine: int, cfg: PageRankConfig, copy_ranks=True, copy_trace=True) -> PageRankResult:
+        cap = int(cfg.max_iterations) if copy_trace else 0
+        cap = min(cap, 1 << 24)
+        errors = np.empty(max(cap, 1), np.float64)
+        l1 = np.empty(max(cap, 1), np.float64)
+        ns = np.empty(max(cap, 1), np.uint64)
+        ranks = np.empty(max(self.n, 1), np.float64) if copy_ranks else None
+        res = _Result()
+        c = cfg._c()
+        _check(lib().fpr_b200_run(self._h, engine, C.byref(c),
+                                  ranks.ctypes.data if copy_ranks else None,
+                                  errors.ctypes.data if copy_trace else None,
+                                  l1.ctypes.data if copy_trace else None,
+                                  ns.ctypes.data if copy_trace else None, cap, C.byref(res)))
+        k = res.iterations
+        trace = ConvergenceTrace(errors[:k].copy() if copy_trace else np.empty(0), k, bool(res.converged),
+                                 l1[:k].copy() if copy_trace else None, ns[:k].copy() if copy_trace else None)
+        rv = RankVector(ranks[: self.n] if copy_ranks else np.empty(0), res.final_error)
+        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches)
+
+
+def run_engine(kind: EngineKind | str, g, cfg: PageRankConfig, **kw) -> PageRankResult:
+    """Run a B200 engine on a host ``Graph`` (uploaded, like the reference's
+    by-reference Graph) or a resident ``DeviceGraph``."""
+    if isinstance(kind, str):
+        kind = parse_engine(kind)
+    if kind not in _B200_ENGINE:
+        raise ValueError(f"{kind.value} is a reference CPU engine, not a B200 engine")
+    if isinstance(g, DeviceGraph):
+        return g.run(_B200_ENGINE[kind], cfg)
+    if g.n == 0:  # init_ranks (pagerank.hpp:56), checked before any device work
+        c = cfg._c()
+        _validate(c)
+        raise ValueError("pagerank: graph has no vertices")
+    with DeviceGraph.from_graph(g, **kw) as dg:
+        return dg.run(_B200_ENGINE[kind], cfg)
+
+
+def _validate(c: _Config) -> None:
+    if not (c.damping > 0.0 and c.damping < 1.0):
+        raise ValueError("pagerank: damping must be in (0,1)")
+    if not (c.threshold > 0.0):
+        raise ValueError("pagerank: threshold must be positive")
+    if c.max_iterations == 0:
+        raise ValueError("pagerank: max_iterations must be positive")
+    if c.thread_count == 0:
+        raise ValueError("pagerank: thread_count must be positive")
+
+
+def pagerank_ec_b200(g, cfg: PageRankConfig | None = None, **kw) -> PageRankResult:
+    return run_engine(EngineKind.EcB200, g, cfg or PageRankConfig(), **kw)
+
+
+def pagerank_fused_b200(g, cfg: PageRankConfig | None = None, **kw) -> PageRankResult:
+    return run_engine(EngineKind.FusedB200, g, cfg or PageRankConfig(), **kw)
+
+
+def pagerank_fused_lockstep_b200(g, cfg: PageRankConfig | None = None, **kw) -> PageRankResult:
+    return run_engine(EngineKind.FusedLockstepB200, g, cfg or PageRankConfig(), **kw)
+
+
+def l1_norm(a, b) -> float:
+    """metrics.hpp:54-62 (host-side metric, not the hot path)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.shape != b.shape:
+        raise ValueError(f"l1_norm: length mismatch ({a.size} vs {b.size})")
+    return float(np.abs(a - b).sum())
+
+
+def linf_norm(a, b) -> float:
+    """metrics.hpp:68-75."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.shape != b.shape:
+        raise ValueError("linf_norm: length mismatch")
+    return float(np.abs(a - b).max()) if a.size else 0.0

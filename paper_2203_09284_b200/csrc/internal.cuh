@@ -1,0 +1,106 @@
+// internal.cuh -- shared device/host declarations of libfpr_b200.so.
+//
+// HBM layout of a resident graph (narrowed):
+//   row      int64[n+1]   in-CSR offsets (fpr::Graph::in_start)
+//   src      int32[m]     in-edge sources, dst-grouped, ascending (in_src)
+//   outdeg   int32[n]     out-degrees (out_degree)
+//   pr       fp64[n]      ranks, updated in place by their owning task
+//   contrib  fp64[2][n]   pr/outdeg; EC/lockstep ping-pong, FUSED uses [0] in place
+//   task_*   merge-path partition of the (n + m) row-end/edge items into
+//            warp tasks of TASK_ITEMS items (Merrill & Garland merge-based SpMV)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fprb {
+
+constexpr int kBlockThreads = 256;
+constexpr int kWarpsPerBlock = kBlockThreads / 32;
+constexpr int kTaskItems = 256;  // merge items (row ends + edges) per warp task
+
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+struct DevGraph {
+  int32_t n = 0;
+  int64_t m = 0;
+  int64_t* row = nullptr;
+  int32_t* src = nullptr;
+  int32_t* outdeg = nullptr;
+};
+
+struct Partition {
+  int32_t ntasks = 0;
+  int32_t* task_row = nullptr;    // ntasks+1: first row whose end marker lies in task t
+  int64_t* task_edge = nullptr;   // ntasks+1: first edge of task t
+  int32_t* head_first = nullptr;  // ntasks: first task holding a piece of t's split head row, -1 if none
+  uint8_t* clean_start = nullptr; // ntasks+1: task t begins at a row boundary
+};
+
+// Everything the persistent solve kernel needs (passed by value).
+struct SolveParams {
+  int32_t n;
+  const int64_t* row;
+  const int32_t* src;
+  const int32_t* outdeg;
+  const int32_t* task_row;
+  const int64_t* task_edge;
+  const int32_t* head_first;
+  int32_t ntasks;
+  const int32_t* wave_task;  // nwaves+1
+  const int32_t* wave_row;   // nwaves+1
+  int32_t nwaves;
+  double* pr;
+  double* contrib0;
+  double* contrib1;
+  int32_t parity0;  // contrib buffer holding the previous sweep at local iteration 0
+  double* tail_partial;
+  unsigned int* tail_flag;
+  unsigned int epoch_base;
+  double damping;
+  double base;
+  double threshold;
+  int32_t norm;
+  uint32_t max_iters;
+  double* errors;     // [max_iters]
+  double* l1errors;   // [max_iters]
+  unsigned long long* iter_ns;  // [max_iters+1] globaltimer stamps
+  double* partials;   // 2 * gridDim.x
+  double* totals;     // 2
+  GridBar* bar;
+  unsigned int* out_iters;
+  int* out_stop;
+};
+
+enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
+
+// kernels.cu
+cudaError_t launch_partition(const DevGraph& g, Partition& p, cudaStream_t s);
+cudaError_t launch_init(const DevGraph& g, double* pr, double* contrib, cudaStream_t s);
+cudaError_t solve_grid(int engine, int num_sms, int* grid_out);
+cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s);
+cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound,
+                              unsigned int* bad_flag, cudaStream_t s);
+cudaError_t launch_check_offsets(const int64_t* row, int32_t n, int64_t m, unsigned int* bad_flag,
+                                 cudaStream_t s);
+cudaError_t launch_widen(const int64_t* row, const int32_t* ids32, uint64_t* out_row,
+                         uint64_t* out_ids, int64_t nrow, int64_t nids, cudaStream_t s);
+
+// generate.cu
+struct GenRequest {
+  int kind;
+  uint32_t scale;
+  uint64_t edge_factor;
+  double a, b, c, d;
+  uint64_t n;
+  uint64_t avg_degree;
+  uint64_t seed;
+};
+// Builds row/src/outdeg on the device (allocates them into g).  Returns a
+// cudaError_t; *msg receives a static description on non-CUDA failures.
+cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t s, const char** msg);
+
+}  // namespace fprb

@@ -1,0 +1,617 @@
+// runtime.cu -- C ABI (include/fpr_b200.h) and host runtime of libfpr_b200.so.
+//
+// Mirrors the reference's engine contract (pagerank.hpp): validation with the
+// same predicates and messages (:40-53, :56), the convergence trace
+// (errors[] = per-iteration max delta, iterations = errors.size(),
+// converged = errors.back() <= threshold, detail::finish :104-109), and
+// non-convergence as a result rather than an error.  There is no CPU
+// fallback: every numeric step runs in the kernels of kernels.cu/generate.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/fpr_b200.h"
+#include "internal.cuh"
+
+using namespace fprb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,     \
+                  std::string("fpr_b200: CUDA error '") + cudaGetErrorString(e_) + "' at " + \
+                      __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")");         \
+    }                                                                                     \
+  } while (0)
+
+constexpr uint32_t kChunkIters = 1u << 16;  // device trace capacity per launch
+
+struct Waves {
+  int32_t nwaves = 0;
+  int32_t* d_task = nullptr;
+  int32_t* d_row = nullptr;
+  std::vector<uint64_t> vertex_start;  // nwaves+1
+};
+
+}  // namespace
+
+struct fpr_b200_graph {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int norm = FPR_B200_NORM_LINF;
+  uint32_t wave_count = 0;
+  DevGraph g;
+  Partition part;
+  double* pr = nullptr;
+  double* contrib[2] = {nullptr, nullptr};
+  double* tail_partial = nullptr;
+  unsigned int* tail_flag = nullptr;
+  unsigned int epoch = 0;
+  int grid_full[2] = {0, 0};  // [0]=Jacobi/lockstep kernel, [1]=async kernel
+  double* partials = nullptr;
+  double* totals = nullptr;
+  GridBar* bar = nullptr;
+  unsigned int* d_iters = nullptr;
+  int* d_stop = nullptr;
+  double* d_errors = nullptr;
+  double* d_l1 = nullptr;
+  unsigned long long* d_ns = nullptr;
+  // pinned host staging
+  unsigned int* h_iters = nullptr;
+  int* h_stop = nullptr;
+  double* h_errors = nullptr;
+  double* h_l1 = nullptr;
+  unsigned long long* h_ns = nullptr;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  std::map<uint32_t, Waves> waves;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int dalloc(fpr_b200_graph* h, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMallocAsync(p, bytes, h->stream);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                std::string("fpr_b200: device allocation of ") + std::to_string(bytes) +
+                    " bytes failed: " + cudaGetErrorString(e));
+  }
+  h->allocs.push_back(*p);
+  return FPR_B200_OK;
+}
+
+template <class T>
+int dalloc_n(fpr_b200_graph* h, T** p, size_t count) {
+  return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+void destroy_handle(fpr_b200_graph* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto* p : {(void*)h->h_iters, (void*)h->h_stop, (void*)h->h_errors, (void*)h->h_l1,
+                  (void*)h->h_ns})
+    if (p) cudaFreeHost(p);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+// Device selection, stream, pool and the per-handle capability checks.
+int open_handle(const fpr_b200_options* opts, fpr_b200_graph** out) {
+  fpr_b200_options o;
+  fpr_b200_options_init(&o);
+  if (opts) o = *opts;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(FPR_B200_ECUDA, std::string("fpr_b200: no CUDA device available (") +
+                                    cudaGetErrorString(e) + ")");
+  auto* h = new fpr_b200_graph;
+  if (o.device >= 0) {
+    h->device = o.device;
+  } else {
+    cudaGetDevice(&h->device);
+  }
+  *out = h;
+  CK(cudaSetDevice(h->device));
+  int coop = 0, cc_major = 0;
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device));
+  CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+  CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, h->device));
+  if (!coop) return fail(FPR_B200_ECUDA, "fpr_b200: device lacks cooperative launch");
+  if (cc_major != 10)
+    return fail(FPR_B200_ECUDA, "fpr_b200: built for sm_100a (B200); device compute capability " +
+                                    std::to_string(cc_major) + ".x is not supported");
+  if (o.stream) {
+    h->stream = static_cast<cudaStream_t>(o.stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  h->norm = o.norm;
+  h->wave_count = o.wave_count;
+  for (auto& ev : h->ev) CK(cudaEventCreate(&ev));
+  CK(cudaMallocHost(&h->h_iters, sizeof(unsigned)));
+  CK(cudaMallocHost(&h->h_stop, sizeof(int)));
+  CK(cudaMallocHost(&h->h_errors, kChunkIters * sizeof(double)));
+  CK(cudaMallocHost(&h->h_l1, kChunkIters * sizeof(double)));
+  CK(cudaMallocHost(&h->h_ns, (kChunkIters + 1) * sizeof(unsigned long long)));
+  return FPR_B200_OK;
+}
+
+// Partition + solver state, common to create/generate.
+int finish_graph(fpr_b200_graph* h) {
+  DevGraph& g = h->g;
+  Partition& p = h->part;
+  const int64_t items = (int64_t)g.n + g.m;
+  const int64_t nt = (items + kTaskItems - 1) / kTaskItems;
+  if (nt >= INT32_MAX) return fail(FPR_B200_ERANGE, "fpr_b200: graph too large for task index");
+  p.ntasks = (int32_t)nt;
+  int rc;
+  if ((rc = dalloc_n(h, &p.task_row, nt + 1)) || (rc = dalloc_n(h, &p.task_edge, nt + 1)) ||
+      (rc = dalloc_n(h, &p.head_first, nt + 1)) || (rc = dalloc_n(h, &p.clean_start, nt + 1)))
+    return rc;
+  if (g.n > 0) CK(launch_partition(g, p, h->stream));
+  if ((rc = dalloc_n(h, &h->pr, g.n)) || (rc = dalloc_n(h, &h->contrib[0], g.n)) ||
+      (rc = dalloc_n(h, &h->contrib[1], g.n)) || (rc = dalloc_n(h, &h->tail_partial, nt + 1)) ||
+      (rc = dalloc_n(h, &h->tail_flag, nt + 1)))
+    return rc;
+  CK(cudaMemsetAsync(h->tail_flag, 0, (nt + 1) * sizeof(unsigned), h->stream));
+  CK(solve_grid(kEC, h->num_sms, &h->grid_full[0]));
+  CK(solve_grid(kFused, h->num_sms, &h->grid_full[1]));
+  const int gmax = std::max(h->grid_full[0], h->grid_full[1]);
+  if ((rc = dalloc_n(h, &h->partials, 2 * gmax)) || (rc = dalloc_n(h, &h->totals, 2)) ||
+      (rc = dalloc_n(h, &h->bar, 1)) || (rc = dalloc_n(h, &h->d_iters, 1)) ||
+      (rc = dalloc_n(h, &h->d_stop, 1)) || (rc = dalloc_n(h, &h->d_errors, kChunkIters)) ||
+      (rc = dalloc_n(h, &h->d_l1, kChunkIters)) || (rc = dalloc_n(h, &h->d_ns, kChunkIters + 1)))
+    return rc;
+  CK(cudaMemsetAsync(h->bar, 0, sizeof(GridBar), h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return FPR_B200_OK;
+}
+
+// Wave boundaries of the lockstep schedule: task indices where a task starts
+// on a row boundary, so that no split row straddles two waves.
+int get_waves(fpr_b200_graph* h, uint32_t wave_count, const Waves** out) {
+  const int64_t items = (int64_t)h->g.n + h->g.m;
+  uint32_t S = wave_count;
+  if (S == 0) {
+    int64_t want = (items + (1 << 22) - 1) >> 22;
+    S = (uint32_t)std::min<int64_t>(64, std::max<int64_t>(8, want));
+  }
+  auto it = h->waves.find(S);
+  if (it != h->waves.end()) {
+    *out = &it->second;
+    return FPR_B200_OK;
+  }
+  const int32_t nt = h->part.ntasks;
+  std::vector<uint8_t> clean(nt + 1);
+  std::vector<int32_t> trow(nt + 1);
+  CK(cudaMemcpyAsync(clean.data(), h->part.clean_start, nt + 1, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(trow.data(), h->part.task_row, (nt + 1) * sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  std::vector<int32_t> wt{0};
+  for (uint32_t w = 1; w < S; ++w) {
+    int64_t t = (int64_t)nt * w / S;
+    if (t <= wt.back()) t = wt.back() + 1;
+    while (t < nt && !clean[t]) ++t;
+    if (t >= nt) break;
+    wt.push_back((int32_t)t);
+  }
+  wt.push_back(nt);
+  Waves wv;
+  wv.nwaves = (int32_t)wt.size() - 1;
+  std::vector<int32_t> wr(wt.size());
+  for (size_t i = 0; i < wt.size(); ++i) {
+    wr[i] = trow[wt[i]];
+    wv.vertex_start.push_back((uint64_t)wr[i]);
+  }
+  int rc;
+  if ((rc = dalloc_n(h, &wv.d_task, wt.size())) || (rc = dalloc_n(h, &wv.d_row, wt.size())))
+    return rc;
+  CK(cudaMemcpyAsync(wv.d_task, wt.data(), wt.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                     h->stream));
+  CK(cudaMemcpyAsync(wv.d_row, wr.data(), wr.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  auto res = h->waves.emplace(S, std::move(wv));
+  *out = &res.first->second;
+  return FPR_B200_OK;
+}
+
+int validate_config(const fpr_config* cfg) {
+  // validate(PageRankConfig), pagerank.hpp:40-53 -- same predicates and text.
+  if (!(cfg->damping > 0.0 && cfg->damping < 1.0))
+    return fail(FPR_B200_EINVAL, "pagerank: damping must be in (0,1)");
+  if (!(cfg->threshold > 0.0)) return fail(FPR_B200_EINVAL, "pagerank: threshold must be positive");
+  if (cfg->max_iterations == 0)
+    return fail(FPR_B200_EINVAL, "pagerank: max_iterations must be positive");
+  if (cfg->thread_count == 0)
+    return fail(FPR_B200_EINVAL, "pagerank: thread_count must be positive");
+  return FPR_B200_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void fpr_b200_options_init(fpr_b200_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->device = -1;
+  o->norm = FPR_B200_NORM_LINF;
+}
+
+void fpr_b200_config_init(fpr_config* c) {
+  if (!c) return;
+  c->damping = 0.85;
+  c->threshold = 1e-15;
+  c->max_iterations = 10000;
+  c->thread_count = 1;
+}
+
+const char* fpr_b200_last_error(void) { return g_last_error.c_str(); }
+
+int fpr_b200_version(void) { return 1; }
+
+int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
+                          fpr_b200_graph** out) {
+  if (!v || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_create: null argument");
+  *out = nullptr;
+  if (v->n >= (1ULL << 31))
+    return fail(FPR_B200_ERANGE, "fpr_b200: n = " + std::to_string(v->n) +
+                                     " exceeds the int32 vertex-id range (n < 2^31)");
+  if (v->n > 0 && !v->in_start) return fail(FPR_B200_EINVAL, "fpr_b200: null in_start");
+  if (v->m > 0 && !v->in_src) return fail(FPR_B200_EINVAL, "fpr_b200: null in_src");
+  if (v->n > 0 && !v->out_degree) return fail(FPR_B200_EINVAL, "fpr_b200: null out_degree");
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  auto bail = [&](int code) {
+    destroy_handle(h);
+    return code;
+  };
+  DevGraph& g = h->g;
+  g.n = (int32_t)v->n;
+  g.m = (int64_t)v->m;
+  if ((rc = dalloc_n(h, &g.row, g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m)) ||
+      (rc = dalloc_n(h, &g.outdeg, g.n)))
+    return bail(rc);
+  unsigned int* bad = nullptr;
+  if ((rc = dalloc_n(h, &bad, 1))) return bail(rc);
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream);
+  if (e == cudaSuccess && g.n > 0)
+    e = cudaMemcpyAsync(g.row, v->in_start, (g.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                        h->stream);
+  // u64 -> int32 through a device staging buffer, chunked.
+  const int64_t chunk = 1 << 23;
+  uint64_t* stage = nullptr;
+  const int64_t need = std::min<int64_t>(chunk, std::max<int64_t>(g.m, g.n));
+  if (e == cudaSuccess && need > 0) {
+    if ((rc = dalloc_n(h, &stage, 2 * need))) return bail(rc);
+    int k = 0;
+    for (int64_t off = 0; e == cudaSuccess && off < g.m; off += chunk, k ^= 1) {
+      const int64_t cnt = std::min<int64_t>(chunk, g.m - off);
+      e = cudaMemcpyAsync(stage + k * need, v->in_src + off, cnt * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, h->stream);
+      if (e == cudaSuccess)
+        e = launch_narrow_ids(stage + k * need, g.src + off, cnt, v->n, bad, h->stream);
+    }
+    for (int64_t off = 0; e == cudaSuccess && off < g.n; off += chunk, k ^= 1) {
+      const int64_t cnt = std::min<int64_t>(chunk, g.n - off);
+      e = cudaMemcpyAsync(stage + k * need, v->out_degree + off, cnt * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, h->stream);
+      if (e == cudaSuccess)
+        e = launch_narrow_ids(stage + k * need, g.outdeg + off, cnt, v->n, bad, h->stream);
+    }
+  }
+  if (e == cudaSuccess && g.n > 0) e = launch_check_offsets(g.row, g.n, g.m, bad, h->stream);
+  unsigned hbad = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->h_iters, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess)
+    return bail(fail(FPR_B200_ECUDA, std::string("fpr_b200_graph_create: ") + cudaGetErrorString(e)));
+  hbad = *h->h_iters;
+  if (hbad & 1u)
+    return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_src/out_degree value outside [0," +
+                                          std::to_string(v->n) + ")"));
+  if (hbad & 6u)
+    return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_start is not a valid CSR offset array "
+                                      "(in_start[0]==0, non-decreasing, in_start[n]==m)"));
+  if ((rc = finish_graph(h))) return bail(rc);
+  *out = h;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* opts,
+                            fpr_b200_graph** out) {
+  if (!prm || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_generate: null argument");
+  *out = nullptr;
+  GenRequest req{prm->kind, prm->scale, prm->edge_factor, prm->a, prm->b, prm->c,
+                 prm->d,    prm->n,     prm->avg_degree, prm->seed};
+  if (req.kind == FPR_B200_GEN_RMAT) {
+    // validate(RmatParams), rmat.hpp:24-35 -- same text.
+    if (req.scale == 0 || req.scale > 32)
+      return fail(FPR_B200_EINVAL, "rmat: scale must be in [1,32], got " + std::to_string(req.scale));
+    if (req.edge_factor == 0) return fail(FPR_B200_EINVAL, "rmat: edge_factor must be positive");
+    if (req.a < 0 || req.b < 0 || req.c < 0 || req.d < 0 ||
+        std::abs(req.a + req.b + req.c + req.d - 1.0) > 1e-9)
+      return fail(FPR_B200_EINVAL,
+                  "rmat: quadrant probabilities must be non-negative and sum to 1");
+    if (req.scale > 30)
+      return fail(FPR_B200_ERANGE, "fpr_b200: rmat scale > 30 exceeds the int32 vertex-id range");
+  } else if (req.kind == FPR_B200_GEN_UNIFORM) {
+    if (req.n == 0) return fail(FPR_B200_EINVAL, "fpr_b200: uniform generator needs n > 0");
+    if (req.n >= (1ULL << 31))
+      return fail(FPR_B200_ERANGE, "fpr_b200: n exceeds the int32 vertex-id range");
+  } else {
+    return fail(FPR_B200_EINVAL, "fpr_b200: unknown generator kind");
+  }
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  const char* msg = nullptr;
+  cudaError_t e = generate_graph(req, h->g, h->stream, &msg);
+  if (e != cudaSuccess || msg) {
+    destroy_handle(h);
+    if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200_graph_generate: ") + msg);
+    return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                std::string("fpr_b200_graph_generate: ") + cudaGetErrorString(e));
+  }
+  // generate_graph allocated g's arrays with cudaMallocAsync on h->stream.
+  h->allocs.push_back(h->g.row);
+  h->allocs.push_back(h->g.src);
+  h->allocs.push_back(h->g.outdeg);
+  if ((rc = finish_graph(h))) {
+    destroy_handle(h);
+    return rc;
+  }
+  *out = h;
+  return FPR_B200_OK;
+}
+
+void fpr_b200_graph_destroy(fpr_b200_graph* h) { destroy_handle(h); }
+
+int fpr_b200_graph_info(const fpr_b200_graph* h, uint64_t* n, uint64_t* m, uint64_t* ntasks) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_info: null graph");
+  if (n) *n = (uint64_t)h->g.n;
+  if (m) *m = (uint64_t)h->g.m;
+  if (ntasks) *ntasks = (uint64_t)h->part.ntasks;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_download_csr(const fpr_b200_graph* hc, uint64_t* in_start, uint64_t* in_src,
+                                uint64_t* out_degree) {
+  auto* h = const_cast<fpr_b200_graph*>(hc);
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: null graph");
+  CK(cudaSetDevice(h->device));
+  const DevGraph& g = h->g;
+  const int64_t chunk = 1 << 24;
+  uint64_t* tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, 2 * chunk * sizeof(uint64_t), h->stream));
+  cudaError_t e = cudaSuccess;
+  if (in_start && g.n >= 0) {
+    for (int64_t off = 0; e == cudaSuccess && off < (int64_t)g.n + 1; off += chunk) {
+      const int64_t cnt = std::min<int64_t>(chunk, (int64_t)g.n + 1 - off);
+      e = launch_widen(g.row + off, nullptr, tmp, nullptr, cnt, 0, h->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(in_start + off, tmp, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                            h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    }
+  }
+  auto ids = [&](const int32_t* d, uint64_t* hout, int64_t count) {
+    for (int64_t off = 0; e == cudaSuccess && off < count; off += chunk) {
+      const int64_t cnt = std::min<int64_t>(chunk, count - off);
+      e = launch_widen(nullptr, d + off, nullptr, tmp + chunk, 0, cnt, h->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hout + off, tmp + chunk, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                            h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    }
+  };
+  if (in_src) ids(g.src, in_src, g.m);
+  if (out_degree) ids(g.outdeg, out_degree, g.n);
+  cudaFreeAsync(tmp, h->stream);
+  cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess)
+    return fail(FPR_B200_ECUDA, std::string("fpr_b200_graph_download_csr: ") + cudaGetErrorString(e));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t* wave_start,
+                               uint64_t cap, uint64_t* nwaves) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_wave_starts: null graph");
+  if (h->g.n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  CK(cudaSetDevice(h->device));
+  const Waves* wv = nullptr;
+  int rc = get_waves(h, wave_count ? wave_count : h->wave_count, &wv);
+  if (rc) return rc;
+  if (nwaves) *nwaves = (uint64_t)wv->nwaves;
+  if (wave_start) {
+    if (cap < wv->vertex_start.size())
+      return fail(FPR_B200_EINVAL, "fpr_b200_graph_wave_starts: buffer too small");
+    std::copy(wv->vertex_start.begin(), wv->vertex_start.end(), wave_start);
+  }
+  return FPR_B200_OK;
+}
+
+const double* fpr_b200_graph_ranks_device(const fpr_b200_graph* h) { return h ? h->pr : nullptr; }
+
+int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* ranks_out,
+                 double* errors_out, double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap,
+                 fpr_b200_result* result) {
+  if (!h || !cfg) return fail(FPR_B200_EINVAL, "fpr_b200_run: null argument");
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (h->g.n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  if (engine != kEC && engine != kFused && engine != kLockstep)
+    return fail(FPR_B200_EINVAL, "fpr_b200: unknown engine " + std::to_string(engine));
+  CK(cudaSetDevice(h->device));
+
+  // Jacobi = one wave; lockstep = the cached wave schedule; async = all tasks.
+  const Waves* wv = nullptr;
+  if ((rc = get_waves(h, engine == kLockstep ? h->wave_count : 1u, &wv))) return rc;
+  if (engine != kLockstep && wv->nwaves != 1) {
+    return fail(FPR_B200_ECUDA, "fpr_b200: internal error (EC wave schedule)");
+  }
+  const int variant = engine == kFused ? 1 : 0;
+  const int64_t want = (h->part.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
+
+  if ((uint64_t)h->epoch + std::min<uint64_t>(cfg->max_iterations, kChunkIters) + 2 >= 0xF0000000ull) {
+    CK(cudaMemsetAsync(h->tail_flag, 0, (h->part.ntasks + 1) * sizeof(unsigned), h->stream));
+    h->epoch = 0;
+  }
+
+  const DevGraph& g = h->g;
+  uint64_t launches = 0;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  CK(launch_init(g, h->pr, h->contrib[0], h->stream));
+  ++launches;
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  float setup_ms = 0.f, solve_ms = 0.f;
+  cudaEventElapsedTime(&setup_ms, h->ev[0], h->ev[1]);
+
+  SolveParams p{};
+  p.n = g.n;
+  p.row = g.row;
+  p.src = g.src;
+  p.outdeg = g.outdeg;
+  p.task_row = h->part.task_row;
+  p.task_edge = h->part.task_edge;
+  p.head_first = h->part.head_first;
+  p.ntasks = h->part.ntasks;
+  p.wave_task = wv->d_task;
+  p.wave_row = wv->d_row;
+  p.nwaves = wv->nwaves;
+  p.pr = h->pr;
+  p.contrib0 = h->contrib[0];
+  p.contrib1 = h->contrib[1];
+  p.tail_partial = h->tail_partial;
+  p.tail_flag = h->tail_flag;
+  p.damping = cfg->damping;
+  p.base = (1.0 - cfg->damping) / (double)g.n;  // pagerank.hpp:81
+  p.threshold = cfg->threshold;
+  p.norm = h->norm;
+  p.errors = h->d_errors;
+  p.l1errors = h->d_l1;
+  p.iter_ns = h->d_ns;
+  p.partials = h->partials;
+  p.totals = h->totals;
+  p.bar = h->bar;
+  p.out_iters = h->d_iters;
+  p.out_stop = h->d_stop;
+
+  uint64_t total = 0;
+  int parity = 0;
+  int stop = 0;
+  double last_err = 1.0, last_l1 = 1.0;
+  while (total < cfg->max_iterations) {
+    const uint64_t chunk = std::min<uint64_t>(cfg->max_iterations - total, kChunkIters);
+    p.max_iters = (uint32_t)chunk;
+    p.epoch_base = h->epoch;
+    p.parity0 = parity;
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(launch_solve(engine, grid, p, h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    ++launches;
+    CK(cudaMemcpyAsync(h->h_iters, h->d_iters, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->h_stop, h->d_stop, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float chunk_ms = 0.f;
+    cudaEventElapsedTime(&chunk_ms, h->ev[1], h->ev[2]);
+    solve_ms += chunk_ms;
+    const uint64_t done = *h->h_iters;
+    stop = *h->h_stop;
+    if (done == 0 || done > chunk) return fail(FPR_B200_ECUDA, "fpr_b200: solver reported bad count");
+    if (errors_out && errors_cap < total + done)
+      return fail(FPR_B200_EINVAL, "fpr_b200_run: errors buffer holds " +
+                                       std::to_string(errors_cap) + " entries, need " +
+                                       std::to_string(total + done));
+    CK(cudaMemcpyAsync(h->h_errors, h->d_errors, done * sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->h_l1, h->d_l1, done * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (iter_ns_out)
+      CK(cudaMemcpyAsync(h->h_ns, h->d_ns, (done + 1) * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (errors_out) std::memcpy(errors_out + total, h->h_errors, done * sizeof(double));
+    if (l1_out) std::memcpy(l1_out + total, h->h_l1, done * sizeof(double));
+    if (iter_ns_out)
+      for (uint64_t k = 0; k < done; ++k) iter_ns_out[total + k] = h->h_ns[k + 1] - h->h_ns[k];
+    last_err = h->h_errors[done - 1];
+    last_l1 = h->h_l1[done - 1];
+    total += done;
+    h->epoch += (unsigned)done;
+    parity ^= (int)(done & 1);
+    if (stop) break;
+  }
+  if (ranks_out)
+    CK(cudaMemcpyAsync(ranks_out, h->pr, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (result) {
+    result->iterations = total;
+    const double crit = h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err;
+    result->converged = (total > 0 && crit <= cfg->threshold) ? 1 : 0;
+    result->final_error = total > 0 ? last_err : 1.0;
+    result->setup_ms = setup_ms;
+    result->solve_ms = solve_ms;
+    result->kernel_launches = launches;
+  }
+  return FPR_B200_OK;
+}
+
+int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* cfg,
+                      const fpr_b200_options* opts, double* ranks_out, double* errors_out,
+                      uint64_t errors_cap, fpr_b200_result* result) {
+  if (!view || !cfg) return fail(FPR_B200_EINVAL, "fpr_b200_pagerank: null argument");
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (view->n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  fpr_b200_graph* h = nullptr;
+  if ((rc = fpr_b200_graph_create(view, opts, &h))) return rc;
+  rc = fpr_b200_run(h, engine, cfg, ranks_out, errors_out, nullptr, nullptr, errors_cap, result);
+  if (result) result->kernel_launches += 0;
+  fpr_b200_graph_destroy(h);
+  return rc;
+}
+
+}  // extern "C"
