@@ -196,7 +196,7 @@ cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t st, 
   GK(cudaGetLastError());
 
   GK(cudaMallocAsync(&g.row, (n + 1) * sizeof(int64_t), st));
-  GK(cudaMallocAsync(&g.src, std::max<uint64_t>(valid, 1) * sizeof(int32_t), st));
+  GK(cudaMallocAsync(&g.src, (valid + 4) * sizeof(int32_t), st));
   GK(cudaMallocAsync(&g.outdeg, n * sizeof(int32_t), st));
   indeg = reinterpret_cast<unsigned long long*>(g.row);  // counts -> offsets in place
   GK(cudaMemsetAsync(g.row, 0, (n + 1) * sizeof(int64_t), st));

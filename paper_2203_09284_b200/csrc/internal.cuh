@@ -28,7 +28,7 @@ struct DevGraph {
   int32_t n = 0;
   int64_t m = 0;
   int64_t* row = nullptr;
-  int32_t* src = nullptr;
+  int32_t* src = nullptr;  // m + 4 entries: 16-B staged loads may overrun by 3
   int32_t* outdeg = nullptr;
 };
 
@@ -57,9 +57,7 @@ struct SolveParams {
   double* contrib0;
   double* contrib1;
   int32_t parity0;  // contrib buffer holding the previous sweep at local iteration 0
-  double* tail_partial;
-  unsigned int* tail_flag;
-  unsigned int epoch_base;
+  double* tail_partial;  // per task: partial of its open row; NaN = not ready
   double damping;
   double base;
   double threshold;

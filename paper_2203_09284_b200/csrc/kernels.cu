@@ -162,72 +162,146 @@ __device__ __forceinline__ void grid_sync_reduce(const SolveParams& p, double bm
 }
 
 // ------------------------------------------------------------ one warp task
-template <bool ASYNC>
-__device__ __forceinline__ void process_task(const SolveParams& p, int t, int fresh_below,
-                                             const double* prev, double* cur, double* vals,
-                                             int lane, unsigned epoch, unsigned long long pol,
-                                             double& lmax, double& lsum) {
-  constexpr int U = kTaskItems / 32;
-  const int i0 = __ldg(p.task_row + t), i1 = __ldg(p.task_row + t + 1);
-  const int64_t j0 = __ldg(p.task_edge + t), j1 = __ldg(p.task_edge + t + 1);
-  const int nE = (int)(j1 - j0);
+// Per-warp shared memory: two in_src staging slices (16-B cp.async chunks, so
+// up to 3 leading pad entries + kTaskItems + 3 trailing) and two gathered
+// value buffers -- a 2-deep cp.async pipeline across the warp's tasks.
+constexpr int kSrcSlots = kTaskItems + 8;
+constexpr int kWarpSmemBytes = 2 * kSrcSlots * 4 + 2 * kTaskItems * 8;
+constexpr int kSolveSmemBytes = kWarpsPerBlock * kWarpSmemBytes;
 
-  // 1. stream the in_src slice (coalesced) and gather contributions.
-  int sidx[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int k = lane + 32 * u;
-    sidx[u] = (k < nE) ? ld_stream_i32(p.src + j0 + k, pol) : 0;
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, unsigned long long pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct TaskMeta {
+  int i0, i1;
+  int64_t j0, j1;
+};
+
+__device__ __forceinline__ TaskMeta load_meta(const SolveParams& p, int t) {
+  TaskMeta m;
+  m.i0 = __ldg(p.task_row + t);
+  m.i1 = __ldg(p.task_row + t + 1);
+  m.j0 = __ldg(p.task_edge + t);
+  m.j1 = __ldg(p.task_edge + t + 1);
+  return m;
+}
+
+// Row metadata of a task's first 32 rows, prefetched one pipeline step early.
+struct RowPre {
+  int64_t a, b;
+  int od;
+  double ov;
+};
+
+__device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMeta& m, int lane) {
+  RowPre r{0, 0, 0, 0.0};
+  const int row = m.i0 + lane;
+  if (row < m.i1) {
+    r.a = __ldg(p.row + row);
+    r.b = __ldg(p.row + row + 1);
+    r.od = __ldg(p.outdeg + row);
+    r.ov = p.pr[row];
   }
-  double v[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int k = lane + 32 * u;
-    if (k < nE) {
-      const int s = sidx[u];
-      if (ASYNC) {
-        v[u] = ld_relaxed_f64(cur + s);  // value-atomic live read (pagerank.hpp:305)
-      } else {
-        const double* basep = (s < fresh_below) ? cur : prev;
-        v[u] = basep[s];
-      }
+  return r;
+}
+
+// Stage the task's in_src slice: 16-B chunks from the 4-element-aligned base.
+__device__ __forceinline__ void issue_src(const SolveParams& p, const TaskMeta& m, int32_t* sbuf,
+                                          int lane, unsigned long long pol) {
+  const int64_t base = m.j0 & ~int64_t(3);
+  const int nchunks = (int)((m.j1 - base + 3) >> 2);
+  for (int c = lane; c < nchunks; c += 32) cp_async16(sbuf + 4 * c, p.src + base + 4 * c, pol);
+}
+
+// Gather contrib[src] for the task's edges straight into shared memory.
+template <bool ASYNC>
+__device__ __forceinline__ void issue_gathers(const TaskMeta& m, const int32_t* sbuf, double* vbuf,
+                                              int fresh_below, const double* prev,
+                                              const double* cur, int lane) {
+  const int off = (int)(m.j0 & 3);
+  const int nE = (int)(m.j1 - m.j0);
+  for (int k = lane; k < nE; k += 32) {
+    const int s = sbuf[off + k];
+    const double* basep = ASYNC ? cur : ((s < fresh_below) ? cur : prev);
+    cp_async8(vbuf + k, basep + s);
+  }
+}
+
+__device__ __forceinline__ double tail_not_ready() { return __longlong_as_double(-1ll); }  // NaN
+
+template <bool ASYNC>
+__device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
+                                             const RowPre& pre, const double* vals, double* cur,
+                                             int lane, double& lmax, double& lsum) {
+  const int i0 = m.i0, i1 = m.i1;
+  const int64_t j0 = m.j0;
+  const int nE = (int)(m.j1 - m.j0);
+
+  // (a) open row at the end of the task: publish this task's partial first,
+  //     so a task waiting on it never waits on this task's own head (no chain).
+  //     The partial IS the flag: ready iff >= 0 (sums of positive contributions).
+  if (i1 < p.n) {
+    const int64_t rs = __ldg(p.row + i1);
+    const int lo = (int)((rs > j0 ? rs : j0) - j0);
+    if (lo < nE) {
+      double a = 0.0;
+      for (int k = lo + lane; k < nE; k += 32) a += vals[k];
+      a = warp_sum(a);
+      if (lane == 0) st_relaxed_f64(p.tail_partial + t, a);
     }
   }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int k = lane + 32 * u;
-    if (k < nE) vals[k] = v[u];
-  }
-  __syncwarp();
-
-  // 2. head row split across earlier tasks: combine their partials in order.
+  // (b) head row split across earlier tasks: combine their partials in task order.
   bool has_head = false;
   double head_sum = 0.0;
-  if (i0 < i1) {
-    const int64_t rs = __ldg(p.row + i0);
-    if (rs < j0) {
-      has_head = true;
-      const int ta = __ldg(p.head_first + t);
-      double acc = 0.0;
-      for (int tt = ta + lane; tt < t; tt += 32) {
-        while (ld_acquire_u32(p.tail_flag + tt) != epoch) __nanosleep(32);
-        acc += ld_relaxed_f64(p.tail_partial + tt);
+  if (i0 < i1 && __shfl_sync(FULL_MASK, pre.a, 0) < j0) {
+    has_head = true;
+    const int ta = __ldg(p.head_first + t);
+    double acc = 0.0;
+    for (int tt = ta + lane; tt < t; tt += 32) {
+      double v = ld_relaxed_f64(p.tail_partial + tt);
+      while (!(v >= 0.0)) {
+        __nanosleep(32);
+        v = ld_relaxed_f64(p.tail_partial + tt);
       }
-      acc = warp_sum(acc);
-      const int hi = (int)(__ldg(p.row + i0 + 1) - j0);
-      double own = 0.0;
-      for (int k = lane; k < hi; k += 32) own += vals[k];
-      head_sum = acc + warp_sum(own);
+      acc += v;
+      st_relaxed_f64(p.tail_partial + tt, tail_not_ready());  // consumed: re-arm for next sweep
     }
+    acc = warp_sum(acc);
+    const int hi = (int)(__shfl_sync(FULL_MASK, pre.b, 0) - j0);
+    double own = 0.0;
+    for (int k = lane; k < hi; k += 32) own += vals[k];
+    head_sum = acc + warp_sum(own);
   }
 
-  // 3. rows whose end marker lies in this task: lane per row.
+  // (c) rows whose end marker lies in this task: lane per row, ascending-src
+  //     sequential sums (the reference's order); long rows warp-cooperative.
   for (int rb = i0; rb < i1; rb += 32) {
     const int r = rb + lane;
     const bool act = r < i1;
+    int64_t a = pre.a, b = pre.b;
+    int od = pre.od;
+    double ov = pre.ov;
+    if (rb != i0 && act) {
+      a = __ldg(p.row + r);
+      b = __ldg(p.row + r + 1);
+      od = __ldg(p.outdeg + r);
+      ov = p.pr[r];
+    }
     int lo = 0, hi = 0;
     if (act) {
-      const int64_t a = __ldg(p.row + r), b = __ldg(p.row + r + 1);
       lo = (int)((a > j0 ? a : j0) - j0);
       hi = (int)(b - j0);
     }
@@ -242,17 +316,15 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, int fr
       const int L = __ffs(lm) - 1;
       lm &= lm - 1;
       const int llo = __shfl_sync(FULL_MASK, lo, L), lhi = __shfl_sync(FULL_MASK, hi, L);
-      double a = 0.0;
-      for (int k = llo + lane; k < lhi; k += 32) a += vals[k];
-      a = warp_sum(a);
-      if (lane == L) sum = a;
+      double acc = 0.0;
+      for (int k = llo + lane; k < lhi; k += 32) acc += vals[k];
+      acc = warp_sum(acc);
+      if (lane == L) sum = acc;
     }
     if (head) sum = head_sum;
     if (act) {
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
-      const double ov = p.pr[r];
       p.pr[r] = nv;
-      const int od = __ldg(p.outdeg + r);
       if (od > 0) {
         const double c = __ddiv_rn(nv, (double)od);
         if (ASYNC)
@@ -265,22 +337,60 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, int fr
       lsum += d;
     }
   }
+}
 
-  // 4. open row at the end of the task: publish this task's partial.
-  if (i1 < p.n) {
-    const int64_t rs = __ldg(p.row + i1);
-    const int lo = (int)((rs > j0 ? rs : j0) - j0);
-    if (lo < nE) {
-      double a = 0.0;
-      for (int k = lo + lane; k < nE; k += 32) a += vals[k];
-      a = warp_sum(a);
-      if (lane == 0) {
-        p.tail_partial[t] = a;
-        __threadfence();
-        st_release_u32(p.tail_flag + t, epoch);
-      }
+// All tasks t = tb + gwarp + k*nwarps < te of this warp, software-pipelined:
+// step k waits for in_src(k), issues in_src(k+1) and gathers(k), prefetches
+// meta(k+2) and row metadata(k), then processes task k-1 while gathers(k)
+// are in flight.  cp.async group order: S0, [empty], S1, G0, S2, G1, ...
+template <bool ASYNC>
+__device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
+                                          int nwarps, int fresh_below, const double* prev,
+                                          double* cur, int32_t* sb, double* vb, int lane,
+                                          unsigned long long pol, double& lmax, double& lsum) {
+  int tk = tb + gwarp;
+  if (tk >= te) return;
+  TaskMeta mA = load_meta(p, tk);
+  issue_src(p, mA, sb, lane, pol);
+  cp_async_commit();
+  cp_async_commit();  // stands in for G_{-1}
+  TaskMeta mB{0, 0, 0, 0};
+  if (tk + nwarps < te) mB = load_meta(p, tk + nwarps);
+  TaskMeta mP{0, 0, 0, 0};
+  RowPre rpP{0, 0, 0, 0.0};
+  int tP = -1;
+  int k = 0;
+  while (true) {
+    const bool haveA = tk < te;
+    cp_async_wait<1>();  // in_src(k) landed
+    __syncwarp();
+    if (haveA && tk + nwarps < te) issue_src(p, mB, sb + ((k + 1) & 1) * kSrcSlots, lane, pol);
+    cp_async_commit();
+    RowPre rpA{0, 0, 0, 0.0};
+    TaskMeta mC{0, 0, 0, 0};
+    if (haveA) {
+      issue_gathers<ASYNC>(mA, sb + (k & 1) * kSrcSlots, vb + (k & 1) * kTaskItems, fresh_below,
+                           prev, cur, lane);
+      if (tk + 2 * nwarps < te) mC = load_meta(p, tk + 2 * nwarps);
+      rpA = load_rowpre(p, mA, lane);
     }
+    cp_async_commit();
+    if (tP >= 0) {
+      cp_async_wait<2>();  // gathers(k-1) landed
+      __syncwarp();
+      process_task<ASYNC>(p, tP, mP, rpP, vb + ((k - 1) & 1) * kTaskItems, cur, lane, lmax, lsum);
+      __syncwarp();
+    }
+    if (!haveA) break;
+    mP = mA;
+    rpP = rpA;
+    tP = tk;
+    mA = mB;
+    mB = mC;
+    tk += nwarps;
+    ++k;
   }
+  cp_async_wait<0>();
   __syncwarp();
 }
 
@@ -288,11 +398,13 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, int fr
 // ASYNC=false: Jacobi (nwaves == 1, EC) or wave-lockstep Gauss-Seidel.
 // ASYNC=true : block-asynchronous Gauss-Seidel, in-place contributions.
 template <bool ASYNC>
-__global__ void __launch_bounds__(kBlockThreads, 4) solve_kernel(SolveParams p) {
-  __shared__ double svals[kWarpsPerBlock * kTaskItems];
+__global__ void __launch_bounds__(kBlockThreads, 2) solve_kernel(SolveParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double sred[2 * kWarpsPerBlock];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* vals = svals + wib * kTaskItems;
+  unsigned char* wsm = smem + wib * kWarpSmemBytes;
+  int32_t* sb = reinterpret_cast<int32_t*>(wsm);
+  double* vb = reinterpret_cast<double*>(wsm + 2 * kSrcSlots * 4);
   const int gwarp = blockIdx.x * kWarpsPerBlock + wib;
   const int nwarps = gridDim.x * kWarpsPerBlock;
   const unsigned long long pol = evict_first_policy();
@@ -300,20 +412,16 @@ __global__ void __launch_bounds__(kBlockThreads, 4) solve_kernel(SolveParams p) 
   if (blockIdx.x == 0 && threadIdx.x == 0) p.iter_ns[0] = globaltimer();
 
   for (uint32_t it = 0; it < p.max_iters; ++it) {
-    const unsigned epoch = p.epoch_base + it + 1;
     double lmax = 0.0, lsum = 0.0;
     if (ASYNC) {
-      double* c = p.contrib0;
-      for (int t = gwarp; t < p.ntasks; t += nwarps)
-        process_task<true>(p, t, 0, c, c, vals, lane, epoch, pol, lmax, lsum);
+      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0, sb, vb, lane, pol,
+                      lmax, lsum);
     } else {
       const double* prev = par ? p.contrib1 : p.contrib0;
       double* cur = par ? p.contrib0 : p.contrib1;
       for (int w = 0; w < p.nwaves; ++w) {
-        const int fresh_below = __ldg(p.wave_row + w);
-        const int tb = __ldg(p.wave_task + w), te = __ldg(p.wave_task + w + 1);
-        for (int t = tb + gwarp; t < te; t += nwarps)
-          process_task<false>(p, t, fresh_below, prev, cur, vals, lane, epoch, pol, lmax, lsum);
+        run_tasks<false>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
+                         __ldg(p.wave_row + w), prev, cur, sb, vb, lane, pol, lmax, lsum);
         if (w + 1 < p.nwaves) grid_sync(p.bar);
       }
       par ^= 1;
@@ -455,11 +563,15 @@ cudaError_t launch_init(const DevGraph& g, double* pr, double* contrib, cudaStre
 
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
   int per_sm = 0;
+  for (const void* fn : {(const void*)solve_kernel<true>, (const void*)solve_kernel<false>}) {
+    cudaError_t a = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemBytes);
+    if (a != cudaSuccess) return a;
+  }
   cudaError_t e = engine == kFused
                       ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<true>,
-                                                                      kBlockThreads, 0)
+                                                                      kBlockThreads, kSolveSmemBytes)
                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<false>,
-                                                                      kBlockThreads, 0);
+                                                                      kBlockThreads, kSolveSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   *grid_out = per_sm * num_sms;
@@ -470,7 +582,7 @@ cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_
   SolveParams copy = p;
   void* args[] = {&copy};
   const void* fn = engine == kFused ? (const void*)solve_kernel<true> : (const void*)solve_kernel<false>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, 0, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, kSolveSmemBytes, s);
 }
 
 cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound,

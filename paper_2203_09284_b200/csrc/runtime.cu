@@ -62,8 +62,6 @@ struct fpr_b200_graph {
   double* pr = nullptr;
   double* contrib[2] = {nullptr, nullptr};
   double* tail_partial = nullptr;
-  unsigned int* tail_flag = nullptr;
-  unsigned int epoch = 0;
   int grid_full[2] = {0, 0};  // [0]=Jacobi/lockstep kernel, [1]=async kernel
   double* partials = nullptr;
   double* totals = nullptr;
@@ -181,10 +179,10 @@ int finish_graph(fpr_b200_graph* h) {
     return rc;
   if (g.n > 0) CK(launch_partition(g, p, h->stream));
   if ((rc = dalloc_n(h, &h->pr, g.n)) || (rc = dalloc_n(h, &h->contrib[0], g.n)) ||
-      (rc = dalloc_n(h, &h->contrib[1], g.n)) || (rc = dalloc_n(h, &h->tail_partial, nt + 1)) ||
-      (rc = dalloc_n(h, &h->tail_flag, nt + 1)))
+      (rc = dalloc_n(h, &h->contrib[1], g.n)) || (rc = dalloc_n(h, &h->tail_partial, nt + 1)))
     return rc;
-  CK(cudaMemsetAsync(h->tail_flag, 0, (nt + 1) * sizeof(unsigned), h->stream));
+  // tail partials start "not ready" (NaN); each consumer re-arms what it reads.
+  CK(cudaMemsetAsync(h->tail_partial, 0xFF, (nt + 1) * sizeof(double), h->stream));
   CK(solve_grid(kEC, h->num_sms, &h->grid_full[0]));
   CK(solve_grid(kFused, h->num_sms, &h->grid_full[1]));
   const int gmax = std::max(h->grid_full[0], h->grid_full[1]);
@@ -306,7 +304,7 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
   DevGraph& g = h->g;
   g.n = (int32_t)v->n;
   g.m = (int64_t)v->m;
-  if ((rc = dalloc_n(h, &g.row, g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m)) ||
+  if ((rc = dalloc_n(h, &g.row, g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m + 4)) ||
       (rc = dalloc_n(h, &g.outdeg, g.n)))
     return bail(rc);
   unsigned int* bad = nullptr;
@@ -495,10 +493,6 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   const int64_t want = (h->part.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
 
-  if ((uint64_t)h->epoch + std::min<uint64_t>(cfg->max_iterations, kChunkIters) + 2 >= 0xF0000000ull) {
-    CK(cudaMemsetAsync(h->tail_flag, 0, (h->part.ntasks + 1) * sizeof(unsigned), h->stream));
-    h->epoch = 0;
-  }
 
   const DevGraph& g = h->g;
   uint64_t launches = 0;
@@ -526,7 +520,6 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.contrib0 = h->contrib[0];
   p.contrib1 = h->contrib[1];
   p.tail_partial = h->tail_partial;
-  p.tail_flag = h->tail_flag;
   p.damping = cfg->damping;
   p.base = (1.0 - cfg->damping) / (double)g.n;  // pagerank.hpp:81
   p.threshold = cfg->threshold;
@@ -547,7 +540,6 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   while (total < cfg->max_iterations) {
     const uint64_t chunk = std::min<uint64_t>(cfg->max_iterations - total, kChunkIters);
     p.max_iters = (uint32_t)chunk;
-    p.epoch_base = h->epoch;
     p.parity0 = parity;
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(launch_solve(engine, grid, p, h->stream));
@@ -580,7 +572,6 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     last_err = h->h_errors[done - 1];
     last_l1 = h->h_l1[done - 1];
     total += done;
-    h->epoch += (unsigned)done;
     parity ^= (int)(done & 1);
     if (stop) break;
   }
