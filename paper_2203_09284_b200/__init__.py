@@ -32,7 +32,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfpr_b200.so")
+LIB_PATH = os.environ.get("FPR_B200_LIB") or os.path.join(HERE, "libfpr_b200.so")
 
 OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 5
 ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2

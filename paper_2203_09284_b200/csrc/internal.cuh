@@ -17,7 +17,9 @@ namespace fprb {
 
 constexpr int kBlockThreads = 256;
 constexpr int kWarpsPerBlock = kBlockThreads / 32;
-constexpr int kTaskItems = 256;  // merge items (row ends + edges) per warp task
+constexpr int kTaskDiag = 192;   // merge-path diagonal stride between warp tasks
+constexpr int kSnapEdges = 60;   // a boundary inside a row of <= kSnapEdges edges moves to the row start
+constexpr int kTaskItems = kTaskDiag + kSnapEdges;  // max items (and edges) per task: 252 (+3 pad <= 256)
 
 struct GridBar {
   unsigned int count;

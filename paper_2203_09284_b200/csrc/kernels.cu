@@ -8,7 +8,7 @@
 // the lockstep schedule) and the stop predicate `error <= threshold`
 // (:141, :185) evaluated identically by every CTA.
 //
-// Work unit: a warp task = kTaskItems consecutive items of the merge path of
+// Work unit: a warp task = ~kTaskDiag consecutive items of the merge path of
 // (row ends, edges) -- the pull restatement of scatter+gather:
 //   * the task's in_src slice is streamed coalesced (4 B/edge, L1 no-allocate,
 //     L2 evict-first so the rank vector stays L2-resident) and its
@@ -162,28 +162,21 @@ __device__ __forceinline__ void grid_sync_reduce(const SolveParams& p, double bm
 }
 
 // ------------------------------------------------------------ one warp task
-// Per-warp shared memory: two in_src staging slices (16-B cp.async chunks, so
-// up to 3 leading pad entries + kTaskItems + 3 trailing) and two gathered
-// value buffers -- a 2-deep cp.async pipeline across the warp's tasks.
-constexpr int kSrcSlots = kTaskItems + 8;
-constexpr int kWarpSmemBytes = 2 * kSrcSlots * 4 + 2 * kTaskItems * 8;
-constexpr int kSolveSmemBytes = kWarpsPerBlock * kWarpSmemBytes;
+// A task covers ~kTaskDiag merge items (<= kTaskItems = 252 edges); its slice [j0, j1) is
+// viewed in 16-B-aligned "position" space p = (e - (j0 & ~3)), so lane L owns
+// positions [8L, 8L+8) and loads them as two aligned int4 (coalesced 1 KB per
+// warp), gathers its <= 8 contributions into registers, and reduces them
+// lane-sequentially in ascending-src order.  Segments (rows) crossing lanes are
+// combined by one warp segmented scan; rows crossing tasks by tail partials.
+constexpr int kLaneItems = 8;
+static_assert(kTaskItems + 3 <= 32 * kLaneItems, "task slice must fit 256 positions");
 
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, unsigned long long pol) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+struct WarpSmem {
+  unsigned startbits[8];          // bit p: a row segment starts at position p
+  unsigned short seg_row[256];    // position -> relative row of the segment starting there
+  double rowsum[kTaskItems + 1];  // in-task sums of finalized rows (relative index)
+};
+constexpr int kSolveSmemBytes = kWarpsPerBlock * (int)sizeof(WarpSmem);
 
 struct TaskMeta {
   int i0, i1;
@@ -199,132 +192,189 @@ __device__ __forceinline__ TaskMeta load_meta(const SolveParams& p, int t) {
   return m;
 }
 
-// Row metadata of a task's first 32 rows, prefetched one pipeline step early.
-struct RowPre {
-  int64_t a, b;
-  int od;
-  double ov;
+__device__ __forceinline__ int4 ld_stream_v4(const int32_t* p, unsigned long long pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// Lane's 8 source ids of a task (two aligned 16-B loads; chunks past j1 skipped).
+struct Src8 {
+  int4 a, b;
 };
-
-__device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMeta& m, int lane) {
-  RowPre r{0, 0, 0, 0.0};
-  const int row = m.i0 + lane;
-  if (row < m.i1) {
-    r.a = __ldg(p.row + row);
-    r.b = __ldg(p.row + row + 1);
-    r.od = __ldg(p.outdeg + row);
-    r.ov = p.pr[row];
-  }
-  return r;
-}
-
-// Stage the task's in_src slice: 16-B chunks from the 4-element-aligned base.
-__device__ __forceinline__ void issue_src(const SolveParams& p, const TaskMeta& m, int32_t* sbuf,
-                                          int lane, unsigned long long pol) {
-  const int64_t base = m.j0 & ~int64_t(3);
-  const int nchunks = (int)((m.j1 - base + 3) >> 2);
-  for (int c = lane; c < nchunks; c += 32) cp_async16(sbuf + 4 * c, p.src + base + 4 * c, pol);
-}
-
-// Gather contrib[src] for the task's edges straight into shared memory.
-template <bool ASYNC>
-__device__ __forceinline__ void issue_gathers(const TaskMeta& m, const int32_t* sbuf, double* vbuf,
-                                              int fresh_below, const double* prev,
-                                              const double* cur, int lane) {
-  const int off = (int)(m.j0 & 3);
-  const int nE = (int)(m.j1 - m.j0);
-  for (int k = lane; k < nE; k += 32) {
-    const int s = sbuf[off + k];
-    const double* basep = ASYNC ? cur : ((s < fresh_below) ? cur : prev);
-    cp_async8(vbuf + k, basep + s);
-  }
+__device__ __forceinline__ Src8 load_src8(const SolveParams& p, const TaskMeta& m, int lane,
+                                          unsigned long long pol) {
+  Src8 s{{0, 0, 0, 0}, {0, 0, 0, 0}};
+  const int64_t base = (m.j0 & ~int64_t(3)) + 8 * lane;
+  if (base < m.j1) s.a = ld_stream_v4(p.src + base, pol);
+  if (base + 4 < m.j1) s.b = ld_stream_v4(p.src + base + 4, pol);
+  return s;
 }
 
 __device__ __forceinline__ double tail_not_ready() { return __longlong_as_double(-1ll); }  // NaN
 
 template <bool ASYNC>
+__device__ __forceinline__ double gather1(int s, int fresh_below, const double* prev,
+                                          const double* cur) {
+  if (ASYNC) return ld_relaxed_f64(cur + s);  // value-atomic live read (pagerank.hpp:305)
+  const double* basep = (s < fresh_below) ? cur : prev;
+#ifdef FPR_GATHER_L1
+  return basep[s];
+#else
+  return __ldcg(basep + s);  // L2 only: random 8-B gathers have no L1 reuse
+#endif
+}
+
+template <bool ASYNC>
 __device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
-                                             const RowPre& pre, const double* vals, double* cur,
-                                             int lane, double& lmax, double& lsum) {
+                                             const Src8& sx, int fresh_below, const double* prev,
+                                             double* cur, WarpSmem& ws, int lane, double& lmax,
+                                             double& lsum) {
   const int i0 = m.i0, i1 = m.i1;
-  const int64_t j0 = m.j0;
-  const int nE = (int)(m.j1 - m.j0);
+  const int64_t j0 = m.j0, j1 = m.j1;
+  const int nE = (int)(j1 - j0);
+  const int off = (int)(j0 & 3);
+  const int pos0 = 8 * lane;
 
-  // (a) open row at the end of the task: publish this task's partial first,
-  //     so a task waiting on it never waits on this task's own head (no chain).
-  //     The partial IS the flag: ready iff >= 0 (sums of positive contributions).
-  if (i1 < p.n) {
-    const int64_t rs = __ldg(p.row + i1);
-    const int lo = (int)((rs > j0 ? rs : j0) - j0);
-    if (lo < nE) {
-      double a = 0.0;
-      for (int k = lo + lane; k < nE; k += 32) a += vals[k];
-      a = warp_sum(a);
-      if (lane == 0) st_relaxed_f64(p.tail_partial + t, a);
-    }
+  // 1. gathers: position q of this lane holds edge q - off when off <= q < off + nE.
+  const int sids[8] = {sx.a.x, sx.a.y, sx.a.z, sx.a.w, sx.b.x, sx.b.y, sx.b.z, sx.b.w};
+  double v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int q = pos0 + i;
+    v[i] = (q >= off && q < off + nE) ? gather1<ASYNC>(sids[i], fresh_below, prev, cur) : 0.0;
   }
-  // (b) head row split across earlier tasks: combine their partials in task order.
-  bool has_head = false;
-  double head_sum = 0.0;
-  if (i0 < i1 && __shfl_sync(FULL_MASK, pre.a, 0) < j0) {
-    has_head = true;
-    const int ta = __ldg(p.head_first + t);
-    double acc = 0.0;
-    for (int tt = ta + lane; tt < t; tt += 32) {
-      double v = ld_relaxed_f64(p.tail_partial + tt);
-      while (!(v >= 0.0)) {
-        __nanosleep(32);
-        v = ld_relaxed_f64(p.tail_partial + tt);
+
+  // 2. segment structure, overlapped with the gathers: rows i0..i1 (i1 = open row).
+  if (lane < 8) ws.startbits[lane] = 0u;
+  __syncwarp();
+  const int nrows = i1 - i0 + (i1 < p.n ? 1 : 0);
+  int64_t a0 = 0, b0 = 0;  // first chunk's row bounds, reused by the finalize pass
+  for (int rb = 0; rb < nrows; rb += 32) {
+    const int rr = rb + lane;
+    if (rr < nrows) {
+      const int64_t a = __ldg(p.row + i0 + rr);
+      const int64_t b = (i0 + rr < i1) ? __ldg(p.row + i0 + rr + 1) : j1;
+      if (rb == 0) {
+        a0 = a;
+        b0 = b;
       }
-      acc += v;
-      st_relaxed_f64(p.tail_partial + tt, tail_not_ready());  // consumed: re-arm for next sweep
+      const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)((b < j1 ? b : j1) - j0);
+      if (lo < hi) {
+        const int q = lo + off;
+        atomicOr(&ws.startbits[q >> 5], 1u << (q & 31));
+        ws.seg_row[q] = (unsigned short)rr;
+      }
     }
-    acc = warp_sum(acc);
-    const int hi = (int)(__shfl_sync(FULL_MASK, pre.b, 0) - j0);
-    double own = 0.0;
-    for (int k = lane; k < hi; k += 32) own += vals[k];
-    head_sum = acc + warp_sum(own);
+  }
+  __syncwarp();
+
+  // 3. lane-sequential segmented sums over positions [pos0, pos0 + 8).
+  const unsigned word = ws.startbits[lane >> 2];
+  const unsigned bits8 = (word >> ((lane & 3) * 8)) & 0xffu;
+  const bool next_starts = (lane == 31) ? true : ((ws.startbits[(lane + 1) >> 2] >> (((lane + 1) & 3) * 8)) & 1u);
+  // start position of the segment covering pos0 (highest start bit <= pos0)
+  int start_head = -1;
+  {
+    const unsigned below = word & (0xffffffffu >> (31 - (pos0 & 31)));  // bits <= pos0 in word
+    if (below) {
+      start_head = (pos0 & ~31) + 31 - __clz(below);
+    } else {
+      for (int w = (pos0 >> 5) - 1; w >= 0; --w) {
+        const unsigned x = ws.startbits[w];
+        if (x) {
+          start_head = w * 32 + 31 - __clz(x);
+          break;
+        }
+      }
+    }
+  }
+  const int valid_lo = off, valid_hi = off + nE;  // valid positions
+  const bool lane_active = pos0 + 7 >= valid_lo && pos0 < valid_hi;
+  double head_acc = 0.0, acc = 0.0;
+  int cur_start = start_head;
+  bool inner = false;  // a segment start at i > 0 inside this lane
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int q = pos0 + i;
+    if (i > 0 && ((bits8 >> i) & 1u) && q < valid_hi) {
+      if (!inner) {
+        head_acc = acc;  // segment [cur_start, q) -- may have begun in an earlier lane
+        inner = true;
+      } else {
+        ws.rowsum[ws.seg_row[cur_start]] = acc;  // complete inside this lane
+      }
+      acc = 0.0;
+      cur_start = q;
+    }
+    acc += v[i];
+  }
+  // warp segmented inclusive scan of the lane tails, keyed by segment start
+  const int key = lane_active ? cur_start : -1 - lane;
+  double S = lane_active ? acc : 0.0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double up = __shfl_up_sync(FULL_MASK, S, d);
+    const int kup = __shfl_up_sync(FULL_MASK, key, d);
+    // lanes L-d..L all share the key iff the key of lane L-d equals ours (keys non-decreasing)
+    if (lane >= d && kup == key) S += up;
+  }
+  const double Sprev = __shfl_up_sync(FULL_MASK, S, 1);
+  const int kprev = __shfl_up_sync(FULL_MASK, key, 1);
+  if (lane_active) {
+    if (inner) {  // head segment ends inside this lane
+      double tot = head_acc;
+      if (lane > 0 && start_head >= 0 && start_head < pos0 && kprev == start_head) tot += Sprev;
+      if (start_head >= 0) ws.rowsum[ws.seg_row[start_head]] = tot;
+    }
+    const bool tail_ends_here = next_starts || (pos0 + 8 >= valid_hi);
+    if (tail_ends_here && cur_start >= 0) {
+      const int rr = ws.seg_row[cur_start];
+      if (i0 + rr == i1) {
+        st_relaxed_f64(p.tail_partial + t, S);  // open row: publish (the partial is the flag)
+      } else {
+        ws.rowsum[rr] = S;
+      }
+    }
+  }
+  __syncwarp();
+
+  // 4. head row split across earlier tasks: combine their partials in task order.
+  double head_extra = 0.0;
+  const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, a0, 0) < j0;
+  if (has_head) {
+    const int ta = __ldg(p.head_first + t);
+    double accp = 0.0;
+    for (int tt = ta + lane; tt < t; tt += 32) {
+      double x = ld_relaxed_f64(p.tail_partial + tt);
+      while (!(x >= 0.0)) {
+        __nanosleep(32);
+        x = ld_relaxed_f64(p.tail_partial + tt);
+      }
+      accp += x;
+      st_relaxed_f64(p.tail_partial + tt, tail_not_ready());  // consumed: re-arm
+    }
+    head_extra = warp_sum(accp);
   }
 
-  // (c) rows whose end marker lies in this task: lane per row, ascending-src
-  //     sequential sums (the reference's order); long rows warp-cooperative.
+  // 5. finalize rows [i0, i1): lane per row, coalesced metadata.
   for (int rb = i0; rb < i1; rb += 32) {
     const int r = rb + lane;
-    const bool act = r < i1;
-    int64_t a = pre.a, b = pre.b;
-    int od = pre.od;
-    double ov = pre.ov;
-    if (rb != i0 && act) {
-      a = __ldg(p.row + r);
-      b = __ldg(p.row + r + 1);
-      od = __ldg(p.outdeg + r);
-      ov = p.pr[r];
-    }
-    int lo = 0, hi = 0;
-    if (act) {
-      lo = (int)((a > j0 ? a : j0) - j0);
-      hi = (int)(b - j0);
-    }
-    const bool head = has_head && r == i0;
-    const bool is_long = act && !head && (hi - lo) > 32;
-    double sum = 0.0;
-    if (act && !head && !is_long) {
-      for (int k = lo; k < hi; ++k) sum += vals[k];
-    }
-    unsigned lm = __ballot_sync(FULL_MASK, is_long);
-    while (lm) {
-      const int L = __ffs(lm) - 1;
-      lm &= lm - 1;
-      const int llo = __shfl_sync(FULL_MASK, lo, L), lhi = __shfl_sync(FULL_MASK, hi, L);
-      double acc = 0.0;
-      for (int k = llo + lane; k < lhi; k += 32) acc += vals[k];
-      acc = warp_sum(acc);
-      if (lane == L) sum = acc;
-    }
-    if (head) sum = head_sum;
-    if (act) {
+    if (r < i1) {
+      int64_t a = a0, b = b0;
+      if (rb != i0) {
+        a = __ldg(p.row + r);
+        b = __ldg(p.row + r + 1);
+      }
+      const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)(b - j0);
+      double sum = (lo < hi) ? ws.rowsum[r - i0] : 0.0;
+      if (r == i0 && has_head) sum = head_extra + sum;
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
+      const double ov = p.pr[r];
       p.pr[r] = nv;
+      const int od = __ldg(p.outdeg + r);
       if (od > 0) {
         const double c = __ddiv_rn(nv, (double)od);
         if (ASYNC)
@@ -337,74 +387,52 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
       lsum += d;
     }
   }
+  __syncwarp();
 }
 
-// All tasks t = tb + gwarp + k*nwarps < te of this warp, software-pipelined:
-// step k waits for in_src(k), issues in_src(k+1) and gathers(k), prefetches
-// meta(k+2) and row metadata(k), then processes task k-1 while gathers(k)
-// are in flight.  cp.async group order: S0, [empty], S1, G0, S2, G1, ...
+// All tasks t = tb + gwarp + k*nwarps < te of this warp.  The next task's
+// metadata and source ids are prefetched into registers while the current
+// task's gathers are in flight.
 template <bool ASYNC>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
-                                          double* cur, int32_t* sb, double* vb, int lane,
+                                          double* cur, WarpSmem& ws, int lane,
                                           unsigned long long pol, double& lmax, double& lsum) {
-  int tk = tb + gwarp;
-  if (tk >= te) return;
-  TaskMeta mA = load_meta(p, tk);
-  issue_src(p, mA, sb, lane, pol);
-  cp_async_commit();
-  cp_async_commit();  // stands in for G_{-1}
-  TaskMeta mB{0, 0, 0, 0};
-  if (tk + nwarps < te) mB = load_meta(p, tk + nwarps);
-  TaskMeta mP{0, 0, 0, 0};
-  RowPre rpP{0, 0, 0, 0.0};
-  int tP = -1;
-  int k = 0;
+  int t = tb + gwarp;
+  if (t >= te) return;
+  TaskMeta m = load_meta(p, t);
+  Src8 sx = load_src8(p, m, lane, pol);
+  TaskMeta mn{0, 0, 0, 0};
+  if (t + nwarps < te) mn = load_meta(p, t + nwarps);
   while (true) {
-    const bool haveA = tk < te;
-    cp_async_wait<1>();  // in_src(k) landed
-    __syncwarp();
-    if (haveA && tk + nwarps < te) issue_src(p, mB, sb + ((k + 1) & 1) * kSrcSlots, lane, pol);
-    cp_async_commit();
-    RowPre rpA{0, 0, 0, 0.0};
-    TaskMeta mC{0, 0, 0, 0};
-    if (haveA) {
-      issue_gathers<ASYNC>(mA, sb + (k & 1) * kSrcSlots, vb + (k & 1) * kTaskItems, fresh_below,
-                           prev, cur, lane);
-      if (tk + 2 * nwarps < te) mC = load_meta(p, tk + 2 * nwarps);
-      rpA = load_rowpre(p, mA, lane);
+    const int tn = t + nwarps;
+    Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
+    TaskMeta mnn{0, 0, 0, 0};
+    if (tn < te) {
+      sn = load_src8(p, mn, lane, pol);
+      if (tn + nwarps < te) mnn = load_meta(p, tn + nwarps);
     }
-    cp_async_commit();
-    if (tP >= 0) {
-      cp_async_wait<2>();  // gathers(k-1) landed
-      __syncwarp();
-      process_task<ASYNC>(p, tP, mP, rpP, vb + ((k - 1) & 1) * kTaskItems, cur, lane, lmax, lsum);
-      __syncwarp();
-    }
-    if (!haveA) break;
-    mP = mA;
-    rpP = rpA;
-    tP = tk;
-    mA = mB;
-    mB = mC;
-    tk += nwarps;
-    ++k;
+    process_task<ASYNC>(p, t, m, sx, fresh_below, prev, cur, ws, lane, lmax, lsum);
+    if (tn >= te) break;
+    t = tn;
+    m = mn;
+    sx = sn;
+    mn = mnn;
   }
-  cp_async_wait<0>();
-  __syncwarp();
 }
 
 // ------------------------------------------------------ persistent solver
 // ASYNC=false: Jacobi (nwaves == 1, EC) or wave-lockstep Gauss-Seidel.
 // ASYNC=true : block-asynchronous Gauss-Seidel, in-place contributions.
 template <bool ASYNC>
-__global__ void __launch_bounds__(kBlockThreads, 2) solve_kernel(SolveParams p) {
+#ifndef FPR_MIN_BLOCKS
+#define FPR_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kBlockThreads, FPR_MIN_BLOCKS) solve_kernel(SolveParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double sred[2 * kWarpsPerBlock];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned char* wsm = smem + wib * kWarpSmemBytes;
-  int32_t* sb = reinterpret_cast<int32_t*>(wsm);
-  double* vb = reinterpret_cast<double*>(wsm + 2 * kSrcSlots * 4);
+  WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem)[wib];
   const int gwarp = blockIdx.x * kWarpsPerBlock + wib;
   const int nwarps = gridDim.x * kWarpsPerBlock;
   const unsigned long long pol = evict_first_policy();
@@ -414,14 +442,14 @@ __global__ void __launch_bounds__(kBlockThreads, 2) solve_kernel(SolveParams p) 
   for (uint32_t it = 0; it < p.max_iters; ++it) {
     double lmax = 0.0, lsum = 0.0;
     if (ASYNC) {
-      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0, sb, vb, lane, pol,
+      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0, ws, lane, pol,
                       lmax, lsum);
     } else {
       const double* prev = par ? p.contrib1 : p.contrib0;
       double* cur = par ? p.contrib0 : p.contrib1;
       for (int w = 0; w < p.nwaves; ++w) {
         run_tasks<false>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
-                         __ldg(p.wave_row + w), prev, cur, sb, vb, lane, pol, lmax, lsum);
+                         __ldg(p.wave_row + w), prev, cur, ws, lane, pol, lmax, lsum);
         if (w + 1 < p.nwaves) grid_sync(p.bar);
       }
       par ^= 1;
@@ -467,11 +495,15 @@ __global__ void partition_kernel(const int64_t* row, int32_t n, int64_t m, int32
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t > ntasks) return;
   const int64_t total = (int64_t)n + m;
-  int64_t diag = t * (int64_t)kTaskItems;
+  int64_t diag = t * (int64_t)kTaskDiag;
   if (diag > total) diag = total;
   const int64_t x = merge_path(diag, row, n, m);
+  int64_t y = diag - x;
+  // Snap: never split a short row -- the boundary moves back to its first
+  // edge, so only rows longer than kSnapEdges ever need cross-task partials.
+  if (x < n && y > row[x] && row[x + 1] - row[x] <= kSnapEdges) y = row[x];
   task_row[t] = (int32_t)x;
-  task_edge[t] = diag - x;
+  task_edge[t] = y;
 }
 
 __global__ void head_kernel(const int64_t* row, int32_t n, int32_t ntasks, const int32_t* task_row,

@@ -170,7 +170,7 @@ int finish_graph(fpr_b200_graph* h) {
   DevGraph& g = h->g;
   Partition& p = h->part;
   const int64_t items = (int64_t)g.n + g.m;
-  const int64_t nt = (items + kTaskItems - 1) / kTaskItems;
+  const int64_t nt = (items + kTaskDiag - 1) / kTaskDiag;
   if (nt >= INT32_MAX) return fail(FPR_B200_ERANGE, "fpr_b200: graph too large for task index");
   p.ntasks = (int32_t)nt;
   int rc;
