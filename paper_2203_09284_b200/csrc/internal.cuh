@@ -17,8 +17,14 @@ namespace fprb {
 
 constexpr int kBlockThreads = 256;
 constexpr int kWarpsPerBlock = kBlockThreads / 32;
-constexpr int kTaskDiag = 192;   // merge-path diagonal stride between warp tasks
-constexpr int kSnapEdges = 60;   // a boundary inside a row of <= kSnapEdges edges moves to the row start
+#ifndef FPR_TASK_DIAG
+#define FPR_TASK_DIAG 224
+#endif
+#ifndef FPR_SNAP_EDGES
+#define FPR_SNAP_EDGES 28
+#endif
+constexpr int kTaskDiag = FPR_TASK_DIAG;    // merge-path diagonal stride between warp tasks
+constexpr int kSnapEdges = FPR_SNAP_EDGES;  // a boundary inside a row of <= kSnapEdges edges moves to its start
 constexpr int kTaskItems = kTaskDiag + kSnapEdges;  // max items (and edges) per task: 252 (+3 pad <= 256)
 
 struct GridBar {

@@ -215,51 +215,81 @@ __device__ __forceinline__ Src8 load_src8(const SolveParams& p, const TaskMeta& 
 
 __device__ __forceinline__ double tail_not_ready() { return __longlong_as_double(-1ll); }  // NaN
 
+// Predicated gather into v (left untouched when !valid).  Inline PTX keeps the
+// compiler from consuming the value (and stalling) before it is needed.
 template <bool ASYNC>
-__device__ __forceinline__ double gather1(int s, int fresh_below, const double* prev,
-                                          const double* cur) {
-  if (ASYNC) return ld_relaxed_f64(cur + s);  // value-atomic live read (pagerank.hpp:305)
-  const double* basep = (s < fresh_below) ? cur : prev;
-#ifdef FPR_GATHER_L1
-  return basep[s];
-#else
-  return __ldcg(basep + s);  // L2 only: random 8-B gathers have no L1 reuse
-#endif
+__device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_below,
+                                        const double* prev, const double* cur) {
+  const double* basep = ASYNC ? cur : ((s < fresh_below) ? cur : prev);
+  const double* addr = basep + s;
+  if (ASYNC) {  // value-atomic live read (pagerank.hpp:305)
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.relaxed.gpu.global.f64 %0, [%1]; }"
+                 : "+d"(v)
+                 : "l"(addr), "r"((int)valid)
+                 : "memory");
+  } else {  // L2 only: random 8-B gathers have no L1 reuse
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cg.f64 %0, [%1]; }"
+                 : "+d"(v)
+                 : "l"(addr), "r"((int)valid));
+  }
+}
+
+// Row metadata of a task's first 32 rows (i0 .. i0+31, including the open
+// row i1 when it falls in that window), prefetched one task ahead.
+struct RowPre {
+  int64_t a, b;  // row[r], and row[r+1] (or j1 for the open row)
+  int od;        // outdeg[r] (finalized rows only)
+  double ov;     // pr[r]     (finalized rows only)
+};
+__device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMeta& m, int lane) {
+  RowPre r{0, 0, 0, 0.0};
+  const int row = m.i0 + lane;
+  if (row < m.i1) {
+    r.a = __ldg(p.row + row);
+    r.b = __ldg(p.row + row + 1);
+    r.od = __ldg(p.outdeg + row);
+    r.ov = p.pr[row];
+  } else if (row == m.i1 && row < p.n) {
+    r.a = __ldg(p.row + row);
+    r.b = m.j1;
+  }
+  return r;
 }
 
 template <bool ASYNC>
 __device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
-                                             const Src8& sx, int fresh_below, const double* prev,
-                                             double* cur, WarpSmem& ws, int lane, double& lmax,
-                                             double& lsum) {
+                                             const Src8& sx, const RowPre& rp, int fresh_below,
+                                             const double* prev, double* cur, WarpSmem& ws,
+                                             int lane, double& lmax, double& lsum) {
   const int i0 = m.i0, i1 = m.i1;
   const int64_t j0 = m.j0, j1 = m.j1;
   const int nE = (int)(j1 - j0);
   const int off = (int)(j0 & 3);
   const int pos0 = 8 * lane;
+  const int valid_hi = off + nE;
 
   // 1. gathers: position q of this lane holds edge q - off when off <= q < off + nE.
+  //    Invalid positions load contrib[0] (harmless) so no value is consumed early.
   const int sids[8] = {sx.a.x, sx.a.y, sx.a.z, sx.a.w, sx.b.x, sx.b.y, sx.b.z, sx.b.w};
   double v[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int q = pos0 + i;
-    v[i] = (q >= off && q < off + nE) ? gather1<ASYNC>(sids[i], fresh_below, prev, cur) : 0.0;
+    v[i] = 0.0;
+    gather1<ASYNC>(v[i], q >= off && q < valid_hi, sids[i], fresh_below, prev, cur);
   }
 
-  // 2. segment structure, overlapped with the gathers: rows i0..i1 (i1 = open row).
+  // 2. segment structure (overlaps the gathers): rows i0..i1 (i1 = open row).
   if (lane < 8) ws.startbits[lane] = 0u;
   __syncwarp();
   const int nrows = i1 - i0 + (i1 < p.n ? 1 : 0);
-  int64_t a0 = 0, b0 = 0;  // first chunk's row bounds, reused by the finalize pass
   for (int rb = 0; rb < nrows; rb += 32) {
     const int rr = rb + lane;
     if (rr < nrows) {
-      const int64_t a = __ldg(p.row + i0 + rr);
-      const int64_t b = (i0 + rr < i1) ? __ldg(p.row + i0 + rr + 1) : j1;
-      if (rb == 0) {
-        a0 = a;
-        b0 = b;
+      int64_t a = rp.a, b = rp.b;
+      if (rb != 0) {
+        a = __ldg(p.row + i0 + rr);
+        b = (i0 + rr < i1) ? __ldg(p.row + i0 + rr + 1) : j1;
       }
       const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)((b < j1 ? b : j1) - j0);
       if (lo < hi) {
@@ -274,11 +304,11 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
   // 3. lane-sequential segmented sums over positions [pos0, pos0 + 8).
   const unsigned word = ws.startbits[lane >> 2];
   const unsigned bits8 = (word >> ((lane & 3) * 8)) & 0xffu;
-  const bool next_starts = (lane == 31) ? true : ((ws.startbits[(lane + 1) >> 2] >> (((lane + 1) & 3) * 8)) & 1u);
-  // start position of the segment covering pos0 (highest start bit <= pos0)
-  int start_head = -1;
+  const bool next_starts =
+      (lane == 31) ? true : ((ws.startbits[(lane + 1) >> 2] >> (((lane + 1) & 3) * 8)) & 1u);
+  int start_head = -1;  // highest segment start <= pos0
   {
-    const unsigned below = word & (0xffffffffu >> (31 - (pos0 & 31)));  // bits <= pos0 in word
+    const unsigned below = word & (0xffffffffu >> (31 - (pos0 & 31)));
     if (below) {
       start_head = (pos0 & ~31) + 31 - __clz(below);
     } else {
@@ -291,17 +321,17 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
       }
     }
   }
-  const int valid_lo = off, valid_hi = off + nE;  // valid positions
-  const bool lane_active = pos0 + 7 >= valid_lo && pos0 < valid_hi;
+  const bool lane_active = pos0 + 7 >= off && pos0 < valid_hi;
   double head_acc = 0.0, acc = 0.0;
   int cur_start = start_head;
-  bool inner = false;  // a segment start at i > 0 inside this lane
+  bool inner = false;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int q = pos0 + i;
-    if (i > 0 && ((bits8 >> i) & 1u) && q < valid_hi) {
+    const bool valid = q >= off && q < valid_hi;
+    if (i > 0 && ((bits8 >> i) & 1u) && valid) {
       if (!inner) {
-        head_acc = acc;  // segment [cur_start, q) -- may have begun in an earlier lane
+        head_acc = acc;
         inner = true;
       } else {
         ws.rowsum[ws.seg_row[cur_start]] = acc;  // complete inside this lane
@@ -309,7 +339,7 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
       acc = 0.0;
       cur_start = q;
     }
-    acc += v[i];
+    if (valid) acc += v[i];
   }
   // warp segmented inclusive scan of the lane tails, keyed by segment start
   const int key = lane_active ? cur_start : -1 - lane;
@@ -318,39 +348,36 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
   for (int d = 1; d < 32; d <<= 1) {
     const double up = __shfl_up_sync(FULL_MASK, S, d);
     const int kup = __shfl_up_sync(FULL_MASK, key, d);
-    // lanes L-d..L all share the key iff the key of lane L-d equals ours (keys non-decreasing)
     if (lane >= d && kup == key) S += up;
   }
   const double Sprev = __shfl_up_sync(FULL_MASK, S, 1);
   const int kprev = __shfl_up_sync(FULL_MASK, key, 1);
   if (lane_active) {
-    if (inner) {  // head segment ends inside this lane
+    if (inner && start_head >= 0) {  // head segment ends inside this lane
       double tot = head_acc;
-      if (lane > 0 && start_head >= 0 && start_head < pos0 && kprev == start_head) tot += Sprev;
-      if (start_head >= 0) ws.rowsum[ws.seg_row[start_head]] = tot;
+      if (lane > 0 && start_head < pos0 && kprev == start_head) tot += Sprev;
+      ws.rowsum[ws.seg_row[start_head]] = tot;
     }
-    const bool tail_ends_here = next_starts || (pos0 + 8 >= valid_hi);
-    if (tail_ends_here && cur_start >= 0) {
+    if ((next_starts || pos0 + 8 >= valid_hi) && cur_start >= 0) {
       const int rr = ws.seg_row[cur_start];
-      if (i0 + rr == i1) {
+      if (i0 + rr == i1)
         st_relaxed_f64(p.tail_partial + t, S);  // open row: publish (the partial is the flag)
-      } else {
+      else
         ws.rowsum[rr] = S;
-      }
     }
   }
   __syncwarp();
 
   // 4. head row split across earlier tasks: combine their partials in task order.
   double head_extra = 0.0;
-  const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, a0, 0) < j0;
+  const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, rp.a, 0) < j0;
   if (has_head) {
     const int ta = __ldg(p.head_first + t);
     double accp = 0.0;
     for (int tt = ta + lane; tt < t; tt += 32) {
       double x = ld_relaxed_f64(p.tail_partial + tt);
       while (!(x >= 0.0)) {
-        __nanosleep(32);
+        __nanosleep(64);
         x = ld_relaxed_f64(p.tail_partial + tt);
       }
       accp += x;
@@ -359,22 +386,24 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
     head_extra = warp_sum(accp);
   }
 
-  // 5. finalize rows [i0, i1): lane per row, coalesced metadata.
+  // 5. finalize rows [i0, i1): lane per row, prefetched metadata for the first 32.
   for (int rb = i0; rb < i1; rb += 32) {
     const int r = rb + lane;
     if (r < i1) {
-      int64_t a = a0, b = b0;
+      int64_t a = rp.a, b = rp.b;
+      int od = rp.od;
+      double ov = rp.ov;
       if (rb != i0) {
         a = __ldg(p.row + r);
         b = __ldg(p.row + r + 1);
+        od = __ldg(p.outdeg + r);
+        ov = p.pr[r];
       }
       const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)(b - j0);
       double sum = (lo < hi) ? ws.rowsum[r - i0] : 0.0;
       if (r == i0 && has_head) sum = head_extra + sum;
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
-      const double ov = p.pr[r];
       p.pr[r] = nv;
-      const int od = __ldg(p.outdeg + r);
       if (od > 0) {
         const double c = __ddiv_rn(nv, (double)od);
         if (ASYNC)
@@ -391,8 +420,9 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
 }
 
 // All tasks t = tb + gwarp + k*nwarps < te of this warp.  The next task's
-// metadata and source ids are prefetched into registers while the current
-// task's gathers are in flight.
+// metadata, source ids and row metadata are prefetched into registers while
+// the current task is reduced, so a task's only exposed latency is its own
+// (overlapped) random gathers.
 template <bool ASYNC>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
@@ -402,21 +432,25 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   if (t >= te) return;
   TaskMeta m = load_meta(p, t);
   Src8 sx = load_src8(p, m, lane, pol);
+  RowPre rp = load_rowpre(p, m, lane);
   TaskMeta mn{0, 0, 0, 0};
   if (t + nwarps < te) mn = load_meta(p, t + nwarps);
   while (true) {
     const int tn = t + nwarps;
     Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
+    RowPre rpn{0, 0, 0, 0.0};
     TaskMeta mnn{0, 0, 0, 0};
     if (tn < te) {
       sn = load_src8(p, mn, lane, pol);
+      rpn = load_rowpre(p, mn, lane);
       if (tn + nwarps < te) mnn = load_meta(p, tn + nwarps);
     }
-    process_task<ASYNC>(p, t, m, sx, fresh_below, prev, cur, ws, lane, lmax, lsum);
+    process_task<ASYNC>(p, t, m, sx, rp, fresh_below, prev, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;
     sx = sn;
+    rp = rpn;
     mn = mnn;
   }
 }
