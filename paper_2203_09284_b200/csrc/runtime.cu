@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,6 +41,47 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr uint32_t kChunkIters = 1u << 16;  // device trace capacity per launch
+
+// Pinned host staging for the per-launch trace readback, pooled process-wide so
+// a one-shot fpr_b200_pagerank() does not pay cudaMallocHost on every call.
+struct HostStaging {
+  unsigned int* iters = nullptr;
+  int* stop = nullptr;
+  double* errors = nullptr;
+  double* l1 = nullptr;
+  unsigned long long* ns = nullptr;
+};
+std::mutex g_staging_mu;
+std::vector<HostStaging*> g_staging_free;
+
+HostStaging* acquire_staging() {
+  {
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    if (!g_staging_free.empty()) {
+      HostStaging* s = g_staging_free.back();
+      g_staging_free.pop_back();
+      return s;
+    }
+  }
+  auto* s = new HostStaging;
+  if (cudaMallocHost(&s->iters, sizeof(unsigned)) != cudaSuccess ||
+      cudaMallocHost(&s->stop, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&s->errors, kChunkIters * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&s->l1, kChunkIters * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&s->ns, (kChunkIters + 1) * sizeof(unsigned long long)) != cudaSuccess) {
+    for (void* p : {(void*)s->iters, (void*)s->stop, (void*)s->errors, (void*)s->l1, (void*)s->ns})
+      if (p) cudaFreeHost(p);
+    delete s;
+    return nullptr;
+  }
+  return s;
+}
+
+void release_staging(HostStaging* s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_staging_mu);
+  g_staging_free.push_back(s);
+}
 
 struct Waves {
   int32_t nwaves = 0;
@@ -71,13 +113,16 @@ struct fpr_b200_graph {
   double* d_errors = nullptr;
   double* d_l1 = nullptr;
   unsigned long long* d_ns = nullptr;
-  // pinned host staging
+  // pinned host staging (pooled)
+  HostStaging* hs = nullptr;
   unsigned int* h_iters = nullptr;
   int* h_stop = nullptr;
   double* h_errors = nullptr;
   double* h_l1 = nullptr;
   unsigned long long* h_ns = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D upload overlapped with narrowing
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t up_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::map<uint32_t, Waves> waves;
   std::vector<void*> allocs;
 };
@@ -108,11 +153,12 @@ void destroy_handle(fpr_b200_graph* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (auto* p : {(void*)h->h_iters, (void*)h->h_stop, (void*)h->h_errors, (void*)h->h_l1,
-                  (void*)h->h_ns})
-    if (p) cudaFreeHost(p);
+  release_staging(h->hs);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->up_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -157,11 +203,13 @@ int open_handle(const fpr_b200_options* opts, fpr_b200_graph** out) {
   h->norm = o.norm;
   h->wave_count = o.wave_count;
   for (auto& ev : h->ev) CK(cudaEventCreate(&ev));
-  CK(cudaMallocHost(&h->h_iters, sizeof(unsigned)));
-  CK(cudaMallocHost(&h->h_stop, sizeof(int)));
-  CK(cudaMallocHost(&h->h_errors, kChunkIters * sizeof(double)));
-  CK(cudaMallocHost(&h->h_l1, kChunkIters * sizeof(double)));
-  CK(cudaMallocHost(&h->h_ns, (kChunkIters + 1) * sizeof(unsigned long long)));
+  h->hs = acquire_staging();
+  if (!h->hs) return fail(FPR_B200_ENOMEM, "fpr_b200: pinned host staging allocation failed");
+  h->h_iters = h->hs->iters;
+  h->h_stop = h->hs->stop;
+  h->h_errors = h->hs->errors;
+  h->h_l1 = h->hs->l1;
+  h->h_ns = h->hs->ns;
   return FPR_B200_OK;
 }
 
@@ -211,6 +259,20 @@ int get_waves(fpr_b200_graph* h, uint32_t wave_count, const Waves** out) {
     return FPR_B200_OK;
   }
   const int32_t nt = h->part.ntasks;
+  if (S == 1) {  // Jacobi: one wave over every task, nothing to download
+    Waves wv;
+    wv.nwaves = 1;
+    const int32_t wt[2] = {0, nt}, wr[2] = {0, h->g.n};
+    wv.vertex_start = {0, (uint64_t)h->g.n};
+    int rc;
+    if ((rc = dalloc_n(h, &wv.d_task, 2)) || (rc = dalloc_n(h, &wv.d_row, 2))) return rc;
+    CK(cudaMemcpyAsync(wv.d_task, wt, sizeof(wt), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(wv.d_row, wr, sizeof(wr), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    auto res = h->waves.emplace(S, std::move(wv));
+    *out = &res.first->second;
+    return FPR_B200_OK;
+  }
   std::vector<uint8_t> clean(nt + 1);
   std::vector<int32_t> trow(nt + 1);
   CK(cudaMemcpyAsync(clean.data(), h->part.clean_start, nt + 1, cudaMemcpyDeviceToHost, h->stream));
@@ -310,29 +372,45 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
   unsigned int* bad = nullptr;
   if ((rc = dalloc_n(h, &bad, 1))) return bail(rc);
   cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream);
-  if (e == cudaSuccess && g.n > 0)
-    e = cudaMemcpyAsync(g.row, v->in_start, (g.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                        h->stream);
-  // u64 -> int32 through a device staging buffer, chunked.
-  const int64_t chunk = 1 << 23;
+  // u64 -> int32 through two device staging buffers: chunk i is copied on the
+  // copy stream while chunk i-1 is narrowed (and range-checked) on the main one.
+  const int64_t chunk = 1 << 24;
   uint64_t* stage = nullptr;
   const int64_t need = std::min<int64_t>(chunk, std::max<int64_t>(g.m, g.n));
   if (e == cudaSuccess && need > 0) {
     if ((rc = dalloc_n(h, &stage, 2 * need))) return bail(rc);
-    int k = 0;
-    for (int64_t off = 0; e == cudaSuccess && off < g.m; off += chunk, k ^= 1) {
-      const int64_t cnt = std::min<int64_t>(chunk, g.m - off);
-      e = cudaMemcpyAsync(stage + k * need, v->in_src + off, cnt * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, h->stream);
+    if (!h->copy_stream) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+    for (auto& ev : h->up_ev)
+      if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    struct Piece {
+      const uint64_t* host;
+      int32_t* dst;
+      int64_t count;
+    };
+    std::vector<Piece> pieces;
+    for (int64_t off = 0; off < g.m; off += chunk)
+      pieces.push_back({v->in_src + off, g.src + off, std::min<int64_t>(chunk, g.m - off)});
+    for (int64_t off = 0; off < g.n; off += chunk)
+      pieces.push_back({v->out_degree + off, g.outdeg + off, std::min<int64_t>(chunk, g.n - off)});
+    if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2], h->stream);  // staging allocated
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2], 0);
+    // in_start first on the copy stream; the main stream's wait on the last
+    // piece's copy event orders it before check_offsets / partitioning.
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(g.row, v->in_start, (g.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                          h->copy_stream);
+    for (size_t i = 0; e == cudaSuccess && i < pieces.size(); ++i) {
+      const int k = (int)(i & 1);
+      uint64_t* buf = stage + k * need;
+      if (i >= 2) e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2 + k], 0);  // buf drained
       if (e == cudaSuccess)
-        e = launch_narrow_ids(stage + k * need, g.src + off, cnt, v->n, bad, h->stream);
-    }
-    for (int64_t off = 0; e == cudaSuccess && off < g.n; off += chunk, k ^= 1) {
-      const int64_t cnt = std::min<int64_t>(chunk, g.n - off);
-      e = cudaMemcpyAsync(stage + k * need, v->out_degree + off, cnt * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, h->stream);
+        e = cudaMemcpyAsync(buf, pieces[i].host, pieces[i].count * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, h->copy_stream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[k], h->copy_stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->up_ev[k], 0);
       if (e == cudaSuccess)
-        e = launch_narrow_ids(stage + k * need, g.outdeg + off, cnt, v->n, bad, h->stream);
+        e = launch_narrow_ids(buf, pieces[i].dst, pieces[i].count, v->n, bad, h->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2 + k], h->stream);
     }
   }
   if (e == cudaSuccess && g.n > 0) e = launch_check_offsets(g.row, g.n, g.m, bad, h->stream);
