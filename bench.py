@@ -47,6 +47,15 @@ def algorithmic_bytes(n: int, m: int) -> int:
     return 12 * m + 36 * n
 
 
+def ncu_traffic(key: str, launches_per_step: int) -> float | None:
+    """DRAM read+write bytes per solve launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return float(json.load(f)[key]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def peaks() -> tuple[float, str]:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -290,7 +299,9 @@ def main() -> None:
             "time_to_converge_ms": ms_step,
             "iteration_us": it_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": ncu_traffic("config2_ec", 1), "peak_kind": peak_kind,
+                         "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+                         "gather_ceiling_gteps": 270.0,
                          "kernel": "solve_kernel<false> (persistent EC, all iterations)",
                          "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": algorithmic_bytes(n, m) * iters},
