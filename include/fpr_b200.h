@@ -58,6 +58,7 @@ extern "C" {
 
 #define FPR_B200_GEN_RMAT 0    /* fpr::generate_rmat (rmat.hpp:42-77) */
 #define FPR_B200_GEN_UNIFORM 1 /* testutil::random_sparse (test_util.hpp:49-58) */
+#define FPR_B200_GEN_CHUNGLU 2 /* config 4 (no reference generator) */
 
 /* Borrowed view of an fpr::Graph (graph.hpp:20-30); host or pinned memory. */
 typedef struct fpr_graph_view {
@@ -99,9 +100,15 @@ typedef struct fpr_gen_params {
   uint32_t scale;        /* rmat: n = 2^scale */
   uint64_t edge_factor;  /* rmat: draws = edge_factor * n */
   double a, b, c, d;     /* rmat quadrant probabilities */
-  uint64_t n;            /* uniform: vertices */
+  uint64_t n;            /* uniform / chung-lu: vertices */
   uint64_t avg_degree;   /* uniform: draws = n * avg_degree */
   uint64_t seed;
+  uint64_t draws;        /* chung-lu: edge draws */
+  double alpha;          /* chung-lu: power-law exponent (> 1) */
+  uint64_t kmax;         /* chung-lu: max weight (min is 1) */
+  int32_t relabel_bfs;   /* 1: relabel vertices in BFS order (config 3) */
+  int32_t reserved0;
+  uint64_t bfs_root;     /* BFS root (old id) */
 } fpr_gen_params;
 
 typedef struct fpr_b200_graph fpr_b200_graph;
@@ -124,6 +131,16 @@ int fpr_b200_graph_info(const fpr_b200_graph* g, uint64_t* n, uint64_t* m, uint6
 /* Downloads the CSR as fpr::Graph arrays (u64). */
 int fpr_b200_graph_download_csr(const fpr_b200_graph* g, uint64_t* in_start, uint64_t* in_src,
                                 uint64_t* out_degree);
+/* Checks build_csr's invariants on the device (graph.hpp:20-30): *flags = 0
+ * when offsets are monotone (row[0]=0, row[n]=m), ids in range, no
+ * self-loops, sources strictly ascending per row, out-degrees consistent. */
+int fpr_b200_graph_validate(fpr_b200_graph* g, uint32_t* flags);
+
+/* Config-3 crawl order of a resident graph: new_id[old] (n entries) of the
+ * BFS from `root` over out-edges, neighbours ascending, unreached vertices
+ * appended in ascending id (the definition fo_bfs_relabel restates). */
+int fpr_b200_graph_bfs_order(fpr_b200_graph* g, uint64_t root, uint64_t* new_id);
+
 /* Vertex boundaries of the lockstep engine's waves for wave_count (0 = auto):
  * writes *nwaves and wave_start[0..*nwaves] (capacity cap). */
 int fpr_b200_graph_wave_starts(fpr_b200_graph* g, uint32_t wave_count, uint64_t* wave_start,

@@ -91,6 +91,14 @@ class Oracle:
             f.restype = C.c_int
         L.fo_dense_oracle.argtypes = [_u64, _u64p, _u64p, _u64p, _f64, _f64, _u64, _f64p]
         L.fo_dense_oracle.restype = C.c_int
+        L.fo_bfs_relabel.argtypes = [_u64, _u64, _u64p, _u64p, _u64, _u64p]
+        L.fo_bfs_relabel.restype = C.c_int
+        L.fo_chunglu_cdf.argtypes = [_f64, _u64, _f64p]
+        L.fo_chunglu_cdf.restype = None
+        L.fo_chunglu_weight.argtypes = [_f64p, _u64, _u64, _u64]
+        L.fo_chunglu_weight.restype = _u64
+        L.fo_generate_chunglu.argtypes = [_u64, _u64, _f64, _u64, _u64, _u64p, _u64p]
+        L.fo_generate_chunglu.restype = C.c_int
         L.fo_l1_norm.argtypes = [_u64, _f64p, _f64p]
         L.fo_l1_norm.restype = _f64
         L.fo_linf_norm.argtypes = [_u64, _f64p, _f64p]
@@ -129,6 +137,31 @@ class Oracle:
         if rc:
             raise RuntimeError(f"fo_build_csr rc={rc}")
         return Graph(n, m.value, in_start, in_src[: m.value].copy(), out_degree[:n].copy())
+
+    def bfs_relabel(self, g: Graph, root: int = 0) -> np.ndarray:
+        """Config-3 crawl order: new_id[old]."""
+        new_id = np.empty(g.n, np.uint64)
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        if self.lib.fo_bfs_relabel(g.n, g.m, g.in_start, in_src, root, new_id):
+            raise ValueError("bfs_relabel: invalid input")
+        return new_id
+
+    def relabel(self, g: Graph, new_id: np.ndarray) -> Graph:
+        """build_csr of g's edges with ids mapped through new_id."""
+        dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start).astype(np.int64))
+        return self.build_csr(g.n, new_id[g.in_src], new_id[dst])
+
+    def chunglu_cdf(self, alpha: float, kmax: int) -> np.ndarray:
+        cdf = np.empty(kmax, np.float64)
+        self.lib.fo_chunglu_cdf(alpha, kmax, cdf)
+        return cdf
+
+    def generate_chunglu(self, n: int, draws: int, seed: int, alpha: float = 2.1, kmax: int = 1_000_000):
+        src = np.empty(draws, np.uint64)
+        dst = np.empty(draws, np.uint64)
+        if self.lib.fo_generate_chunglu(n, draws, alpha, kmax, seed, src, dst):
+            raise ValueError("chung-lu: invalid parameters")
+        return n, src, dst
 
     # ---- engines ----------------------------------------------------------
     def _run(self, fn, g: Graph, damping, threshold, max_iterations, norm, extra, history_cap):

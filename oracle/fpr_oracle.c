@@ -153,6 +153,121 @@ int fo_build_csr(uint64_t n, uint64_t ne, const uint64_t* src, const uint64_t* d
   return FO_OK;
 }
 
+/* Config-3 relabel: sequential FIFO BFS over out-edges. */
+int fo_bfs_relabel(uint64_t n, uint64_t m, const uint64_t* in_start, const uint64_t* in_src,
+                   uint64_t root, uint64_t* new_id) {
+  if (n == 0 || root >= n) return FO_EINVAL;
+  uint64_t* out_start = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
+  uint64_t* out_dst = (uint64_t*)malloc((m ? m : 1) * sizeof(uint64_t));
+  uint64_t* cursor = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint64_t* queue = (uint64_t*)malloc(n * sizeof(uint64_t));
+  if (!out_start || !out_dst || !cursor || !queue) {
+    free(out_start); free(out_dst); free(cursor); free(queue);
+    return FO_ENOMEM;
+  }
+  for (uint64_t e = 0; e < m; ++e) out_start[in_src[e] + 1]++;
+  for (uint64_t u = 0; u < n; ++u) out_start[u + 1] += out_start[u];
+  memcpy(cursor, out_start, n * sizeof(uint64_t));
+  /* walking destinations ascending leaves every out-list ascending */
+  for (uint64_t d = 0; d < n; ++d)
+    for (uint64_t e = in_start[d]; e < in_start[d + 1]; ++e) out_dst[cursor[in_src[e]]++] = d;
+  for (uint64_t u = 0; u < n; ++u) new_id[u] = UINT64_MAX;
+  uint64_t head = 0, tail = 0, next = 0;
+  queue[tail++] = root;
+  new_id[root] = next++;
+  while (head < tail) {
+    const uint64_t u = queue[head++];
+    for (uint64_t e = out_start[u]; e < out_start[u + 1]; ++e) {
+      const uint64_t v = out_dst[e];
+      if (new_id[v] == UINT64_MAX) {
+        new_id[v] = next++;
+        queue[tail++] = v;
+      }
+    }
+  }
+  for (uint64_t u = 0; u < n; ++u)
+    if (new_id[u] == UINT64_MAX) new_id[u] = next++;
+  free(out_start); free(out_dst); free(cursor); free(queue);
+  return FO_OK;
+}
+
+/* Config-4 Chung-Lu.  Discrete power law P(k) ~ k^-alpha on
+ * [1, kmax]: cdf[k-1] = (sum_{j<=k} j^-alpha) / Z, summed in ascending k. */
+void fo_chunglu_cdf(double alpha, uint64_t kmax, double* cdf) {
+  double z = 0.0;
+  for (uint64_t k = 1; k <= kmax; ++k) z += pow((double)k, -alpha);
+  double acc = 0.0;
+  for (uint64_t k = 1; k <= kmax; ++k) {
+    acc += pow((double)k, -alpha);
+    cdf[k - 1] = acc / z;
+  }
+}
+
+/* weight of vertex i: smallest k with u_i < cdf[k-1] (kmax if none), where
+ * u_i = next_unit of SplitMix64(mix(seed + (i+1) gamma)). */
+uint64_t fo_chunglu_weight(const double* cdf, uint64_t kmax, uint64_t seed, uint64_t i) {
+  const uint64_t child = mix64(seed + (i + 1) * GAMMA);
+  const double u = (double)(mix64(child + GAMMA) >> 11) * 0x1.0p-53;
+  uint64_t lo = 0, hi = kmax;  /* first index with cdf > u */
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] > u) hi = mid; else lo = mid + 1;
+  }
+  return lo < kmax ? lo + 1 : kmax;
+}
+
+#define CL_SEED_DRAW 0x632be59bd9b4e019ULL
+#define CL_SEED_PERM 0x9e6c63d0676a9a99ULL
+
+static int cmp_u64pair(const void* a, const void* b) {
+  const uint64_t* x = (const uint64_t*)a;
+  const uint64_t* y = (const uint64_t*)b;
+  if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+  return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+
+/* Draw j: r = mix(seed_d + (2j+1) gamma) % W for the source (+2 for the
+ * destination), vertex = first i with inclusive prefix C_i > r; ids then go
+ * through the permutation new = rank of (mix(seed_p + (i+1) gamma), i). */
+int fo_generate_chunglu(uint64_t n, uint64_t draws, double alpha, uint64_t kmax, uint64_t seed,
+                        uint64_t* src, uint64_t* dst) {
+  if (n == 0 || kmax == 0 || !(alpha > 1.0)) return FO_EINVAL;
+  double* cdf = (double*)malloc(kmax * sizeof(double));
+  uint64_t* C = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint64_t* kp = (uint64_t*)malloc(2 * n * sizeof(uint64_t));
+  uint64_t* perm = (uint64_t*)malloc(n * sizeof(uint64_t));
+  if (!cdf || !C || !kp || !perm) {
+    free(cdf); free(C); free(kp); free(perm);
+    return FO_ENOMEM;
+  }
+  fo_chunglu_cdf(alpha, kmax, cdf);
+  uint64_t W = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    W += fo_chunglu_weight(cdf, kmax, seed, i);
+    C[i] = W;
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    kp[2 * i] = mix64(seed + CL_SEED_PERM + (i + 1) * GAMMA);
+    kp[2 * i + 1] = i;
+  }
+  qsort(kp, n, 2 * sizeof(uint64_t), cmp_u64pair);
+  for (uint64_t r = 0; r < n; ++r) perm[kp[2 * r + 1]] = r;
+  const uint64_t sd = seed + CL_SEED_DRAW;
+  for (uint64_t j = 0; j < draws; ++j) {
+    for (int side = 0; side < 2; ++side) {
+      const uint64_t r = mix64(sd + (2 * j + 1 + (uint64_t)side) * GAMMA) % W;
+      uint64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (C[mid] > r) hi = mid; else lo = mid + 1;
+      }
+      (side ? dst : src)[j] = perm[lo];
+    }
+  }
+  free(cdf); free(C); free(kp); free(perm);
+  return FO_OK;
+}
+
 /* validate(PageRankConfig) (pagerank.hpp:40-53) and init_ranks' n>0 check
  * (:55-57).  thread_count has no meaning here. */
 static int check_config(uint64_t n, double damping, double threshold, uint64_t max_iterations) {

@@ -49,6 +49,21 @@ int fo_build_csr(uint64_t n, uint64_t ne, const uint64_t* src, const uint64_t* d
                  uint64_t* in_start, uint64_t* in_src, uint64_t* out_degree, uint64_t* m_out,
                  uint64_t* bad_edge);
 
+/* BASELINE config 3's crawl-order relabel (defined in SURVEY.md §8(d); no
+ * reference generator exists): BFS from `root` over OUT-edges of the
+ * normalised graph, neighbours in ascending old id, FIFO order; unreached
+ * vertices appended in ascending old id.  new_id[old] = discovery index. */
+int fo_bfs_relabel(uint64_t n, uint64_t m, const uint64_t* in_start, const uint64_t* in_src,
+                   uint64_t root, uint64_t* new_id);
+
+/* BASELINE config 4's Chung-Lu graph (definition in DESIGN.md §4.1; no
+ * reference generator exists).  cdf: kmax doubles; draws raw edges with the
+ * permuted ids (self-loops/duplicates kept; build_csr removes them). */
+void fo_chunglu_cdf(double alpha, uint64_t kmax, double* cdf);
+uint64_t fo_chunglu_weight(const double* cdf, uint64_t kmax, uint64_t seed, uint64_t i);
+int fo_generate_chunglu(uint64_t n, uint64_t draws, double alpha, uint64_t kmax, uint64_t seed,
+                        uint64_t* src, uint64_t* dst);
+
 /* Engines.  ranks: n doubles out.  errors / l1_errors: max_iterations
  * doubles (per-iteration max and sum of |delta|); l1_errors may be NULL.
  * history: NULL or (history_cap x n) doubles, receives the rank vector

@@ -37,7 +37,7 @@ LIB_PATH = os.environ.get("FPR_B200_LIB") or os.path.join(HERE, "libfpr_b200.so"
 OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 5
 ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2
 NORM_LINF, NORM_L1 = 0, 1
-GEN_RMAT, GEN_UNIFORM = 0, 1
+GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
 
 
 class B200Error(RuntimeError):
@@ -71,14 +71,17 @@ class _Result(C.Structure):
 class _GenParams(C.Structure):
     _fields_ = [("kind", C.c_int32), ("scale", C.c_uint32), ("edge_factor", C.c_uint64),
                 ("a", C.c_double), ("b", C.c_double), ("c", C.c_double), ("d", C.c_double),
-                ("n", C.c_uint64), ("avg_degree", C.c_uint64), ("seed", C.c_uint64)]
+                ("n", C.c_uint64), ("avg_degree", C.c_uint64), ("seed", C.c_uint64),
+                ("draws", C.c_uint64), ("alpha", C.c_double), ("kmax", C.c_uint64),
+                ("relabel_bfs", C.c_int32), ("reserved0", C.c_int32), ("bfs_root", C.c_uint64)]
 
 
 EXPORTS = [
     "fpr_b200_options_init", "fpr_b200_config_init", "fpr_b200_last_error", "fpr_b200_version",
     "fpr_b200_graph_create", "fpr_b200_graph_generate", "fpr_b200_graph_destroy",
     "fpr_b200_graph_info", "fpr_b200_graph_download_csr", "fpr_b200_graph_wave_starts",
-    "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank",
+    "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank", "fpr_b200_graph_bfs_order",
+    "fpr_b200_graph_validate",
 ]
 
 _lib = None
@@ -103,6 +106,8 @@ def lib() -> C.CDLL:
         L.fpr_b200_graph_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
         L.fpr_b200_graph_download_csr.argtypes = [vp, vp, vp, vp]
         L.fpr_b200_graph_wave_starts.argtypes = [vp, C.c_uint32, vp, u64, C.POINTER(u64)]
+        L.fpr_b200_graph_bfs_order.argtypes = [vp, u64, vp]
+        L.fpr_b200_graph_validate.argtypes = [vp, C.POINTER(C.c_uint32)]
         L.fpr_b200_run.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, vp, u64, C.POINTER(_Result)]
         L.fpr_b200_graph_ranks_device.argtypes = [vp]
         L.fpr_b200_graph_ranks_device.restype = vp
@@ -248,21 +253,45 @@ class DeviceGraph:
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
-    def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None):
-        gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed)
+    def _generate(cls, gp, device, norm, wave_count, stream):
         h = C.c_void_p()
         _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream)),
                                              C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
+    def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None,
+                      relabel_bfs=False, bfs_root=0):
+        """build_csr(generate_rmat(p)) on the device; relabel_bfs=True gives
+        BASELINE config 3's crawl order (BFS from bfs_root over out-edges)."""
+        gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed,
+                        0, 0.0, 0, int(relabel_bfs), 0, bfs_root)
+        return cls._generate(gp, device, norm, wave_count, stream)
+
+    @classmethod
     def generate_uniform(cls, n: int, avg_degree: int, seed: int, device=-1, norm=NORM_LINF,
                          wave_count=0, stream=None):
+        """build_csr(testutil::random_sparse(n, avg_degree, SplitMix64(seed)))."""
         gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, n, avg_degree, seed)
-        h = C.c_void_p()
-        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream)),
-                                             C.byref(h)))
-        return cls(h.value, device, norm, wave_count)
+        return cls._generate(gp, device, norm, wave_count, stream)
+
+    @classmethod
+    def generate_chunglu(cls, n: int, draws: int, seed: int, alpha: float = 2.1, kmax: int = 1_000_000,
+                         device=-1, norm=NORM_LINF, wave_count=0, stream=None):
+        """BASELINE config 4 (definition: DESIGN.md §4.1; oracle fo_generate_chunglu)."""
+        gp = _GenParams(GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, n, 0, seed, draws, alpha, kmax)
+        return cls._generate(gp, device, norm, wave_count, stream)
+
+    def validate(self) -> int:
+        """0 iff the resident CSR satisfies build_csr's invariants (device check)."""
+        f = C.c_uint32()
+        _check(lib().fpr_b200_graph_validate(self._h, C.byref(f)))
+        return f.value
+
+    def bfs_order(self, root: int = 0) -> np.ndarray:
+        out = np.empty(self.n, np.uint64)
+        _check(lib().fpr_b200_graph_bfs_order(self._h, root, out.ctypes.data))
+        return out
 
     def close(self) -> None:
         if self._h:

@@ -92,21 +92,30 @@ cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, u
                               unsigned int* bad_flag, cudaStream_t s);
 cudaError_t launch_check_offsets(const int64_t* row, int32_t n, int64_t m, unsigned int* bad_flag,
                                  cudaStream_t s);
+cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* bad, cudaStream_t s);
 cudaError_t launch_widen(const int64_t* row, const int32_t* ids32, uint64_t* out_row,
                          uint64_t* out_ids, int64_t nrow, int64_t nids, cudaStream_t s);
 
 // generate.cu
 struct GenRequest {
-  int kind;
+  int kind;  // 0 rmat, 1 uniform, 2 chung-lu
   uint32_t scale;
   uint64_t edge_factor;
   double a, b, c, d;
   uint64_t n;
   uint64_t avg_degree;
   uint64_t seed;
+  uint64_t draws;    // chung-lu
+  double alpha;      // chung-lu
+  uint64_t kmax;     // chung-lu
+  int relabel_bfs;   // config 3: BFS crawl-order relabel
+  uint64_t bfs_root;
 };
 // Builds row/src/outdeg on the device (allocates them into g).  Returns a
 // cudaError_t; *msg receives a static description on non-CUDA failures.
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t s, const char** msg);
+// BFS discovery order of g (config-3 relabel) into a host buffer of n int32.
+cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_out,
+                              cudaStream_t s, const char** msg);
 
 }  // namespace fprb

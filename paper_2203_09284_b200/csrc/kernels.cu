@@ -596,6 +596,37 @@ __global__ void check_offsets_kernel(const int64_t* row, int32_t n, int64_t m, u
   }
 }
 
+// build_csr invariants (graph.hpp:20-30): offsets monotone with row[0]=0 and
+// row[n]=m, ids in range, no self-loops, strictly ascending sources per row
+// (sorted + deduplicated), out-degrees equal to the per-source edge counts.
+__global__ void validate_kernel(const int64_t* row, const int32_t* src, int32_t n, int64_t m,
+                                int32_t* recount, unsigned int* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < n; d += stride) {
+    const int64_t a = row[d], b = row[d + 1];
+    if (b < a) atomicOr(bad, 1u);
+    int32_t prev = -1;
+    for (int64_t e = a; e < b; ++e) {
+      const int32_t s = src[e];
+      if (s < 0 || s >= n) {
+        atomicOr(bad, 2u);
+        continue;
+      }
+      if (s == (int32_t)d) atomicOr(bad, 4u);
+      if (s <= prev) atomicOr(bad, 8u);
+      prev = s;
+      atomicAdd(&recount[s], 1);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (row[0] != 0 || row[n] != m)) atomicOr(bad, 16u);
+}
+
+__global__ void compare_counts_kernel(const int32_t* a, const int32_t* b, int32_t n, unsigned int* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (a[i] != b[i]) atomicOr(bad, 32u);
+}
+
 __global__ void widen_kernel(const int64_t* row, const int32_t* ids, uint64_t* out_row,
                              uint64_t* out_ids, int64_t nrow, int64_t nids) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -661,6 +692,12 @@ cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, u
 cudaError_t launch_check_offsets(const int64_t* row, int32_t n, int64_t m, unsigned int* bad_flag,
                                  cudaStream_t s) {
   check_offsets_kernel<<<grid_for(n), 256, 0, s>>>(row, n, m, bad_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* bad, cudaStream_t s) {
+  validate_kernel<<<grid_for(g.n), 256, 0, s>>>(g.row, g.src, g.n, g.m, recount, bad);
+  compare_counts_kernel<<<grid_for(g.n), 256, 0, s>>>(recount, g.outdeg, g.n, bad);
   return cudaGetLastError();
 }
 

@@ -436,8 +436,10 @@ int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* o
                             fpr_b200_graph** out) {
   if (!prm || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_generate: null argument");
   *out = nullptr;
-  GenRequest req{prm->kind, prm->scale, prm->edge_factor, prm->a, prm->b, prm->c,
-                 prm->d,    prm->n,     prm->avg_degree, prm->seed};
+  GenRequest req{prm->kind, prm->scale,      prm->edge_factor, prm->a,
+                 prm->b,    prm->c,          prm->d,           prm->n,
+                 prm->avg_degree, prm->seed, prm->draws,      prm->alpha,
+                 prm->kmax, prm->relabel_bfs, prm->bfs_root};
   if (req.kind == FPR_B200_GEN_RMAT) {
     // validate(RmatParams), rmat.hpp:24-35 -- same text.
     if (req.scale == 0 || req.scale > 32)
@@ -453,8 +455,18 @@ int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* o
     if (req.n == 0) return fail(FPR_B200_EINVAL, "fpr_b200: uniform generator needs n > 0");
     if (req.n >= (1ULL << 31))
       return fail(FPR_B200_ERANGE, "fpr_b200: n exceeds the int32 vertex-id range");
+  } else if (req.kind == FPR_B200_GEN_CHUNGLU) {
+    if (req.n == 0) return fail(FPR_B200_EINVAL, "fpr_b200: chung-lu generator needs n > 0");
+    if (req.n >= (1ULL << 31))
+      return fail(FPR_B200_ERANGE, "fpr_b200: n exceeds the int32 vertex-id range");
+    if (!(req.alpha > 1.0) || req.kmax == 0 || req.kmax > (1ull << 28))
+      return fail(FPR_B200_EINVAL, "fpr_b200: chung-lu needs alpha > 1 and 1 <= kmax <= 2^28");
   } else {
     return fail(FPR_B200_EINVAL, "fpr_b200: unknown generator kind");
+  }
+  if (req.relabel_bfs) {
+    const uint64_t nn = req.kind == FPR_B200_GEN_RMAT ? (1ull << req.scale) : req.n;
+    if (req.bfs_root >= nn) return fail(FPR_B200_EINVAL, "fpr_b200: bfs_root outside [0,n)");
   }
   fpr_b200_graph* h = nullptr;
   int rc = open_handle(opts, &h);
@@ -528,6 +540,36 @@ int fpr_b200_graph_download_csr(const fpr_b200_graph* hc, uint64_t* in_start, ui
   cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess)
     return fail(FPR_B200_ECUDA, std::string("fpr_b200_graph_download_csr: ") + cudaGetErrorString(e));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_validate(fpr_b200_graph* h, uint32_t* flags) {
+  if (!h || !flags) return fail(FPR_B200_EINVAL, "fpr_b200_graph_validate: null argument");
+  CK(cudaSetDevice(h->device));
+  int32_t* recount = nullptr;
+  unsigned int* bad = nullptr;
+  CK(cudaMallocAsync(&recount, std::max<int64_t>(h->g.n, 1) * sizeof(int32_t), h->stream));
+  CK(cudaMallocAsync(&bad, sizeof(unsigned int), h->stream));
+  CK(cudaMemsetAsync(recount, 0, std::max<int64_t>(h->g.n, 1) * sizeof(int32_t), h->stream));
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned int), h->stream));
+  if (h->g.n > 0) CK(launch_validate(h->g, recount, bad, h->stream));
+  CK(cudaMemcpyAsync(h->h_iters, bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, h->stream));
+  cudaFreeAsync(recount, h->stream);
+  cudaFreeAsync(bad, h->stream);
+  CK(cudaStreamSynchronize(h->stream));
+  *flags = *h->h_iters;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_bfs_order(fpr_b200_graph* h, uint64_t root, uint64_t* new_id) {
+  if (!h || !new_id) return fail(FPR_B200_EINVAL, "fpr_b200_graph_bfs_order: null argument");
+  if (root >= (uint64_t)h->g.n) return fail(FPR_B200_EINVAL, "fpr_b200: bfs root outside [0,n)");
+  CK(cudaSetDevice(h->device));
+  std::vector<int32_t> tmp(h->g.n);
+  const char* msg = nullptr;
+  CK(relabel_order_bfs(h->g, (int32_t)root, tmp.data(), h->stream, &msg));
+  if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200_graph_bfs_order: ") + msg);
+  for (int32_t i = 0; i < h->g.n; ++i) new_id[i] = (uint64_t)tmp[i];
   return FPR_B200_OK;
 }
 

@@ -55,3 +55,38 @@ def test_config2_uniform_generate_and_ec(oracle):
 
     ref = oracle.pagerank_ec(OGraph(g.n, g.m, g.in_start, g.in_src, g.out_degree), threshold=1e-10)
     assert float(np.max(np.abs(r.ranks.values - ref.ranks) / ref.ranks)) <= 1e-12
+
+
+# ---------------------------------------------------------------- config 3/4
+def test_bfs_order_matches_oracle(oracle):
+    """Device level-synchronous BFS == the sequential FIFO restatement."""
+    n, s, d = oracle.generate_rmat(16, 16, seed=1)
+    g = oracle.build_csr(n, s, d)
+    with fb.DeviceGraph.from_graph(fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)) as dg:
+        for root in (0, 12345):
+            np.testing.assert_array_equal(dg.bfs_order(root), oracle.bfs_relabel(g, root))
+
+
+def test_rmat_relabel_generate_matches_oracle(oracle):
+    n, s, d = oracle.generate_rmat(14, 16, seed=3)
+    g = oracle.build_csr(n, s, d)
+    want = oracle.relabel(g, oracle.bfs_relabel(g, 0))
+    with fb.DeviceGraph.generate_rmat(fb.RmatParams(14, 16, seed=3), relabel_bfs=True) as dg:
+        got = dg.download()
+        assert dg.validate() == 0
+    assert got.m == want.m == g.m
+    np.testing.assert_array_equal(got.in_start, want.in_start)
+    np.testing.assert_array_equal(got.in_src, want.in_src)
+    np.testing.assert_array_equal(got.out_degree, want.out_degree)
+
+
+def test_chunglu_generate_matches_oracle(oracle):
+    n, s, d = oracle.generate_chunglu(1 << 14, 1 << 18, seed=4, kmax=10_000)
+    want = oracle.build_csr(n, s, d)
+    with fb.DeviceGraph.generate_chunglu(1 << 14, 1 << 18, seed=4, kmax=10_000) as dg:
+        got = dg.download()
+        assert dg.validate() == 0
+    assert got.m == want.m
+    np.testing.assert_array_equal(got.in_start, want.in_start)
+    np.testing.assert_array_equal(got.in_src, want.in_src)
+    np.testing.assert_array_equal(got.out_degree, want.out_degree)
