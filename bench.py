@@ -218,6 +218,9 @@ def main() -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_multi(args, fb, dist, ws, rank, local)
+        dist.destroy_process_group()
+        return
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -315,6 +318,64 @@ def main() -> None:
     dg.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_multi(args, fb, dist, ws, rank, local) -> None:
+    """N GPUs: destination-range partition of config 2 (strong scaling), one
+    NCCL all-gather of contribution slices + one residual all-gather per
+    iteration (paper_2203_09284_b200/dist.py)."""
+    import torch
+
+    from paper_2203_09284_b200.dist import B200Part, TorchExchange, solve_partitioned
+
+    sptr = torch.cuda.current_stream().cuda_stream
+    full = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
+    n, m = full.n, full.m
+    part = B200Part(full, ws, rank, device=local, stream=sptr)
+    full.close()
+    ex = TorchExchange()
+    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
+    dev = f"cuda:{local}"
+    for _ in range(args.warmup):
+        r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev)
+    iters = r.iterations
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev)
+            assert r.iterations == iters
+        ev1.record(stream)
+        barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    fr = solve_partitioned(part, ex, fb.ENGINE_FUSED, cfg, device=dev)
+    if rank == 0:
+        line = {
+            "metric": "GTEPS/iter (ec_b200 time-to-converge, config 2)",
+            "value": m * iters / (ms_step * 1e-3) / 1e9, "unit": "GTEPS", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
+            "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
+                       "norm": "linf", "step": "1 full EC solve (time-to-converge)",
+                       "parallelism": f"dst-range partition x{ws}, NCCL all-gather per iteration",
+                       "slice": part.slice, "l2": "inputs larger than L2; no flush"},
+            "time_to_converge_ms": ms_step,
+            "fused": {"engine": "fused_b200", "iterations": fr.iterations},
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": int(args.steps * iters), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    part.close()
 
 
 def e2e_leg(fb, g, device, args, iters) -> dict:

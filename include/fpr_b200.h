@@ -157,6 +157,29 @@ int fpr_b200_run(fpr_b200_graph* g, int engine, const fpr_config* cfg, double* r
 /* Device pointer of the rank vector left by the last run (n doubles). */
 const double* fpr_b200_graph_ranks_device(const fpr_b200_graph* g);
 
+/* ---- multi-GPU destination-range partitioning -------------
+ * Part r of nparts owns rows [bounds[r], bounds[r+1]) (edge-balanced merge-
+ * path split) with its in-edges; source ids are remapped into a padded
+ * exchange space of nparts*slice doubles (part(s)*slice + s - bounds[part(s)])
+ * so each iteration's exchange is ONE equal-size all-gather (NCCL over
+ * NVLink), plus an all-reduce of the (max, sum) residual pair.  The caller
+ * owns the exchange vectors (device memory, nparts*slice doubles) and the
+ * collectives (paper_2203_09284_b200/dist.py). */
+int fpr_b200_graph_partition(const fpr_b200_graph* full, uint32_t nparts, uint32_t part,
+                             const fpr_b200_options* opts, uint64_t* bounds_out,
+                             uint64_t* slice_out, fpr_b200_graph** out);
+int fpr_b200_part_info(const fpr_b200_graph* g, uint64_t* n_global, uint64_t* row_begin,
+                       uint64_t* slice, uint32_t* nparts, uint32_t* part);
+/* pr = 1/n_global for the part's rows; their contributions into exchange's slice. */
+int fpr_b200_part_init(fpr_b200_graph* g, double* exchange);
+/* One sweep on the part's stream, reading sources through exch_read and
+ * writing the part's contributions into exch_write's slice (EC: distinct
+ * vectors; FUSED: the same vector, in place).  pair_out (device, 2 doubles)
+ * receives this part's (max |delta|, sum |delta|).  Does not synchronise. */
+int fpr_b200_part_sweep(fpr_b200_graph* g, int engine, const fpr_config* cfg,
+                        const double* exch_read, double* exch_write, double* pair_out);
+int fpr_b200_part_ranks(fpr_b200_graph* g, double* ranks_out);
+
 /* One-shot drop-in: create from host view, run, copy results, destroy. */
 int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* cfg,
                       const fpr_b200_options* opts, double* ranks_out, double* errors_out,

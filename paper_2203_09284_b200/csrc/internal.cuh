@@ -65,6 +65,7 @@ struct SolveParams {
   double* contrib0;
   double* contrib1;
   int32_t parity0;  // contrib buffer holding the previous sweep at local iteration 0
+  int64_t write_off;  // multi-GPU: this part's slice offset in the exchange vector (0 otherwise)
   double* tail_partial;  // per task: partial of its open row; NaN = not ready
   double damping;
   double base;
@@ -92,6 +93,12 @@ cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, u
                               unsigned int* bad_flag, cudaStream_t s);
 cudaError_t launch_check_offsets(const int64_t* row, int32_t n, int64_t m, unsigned int* bad_flag,
                                  cudaStream_t s);
+cudaError_t launch_part_bounds(const DevGraph& g, uint32_t nparts, int64_t* bounds, cudaStream_t s);
+cudaError_t launch_part_extract(const DevGraph& g, const int64_t* bounds, uint32_t nparts,
+                                uint32_t part, int64_t slice, int64_t nloc, int64_t mloc,
+                                DevGraph& out, cudaStream_t s);
+cudaError_t launch_part_init(const DevGraph& g, double init, double* pr, double* contrib_slice,
+                             cudaStream_t s);
 cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* bad, cudaStream_t s);
 cudaError_t launch_widen(const int64_t* row, const int32_t* ids32, uint64_t* out_row,
                          uint64_t* out_ids, int64_t nrow, int64_t nids, cudaStream_t s);

@@ -220,7 +220,7 @@ __device__ __forceinline__ double tail_not_ready() { return __longlong_as_double
 template <bool ASYNC>
 __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_below,
                                         const double* prev, const double* cur) {
-  const double* basep = ASYNC ? cur : ((s < fresh_below) ? cur : prev);
+  const double* basep = ASYNC ? prev : ((s < fresh_below) ? cur : prev);
   const double* addr = basep + s;
   if (ASYNC) {  // value-atomic live read (pagerank.hpp:305)
     asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.relaxed.gpu.global.f64 %0, [%1]; }"
@@ -476,11 +476,12 @@ __global__ void __launch_bounds__(kBlockThreads, FPR_MIN_BLOCKS) solve_kernel(So
   for (uint32_t it = 0; it < p.max_iters; ++it) {
     double lmax = 0.0, lsum = 0.0;
     if (ASYNC) {
-      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0, ws, lane, pol,
+      // in place: reads through the full vector, writes to this part's slice
+      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0 + p.write_off, ws, lane, pol,
                       lmax, lsum);
     } else {
       const double* prev = par ? p.contrib1 : p.contrib0;
-      double* cur = par ? p.contrib0 : p.contrib1;
+      double* cur = (par ? p.contrib0 : p.contrib1) + p.write_off;
       for (int w = 0; w < p.nwaves; ++w) {
         run_tasks<false>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
                          __ldg(p.wave_row + w), prev, cur, ws, lane, pol, lmax, lsum);
@@ -596,6 +597,56 @@ __global__ void check_offsets_kernel(const int64_t* row, int32_t n, int64_t m, u
   }
 }
 
+// Multi-GPU destination-range partition: part r owns rows
+// [bounds[r], bounds[r+1]); its sources are remapped into the padded exchange
+// space part(s)*slice + (s - bounds[part(s)]) so one equal-size all-gather per
+// iteration rebuilds every part's view of the contribution vector.
+__global__ void part_bounds_kernel(const int64_t* row, int32_t n, int64_t m, uint32_t nparts,
+                                   int64_t* bounds) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > nparts) return;
+  const int64_t total = (int64_t)n + m;
+  const int64_t diag = (int64_t)((__int128)total * r / nparts);
+  bounds[r] = r == nparts ? n : merge_path(diag, row, n, m);
+}
+
+__global__ void part_extract_kernel(const int64_t* row, const int32_t* src, const int32_t* outdeg,
+                                    const int64_t* bounds, uint32_t nparts, uint32_t part,
+                                    int64_t slice, int64_t* lrow, int32_t* lsrc, int32_t* lout) {
+  __shared__ int64_t sb[65];
+  for (uint32_t i = threadIdx.x; i <= nparts; i += blockDim.x) sb[i] = bounds[i];
+  __syncthreads();
+  const int64_t v0 = sb[part], v1 = sb[part + 1];
+  const int64_t e0 = row[v0], e1 = row[v1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= v1 - v0; i += stride) {
+    lrow[i] = row[v0 + i] - e0;
+    if (i < v1 - v0) lout[i] = outdeg[v0 + i];
+  }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1 - e0; e += stride) {
+    const int32_t s = src[e0 + e];
+    uint32_t lo = 0, hi = nparts;  // last part with bounds[part] <= s
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sb[mid] <= s)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    lsrc[e] = (int32_t)((int64_t)lo * slice + (s - sb[lo]));
+  }
+}
+
+__global__ void part_init_kernel(int32_t n, const int32_t* outdeg, double init, double* pr,
+                                 double* contrib_slice) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    pr[u] = init;
+    const int od = outdeg[u];
+    contrib_slice[u] = od > 0 ? __ddiv_rn(init, (double)od) : 0.0;
+  }
+}
+
 // build_csr invariants (graph.hpp:20-30): offsets monotone with row[0]=0 and
 // row[n]=m, ids in range, no self-loops, strictly ascending sources per row
 // (sorted + deduplicated), out-degrees equal to the per-source edge counts.
@@ -692,6 +743,25 @@ cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, u
 cudaError_t launch_check_offsets(const int64_t* row, int32_t n, int64_t m, unsigned int* bad_flag,
                                  cudaStream_t s) {
   check_offsets_kernel<<<grid_for(n), 256, 0, s>>>(row, n, m, bad_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_bounds(const DevGraph& g, uint32_t nparts, int64_t* bounds, cudaStream_t s) {
+  part_bounds_kernel<<<1, 128, 0, s>>>(g.row, g.n, g.m, nparts, bounds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_extract(const DevGraph& g, const int64_t* bounds, uint32_t nparts,
+                                uint32_t part, int64_t slice, int64_t nloc, int64_t mloc,
+                                DevGraph& out, cudaStream_t s) {
+  part_extract_kernel<<<grid_for(nloc > mloc ? nloc : mloc), 256, 0, s>>>(
+      g.row, g.src, g.outdeg, bounds, nparts, part, slice, out.row, out.src, out.outdeg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_init(const DevGraph& g, double init, double* pr, double* contrib_slice,
+                             cudaStream_t s) {
+  part_init_kernel<<<grid_for(g.n), 256, 0, s>>>(g.n, g.outdeg, init, pr, contrib_slice);
   return cudaGetLastError();
 }
 

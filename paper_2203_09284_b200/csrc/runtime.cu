@@ -125,6 +125,9 @@ struct fpr_b200_graph {
   cudaEvent_t up_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::map<uint32_t, Waves> waves;
   std::vector<void*> allocs;
+  // multi-GPU part (fpr_b200_graph_partition); nparts == 1 for a whole graph
+  uint32_t nparts = 1, part_id = 0;
+  uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
 
 namespace {
@@ -642,6 +645,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.tail_partial = h->tail_partial;
   p.damping = cfg->damping;
   p.base = (1.0 - cfg->damping) / (double)g.n;  // pagerank.hpp:81
+  p.write_off = 0;
   p.threshold = cfg->threshold;
   p.norm = h->norm;
   p.errors = h->d_errors;
@@ -707,6 +711,159 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     result->solve_ms = solve_ms;
     result->kernel_launches = launches;
   }
+  return FPR_B200_OK;
+}
+
+// ------------------------------------------------------------ multi-GPU parts
+int fpr_b200_graph_partition(const fpr_b200_graph* fullc, uint32_t nparts, uint32_t part,
+                             const fpr_b200_options* opts, uint64_t* bounds_out,
+                             uint64_t* slice_out, fpr_b200_graph** out) {
+  auto* full = const_cast<fpr_b200_graph*>(fullc);
+  if (!full || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_partition: null argument");
+  *out = nullptr;
+  if (nparts == 0 || nparts > 64 || part >= nparts)
+    return fail(FPR_B200_EINVAL, "fpr_b200_graph_partition: need 1 <= nparts <= 64, part < nparts");
+  if (full->nparts != 1) return fail(FPR_B200_EINVAL, "fpr_b200_graph_partition: already a part");
+  if (full->g.n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  CK(cudaSetDevice(full->device));
+  int64_t* d_bounds = nullptr;
+  CK(cudaMallocAsync(&d_bounds, (nparts + 1) * sizeof(int64_t), full->stream));
+  CK(launch_part_bounds(full->g, nparts, d_bounds, full->stream));
+  std::vector<int64_t> b(nparts + 1);
+  CK(cudaMemcpyAsync(b.data(), d_bounds, (nparts + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                     full->stream));
+  CK(cudaStreamSynchronize(full->stream));
+  int64_t slice = 0;
+  for (uint32_t r = 0; r < nparts; ++r) slice = std::max<int64_t>(slice, b[r + 1] - b[r]);
+  if ((int64_t)nparts * slice >= INT32_MAX) {
+    cudaFreeAsync(d_bounds, full->stream);
+    return fail(FPR_B200_ERANGE, "fpr_b200: padded exchange space exceeds int32 ids");
+  }
+  int64_t rows[2];
+  CK(cudaMemcpyAsync(&rows[0], full->g.row + b[part], sizeof(int64_t), cudaMemcpyDeviceToHost, full->stream));
+  CK(cudaMemcpyAsync(&rows[1], full->g.row + b[part + 1], sizeof(int64_t), cudaMemcpyDeviceToHost, full->stream));
+  CK(cudaStreamSynchronize(full->stream));
+  fpr_b200_graph* h = nullptr;
+  fpr_b200_options o;
+  fpr_b200_options_init(&o);
+  if (opts) o = *opts;
+  o.device = full->device;
+  int rc = open_handle(&o, &h);
+  auto bail = [&](int code) {
+    cudaFreeAsync(d_bounds, full->stream);
+    destroy_handle(h);
+    return code;
+  };
+  if (rc) return bail(rc);
+  const int64_t nloc = b[part + 1] - b[part], mloc = rows[1] - rows[0];
+  h->g.n = (int32_t)nloc;
+  h->g.m = mloc;
+  if ((rc = dalloc_n(h, &h->g.row, nloc + 1)) || (rc = dalloc_n(h, &h->g.src, mloc + 8)) ||
+      (rc = dalloc_n(h, &h->g.outdeg, std::max<int64_t>(nloc, 1))))
+    return bail(rc);
+  // the full graph's stream finished the bounds; order the extract after it
+  CK(cudaStreamSynchronize(full->stream));
+  cudaError_t e = launch_part_extract(full->g, d_bounds, nparts, part, slice, nloc, mloc, h->g, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess)
+    return bail(fail(FPR_B200_ECUDA, std::string("fpr_b200_graph_partition: ") + cudaGetErrorString(e)));
+  cudaFreeAsync(d_bounds, full->stream);
+  d_bounds = nullptr;
+  h->nparts = nparts;
+  h->part_id = part;
+  h->n_global = (uint64_t)full->g.n;
+  h->row_begin = (uint64_t)b[part];
+  h->slice = (uint64_t)slice;
+  if ((rc = finish_graph(h))) {
+    destroy_handle(h);
+    return rc;
+  }
+  if (bounds_out)
+    for (uint32_t r = 0; r <= nparts; ++r) bounds_out[r] = (uint64_t)b[r];
+  if (slice_out) *slice_out = (uint64_t)slice;
+  *out = h;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_init(fpr_b200_graph* h, double* exchange) {
+  if (!h || !exchange) return fail(FPR_B200_EINVAL, "fpr_b200_part_init: null argument");
+  CK(cudaSetDevice(h->device));
+  const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
+  CK(launch_part_init(h->g, 1.0 / (double)ng, h->pr, exchange + (uint64_t)h->part_id * h->slice,
+                      h->stream));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_sweep(fpr_b200_graph* h, int engine, const fpr_config* cfg,
+                        const double* exch_read, double* exch_write, double* pair_out) {
+  if (!h || !cfg || !exch_read || !exch_write || !pair_out)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: null argument");
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (engine != kEC && engine != kFused)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: engine must be EC or FUSED");
+  if (engine == kFused && exch_read != exch_write)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: FUSED updates the exchange vector in place");
+  CK(cudaSetDevice(h->device));
+  const Waves* wv = nullptr;
+  if ((rc = get_waves(h, 1u, &wv))) return rc;
+  const int variant = engine == kFused ? 1 : 0;
+  const int64_t want = (h->part.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
+  const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
+  SolveParams p{};
+  p.n = h->g.n;
+  p.row = h->g.row;
+  p.src = h->g.src;
+  p.outdeg = h->g.outdeg;
+  p.task_row = h->part.task_row;
+  p.task_edge = h->part.task_edge;
+  p.head_first = h->part.head_first;
+  p.ntasks = h->part.ntasks;
+  p.wave_task = wv->d_task;
+  p.wave_row = wv->d_row;
+  p.nwaves = wv->nwaves;
+  p.pr = h->pr;
+  p.contrib0 = const_cast<double*>(exch_read);
+  p.contrib1 = exch_write;
+  p.parity0 = 0;
+  p.write_off = (int64_t)h->part_id * (int64_t)h->slice;
+  p.tail_partial = h->tail_partial;
+  p.damping = cfg->damping;
+  p.base = (1.0 - cfg->damping) / (double)ng;
+  p.threshold = 0.0;  // one sweep; the caller decides after the all-reduce
+  p.norm = h->norm;
+  p.max_iters = 1;
+  p.errors = h->d_errors;
+  p.l1errors = h->d_l1;
+  p.iter_ns = h->d_ns;
+  p.partials = h->partials;
+  p.totals = h->totals;
+  p.bar = h->bar;
+  p.out_iters = h->d_iters;
+  p.out_stop = h->d_stop;
+  CK(launch_solve(engine, grid, p, h->stream));
+  CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_info(const fpr_b200_graph* h, uint64_t* n_global, uint64_t* row_begin,
+                       uint64_t* slice, uint32_t* nparts, uint32_t* part) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_part_info: null graph");
+  if (n_global) *n_global = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
+  if (row_begin) *row_begin = h->row_begin;
+  if (slice) *slice = h->nparts > 1 ? h->slice : (uint64_t)h->g.n;
+  if (nparts) *nparts = h->nparts;
+  if (part) *part = h->part_id;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_ranks(fpr_b200_graph* h, double* ranks_out) {
+  if (!h || !ranks_out) return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks: null argument");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(ranks_out, h->pr, h->g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   return FPR_B200_OK;
 }
 
