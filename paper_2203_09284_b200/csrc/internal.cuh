@@ -21,11 +21,11 @@ constexpr int kWarpsPerBlock = kBlockThreads / 32;
 #define FPR_TASK_DIAG 224
 #endif
 #ifndef FPR_SNAP_EDGES
-#define FPR_SNAP_EDGES 28
+#define FPR_SNAP_EDGES 25
 #endif
 constexpr int kTaskDiag = FPR_TASK_DIAG;    // merge-path diagonal stride between warp tasks
 constexpr int kSnapEdges = FPR_SNAP_EDGES;  // a boundary inside a row of <= kSnapEdges edges moves to its start
-constexpr int kTaskItems = kTaskDiag + kSnapEdges;  // max items (and edges) per task: 252 (+3 pad <= 256)
+constexpr int kTaskItems = kTaskDiag + kSnapEdges;  // max items (and edges) per task: 249 (+7 pad <= 256)
 
 struct GridBar {
   unsigned int count;
@@ -36,7 +36,7 @@ struct DevGraph {
   int32_t n = 0;
   int64_t m = 0;
   int64_t* row = nullptr;
-  int32_t* src = nullptr;  // m + 4 entries: 16-B staged loads may overrun by 3
+  int32_t* src = nullptr;  // m + 8 entries: aligned 32-B loads may overrun by 7
   int32_t* outdeg = nullptr;
 };
 

@@ -162,14 +162,14 @@ __device__ __forceinline__ void grid_sync_reduce(const SolveParams& p, double bm
 }
 
 // ------------------------------------------------------------ one warp task
-// A task covers ~kTaskDiag merge items (<= kTaskItems = 252 edges); its slice [j0, j1) is
-// viewed in 16-B-aligned "position" space p = (e - (j0 & ~3)), so lane L owns
-// positions [8L, 8L+8) and loads them as two aligned int4 (coalesced 1 KB per
+// A task covers ~kTaskDiag merge items (<= kTaskItems = 249 edges); its slice [j0, j1) is
+// viewed in 32-B-aligned "position" space p = (e - (j0 & ~7)), so lane L owns
+// positions [8L, 8L+8) and loads them as one aligned 32-B vector (coalesced 1 KB per
 // warp), gathers its <= 8 contributions into registers, and reduces them
 // lane-sequentially in ascending-src order.  Segments (rows) crossing lanes are
 // combined by one warp segmented scan; rows crossing tasks by tail partials.
 constexpr int kLaneItems = 8;
-static_assert(kTaskItems + 3 <= 32 * kLaneItems, "task slice must fit 256 positions");
+
 
 struct WarpSmem {
   unsigned startbits[8];          // bit p: a row segment starts at position p
@@ -177,6 +177,8 @@ struct WarpSmem {
   double rowsum[kTaskItems + 1];  // in-task sums of finalized rows (relative index)
 };
 constexpr int kSolveSmemBytes = kWarpsPerBlock * (int)sizeof(WarpSmem);
+
+static_assert(kTaskItems + 7 <= 32 * kLaneItems, "task slice (+ alignment pad) must fit 256 positions");
 
 struct TaskMeta {
   int i0, i1;
@@ -192,24 +194,24 @@ __device__ __forceinline__ TaskMeta load_meta(const SolveParams& p, int t) {
   return m;
 }
 
-__device__ __forceinline__ int4 ld_stream_v4(const int32_t* p, unsigned long long pol) {
-  int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
 
-// Lane's 8 source ids of a task (two aligned 16-B loads; chunks past j1 skipped).
+// Lane's 8 source ids of a task: one aligned 32-B load (LDG.256) per lane, so
+// the warp's 1 KB of in_src costs exactly one L2 request per sector.
 struct Src8 {
   int4 a, b;
 };
+constexpr int kPosAlign = 8;
 __device__ __forceinline__ Src8 load_src8(const SolveParams& p, const TaskMeta& m, int lane,
                                           unsigned long long pol) {
   Src8 s{{0, 0, 0, 0}, {0, 0, 0, 0}};
-  const int64_t base = (m.j0 & ~int64_t(3)) + 8 * lane;
-  if (base < m.j1) s.a = ld_stream_v4(p.src + base, pol);
-  if (base + 4 < m.j1) s.b = ld_stream_v4(p.src + base + 4, pol);
+  const int64_t base = (m.j0 & ~int64_t(kPosAlign - 1)) + 8 * lane;
+  if (base < m.j1) {
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(s.a.x), "=r"(s.a.y), "=r"(s.a.z), "=r"(s.a.w), "=r"(s.b.x), "=r"(s.b.y),
+          "=r"(s.b.z), "=r"(s.b.w)
+        : "l"(p.src + base), "l"(pol));
+  }
   return s;
 }
 
@@ -256,28 +258,35 @@ __device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMe
   return r;
 }
 
+// 1. gathers: position q of this lane holds edge q - off when off <= q < off + nE;
+//    invalid positions keep 0 (predicated loads, nothing consumed early).
 template <bool ASYNC>
-__device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
-                                             const Src8& sx, const RowPre& rp, int fresh_below,
-                                             const double* prev, double* cur, WarpSmem& ws,
-                                             int lane, double& lmax, double& lsum) {
-  const int i0 = m.i0, i1 = m.i1;
-  const int64_t j0 = m.j0, j1 = m.j1;
-  const int nE = (int)(j1 - j0);
-  const int off = (int)(j0 & 3);
+__device__ __forceinline__ void issue_gathers8(const TaskMeta& m, const Src8& sx, int lane,
+                                               int fresh_below, const double* prev,
+                                               const double* cur, double (&v)[8]) {
+  const int off = (int)(m.j0 & (kPosAlign - 1));
+  const int valid_hi = off + (int)(m.j1 - m.j0);
   const int pos0 = 8 * lane;
-  const int valid_hi = off + nE;
-
-  // 1. gathers: position q of this lane holds edge q - off when off <= q < off + nE.
-  //    Invalid positions load contrib[0] (harmless) so no value is consumed early.
   const int sids[8] = {sx.a.x, sx.a.y, sx.a.z, sx.a.w, sx.b.x, sx.b.y, sx.b.z, sx.b.w};
-  double v[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int q = pos0 + i;
     v[i] = 0.0;
     gather1<ASYNC>(v[i], q >= off && q < valid_hi, sids[i], fresh_below, prev, cur);
   }
+}
+
+template <bool ASYNC>
+__device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
+                                             const double (&v)[8], const RowPre& rp,
+                                             double* cur, WarpSmem& ws, int lane, double& lmax,
+                                             double& lsum) {
+  const int i0 = m.i0, i1 = m.i1;
+  const int64_t j0 = m.j0, j1 = m.j1;
+  const int nE = (int)(j1 - j0);
+  const int off = (int)(j0 & (kPosAlign - 1));
+  const int pos0 = 8 * lane;
+  const int valid_hi = off + nE;
 
   // 2. segment structure (overlaps the gathers): rows i0..i1 (i1 = open row).
   if (lane < 8) ws.startbits[lane] = 0u;
@@ -423,6 +432,9 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
 // metadata, source ids and row metadata are prefetched into registers while
 // the current task is reduced, so a task's only exposed latency is its own
 // (overlapped) random gathers.
+// The current task's gathers are issued first (they own the LSU queue), then
+// the next task's metadata, source ids and row metadata are prefetched into
+// registers while the current task is reduced.
 template <bool ASYNC>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
@@ -437,6 +449,8 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   if (t + nwarps < te) mn = load_meta(p, t + nwarps);
   while (true) {
     const int tn = t + nwarps;
+    double v[8];
+    issue_gathers8<ASYNC>(m, sx, lane, fresh_below, prev, cur, v);
     Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
     RowPre rpn{0, 0, 0, 0.0};
     TaskMeta mnn{0, 0, 0, 0};
@@ -445,7 +459,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
       rpn = load_rowpre(p, mn, lane);
       if (tn + nwarps < te) mnn = load_meta(p, tn + nwarps);
     }
-    process_task<ASYNC>(p, t, m, sx, rp, fresh_below, prev, cur, ws, lane, lmax, lsum);
+    process_task<ASYNC>(p, t, m, v, rp, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;

@@ -369,7 +369,7 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
   DevGraph& g = h->g;
   g.n = (int32_t)v->n;
   g.m = (int64_t)v->m;
-  if ((rc = dalloc_n(h, &g.row, g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m + 4)) ||
+  if ((rc = dalloc_n(h, &g.row, g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m + 8)) ||
       (rc = dalloc_n(h, &g.outdeg, g.n)))
     return bail(rc);
   unsigned int* bad = nullptr;
