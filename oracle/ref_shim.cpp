@@ -12,6 +12,7 @@
 #include <string>
 
 #include "fpr/graph.hpp"
+#include "fpr/graph_cache.hpp"
 #include "fpr/layout.hpp"
 #include "fpr/metrics.hpp"
 #include "fpr/pagerank.hpp"
@@ -152,6 +153,33 @@ int ref_dense_oracle(uint64_t n, uint64_t m, const uint64_t* in_start, const uin
     cfg.max_iterations = max_iter;
     fpr::RankVector rv = fpr::pagerank_dense_oracle(g, cfg);
     std::memcpy(ranks, rv.values.data(), n * sizeof(double));
+  });
+}
+
+// fpr::save_cache / load_cache (graph_cache.hpp:65-97) for format interop tests.
+int ref_save_cache(uint64_t n, uint64_t m, const uint64_t* in_start, const uint64_t* in_src,
+                   const uint64_t* out_degree, const char* path) {
+  return guarded([&] {
+    fpr::Graph g;
+    g.n = n;
+    g.m = m;
+    g.in_start.assign(in_start, in_start + n + 1);
+    g.in_src.assign(in_src, in_src + m);
+    g.out_degree.assign(out_degree, out_degree + n);
+    fpr::save_cache(g, path);
+  });
+}
+
+// Returns 0 and fills *n, *m (arrays NULL) or the arrays (sized by a first call).
+int ref_load_cache(const char* path, uint64_t* n, uint64_t* m, uint64_t* in_start,
+                   uint64_t* in_src, uint64_t* out_degree) {
+  return guarded([&] {
+    fpr::Graph g = fpr::load_cache(path);
+    *n = g.n;
+    *m = g.m;
+    if (in_start) std::memcpy(in_start, g.in_start.data(), (g.n + 1) * sizeof(uint64_t));
+    if (in_src) std::memcpy(in_src, g.in_src.data(), g.m * sizeof(uint64_t));
+    if (out_degree) std::memcpy(out_degree, g.out_degree.data(), g.n * sizeof(uint64_t));
   });
 }
 

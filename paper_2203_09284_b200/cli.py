@@ -1,0 +1,220 @@
+"""fpr-b200: the reference's missing bench CLI over the B200
+engines.  Subcommands run / bench / gen / compare; CSV schema and exit codes
+as specified (0 ok, 1 usage, 2 I/O, 3 non-convergence).
+
+Graph sources:
+  --graph PATH.fprg           FPRG cache (graph_cache.hpp format)
+  --rmat SCALE:EF:SEED        fpr::generate_rmat (+ build_csr) on the device
+  --rmat-bfs SCALE:EF:SEED    ... relabelled in BFS crawl order (config 3)
+  --uniform N:DEG:SEED        testutil::random_sparse semantics (config 2)
+  --chunglu N:DRAWS:SEED      config 4
+
+Engines: ec_b200, fused_b200, fused_lockstep_b200.  The L1 reference column
+(l1_vs_seq_ec) is taken from ec_b200, which equals the reference's ec_seq
+within 1e-12 relative per iteration (tests/test_gpu_engines.py).
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import sys
+import time
+
+import numpy as np
+
+from . import (DeviceGraph, EngineKind, NORM_L1, NORM_LINF, PageRankConfig, RmatParams,
+               l1_norm, parse_engine, ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP)
+from .cache import CacheError, load_cache, save_cache
+
+EXIT_OK, EXIT_USAGE, EXIT_IO, EXIT_NONCONV = 0, 1, 2, 3
+CSV_COLUMNS = ["graph", "engine", "threshold", "threads", "iterations", "wall_time_s",
+               "l1_vs_seq_ec", "converged"]
+_ENGINES = {EngineKind.EcB200: ENGINE_EC, EngineKind.FusedB200: ENGINE_FUSED,
+            EngineKind.FusedLockstepB200: ENGINE_FUSED_LOCKSTEP}
+
+
+class UsageError(Exception):
+    pass
+
+
+def _triple(text: str, name: str) -> tuple[int, int, int]:
+    try:
+        a, b, c = (int(x) for x in text.split(":"))
+        return a, b, c
+    except ValueError:
+        raise UsageError(f"--{name} expects A:B:C integers, got '{text}'")
+
+
+def open_graph(args, norm=NORM_LINF) -> tuple[DeviceGraph, str]:
+    given = [k for k in ("graph", "rmat", "rmat_bfs", "uniform", "chunglu") if getattr(args, k, None)]
+    if len(given) != 1:
+        raise UsageError("exactly one graph source is required (--graph/--rmat/--rmat-bfs/--uniform/--chunglu)")
+    k = given[0]
+    v = getattr(args, k)
+    if k == "graph":
+        g = load_cache(v)  # CacheError -> I/O exit code
+        return DeviceGraph.from_graph(g, norm=norm), v
+    a, b, c = _triple(v, k.replace("_", "-"))
+    if k in ("rmat", "rmat_bfs"):
+        return DeviceGraph.generate_rmat(RmatParams(scale=a, edge_factor=b, seed=c), norm=norm,
+                                         relabel_bfs=(k == "rmat_bfs")), f"{k}:{v}"
+    if k == "uniform":
+        return DeviceGraph.generate_uniform(a, b, c, norm=norm), f"uniform:{v}"
+    return DeviceGraph.generate_chunglu(a, b, c, norm=norm), f"chunglu:{v}"
+
+
+def _engine(tag: str) -> int:
+    kind = parse_engine(tag)
+    if kind not in _ENGINES:
+        raise UsageError(f"engine '{tag}' is a reference CPU engine; this CLI runs "
+                         + "|".join(k.value for k in _ENGINES))
+    return _ENGINES[kind]
+
+
+def _cfg(args, threshold=None) -> PageRankConfig:
+    return PageRankConfig(damping=args.damping, threshold=threshold if threshold is not None else args.threshold,
+                          max_iterations=args.max_iters, thread_count=max(1, args.threads))
+
+
+def cmd_run(args, out) -> int:
+    engine = _engine(args.engine)  # usage errors before any device work
+    dg, label = open_graph(args)
+    with dg:
+        t0 = time.perf_counter()
+        r = dg.run(engine, _cfg(args))
+        wall = time.perf_counter() - t0
+    vals = r.ranks.values
+    order = sorted(range(len(vals)), key=lambda i: (-vals[i], i))[: args.topk]  # ties: ascending id
+    out.write(f"graph={label} engine={args.engine} iterations={r.trace.iterations} "
+              f"wall_time_s={wall:.6f} solve_ms={r.solve_ms:.3f} converged={str(r.trace.converged).lower()}\n")
+    out.write(", ".join(f"{i}:{vals[i]:.17g}" for i in order) + "\n")
+    return EXIT_OK if r.trace.converged else EXIT_NONCONV
+
+
+def cmd_bench(args, out) -> int:
+    engines = [e.strip() for e in args.engines.split(",") if e.strip()]
+    thresholds = [float(t) for t in args.thresholds.split(",")]
+    if not engines or not thresholds:
+        raise UsageError("bench needs at least one engine and one threshold")
+    for e in engines:
+        _engine(e)
+    dg, label = open_graph(args)
+    rows = []
+    with dg:
+        for t in thresholds:
+            ref = dg.run(ENGINE_EC, _cfg(args, t))  # the L1 reference, run first
+            for e in engines:
+                best, res = None, None
+                for _ in range(max(1, args.reps)):  # min over repetitions
+                    t0 = time.perf_counter()
+                    r = dg.run(_engine(e), _cfg(args, t))
+                    w = time.perf_counter() - t0
+                    if best is None or w < best:
+                        best, res = w, r
+                rows.append({"graph": label, "engine": e, "threshold": repr(t), "threads": args.threads,
+                             "iterations": res.trace.iterations, "wall_time_s": f"{best:.6f}",
+                             "l1_vs_seq_ec": repr(l1_norm(res.ranks.values, ref.ranks.values)),
+                             "converged": str(res.trace.converged).lower()})
+    if args.format == "json":
+        out.write(json.dumps(rows) + "\n")
+    else:
+        w = csv.DictWriter(out, fieldnames=CSV_COLUMNS, lineterminator="\n")
+        w.writeheader()
+        w.writerows(rows)
+    return EXIT_OK
+
+
+def cmd_gen(args, out) -> int:
+    dg, label = open_graph(args)
+    with dg:
+        g = dg.download()
+    save_cache(g, args.out)  # FPRG (graph_cache.hpp); CacheError -> I/O
+    out.write(f"wrote {args.out}: {label} n={g.n} m={g.m}\n")
+    return EXIT_OK
+
+
+def cmd_compare(args, out) -> int:
+    dg, label = open_graph(args)
+    traces, ranks = {}, {}
+    with dg:
+        for kind in _ENGINES:
+            r = dg.run(_ENGINES[kind], _cfg(args))
+            traces[kind.value], ranks[kind.value] = r.trace.errors, r.ranks.values
+    names = list(traces)
+    w = csv.writer(out, lineterminator="\n")
+    w.writerow(["iteration"] + names)
+    for i in range(max(len(t) for t in traces.values())):
+        w.writerow([i + 1] + [repr(float(traces[n][i])) if i < len(traces[n]) else "" for n in names])
+    out.write("\n")
+    w.writerow(["l1"] + names)
+    for a in names:
+        w.writerow([a] + [repr(l1_norm(ranks[a], ranks[b])) for b in names])
+    return EXIT_OK
+
+
+def build_parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="fpr-b200", description=__doc__.split("\n")[0])
+    sub = ap.add_subparsers(dest="cmd", required=True)
+
+    def common(p):
+        p.add_argument("--graph")
+        p.add_argument("--rmat")
+        p.add_argument("--rmat-bfs", dest="rmat_bfs")
+        p.add_argument("--uniform")
+        p.add_argument("--chunglu")
+        p.add_argument("--damping", type=float, default=0.85)
+        p.add_argument("--threshold", type=float, default=1e-15)
+        p.add_argument("--threads", type=int, default=1)
+        p.add_argument("--max-iters", dest="max_iters", type=int, default=10000)
+
+    p = sub.add_parser("run")
+    common(p)
+    p.add_argument("--engine", default="ec_b200")
+    p.add_argument("--topk", type=int, default=10)
+    p = sub.add_parser("bench")
+    common(p)
+    p.add_argument("--engines", default="ec_b200,fused_b200")
+    p.add_argument("--thresholds", default="1e-8,1e-12")
+    p.add_argument("--reps", type=int, default=1)
+    p.add_argument("--format", choices=["csv", "json"], default="csv")
+    p.add_argument("--out")
+    p = sub.add_parser("gen")
+    common(p)
+    p.add_argument("--out", required=True)
+    p = sub.add_parser("compare")
+    common(p)
+    return ap
+
+
+def main(argv=None, out=None) -> int:
+    out = out or sys.stdout
+    try:
+        args = build_parser().parse_args(argv)
+    except SystemExit as e:
+        return EXIT_USAGE if e.code else EXIT_OK
+    try:
+        buf = io.StringIO() if getattr(args, "out", None) and args.cmd == "bench" else out
+        rc = {"run": cmd_run, "bench": cmd_bench, "gen": cmd_gen, "compare": cmd_compare}[args.cmd](args, buf)
+        if buf is not out:
+            try:
+                with open(args.out, "w") as f:
+                    f.write(buf.getvalue())
+            except OSError as e:
+                sys.stderr.write(f"fpr-b200: cannot write {args.out}: {e}\n")
+                return EXIT_IO
+        return rc
+    except UsageError as e:
+        sys.stderr.write(f"fpr-b200: {e}\n")
+        return EXIT_USAGE
+    except (CacheError, OSError) as e:
+        sys.stderr.write(f"fpr-b200: {e}\n")
+        return EXIT_IO
+    except ValueError as e:  # reference validation messages (invalid_argument)
+        sys.stderr.write(f"fpr-b200: {e}\n")
+        return EXIT_USAGE
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,61 @@
+"""SPEC bench-cli contract for the B200 engines."""
+import csv
+import io
+
+import numpy as np
+import pytest
+
+from paper_2203_09284_b200 import Graph
+from paper_2203_09284_b200.cache import save_cache
+from paper_2203_09284_b200.cli import CSV_COLUMNS, EXIT_IO, EXIT_NONCONV, EXIT_OK, EXIT_USAGE, main
+
+
+def _run(argv):
+    out = io.StringIO()
+    rc = main(argv, out)
+    return rc, out.getvalue()
+
+
+def test_usage_errors():
+    assert _run(["run"])[0] == EXIT_USAGE  # no graph source
+    assert _run(["run", "--rmat", "bad"])[0] == EXIT_USAGE
+    assert _run(["nosuch"])[0] == EXIT_USAGE
+    assert _run(["run", "--rmat", "4:2:1", "--engine", "ec_seq"])[0] == EXIT_USAGE
+
+
+def test_missing_file_is_io_error(tmp_path):
+    assert _run(["run", "--graph", str(tmp_path / "missing.fprg")])[0] == EXIT_IO
+
+
+@pytest.mark.gpu
+def test_run_two_cycle(tmp_path):
+    p = str(tmp_path / "c2.fprg")
+    save_cache(Graph(2, 2, np.array([0, 1, 2], np.uint64), np.array([1, 0], np.uint64),
+                     np.array([1, 1], np.uint64)), p)
+    rc, text = _run(["run", "--graph", p, "--engine", "ec_b200"])
+    assert rc == EXIT_OK
+    assert "iterations=1" in text and text.splitlines()[1] == "0:0.5, 1:0.5"
+    rc, _ = _run(["run", "--rmat", "10:16:1", "--threshold", "1e-15", "--max-iters", "3"])
+    assert rc == EXIT_NONCONV
+
+
+@pytest.mark.gpu
+def test_bench_csv_schema(tmp_path):
+    out = tmp_path / "b.csv"
+    rc, _ = _run(["bench", "--rmat", "8:16:1", "--engines", "ec_b200,fused_lockstep_b200",
+                  "--thresholds", "1e-8,1e-12", "--out", str(out)])
+    assert rc == EXIT_OK
+    rows = list(csv.DictReader(open(out)))
+    assert list(rows[0].keys()) == CSV_COLUMNS and len(rows) == 4
+    for r in rows:
+        if r["engine"] == "ec_b200":
+            assert float(r["l1_vs_seq_ec"]) == 0.0
+        assert r["converged"] == "true"
+
+
+@pytest.mark.gpu
+def test_gen_and_compare(tmp_path):
+    p = str(tmp_path / "g.fprg")
+    assert _run(["gen", "--rmat", "6:4:3", "--out", p])[0] == EXIT_OK
+    rc, text = _run(["compare", "--graph", p, "--threshold", "1e-12"])
+    assert rc == EXIT_OK and text.startswith("iteration,ec_b200,fused_b200,fused_lockstep_b200")
