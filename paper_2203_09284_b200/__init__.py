@@ -81,7 +81,8 @@ EXPORTS = [
     "fpr_b200_graph_create", "fpr_b200_graph_generate", "fpr_b200_graph_destroy",
     "fpr_b200_graph_info", "fpr_b200_graph_download_csr", "fpr_b200_graph_wave_starts",
     "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank", "fpr_b200_graph_bfs_order",
-    "fpr_b200_graph_validate",
+    "fpr_b200_graph_validate", "fpr_b200_graph_partition", "fpr_b200_part_info",
+    "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
 ]
 
 _lib = None
