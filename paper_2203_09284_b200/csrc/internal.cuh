@@ -46,6 +46,7 @@ struct Partition {
   int64_t* task_edge = nullptr;   // ntasks+1: first edge of task t
   int32_t* head_first = nullptr;  // ntasks: first task holding a piece of t's split head row, -1 if none
   uint8_t* clean_start = nullptr; // ntasks+1: task t begins at a row boundary
+  uint32_t* task_bits = nullptr;  // ntasks x 8 words: bit p = a row segment starts at position p
 };
 
 // Everything the persistent solve kernel needs (passed by value).
@@ -57,6 +58,7 @@ struct SolveParams {
   const int32_t* task_row;
   const int64_t* task_edge;
   const int32_t* head_first;
+  const uint32_t* task_bits;  // ntasks x 8
   int32_t ntasks;
   const int32_t* wave_task;  // nwaves+1
   const int32_t* wave_row;   // nwaves+1

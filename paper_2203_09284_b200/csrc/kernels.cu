@@ -169,12 +169,12 @@ __device__ __forceinline__ void grid_sync_reduce(const SolveParams& p, double bm
 // lane-sequentially in ascending-src order.  Segments (rows) crossing lanes are
 // combined by one warp segmented scan; rows crossing tasks by tail partials.
 constexpr int kLaneItems = 8;
+constexpr int kPos = 32 * kLaneItems;  // 256 positions per task
 
 
-struct WarpSmem {
-  unsigned startbits[8];          // bit p: a row segment starts at position p
-  unsigned short seg_row[256];    // position -> relative row of the segment starting there
-  double rowsum[kTaskItems + 1];  // in-task sums of finalized rows (relative index)
+struct alignas(16) WarpSmem {
+  double pacc[kPos];  // per position: lane-local running sum since the last segment start
+  double carry[33];   // carry[L] = inclusive segmented scan of lane L-1's tail (0 for L=0)
 };
 constexpr int kSolveSmemBytes = kWarpsPerBlock * (int)sizeof(WarpSmem);
 
@@ -237,23 +237,27 @@ __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_
 }
 
 // Row metadata of a task's first 32 rows (i0 .. i0+31, including the open
-// row i1 when it falls in that window), prefetched one task ahead.
+// row i1 when it falls in that window), prefetched one task ahead, with the
+// row bounds already relative to the task's first edge j0.
 struct RowPre {
-  int64_t a, b;  // row[r], and row[r+1] (or j1 for the open row)
-  int od;        // outdeg[r] (finalized rows only)
-  double ov;     // pr[r]     (finalized rows only)
+  int lo;     // max(row[r], j0) - j0, or -1 when row r began before j0 (split head)
+  int hi;     // row[r+1] - j0 (finalized rows) or j1 - j0 (open row)
+  int od;     // outdeg[r] (finalized rows only)
+  double ov;  // pr[r]     (finalized rows only)
 };
 __device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMeta& m, int lane) {
   RowPre r{0, 0, 0, 0.0};
   const int row = m.i0 + lane;
   if (row < m.i1) {
-    r.a = __ldg(p.row + row);
-    r.b = __ldg(p.row + row + 1);
+    const int64_t a = __ldg(p.row + row), b = __ldg(p.row + row + 1);
+    r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
+    r.hi = (int)(b - m.j0);
     r.od = __ldg(p.outdeg + row);
     r.ov = p.pr[row];
   } else if (row == m.i1 && row < p.n) {
-    r.a = __ldg(p.row + row);
-    r.b = m.j1;
+    const int64_t a = __ldg(p.row + row);
+    r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
+    r.hi = (int)(m.j1 - m.j0);
   }
   return r;
 }
@@ -278,108 +282,61 @@ __device__ __forceinline__ void issue_gathers8(const TaskMeta& m, const Src8& sx
 
 template <bool ASYNC>
 __device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
-                                             const double (&v)[8], const RowPre& rp,
+                                             double (&v)[8], unsigned bits8, const RowPre& rp,
                                              double* cur, WarpSmem& ws, int lane, double& lmax,
                                              double& lsum) {
   const int i0 = m.i0, i1 = m.i1;
   const int64_t j0 = m.j0, j1 = m.j1;
-  const int nE = (int)(j1 - j0);
   const int off = (int)(j0 & (kPosAlign - 1));
-  const int pos0 = 8 * lane;
-  const int valid_hi = off + nE;
+  const int valid_hi = off + (int)(j1 - j0);
 
-  // 2. segment structure (overlaps the gathers): rows i0..i1 (i1 = open row).
-  if (lane < 8) ws.startbits[lane] = 0u;
-  __syncwarp();
-  const int nrows = i1 - i0 + (i1 < p.n ? 1 : 0);
-  for (int rb = 0; rb < nrows; rb += 32) {
-    const int rr = rb + lane;
-    if (rr < nrows) {
-      int64_t a = rp.a, b = rp.b;
-      if (rb != 0) {
-        a = __ldg(p.row + i0 + rr);
-        b = (i0 + rr < i1) ? __ldg(p.row + i0 + rr + 1) : j1;
-      }
-      const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)((b < j1 ? b : j1) - j0);
-      if (lo < hi) {
-        const int q = lo + off;
-        atomicOr(&ws.startbits[q >> 5], 1u << (q & 31));
-        ws.seg_row[q] = (unsigned short)rr;
-      }
-    }
-  }
-  __syncwarp();
-
-  // 3. lane-sequential segmented sums over positions [pos0, pos0 + 8).
-  const unsigned word = ws.startbits[lane >> 2];
-  const unsigned bits8 = (word >> ((lane & 3) * 8)) & 0xffu;
-  const bool next_starts =
-      (lane == 31) ? true : ((ws.startbits[(lane + 1) >> 2] >> (((lane + 1) & 3) * 8)) & 1u);
-  int start_head = -1;  // highest segment start <= pos0
-  {
-    const unsigned below = word & (0xffffffffu >> (31 - (pos0 & 31)));
-    if (below) {
-      start_head = (pos0 & ~31) + 31 - __clz(below);
-    } else {
-      for (int w = (pos0 >> 5) - 1; w >= 0; --w) {
-        const unsigned x = ws.startbits[w];
-        if (x) {
-          start_head = w * 32 + 31 - __clz(x);
-          break;
-        }
-      }
-    }
-  }
-  const bool lane_active = pos0 + 7 >= off && pos0 < valid_hi;
-  double head_acc = 0.0, acc = 0.0;
-  int cur_start = start_head;
-  bool inner = false;
+  // 2. lane-sequential running sums, reset at every segment start (ascending
+  //    source order inside a row, as gather_ranks_jacobi sums, :85-87).
+  double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int q = pos0 + i;
-    const bool valid = q >= off && q < valid_hi;
-    if (i > 0 && ((bits8 >> i) & 1u) && valid) {
-      if (!inner) {
-        head_acc = acc;
-        inner = true;
-      } else {
-        ws.rowsum[ws.seg_row[cur_start]] = acc;  // complete inside this lane
-      }
-      acc = 0.0;
-      cur_start = q;
-    }
-    if (valid) acc += v[i];
+    if ((bits8 >> i) & 1u) acc = 0.0;
+    acc += v[i];
+    v[i] = acc;
   }
-  // warp segmented inclusive scan of the lane tails, keyed by segment start
-  const int key = lane_active ? cur_start : -1 - lane;
-  double S = lane_active ? acc : 0.0;
+  // 3. carries across lanes: inclusive segmented scan of the lane tails; a
+  //    lane holding a segment start breaks the chain.
+  double S = acc;
+  bool brk = bits8 != 0u;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const double up = __shfl_up_sync(FULL_MASK, S, d);
-    const int kup = __shfl_up_sync(FULL_MASK, key, d);
-    if (lane >= d && kup == key) S += up;
+    const bool ub = __shfl_up_sync(FULL_MASK, brk, d);
+    if (lane >= d) {
+      if (!brk) S += up;
+      brk = brk || ub;
+    }
   }
-  const double Sprev = __shfl_up_sync(FULL_MASK, S, 1);
-  const int kprev = __shfl_up_sync(FULL_MASK, key, 1);
-  if (lane_active) {
-    if (inner && start_head >= 0) {  // head segment ends inside this lane
-      double tot = head_acc;
-      if (lane > 0 && start_head < pos0 && kprev == start_head) tot += Sprev;
-      ws.rowsum[ws.seg_row[start_head]] = tot;
+  double4* pa = reinterpret_cast<double4*>(ws.pacc + 8 * lane);
+  pa[0] = make_double4(v[0], v[1], v[2], v[3]);
+  pa[1] = make_double4(v[4], v[5], v[6], v[7]);
+  ws.carry[lane + 1] = S;
+  if (lane == 0) ws.carry[0] = 0.0;
+  // open row at the end of the task: publish its partial first (the partial
+  // IS the flag: >= 0 once written), before waiting on any earlier task.
+  {
+    const int orr = i1 - i0;  // relative index of the open row
+    bool has_piece = false;
+    if (i1 < p.n) {
+      if (orr < 32) {
+        const int lo = __shfl_sync(FULL_MASK, rp.lo, orr), hi = __shfl_sync(FULL_MASK, rp.hi, orr);
+        has_piece = (lo < 0 ? 0 : lo) < hi;
+      } else {
+        has_piece = __ldg(p.row + i1) < j1;
+      }
     }
-    if ((next_starts || pos0 + 8 >= valid_hi) && cur_start >= 0) {
-      const int rr = ws.seg_row[cur_start];
-      if (i0 + rr == i1)
-        st_relaxed_f64(p.tail_partial + t, S);  // open row: publish (the partial is the flag)
-      else
-        ws.rowsum[rr] = S;
-    }
+    if (has_piece && lane == ((valid_hi - 1) >> 3)) st_relaxed_f64(p.tail_partial + t, S);
   }
   __syncwarp();
 
   // 4. head row split across earlier tasks: combine their partials in task order.
   double head_extra = 0.0;
-  const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, rp.a, 0) < j0;
+  const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, rp.lo, 0) < 0;
   if (has_head) {
     const int ta = __ldg(p.head_first + t);
     double accp = 0.0;
@@ -395,21 +352,27 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
     head_extra = warp_sum(accp);
   }
 
-  // 5. finalize rows [i0, i1): lane per row, prefetched metadata for the first 32.
+  // 5. finalize rows [i0, i1): lane per row.  A row's in-task sum is the
+  //    running sum at its last position plus the carry into that lane when
+  //    the row began in an earlier lane.
   for (int rb = i0; rb < i1; rb += 32) {
     const int r = rb + lane;
     if (r < i1) {
-      int64_t a = rp.a, b = rp.b;
+      int lo = rp.lo < 0 ? 0 : rp.lo, hi = rp.hi;
       int od = rp.od;
       double ov = rp.ov;
       if (rb != i0) {
-        a = __ldg(p.row + r);
-        b = __ldg(p.row + r + 1);
+        lo = (int)(__ldg(p.row + r) - j0);
+        hi = (int)(__ldg(p.row + r + 1) - j0);
         od = __ldg(p.outdeg + r);
         ov = p.pr[r];
       }
-      const int lo = (int)((a > j0 ? a : j0) - j0), hi = (int)(b - j0);
-      double sum = (lo < hi) ? ws.rowsum[r - i0] : 0.0;
+      double sum = 0.0;
+      if (lo < hi) {
+        const int e = hi - 1 + off;
+        sum = ws.pacc[e];
+        if (lo + off < (e & ~7)) sum = ws.carry[e >> 3] + sum;
+      }
       if (r == i0 && has_head) sum = head_extra + sum;
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
       p.pr[r] = nv;
@@ -428,13 +391,13 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
   __syncwarp();
 }
 
-// All tasks t = tb + gwarp + k*nwarps < te of this warp.  The next task's
-// metadata, source ids and row metadata are prefetched into registers while
-// the current task is reduced, so a task's only exposed latency is its own
-// (overlapped) random gathers.
 // The current task's gathers are issued first (they own the LSU queue), then
 // the next task's metadata, source ids and row metadata are prefetched into
 // registers while the current task is reduced.
+__device__ __forceinline__ unsigned load_bits8(const SolveParams& p, int t, int lane) {
+  return (__ldg(p.task_bits + 8 * (int64_t)t + (lane >> 2)) >> ((lane & 3) * 8)) & 0xffu;
+}
+
 template <bool ASYNC>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
@@ -445,6 +408,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   TaskMeta m = load_meta(p, t);
   Src8 sx = load_src8(p, m, lane, pol);
   RowPre rp = load_rowpre(p, m, lane);
+  unsigned bits = load_bits8(p, t, lane);
   TaskMeta mn{0, 0, 0, 0};
   if (t + nwarps < te) mn = load_meta(p, t + nwarps);
   while (true) {
@@ -454,17 +418,20 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
     Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
     RowPre rpn{0, 0, 0, 0.0};
     TaskMeta mnn{0, 0, 0, 0};
+    unsigned bitsn = 0;
     if (tn < te) {
       sn = load_src8(p, mn, lane, pol);
       rpn = load_rowpre(p, mn, lane);
+      bitsn = load_bits8(p, tn, lane);
       if (tn + nwarps < te) mnn = load_meta(p, tn + nwarps);
     }
-    process_task<ASYNC>(p, t, m, v, rp, cur, ws, lane, lmax, lsum);
+    process_task<ASYNC>(p, t, m, v, bits, rp, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;
     sx = sn;
     rp = rpn;
+    bits = bitsn;
     mn = mnn;
   }
 }
@@ -579,6 +546,32 @@ __global__ void head_kernel(const int64_t* row, int32_t n, int32_t ntasks, const
     hf = (int32_t)(lo - 1);
   }
   head_first[t] = hf;
+}
+
+// Per-task segment-start bitmap (iteration-invariant): in the task's
+// position space p = e - (j0 & ~7), bit p is set when the in-task segment of
+// one of the rows i0..i1 (i1 = the open row) starts at edge e.
+__global__ void task_bits_kernel(const int64_t* row, int32_t n, int32_t ntasks,
+                                 const int32_t* task_row, const int64_t* task_edge,
+                                 uint32_t* bits) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntasks) return;
+  const int32_t i0 = task_row[t], i1 = task_row[t + 1];
+  const int64_t j0 = task_edge[t], j1 = task_edge[t + 1];
+  const int off = (int)(j0 & 7);
+  uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int32_t last = i1 < n ? i1 : i1 - 1;
+  for (int32_t r = i0; r <= last; ++r) {
+    const int64_t a = row[r], b = r < i1 ? row[r + 1] : j1;
+    const int64_t lo = (a > j0 ? a : j0) - j0, hi = (b < j1 ? b : j1) - j0;
+    if (lo < hi) {
+      const int q = (int)lo + off;
+      w[q >> 5] |= 1u << (q & 31);
+    }
+  }
+  uint4* out = reinterpret_cast<uint4*>(bits + 8 * t);
+  out[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  out[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
 __global__ void init_kernel(int32_t n, const int32_t* outdeg, double init, double* pr,
@@ -713,6 +706,7 @@ cudaError_t launch_partition(const DevGraph& g, Partition& p, cudaStream_t s) {
   const int64_t nt = p.ntasks;
   const int blocks = (int)((nt + 1 + 255) / 256);
   partition_kernel<<<blocks, 256, 0, s>>>(g.row, g.n, g.m, p.ntasks, p.task_row, p.task_edge);
+  task_bits_kernel<<<blocks, 256, 0, s>>>(g.row, g.n, p.ntasks, p.task_row, p.task_edge, p.task_bits);
   head_kernel<<<blocks, 256, 0, s>>>(g.row, g.n, p.ntasks, p.task_row, p.task_edge, p.head_first,
                                      p.clean_start);
   return cudaGetLastError();

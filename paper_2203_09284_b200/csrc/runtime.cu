@@ -226,7 +226,8 @@ int finish_graph(fpr_b200_graph* h) {
   p.ntasks = (int32_t)nt;
   int rc;
   if ((rc = dalloc_n(h, &p.task_row, nt + 1)) || (rc = dalloc_n(h, &p.task_edge, nt + 1)) ||
-      (rc = dalloc_n(h, &p.head_first, nt + 1)) || (rc = dalloc_n(h, &p.clean_start, nt + 1)))
+      (rc = dalloc_n(h, &p.head_first, nt + 1)) || (rc = dalloc_n(h, &p.clean_start, nt + 1)) ||
+      (rc = dalloc_n(h, &p.task_bits, 8 * (nt + 1))))
     return rc;
   if (g.n > 0) CK(launch_partition(g, p, h->stream));
   if ((rc = dalloc_n(h, &h->pr, g.n)) || (rc = dalloc_n(h, &h->contrib[0], g.n)) ||
@@ -635,6 +636,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.task_row = h->part.task_row;
   p.task_edge = h->part.task_edge;
   p.head_first = h->part.head_first;
+  p.task_bits = h->part.task_bits;
   p.ntasks = h->part.ntasks;
   p.wave_task = wv->d_task;
   p.wave_row = wv->d_row;
@@ -819,6 +821,7 @@ int fpr_b200_part_sweep(fpr_b200_graph* h, int engine, const fpr_config* cfg,
   p.task_row = h->part.task_row;
   p.task_edge = h->part.task_edge;
   p.head_first = h->part.head_first;
+  p.task_bits = h->part.task_bits;
   p.ntasks = h->part.ntasks;
   p.wave_task = wv->d_task;
   p.wave_row = wv->d_row;
