@@ -302,14 +302,17 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
   // 3. carries across lanes: inclusive segmented scan of the lane tails; a
   //    lane holding a segment start breaks the chain.
   double S = acc;
-  bool brk = bits8 != 0u;
+  bool brk = bits8 != 0u || lane == 0;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
+    if (__all_sync(FULL_MASK, brk)) break;  // every chain resolved (rows rarely span many lanes)
     const double up = __shfl_up_sync(FULL_MASK, S, d);
     const bool ub = __shfl_up_sync(FULL_MASK, brk, d);
     if (lane >= d) {
       if (!brk) S += up;
       brk = brk || ub;
+    } else {
+      brk = true;
     }
   }
   double4* pa = reinterpret_cast<double4*>(ws.pacc + 8 * lane);
