@@ -15,7 +15,10 @@
 
 namespace fprb {
 
-constexpr int kBlockThreads = 256;
+#ifndef FPR_BLOCK_THREADS
+#define FPR_BLOCK_THREADS 256
+#endif
+constexpr int kBlockThreads = FPR_BLOCK_THREADS;
 constexpr int kWarpsPerBlock = kBlockThreads / 32;
 #ifndef FPR_TASK_DIAG
 #define FPR_TASK_DIAG 224
@@ -90,6 +93,7 @@ enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
 cudaError_t launch_partition(const DevGraph& g, Partition& p, cudaStream_t s);
 cudaError_t launch_init(const DevGraph& g, double* pr, double* contrib, cudaStream_t s);
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out);
+int solve_block_threads(int engine);  // threads per CTA of the engine's solve kernel
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s);
 cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound,
                               unsigned int* bad_flag, cudaStream_t s);

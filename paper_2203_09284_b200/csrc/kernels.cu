@@ -176,7 +176,23 @@ struct alignas(16) WarpSmem {
   double pacc[kPos];  // per position: lane-local running sum since the last segment start
   double carry[33];   // carry[L] = inclusive segmented scan of lane L-1's tail (0 for L=0)
 };
-constexpr int kSolveSmemBytes = kWarpsPerBlock * (int)sizeof(WarpSmem);
+// Launch shape per engine: Jacobi/lockstep run 20 warps/SM (160-thread CTAs,
+// <= 102 registers, no spills); the async engine runs 16 warps/SM, which its
+// relaxed in-place traffic prefers (measured).
+#ifndef FPR_EC_BLOCK
+#define FPR_EC_BLOCK 160
+#endif
+#ifndef FPR_EC_MINB
+#define FPR_EC_MINB 4
+#endif
+#ifndef FPR_ASYNC_BLOCK
+#define FPR_ASYNC_BLOCK 256
+#endif
+#ifndef FPR_ASYNC_MINB
+#define FPR_ASYNC_MINB 2
+#endif
+template <int BT>
+constexpr int solve_smem_bytes() { return (BT / 32) * (int)sizeof(WarpSmem); }
 
 static_assert(kTaskItems + 7 <= 32 * kLaneItems, "task slice (+ alignment pad) must fit 256 positions");
 
@@ -280,25 +296,34 @@ __device__ __forceinline__ void issue_gathers8(const TaskMeta& m, const Src8& sx
   }
 }
 
+// 2. lane-sequential running sums, reset at every segment start (ascending
+//    source order inside a row, as gather_ranks_jacobi sums, :85-87); the 8
+//    partial sums go to shared memory so v can take the next task's gathers.
+__device__ __forceinline__ double task_sums(const double (&v)[8], unsigned bits8, WarpSmem& ws,
+                                            int lane) {
+  double acc = 0.0, w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if ((bits8 >> i) & 1u) acc = 0.0;
+    acc += v[i];
+    w[i] = acc;
+  }
+  double4* pa = reinterpret_cast<double4*>(ws.pacc + 8 * lane);
+  pa[0] = make_double4(w[0], w[1], w[2], w[3]);
+  pa[1] = make_double4(w[4], w[5], w[6], w[7]);
+  return acc;
+}
+
 template <bool ASYNC>
-__device__ __forceinline__ void process_task(const SolveParams& p, int t, const TaskMeta& m,
-                                             double (&v)[8], unsigned bits8, const RowPre& rp,
-                                             double* cur, WarpSmem& ws, int lane, double& lmax,
-                                             double& lsum) {
+__device__ __forceinline__ void task_finish(const SolveParams& p, int t, const TaskMeta& m,
+                                            double acc, unsigned bits8, const RowPre& rp,
+                                            double* cur, WarpSmem& ws, int lane, double& lmax,
+                                            double& lsum) {
   const int i0 = m.i0, i1 = m.i1;
   const int64_t j0 = m.j0, j1 = m.j1;
   const int off = (int)(j0 & (kPosAlign - 1));
   const int valid_hi = off + (int)(j1 - j0);
 
-  // 2. lane-sequential running sums, reset at every segment start (ascending
-  //    source order inside a row, as gather_ranks_jacobi sums, :85-87).
-  double acc = 0.0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if ((bits8 >> i) & 1u) acc = 0.0;
-    acc += v[i];
-    v[i] = acc;
-  }
   // 3. carries across lanes: inclusive segmented scan of the lane tails; a
   //    lane holding a segment start breaks the chain.
   double S = acc;
@@ -315,9 +340,6 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
       brk = true;
     }
   }
-  double4* pa = reinterpret_cast<double4*>(ws.pacc + 8 * lane);
-  pa[0] = make_double4(v[0], v[1], v[2], v[3]);
-  pa[1] = make_double4(v[4], v[5], v[6], v[7]);
   ws.carry[lane + 1] = S;
   if (lane == 0) ws.carry[0] = 0.0;
   // open row at the end of the task: publish its partial first (the partial
@@ -394,9 +416,11 @@ __device__ __forceinline__ void process_task(const SolveParams& p, int t, const 
   __syncwarp();
 }
 
-// The current task's gathers are issued first (they own the LSU queue), then
-// the next task's metadata, source ids and row metadata are prefetched into
-// registers while the current task is reduced.
+// All tasks t = tb + gwarp + k*nwarps < te of this warp, software-pipelined
+// without extra registers: once a task's gathered values are folded into
+// shared memory, the next task's gathers are issued into the same registers
+// and fly while this task's carry scan and row finalize run.  Source ids are
+// prefetched two tasks ahead, row metadata and bitmaps one task ahead.
 __device__ __forceinline__ unsigned load_bits8(const SolveParams& p, int t, int lane) {
   return (__ldg(p.task_bits + 8 * (int64_t)t + (lane >> 2)) >> ((lane & 3) * 8)) & 0xffu;
 }
@@ -409,50 +433,60 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   int t = tb + gwarp;
   if (t >= te) return;
   TaskMeta m = load_meta(p, t);
-  Src8 sx = load_src8(p, m, lane, pol);
+  double v[8];
+  {
+    const Src8 sx = load_src8(p, m, lane, pol);
+    issue_gathers8<ASYNC>(m, sx, lane, fresh_below, prev, cur, v);
+  }
   RowPre rp = load_rowpre(p, m, lane);
   unsigned bits = load_bits8(p, t, lane);
-  TaskMeta mn{0, 0, 0, 0};
-  if (t + nwarps < te) mn = load_meta(p, t + nwarps);
+  TaskMeta mn{0, 0, 0, 0}, mnn{0, 0, 0, 0};
+  Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
+  if (t + nwarps < te) {
+    mn = load_meta(p, t + nwarps);
+    sn = load_src8(p, mn, lane, pol);
+    if (t + 2 * nwarps < te) mnn = load_meta(p, t + 2 * nwarps);
+  }
   while (true) {
     const int tn = t + nwarps;
-    double v[8];
-    issue_gathers8<ASYNC>(m, sx, lane, fresh_below, prev, cur, v);
-    Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
+    const double acc = task_sums(v, bits, ws, lane);
     RowPre rpn{0, 0, 0, 0.0};
-    TaskMeta mnn{0, 0, 0, 0};
     unsigned bitsn = 0;
+    Src8 snn{{0, 0, 0, 0}, {0, 0, 0, 0}};
+    TaskMeta mnnn{0, 0, 0, 0};
     if (tn < te) {
-      sn = load_src8(p, mn, lane, pol);
+      issue_gathers8<ASYNC>(mn, sn, lane, fresh_below, prev, cur, v);
       rpn = load_rowpre(p, mn, lane);
       bitsn = load_bits8(p, tn, lane);
-      if (tn + nwarps < te) mnn = load_meta(p, tn + nwarps);
+      if (tn + nwarps < te) {
+        snn = load_src8(p, mnn, lane, pol);
+        if (tn + 2 * nwarps < te) mnnn = load_meta(p, tn + 2 * nwarps);
+      }
     }
-    process_task<ASYNC>(p, t, m, v, bits, rp, cur, ws, lane, lmax, lsum);
+    task_finish<ASYNC>(p, t, m, acc, bits, rp, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;
-    sx = sn;
     rp = rpn;
     bits = bitsn;
     mn = mnn;
+    sn = snn;
+    mnn = mnnn;
   }
 }
 
 // ------------------------------------------------------ persistent solver
 // ASYNC=false: Jacobi (nwaves == 1, EC) or wave-lockstep Gauss-Seidel.
 // ASYNC=true : block-asynchronous Gauss-Seidel, in-place contributions.
-template <bool ASYNC>
-#ifndef FPR_MIN_BLOCKS
-#define FPR_MIN_BLOCKS 3
-#endif
-__global__ void __launch_bounds__(kBlockThreads, FPR_MIN_BLOCKS) solve_kernel(SolveParams p) {
+template <bool ASYNC, int BT, int MB>
+__global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
+  constexpr int kWPB = BT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double sred[2 * kWarpsPerBlock];
+  __shared__ double sred[2 * kWPB];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem)[wib];
-  const int gwarp = blockIdx.x * kWarpsPerBlock + wib;
-  const int nwarps = gridDim.x * kWarpsPerBlock;
+  const int gwarp = blockIdx.x * kWPB + wib;
+  const int nwarps = gridDim.x * kWPB;
   const unsigned long long pol = evict_first_policy();
   int par = p.parity0;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.iter_ns[0] = globaltimer();
@@ -720,17 +754,28 @@ cudaError_t launch_init(const DevGraph& g, double* pr, double* contrib, cudaStre
   return cudaGetLastError();
 }
 
+struct SolveShape {
+  const void* fn;
+  int block;
+  int smem;
+};
+
+static SolveShape solve_shape(int engine) {
+  if (engine == kFused)
+    return {(const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB>, FPR_ASYNC_BLOCK,
+            solve_smem_bytes<FPR_ASYNC_BLOCK>()};
+  return {(const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB>, FPR_EC_BLOCK,
+          solve_smem_bytes<FPR_EC_BLOCK>()};
+}
+
+int solve_block_threads(int engine) { return solve_shape(engine).block; }
+
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
+  const SolveShape sh = solve_shape(engine);
+  cudaError_t e = cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  for (const void* fn : {(const void*)solve_kernel<true>, (const void*)solve_kernel<false>}) {
-    cudaError_t a = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemBytes);
-    if (a != cudaSuccess) return a;
-  }
-  cudaError_t e = engine == kFused
-                      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<true>,
-                                                                      kBlockThreads, kSolveSmemBytes)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<false>,
-                                                                      kBlockThreads, kSolveSmemBytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.block, sh.smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   *grid_out = per_sm * num_sms;
@@ -738,10 +783,10 @@ cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
 }
 
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s) {
+  const SolveShape sh = solve_shape(engine);
   SolveParams copy = p;
   void* args[] = {&copy};
-  const void* fn = engine == kFused ? (const void*)solve_kernel<true> : (const void*)solve_kernel<false>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, kSolveSmemBytes, s);
+  return cudaLaunchCooperativeKernel(sh.fn, dim3(grid), dim3(sh.block), args, sh.smem, s);
 }
 
 cudaError_t launch_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound,

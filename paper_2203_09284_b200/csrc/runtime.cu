@@ -614,7 +614,8 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     return fail(FPR_B200_ECUDA, "fpr_b200: internal error (EC wave schedule)");
   }
   const int variant = engine == kFused ? 1 : 0;
-  const int64_t want = (h->part.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int wpb = solve_block_threads(engine) / 32;
+  const int64_t want = (h->part.ntasks + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
 
 
@@ -813,7 +814,8 @@ int fpr_b200_part_sweep(fpr_b200_graph* h, int engine, const fpr_config* cfg,
   const Waves* wv = nullptr;
   if ((rc = get_waves(h, 1u, &wv))) return rc;
   const int variant = engine == kFused ? 1 : 0;
-  const int64_t want = (h->part.ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int wpb = solve_block_threads(engine) / 32;
+  const int64_t want = (h->part.ntasks + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
   const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
   SolveParams p{};
