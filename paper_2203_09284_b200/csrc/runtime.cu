@@ -254,8 +254,12 @@ int get_waves(fpr_b200_graph* h, uint32_t wave_count, const Waves** out) {
   const int64_t items = (int64_t)h->g.n + h->g.m;
   uint32_t S = wave_count;
   if (S == 0) {
-    int64_t want = (items + (1 << 22) - 1) >> 22;
-    S = (uint32_t)std::min<int64_t>(64, std::max<int64_t>(8, want));
+    // Auto: one wave per ~16M items keeps the per-wave barrier + pipeline
+    // refill (~10 us) near 10% of a sweep; 2..16 waves recover most of the
+    // Gauss-Seidel gain (RMAT s20: 1/2/4/8/16 waves -> 69/60/52/48/46 sweeps,
+    // fused_seq 45).
+    const int64_t want = (items + (1 << 24) - 1) >> 24;
+    S = (uint32_t)std::min<int64_t>(16, std::max<int64_t>(2, want));
   }
   auto it = h->waves.find(S);
   if (it != h->waves.end()) {
