@@ -203,6 +203,8 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the multi-GPU partitioned path even at N=1 (NCCL world of 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -216,15 +218,22 @@ def main() -> None:
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    if ws > 1 or args.partitioned:
+        import os as _os
+
         import torch.distributed as dist
 
+        if ws == 1:
+            _os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            _os.environ.setdefault("MASTER_PORT", "29531")
+            _os.environ.setdefault("RANK", "0")
+            _os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         run_multi(args, fb, dist, ws, rank, local)
         dist.destroy_process_group()
         return
     stream = torch.cuda.current_stream()
-    sptr = stream.cuda_stream
+    sptr = fb.torch_stream_handle()
 
     dg = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
     n, m = dg.n, dg.m
@@ -330,7 +339,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
 
     from paper_2203_09284_b200.dist import B200Part, TorchExchange, solve_partitioned
 
-    sptr = torch.cuda.current_stream().cuda_stream
+    sptr = fb.torch_stream_handle()
     full = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
     n, m = full.n, full.m
     part = B200Part(full, ws, rank, device=local, stream=sptr)
@@ -339,7 +348,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     dev = f"cuda:{local}"
     for _ in range(args.warmup):
-        r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev)
+        r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=False)
     iters = r.iterations
 
     def barrier():
@@ -352,14 +361,14 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev)
+            r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=False)
             assert r.iterations == iters
         ev1.record(stream)
         barrier()
     t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    fr = solve_partitioned(part, ex, fb.ENGINE_FUSED, cfg, device=dev)
+    fr = solve_partitioned(part, ex, fb.ENGINE_FUSED, cfg, device=dev, want_ranks=False)
     if rank == 0:
         line = {
             "metric": "GTEPS/iter (ec_b200 time-to-converge, config 2)",
@@ -396,7 +405,7 @@ def e2e_leg(fb, g, device, args, iters) -> dict:
     errs_t = torch.empty(10000, dtype=torch.float64, pin_memory=True)
     view = fb._GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data, od.ctypes.data)
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)._c()
-    opts = fb._options(device=device)
+    opts = fb._options(device=device, stream=fb.torch_stream_handle())
     res = fb._Result()
     L = fb.lib()
 

@@ -219,6 +219,20 @@ _B200_ENGINE = {EngineKind.EcB200: ENGINE_EC, EngineKind.FusedB200: ENGINE_FUSED
                 EngineKind.FusedLockstepB200: ENGINE_FUSED_LOCKSTEP}
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
+def torch_stream_handle() -> int:
+    """cudaStream_t of torch's current stream for fpr_b200_options.stream.
+    torch reports its default stream as 0, which the C ABI reads as "make a
+    library stream"; map it to cudaStreamLegacy so the library's work is
+    ordered with torch's kernels, events and NCCL collectives."""
+    import torch
+
+    h = torch.cuda.current_stream().cuda_stream
+    return h if h else CUDA_STREAM_LEGACY
+
+
 def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None) -> _Options:
     o = _Options()
     lib().fpr_b200_options_init(C.byref(o))

@@ -168,8 +168,9 @@ def _reduce_pairs(pairs: np.ndarray) -> tuple[float, float]:
 
 
 def solve_partitioned(local, exchange: TorchExchange, engine: int, cfg: PageRankConfig,
-                      norm: int = NORM_LINF, device="cuda") -> PartResult:
-    """Run `engine` to convergence on this rank's part (one process per GPU)."""
+                      norm: int = NORM_LINF, device="cuda", want_ranks: bool = True) -> PartResult:
+    """Run `engine` to convergence on this rank's part (one process per GPU).
+    want_ranks=False leaves the part's ranks on the device (benchmarking)."""
     import torch
 
     if engine not in (ENGINE_EC, ENGINE_FUSED):
@@ -197,7 +198,8 @@ def solve_partitioned(local, exchange: TorchExchange, engine: int, cfg: PageRank
             break
     crit = res.l1_errors[-1] if norm == NORM_L1 else res.errors[-1]
     res.converged = crit <= cfg.threshold
-    res.ranks = local.ranks()
+    if want_ranks:
+        res.ranks = local.ranks()
     return res
 
 

@@ -17,7 +17,7 @@ def test_partitioned_ec_matches_oracle(oracle, P):
     n, s, d = oracle.generate_rmat(16, 16, seed=1)
     g = oracle.build_csr(n, s, d)
     ref = oracle.pagerank_ec(g, threshold=1e-10)
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = fb.torch_stream_handle()
     with fb.DeviceGraph.from_graph(fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)) as full:
         parts = [B200Part(full, P, r, stream=stream) for r in range(P)]
     np.testing.assert_array_equal(parts[0].bounds, partition_bounds(g.in_start, P))
