@@ -369,6 +369,9 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
     fr = solve_partitioned(part, ex, fb.ENGINE_FUSED, cfg, device=dev, want_ranks=False)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_multi(args, fb, dist, part, ex, cfg, dev, local, iters)
     if rank == 0:
         line = {
             "metric": "GTEPS/iter (ec_b200 time-to-converge, config 2)",
@@ -382,11 +385,59 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
                        "slice": part.slice, "l2": "inputs larger than L2; no flush"},
             "time_to_converge_ms": ms_step,
             "fused": {"engine": "fused_b200", "iterations": fr.iterations},
-            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "roofline": None, "cpu_baseline": None, "e2e": e2e,
             "gpu_launches": int(args.steps * iters), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     part.close()
+
+
+def e2e_multi(args, fb, dist, part, ex, cfg, dev, local, iters) -> dict:
+    """N GPUs end to end through the public API: every rank uploads the pinned
+    host CSR (fpr_b200_graph_create), partitions it on its device, solves with
+    the NCCL exchange and downloads its rank slice.  Max over ranks."""
+    import torch
+
+    from paper_2203_09284_b200.dist import B200Part, solve_partitioned
+
+    g = None
+    with fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local,
+                                         stream=fb.torch_stream_handle()) as dg:
+        g = dg.download()
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
+        v = t.numpy().view(np.uint64)
+        v[:] = a
+        return t, v
+
+    keep = [pinned(g.in_start), pinned(g.in_src), pinned(g.out_degree)]
+    hg = fb.Graph(g.n, g.m, keep[0][1], keep[1][1], keep[2][1])
+    ws, rank = dist.get_world_size(), dist.get_rank()
+
+    def call():
+        with fb.DeviceGraph.from_graph(hg, device=local, stream=fb.torch_stream_handle()) as full_g:
+            p = B200Part(full_g, ws, rank, device=local, stream=fb.torch_stream_handle())
+        r = solve_partitioned(p, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=True)
+        p.close()
+        return r
+
+    call()
+    steps = max(3, min(args.steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = call()
+    torch.cuda.synchronize()
+    t = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    h2d = 8 * (g.n + 1) + 8 * g.m + 8 * g.n
+    d2h = 8 * len(r.ranks) + 16 * ws * r.iterations
+    return {"value": g.m * r.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "api": "fpr_b200_graph_create + fpr_b200_graph_partition + fpr_b200_part_* (pinned host u64 CSR, per rank)"}
 
 
 def e2e_leg(fb, g, device, args, iters) -> dict:
