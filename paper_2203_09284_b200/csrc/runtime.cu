@@ -83,6 +83,82 @@ void release_staging(HostStaging* s) {
   g_staging_free.push_back(s);
 }
 
+// Pinned ring for uploads from PAGEABLE host memory (std::vector graphs of
+// the C++ drop-in): host threads narrow u64 -> int32 (range-checking as they
+// go) into a pinned buffer while the previous buffer's DMA is in flight, so
+// the link carries 4 B per edge instead of 8.  One ring per device, reused.
+constexpr int kRingBufs = 4;
+constexpr int64_t kRingBytes = 32ll << 20;
+struct UploadRing {
+  int device = -1;
+  void* buf[kRingBufs] = {};
+  cudaEvent_t done[kRingBufs] = {};
+  bool used[kRingBufs] = {};
+  std::mutex mu;
+};
+std::mutex g_ring_mu;
+std::vector<UploadRing*> g_rings;
+
+UploadRing* get_ring(int device) {
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  for (auto* r : g_rings)
+    if (r->device == device) return r;
+  auto* r = new UploadRing;
+  r->device = device;
+  for (int k = 0; k < kRingBufs; ++k) {
+    if (cudaMallocHost(&r->buf[k], kRingBytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r->done[k], cudaEventDisableTiming) != cudaSuccess) {
+      for (int j = 0; j <= k; ++j) {
+        if (r->buf[j]) cudaFreeHost(r->buf[j]);
+        if (r->done[j]) cudaEventDestroy(r->done[j]);
+      }
+      delete r;
+      return nullptr;
+    }
+  }
+  g_rings.push_back(r);
+  return r;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Uploads `count` u64 values as T (int32 narrowed + range-checked against
+// `bound`, or int64 verbatim) through the ring on stream s.  Returns false on
+// an out-of-range value; *e receives CUDA errors.
+template <class T>
+bool ring_upload(UploadRing* r, const uint64_t* src, T* dst, int64_t count, uint64_t bound,
+                 cudaStream_t s, int& k, cudaError_t* e) {
+  const int64_t per = kRingBytes / (int64_t)sizeof(T);
+  bool ok = true;
+  for (int64_t off = 0; off < count && *e == cudaSuccess; off += per) {
+    const int64_t cnt = std::min<int64_t>(per, count - off);
+    if (r->used[k]) *e = cudaEventSynchronize(r->done[k]);
+    if (*e != cudaSuccess) break;
+    T* stage = static_cast<T*>(r->buf[k]);
+    const uint64_t* in = src + off;
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t i = 0; i < cnt; ++i) {
+      const uint64_t x = in[i];
+      if (sizeof(T) == 4) bad |= x >= bound ? 1 : 0;
+      stage[i] = (T)x;
+    }
+    ok = ok && !bad;
+    *e = cudaMemcpyAsync(dst + off, stage, cnt * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (*e == cudaSuccess) *e = cudaEventRecord(r->done[k], s);
+    r->used[k] = true;
+    k = (k + 1) % kRingBufs;
+  }
+  return ok;
+}
+
 struct Waves {
   int32_t nwaves = 0;
   int32_t* d_task = nullptr;
@@ -380,12 +456,28 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
   unsigned int* bad = nullptr;
   if ((rc = dalloc_n(h, &bad, 1))) return bail(rc);
   cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream);
-  // u64 -> int32 through two device staging buffers: chunk i is copied on the
-  // copy stream while chunk i-1 is narrowed (and range-checked) on the main one.
+  const bool pinned = g.n > 0 && is_pinned(v->in_start) && (g.m == 0 || is_pinned(v->in_src)) &&
+                      is_pinned(v->out_degree);
+  if (e == cudaSuccess && g.n > 0 && !pinned) {
+    // Pageable source: host-side narrowing through the pinned ring.
+    UploadRing* ring = get_ring(h->device);
+    if (!ring) return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
+    std::lock_guard<std::mutex> lk(ring->mu);
+    int k = 0;
+    bool ok = ring_upload<int64_t>(ring, v->in_start, g.row, (int64_t)g.n + 1, 0, h->stream, k, &e);
+    ok = ring_upload<int32_t>(ring, v->in_src, g.src, g.m, v->n, h->stream, k, &e) && ok;
+    ok = ring_upload<int32_t>(ring, v->out_degree, g.outdeg, g.n, v->n, h->stream, k, &e) && ok;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // ring reusable once we return
+    if (e == cudaSuccess && !ok)
+      return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_src/out_degree value outside [0," +
+                                            std::to_string(v->n) + ")"));
+  }
+  // Pinned source: u64 -> int32 through two device staging buffers: chunk i is
+  // copied on the copy stream while chunk i-1 is narrowed on the main one.
   const int64_t chunk = 1 << 24;
   uint64_t* stage = nullptr;
   const int64_t need = std::min<int64_t>(chunk, std::max<int64_t>(g.m, g.n));
-  if (e == cudaSuccess && need > 0) {
+  if (e == cudaSuccess && need > 0 && pinned) {
     if ((rc = dalloc_n(h, &stage, 2 * need))) return bail(rc);
     if (!h->copy_stream) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     for (auto& ev : h->up_ev)
