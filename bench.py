@@ -170,8 +170,9 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_leg(g_host) -> dict:
-    """Rank 0, N=1: the reference's ec_par, all host threads, one full solve."""
+def cpu_baseline_leg(g_host, gpu_ranks=None, gpu_iters=None) -> dict:
+    """Rank 0, N=1: the reference's ec_par, all host threads, one full solve.
+    Its converged vector doubles as a live parity check of the GPU result."""
     from oracle import Graph as OGraph
     from oracle import Oracle, load_reference
 
@@ -184,9 +185,13 @@ def cpu_baseline_leg(g_host) -> dict:
             r = ref.run(og, "ec_par", DAMPING, THRESHOLD, 10000, threads, handle=h)
         finally:
             ref.destroy(h)
-        return {"value": og.m * r.iterations / r.seconds / 1e9, "unit": "GTEPS", "cores": threads,
-                "kind": "reference", "iterations": r.iterations, "seconds": r.seconds,
-                "sample": "1 full pagerank_ec_par solve of config 2 (oracle/_ref, -O3, T=nproc)"}
+        out = {"value": og.m * r.iterations / r.seconds / 1e9, "unit": "GTEPS", "cores": threads,
+               "kind": "reference", "iterations": r.iterations, "seconds": r.seconds,
+               "sample": "1 full pagerank_ec_par solve of config 2 (oracle/_ref, -O3, T=nproc)"}
+        if gpu_ranks is not None:
+            out["parity"] = {"ec_b200_vs_reference_max_rel": float(np.max(np.abs(gpu_ranks - r.ranks) / r.ranks)),
+                             "iterations_equal": bool(gpu_iters == r.iterations), "tolerance": 1e-12}
+        return out
     o = Oracle()
     t0 = time.perf_counter()
     r = o.pagerank_ec(og, DAMPING, THRESHOLD, 2)
@@ -299,7 +304,8 @@ def main() -> None:
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         if g_host is None:
             g_host = dg.download()
-        cpu = cpu_baseline_leg(g_host)
+        final = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True, copy_trace=False)
+        cpu = cpu_baseline_leg(g_host, final.ranks.values, final.trace.iterations)
 
     if rank == 0:
         line = {
