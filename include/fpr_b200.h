@@ -77,11 +77,15 @@ typedef struct fpr_config {
   uint32_t thread_count;   /* validated, ignored on the GPU */
 } fpr_config;
 
+#define FPR_B200_OPT_REORDER 1u /* renumber vertices by descending out-degree inside
+                                  the library (locality for contrib gathers); ranks
+                                  and traces are reported in the caller's ids */
+
 typedef struct fpr_b200_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */
   int32_t norm;         /* FPR_B200_NORM_* stop rule */
   uint32_t wave_count;  /* lockstep engine: waves per sweep (0 = auto) */
-  uint32_t reserved0;
+  uint32_t flags;       /* FPR_B200_OPT_* */
   void* stream;         /* cudaStream_t to run on; NULL = library stream */
 } fpr_b200_options;
 
@@ -128,7 +132,8 @@ int fpr_b200_graph_generate(const fpr_gen_params* params, const fpr_b200_options
                             fpr_b200_graph** out);
 void fpr_b200_graph_destroy(fpr_b200_graph* g);
 int fpr_b200_graph_info(const fpr_b200_graph* g, uint64_t* n, uint64_t* m, uint64_t* ntasks);
-/* Downloads the CSR as fpr::Graph arrays (u64). */
+/* Downloads the CSR as fpr::Graph arrays (u64).  EINVAL for a graph created
+ * with FPR_B200_OPT_REORDER (its resident CSR is in internal ids). */
 int fpr_b200_graph_download_csr(const fpr_b200_graph* g, uint64_t* in_start, uint64_t* in_src,
                                 uint64_t* out_degree);
 /* Checks build_csr's invariants on the device (graph.hpp:20-30): *flags = 0

@@ -38,6 +38,7 @@ OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 5
 ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2
 NORM_LINF, NORM_L1 = 0, 1
 GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
+OPT_REORDER = 1  # FPR_B200_OPT_REORDER
 
 
 class B200Error(RuntimeError):
@@ -59,7 +60,7 @@ class _Config(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("norm", C.c_int32), ("wave_count", C.c_uint32),
-                ("reserved0", C.c_uint32), ("stream", C.c_void_p)]
+                ("flags", C.c_uint32), ("stream", C.c_void_p)]
 
 
 class _Result(C.Structure):
@@ -233,12 +234,13 @@ def torch_stream_handle() -> int:
     return h if h else CUDA_STREAM_LEGACY
 
 
-def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None) -> _Options:
+def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False) -> _Options:
     o = _Options()
     lib().fpr_b200_options_init(C.byref(o))
     o.device = device
     o.norm = norm
     o.wave_count = wave_count
+    o.flags = OPT_REORDER if reorder else 0
     o.stream = stream
     return o
 
@@ -259,43 +261,43 @@ class DeviceGraph:
 
     # -- construction ---------------------------------------------------
     @classmethod
-    def from_graph(cls, g: Graph, device=-1, norm=NORM_LINF, wave_count=0, stream=None):
+    def from_graph(cls, g: Graph, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False):
         ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
         v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
         h = C.c_void_p()
-        _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream)),
+        _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream, reorder)),
                                            C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
-    def _generate(cls, gp, device, norm, wave_count, stream):
+    def _generate(cls, gp, device, norm, wave_count, stream, reorder=False):
         h = C.c_void_p()
-        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream)),
+        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream, reorder)),
                                              C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
     def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None,
-                      relabel_bfs=False, bfs_root=0):
+                      relabel_bfs=False, bfs_root=0, reorder=False):
         """build_csr(generate_rmat(p)) on the device; relabel_bfs=True gives
         BASELINE config 3's crawl order (BFS from bfs_root over out-edges)."""
         gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed,
                         0, 0.0, 0, int(relabel_bfs), 0, bfs_root)
-        return cls._generate(gp, device, norm, wave_count, stream)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder)
 
     @classmethod
     def generate_uniform(cls, n: int, avg_degree: int, seed: int, device=-1, norm=NORM_LINF,
-                         wave_count=0, stream=None):
+                         wave_count=0, stream=None, reorder=False):
         """build_csr(testutil::random_sparse(n, avg_degree, SplitMix64(seed)))."""
         gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, n, avg_degree, seed)
-        return cls._generate(gp, device, norm, wave_count, stream)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder)
 
     @classmethod
     def generate_chunglu(cls, n: int, draws: int, seed: int, alpha: float = 2.1, kmax: int = 1_000_000,
-                         device=-1, norm=NORM_LINF, wave_count=0, stream=None):
+                         device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False):
         """BASELINE config 4 (definition: DESIGN.md §4.1; oracle fo_generate_chunglu)."""
         gp = _GenParams(GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, n, 0, seed, draws, alpha, kmax)
-        return cls._generate(gp, device, norm, wave_count, stream)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder)
 
     def validate(self) -> int:
         """0 iff the resident CSR satisfies build_csr's invariants (device check)."""

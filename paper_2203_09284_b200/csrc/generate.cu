@@ -616,6 +616,58 @@ cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_o
   return e;
 }
 
+// Locality reorder (opt-in, FPR_B200_OPT_REORDER): vertices renumbered by
+// descending out-degree (ties by id) -- the gather frequency of contrib[s] is
+// out_degree(s), so hot contributions share sectors and stay L2-resident.
+// Returns the new CSR in `out` and new_of_old (device, n int32) in *perm.
+__global__ void degree_key_kernel(const int32_t* outdeg, int32_t n, uint64_t* keys, int32_t* ids) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    keys[i] = ((uint64_t)(uint32_t)(INT32_MAX - outdeg[i]) << 32) | (uint32_t)i;
+    ids[i] = (int32_t)i;
+  }
+}
+
+cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, cudaStream_t st,
+                              const char** msg) {
+  *msg = nullptr;
+  *perm = nullptr;
+  cudaError_t e = cudaSuccess;
+  const int32_t n = g.n;
+  uint64_t* k1 = nullptr;
+  uint64_t* k2 = nullptr;
+  int32_t* i1 = nullptr;
+  int32_t* i2 = nullptr;
+  int32_t* p = nullptr;
+  int32_t* dst_of_edge = nullptr;
+  void* temp = nullptr;
+  size_t tb = 0;
+  GK(cudaMallocAsync(&k1, n * sizeof(uint64_t), st));
+  GK(cudaMallocAsync(&k2, n * sizeof(uint64_t), st));
+  GK(cudaMallocAsync(&i1, n * sizeof(int32_t), st));
+  GK(cudaMallocAsync(&i2, n * sizeof(int32_t), st));
+  GK(cudaMallocAsync(&p, n * sizeof(int32_t), st));
+  degree_key_kernel<<<blocks_for(n), 256, 0, st>>>(g.outdeg, n, k1, i1);
+  GK(cudaGetLastError());
+  GK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, i1, i2, (int64_t)n, 0, 64, st));
+  GK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));
+  GK(cub::DeviceRadixSort::SortPairs(temp, tb, k1, k2, i1, i2, (int64_t)n, 0, 64, st));
+  invert_perm_kernel<<<blocks_for(n), 256, 0, st>>>(i2, (uint64_t)n, p);
+  GK(cudaGetLastError());
+  GK(cudaMallocAsync(&dst_of_edge, std::max<int64_t>(g.m, 1) * sizeof(int32_t), st));
+  row_of_edge_kernel<<<blocks_for(n), 256, 0, st>>>(g.row, n, dst_of_edge);
+  GK(cudaGetLastError());
+  GK(build_csr_from(CsrSource{g.src, dst_of_edge, p, 0}, (uint64_t)g.m, (uint64_t)n, out, st, msg));
+  if (*msg) goto out;
+  *perm = p;
+  p = nullptr;
+out:
+  for (void* q : {(void*)k1, (void*)k2, (void*)i1, (void*)i2, (void*)p, (void*)dst_of_edge, temp})
+    if (q) cudaFreeAsync(q, st);
+  cudaStreamSynchronize(st);
+  return e;
+}
+
 #undef GK
 
 }  // namespace fprb

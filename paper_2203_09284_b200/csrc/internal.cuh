@@ -106,6 +106,8 @@ cudaError_t launch_part_extract(const DevGraph& g, const int64_t* bounds, uint32
 cudaError_t launch_part_init(const DevGraph& g, double init, double* pr, double* contrib_slice,
                              cudaStream_t s);
 cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* bad, cudaStream_t s);
+cudaError_t launch_gather_ranks(const double* pr, const int32_t* new_of_old, int32_t n, double* out,
+                               cudaStream_t s);
 cudaError_t launch_widen(const int64_t* row, const int32_t* ids32, uint64_t* out_row,
                          uint64_t* out_ids, int64_t nrow, int64_t nids, cudaStream_t s);
 
@@ -127,6 +129,10 @@ struct GenRequest {
 // Builds row/src/outdeg on the device (allocates them into g).  Returns a
 // cudaError_t; *msg receives a static description on non-CUDA failures.
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t s, const char** msg);
+// Locality reorder by descending out-degree: new CSR in `out` (allocated on
+// stream s), *perm = device new_of_old (n int32, caller frees).
+cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, cudaStream_t s,
+                              const char** msg);
 // BFS discovery order of g (config-3 relabel) into a host buffer of n int32.
 cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_out,
                               cudaStream_t s, const char** msg);

@@ -827,6 +827,19 @@ cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* b
   return cudaGetLastError();
 }
 
+__global__ void gather_ranks_kernel(const double* pr, const int32_t* new_of_old, int32_t n,
+                                    double* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = pr[new_of_old[i]];
+}
+
+cudaError_t launch_gather_ranks(const double* pr, const int32_t* new_of_old, int32_t n, double* out,
+                               cudaStream_t s) {
+  gather_ranks_kernel<<<grid_for(n), 256, 0, s>>>(pr, new_of_old, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_widen(const int64_t* row, const int32_t* ids32, uint64_t* out_row,
                          uint64_t* out_ids, int64_t nrow, int64_t nids, cudaStream_t s) {
   widen_kernel<<<grid_for(nrow > nids ? nrow : nids), 256, 0, s>>>(row, ids32, out_row, out_ids,

@@ -203,6 +203,9 @@ struct fpr_b200_graph {
   std::vector<void*> allocs;
   // multi-GPU part (fpr_b200_graph_partition); nparts == 1 for a whole graph
   uint32_t nparts = 1, part_id = 0;
+  uint32_t flags = 0;
+  int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
+  double* ranks_tmp = nullptr;    // reordered ranks gathered back to caller order
   uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
 
@@ -281,6 +284,7 @@ int open_handle(const fpr_b200_options* opts, fpr_b200_graph** out) {
   }
   h->norm = o.norm;
   h->wave_count = o.wave_count;
+  h->flags = o.flags;
   for (auto& ev : h->ev) CK(cudaEventCreate(&ev));
   h->hs = acquire_staging();
   if (!h->hs) return fail(FPR_B200_ENOMEM, "fpr_b200: pinned host staging allocation failed");
@@ -292,8 +296,24 @@ int open_handle(const fpr_b200_options* opts, fpr_b200_graph** out) {
   return FPR_B200_OK;
 }
 
-// Partition + solver state, common to create/generate.
+// Partition + solver state, common to create/generate (after the optional
+// locality reorder, which swaps in the renumbered CSR).
 int finish_graph(fpr_b200_graph* h) {
+  if ((h->flags & FPR_B200_OPT_REORDER) && h->g.n > 1) {
+    DevGraph re;
+    int32_t* perm = nullptr;
+    const char* msg = nullptr;
+    CK(reorder_by_degree(h->g, re, &perm, h->stream, &msg));
+    if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200 reorder: ") + msg);
+    h->allocs.push_back(re.row);
+    h->allocs.push_back(re.src);
+    h->allocs.push_back(re.outdeg);
+    h->allocs.push_back(perm);
+    h->g = re;  // the original arrays stay owned by allocs until destroy
+    h->new_of_old = perm;
+    int rc2 = dalloc_n(h, &h->ranks_tmp, h->g.n);
+    if (rc2) return rc2;
+  }
   DevGraph& g = h->g;
   Partition& p = h->part;
   const int64_t items = (int64_t)g.n + g.m;
@@ -608,6 +628,9 @@ int fpr_b200_graph_download_csr(const fpr_b200_graph* hc, uint64_t* in_start, ui
                                 uint64_t* out_degree) {
   auto* h = const_cast<fpr_b200_graph*>(hc);
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: null graph");
+  if (h->new_of_old)
+    return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: graph was created with "
+                                 "FPR_B200_OPT_REORDER (resident CSR uses internal ids)");
   CK(cudaSetDevice(h->device));
   const DevGraph& g = h->g;
   const int64_t chunk = 1 << 24;
@@ -801,8 +824,14 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     parity ^= (int)(done & 1);
     if (stop) break;
   }
-  if (ranks_out)
-    CK(cudaMemcpyAsync(ranks_out, h->pr, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (ranks_out) {
+    const double* src = h->pr;
+    if (h->new_of_old) {  // back to the caller's vertex ids
+      CK(launch_gather_ranks(h->pr, h->new_of_old, g.n, h->ranks_tmp, h->stream));
+      src = h->ranks_tmp;
+    }
+    CK(cudaMemcpyAsync(ranks_out, src, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
   CK(cudaStreamSynchronize(h->stream));
   if (result) {
     result->iterations = total;

@@ -192,3 +192,22 @@ def test_upload_download_roundtrip(config1):
     np.testing.assert_array_equal(back.in_start, g.in_start)
     np.testing.assert_array_equal(back.in_src, g.in_src)
     np.testing.assert_array_equal(back.out_degree, g.out_degree)
+
+
+def test_reorder_option_preserves_results(config1, oracle):
+    """FPR_B200_OPT_REORDER renumbers vertices internally by out-degree; EC
+    results come back in the caller's ids, per-iteration within 1e-12, with
+    the same iteration count (Jacobi is relabel-invariant)."""
+    rec, g, dg = config1
+    ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
+    with fb.DeviceGraph.from_graph(to_fb(g), reorder=True) as d2:
+        r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
+        assert rel(r1.ranks.values, ref.history[2]) <= EC_RTOL
+        r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))
+        with pytest.raises(ValueError, match="REORDER"):
+            d2.download()
+    assert r.trace.iterations == ref.iterations
+    assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
+    xstar = oracle.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
+    assert fu.trace.converged and fb.l1_norm(fu.ranks.values, xstar) <= g.n * 1e-10 * 0.85 / 0.15
