@@ -137,4 +137,7 @@ cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, 
 cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_out,
                               cudaStream_t s, const char** msg);
 
+// host_narrow.cpp: out[i] = (int32)in[i]; true if any in[i] >= bound.
+bool host_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound);
+
 }  // namespace fprb

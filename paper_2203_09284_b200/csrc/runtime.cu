@@ -7,9 +7,11 @@
 // non-convergence as a result rather than an error.  There is no CPU
 // fallback: every numeric step runs in the kernels of kernels.cu/generate.cu.
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -88,6 +90,7 @@ void release_staging(HostStaging* s) {
 // go) into a pinned buffer while the previous buffer's DMA is in flight, so
 // the link carries 4 B per edge instead of 8.  One ring per device, reused.
 constexpr int kRingBufs = 4;
+constexpr double kHostNarrowShare = 0.9;  // measured default, see host_narrow_share()
 constexpr int64_t kRingBytes = 32ll << 20;
 struct UploadRing {
   int device = -1;
@@ -120,6 +123,17 @@ UploadRing* get_ring(int device) {
   return r;
 }
 
+// Share of a PINNED in_src that host threads narrow (the rest is DMA'd raw
+// and narrowed on the device).  Measured on the 16-core B200 hosts (config 2
+// upload, scripts/narrow_sweep.py): 0 -> 11.2 ms, 0.7 -> 8.5, 0.9 -> 7.6,
+// 1.0 -> 7.7 (host-bound).  Fewer host threads narrow proportionally less.
+// FPR_B200_HOST_NARROW overrides (0..1).
+double host_narrow_share() {
+  const char* s = std::getenv("FPR_B200_HOST_NARROW");
+  const double x = s ? std::atof(s) : kHostNarrowShare * std::min(1.0, omp_get_max_threads() / 16.0);
+  return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -143,14 +157,12 @@ bool ring_upload(UploadRing* r, const uint64_t* src, T* dst, int64_t count, uint
     if (*e != cudaSuccess) break;
     T* stage = static_cast<T*>(r->buf[k]);
     const uint64_t* in = src + off;
-    int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-    for (int64_t i = 0; i < cnt; ++i) {
-      const uint64_t x = in[i];
-      if (sizeof(T) == 4) bad |= x >= bound ? 1 : 0;
-      stage[i] = (T)x;
+    if constexpr (sizeof(T) == 4) {
+      ok = !host_narrow_ids(in, reinterpret_cast<int32_t*>(stage), cnt, bound) && ok;
+    } else {
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < cnt; ++i) stage[i] = (T)in[i];
     }
-    ok = ok && !bad;
     *e = cudaMemcpyAsync(dst + off, stage, cnt * sizeof(T), cudaMemcpyHostToDevice, s);
     if (*e == cudaSuccess) *e = cudaEventRecord(r->done[k], s);
     r->used[k] = true;
@@ -197,6 +209,8 @@ struct fpr_b200_graph {
   double* h_l1 = nullptr;
   unsigned long long* h_ns = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D upload overlapped with narrowing
+  cudaStream_t ring_stream = nullptr;  // host-narrowed share of a pinned upload
+  cudaEvent_t ring_ev = nullptr;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t up_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::map<uint32_t, Waves> waves;
@@ -241,6 +255,8 @@ void destroy_handle(fpr_b200_graph* h) {
   for (auto& e : h->up_ev)
     if (e) cudaEventDestroy(e);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->ring_ev) cudaEventDestroy(h->ring_ev);
+  if (h->ring_stream) cudaStreamDestroy(h->ring_stream);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -507,9 +523,18 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
       int32_t* dst;
       int64_t count;
     };
+    // The link is the bound (8 B per edge raw).  Host threads narrow the
+    // last `host_share` of in_src to 4 B per edge through the pinned ring,
+    // concurrently with the raw DMA of the rest, so the link carries fewer
+    // bytes while both halves finish together (e2e).
+    const int64_t m_host = (int64_t)((double)g.m * host_narrow_share());
+    const int64_t m_dev = g.m - m_host;
+    UploadRing* ring = m_host > 0 ? get_ring(h->device) : nullptr;
+    if (m_host > 0 && !ring)
+      return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
     std::vector<Piece> pieces;
-    for (int64_t off = 0; off < g.m; off += chunk)
-      pieces.push_back({v->in_src + off, g.src + off, std::min<int64_t>(chunk, g.m - off)});
+    for (int64_t off = 0; off < m_dev; off += chunk)
+      pieces.push_back({v->in_src + off, g.src + off, std::min<int64_t>(chunk, m_dev - off)});
     for (int64_t off = 0; off < g.n; off += chunk)
       pieces.push_back({v->out_degree + off, g.outdeg + off, std::min<int64_t>(chunk, g.n - off)});
     if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2], h->stream);  // staging allocated
@@ -531,6 +556,20 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
       if (e == cudaSuccess)
         e = launch_narrow_ids(buf, pieces[i].dst, pieces[i].count, v->n, bad, h->stream);
       if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2 + k], h->stream);
+    }
+    if (e == cudaSuccess && m_host > 0) {
+      if (!h->ring_stream) e = cudaStreamCreateWithFlags(&h->ring_stream, cudaStreamNonBlocking);
+      if (e == cudaSuccess && !h->ring_ev) e = cudaEventCreateWithFlags(&h->ring_ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ring_ev, h->stream);  // g.src allocated
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->ring_stream, h->ring_ev, 0);
+      std::lock_guard<std::mutex> lk(ring->mu);
+      int k = 0;
+      bool ok = e == cudaSuccess &&
+                ring_upload<int32_t>(ring, v->in_src + m_dev, g.src + m_dev, m_host, v->n, h->ring_stream, k, &e);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ring_ev, h->ring_stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->ring_ev, 0);
+      if (e == cudaSuccess && !ok)
+        e = cudaMemsetAsync(bad, 1, 1, h->stream);  // reported with the device-side range check
     }
   }
   if (e == cudaSuccess && g.n > 0) e = launch_check_offsets(g.row, g.n, g.m, bad, h->stream);

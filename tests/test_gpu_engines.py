@@ -211,3 +211,36 @@ def test_reorder_option_preserves_results(config1, oracle):
     assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
     xstar = oracle.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
     assert fu.trace.converged and fb.l1_norm(fu.ranks.values, xstar) <= g.n * 1e-10 * 0.85 / 0.15
+
+
+@pytest.mark.parametrize("share", ["0", "0.5", "1"])
+def test_pinned_upload_split(config1, share, monkeypatch):
+    """Pinned sources: the first (1-share) of in_src is DMA'd raw and narrowed
+    on the device, the rest narrowed by host threads (AVX-512) into the
+    pinned ring -- both halves land bit-exactly and both range-check."""
+    import torch
+
+    rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_HOST_NARROW", share)
+
+    def pinned(a):
+        t = torch.empty(len(a), dtype=torch.int64, pin_memory=True)
+        v = t.numpy().view(np.uint64)
+        v[:] = a
+        return t, v
+
+    keep = [pinned(g.in_start), pinned(g.in_src), pinned(g.out_degree)]
+    pg = fb.Graph(g.n, g.m, keep[0][1], keep[1][1], keep[2][1])
+    with fb.DeviceGraph.from_graph(pg) as d2:
+        back = d2.download()
+    np.testing.assert_array_equal(back.in_src, g.in_src)
+    np.testing.assert_array_equal(back.out_degree, g.out_degree)
+    for pos in (0, g.m // 2 + 17, g.m - 1):  # raw half, either side of the split, host half
+        src = keep[1][1]
+        old = int(src[pos])
+        src[pos] = g.n + pos
+        try:
+            with pytest.raises(ValueError, match="outside"):
+                fb.DeviceGraph.from_graph(pg)
+        finally:
+            src[pos] = old
