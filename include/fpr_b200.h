@@ -22,6 +22,9 @@
  *                              (rmat.hpp:42, graph.hpp:35) and
  *                              testutil::random_sparse (tests/test_util.hpp:49)
  *   fpr_b200_graph_download_csr -> the fpr::Graph arrays of build_csr
+ *   fpr_b200_parse_edge_list -> fpr::parse_edge_list     (edge_list.hpp:39-80)
+ *   fpr_b200_graph_from_edge_list
+ *                           -> fpr::build_csr(fpr::parse_edge_list(in))
  *
  * Errors: every function returns a status code; fpr_b200_last_error() gives
  * the thread-local message.  FPR_B200_EINVAL carries the reference's exact
@@ -48,6 +51,7 @@ extern "C" {
 #define FPR_B200_ENCCL 3  /* collective error (multi-GPU path) */
 #define FPR_B200_ENOMEM 4 /* device/host allocation failed */
 #define FPR_B200_ERANGE 5 /* n >= 2^31 (int32 vertex ids) */
+#define FPR_B200_EPARSE 6 /* fpr::ParseError (edge_list.hpp:17-21); see fpr_parse_error */
 
 #define FPR_B200_ENGINE_EC 0             /* Jacobi, bit-deterministic */
 #define FPR_B200_ENGINE_FUSED 1          /* block-asynchronous Gauss-Seidel */
@@ -184,6 +188,33 @@ int fpr_b200_part_init(fpr_b200_graph* g, double* exchange);
 int fpr_b200_part_sweep(fpr_b200_graph* g, int engine, const fpr_config* cfg,
                         const double* exch_read, double* exch_write, double* pair_out);
 int fpr_b200_part_ranks(fpr_b200_graph* g, double* ranks_out);
+
+/* Edge-list text ingest (SNAP style, edge_list.hpp:33-80): '#'/'%' comment
+ * lines and blank/whitespace-only lines skipped, every other line exactly two
+ * decimal u64 tokens separated by ' ', '\t' or '\r'; ids compacted to [0, n)
+ * in first-appearance order.  Parsing and compaction run on the device.
+ * FPR_B200_EPARSE reports the reference's ParseError for the FIRST malformed
+ * line: line = its 1-based number, message = ParseError::what(). */
+#define FPR_B200_PARSE_TOKENS 1    /* "expected two integer tokens" */
+#define FPR_B200_PARSE_BAD_TOKEN 2 /* "bad token '<token>'" (incl. u64 overflow) */
+#define FPR_B200_PARSE_TRAILING 3  /* "trailing characters after edge" */
+typedef struct fpr_parse_error {
+  uint64_t line;       /* 1-based line number (ParseError::line_number); 0 = none */
+  int32_t kind;         /* FPR_B200_PARSE_* ; 0 = none */
+  uint32_t message_len; /* strlen(message) */
+  char message[256];    /* ParseError::what() as a C string, truncated to 255 bytes */
+} fpr_parse_error;
+
+/* fpr::parse_edge_list: *n_out = EdgeSet::n, *m_out = edges.size().  When
+ * edges_out is non-null it receives the m (src, dst) pairs in input order
+ * (2*m u64); edges_cap (in edges) smaller than m returns FPR_B200_ERANGE
+ * after setting *n_out / *m_out.  err may be null. */
+int fpr_b200_parse_edge_list(const char* text, uint64_t len, const fpr_b200_options* opts,
+                             uint64_t* n_out, uint64_t* m_out, uint64_t* edges_out,
+                             uint64_t edges_cap, fpr_parse_error* err);
+/* build_csr(parse_edge_list(text)) into a resident graph handle. */
+int fpr_b200_graph_from_edge_list(const char* text, uint64_t len, const fpr_b200_options* opts,
+                                  fpr_b200_graph** out, fpr_parse_error* err);
 
 /* One-shot drop-in: create from host view, run, copy results, destroy. */
 int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* cfg,

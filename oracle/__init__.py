@@ -64,6 +64,20 @@ class Run:
         return True
 
 
+@dataclass
+class Parsed:
+    """``fpr::EdgeSet`` from ``parse_edge_list`` (edge_list.hpp:39-80), or the
+    ``ParseError`` it threw (error_line > 0, error = what())."""
+
+    n: int
+    edges: np.ndarray  # (m, 2) u64 dense ids, input order
+    error_line: int = 0
+    error: str = ""
+
+
+_PARSE_WHAT = {1: "expected two integer tokens", 3: "trailing characters after edge"}
+
+
 def _ensure_built() -> None:
     if not os.path.exists(ORACLE_SO):
         subprocess.run(["make", "-s", "-C", HERE, os.path.abspath(ORACLE_SO)], check=True)
@@ -99,6 +113,10 @@ class Oracle:
         L.fo_chunglu_weight.restype = _u64
         L.fo_generate_chunglu.argtypes = [_u64, _u64, _f64, _u64, _u64, _u64p, _u64p]
         L.fo_generate_chunglu.restype = C.c_int
+        L.fo_parse_edge_list.argtypes = [C.c_char_p, _u64, C.POINTER(_u64), C.POINTER(_u64), C.c_void_p,
+                                         _u64, C.POINTER(_u64), C.POINTER(C.c_int), C.POINTER(_u64),
+                                         C.POINTER(_u64)]
+        L.fo_parse_edge_list.restype = C.c_int
         L.fo_l1_norm.argtypes = [_u64, _f64p, _f64p]
         L.fo_l1_norm.restype = _f64
         L.fo_linf_norm.argtypes = [_u64, _f64p, _f64p]
@@ -120,6 +138,26 @@ class Oracle:
         dst = np.empty(n * avg_degree, np.uint64)
         k = self.lib.fo_random_sparse(n, avg_degree, seed, src, dst)
         return n, src[:k].copy(), dst[:k].copy()
+
+    def parse_edge_list(self, text: bytes) -> Parsed:
+        """fo_parse_edge_list; the message restates ParseError::what()
+        (edge_list.hpp:17-21, 60-73)."""
+        n, m, line, tok_off, tok_len = _u64(0), _u64(0), _u64(0), _u64(0), _u64(0)
+        kind = C.c_int(0)
+        args = (C.byref(line), C.byref(kind), C.byref(tok_off), C.byref(tok_len))
+        rc = self.lib.fo_parse_edge_list(text, len(text), C.byref(n), C.byref(m), None, 0, *args)
+        if rc == 6:
+            what = (_PARSE_WHAT[kind.value] if kind.value != 2 else
+                    "bad token '" + text[tok_off.value:tok_off.value + tok_len.value].decode("latin-1") + "'")
+            what = f"line {line.value}: {what}".split("\x00")[0]  # what() is a C string
+            return Parsed(0, np.zeros((0, 2), np.uint64), line.value, what)
+        if rc:
+            raise MemoryError("fo_parse_edge_list")
+        edges = np.empty((max(m.value, 1), 2), np.uint64)
+        rc = self.lib.fo_parse_edge_list(text, len(text), C.byref(n), C.byref(m), edges.ctypes.data,
+                                         m.value, *args)
+        assert rc == 0
+        return Parsed(n.value, edges[: m.value].copy())
 
     def build_csr(self, n, src, dst) -> Graph:
         src = np.ascontiguousarray(src, np.uint64)
@@ -231,7 +269,7 @@ class Reference:
 
     def __init__(self, path: str = REF_SO) -> None:
         L = C.CDLL(path)
-        L.ref_last_error.restype = C.c_char_p
+        L.ref_last_error.restype = C.c_void_p
         L.ref_generate_rmat.argtypes = [C.c_uint32, _u64, _f64, _f64, _f64, _f64, _u64, _u64p, _u64p]
         L.ref_random_sparse.argtypes = [_u64, _u64, _u64, _u64p, _u64p]
         L.ref_random_sparse.restype = _u64
@@ -243,10 +281,28 @@ class Reference:
                                     C.POINTER(_u64), C.POINTER(C.c_int), C.POINTER(_f64),
                                     C.POINTER(_f64)]
         L.ref_dense_oracle.argtypes = [_u64, _u64, _u64p, _u64p, _u64p, _f64, _f64, _u64, _f64p]
+        L.ref_last_error_len.restype = _u64
+        L.ref_parse_edge_list.argtypes = [C.c_char_p, _u64, C.POINTER(_u64), C.POINTER(_u64), C.c_void_p,
+                                          _u64, C.POINTER(_u64)]
         self.lib = L
 
+    def parse_edge_list(self, text: bytes) -> Parsed:
+        """fpr::parse_edge_list itself (edge_list.hpp:39-80)."""
+        n, m, line = _u64(0), _u64(0), _u64(0)
+        rc = self.lib.ref_parse_edge_list(text, len(text), C.byref(n), C.byref(m), None, 0, C.byref(line))
+        if rc == 3:
+            what = C.string_at(self.lib.ref_last_error(), self.lib.ref_last_error_len())
+            return Parsed(0, np.zeros((0, 2), np.uint64), line.value, what.decode("latin-1"))
+        if rc:
+            raise RuntimeError(self._err())
+        edges = np.empty((max(m.value, 1), 2), np.uint64)
+        rc = self.lib.ref_parse_edge_list(text, len(text), C.byref(n), C.byref(m), edges.ctypes.data,
+                                          m.value, C.byref(line))
+        assert rc == 0
+        return Parsed(n.value, edges[: m.value].copy())
+
     def _err(self) -> str:
-        return self.lib.ref_last_error().decode()
+        return C.string_at(self.lib.ref_last_error()).decode()
 
     def generate_rmat(self, scale, edge_factor, a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
         draws = edge_factor << scale

@@ -483,3 +483,145 @@ double fo_linf_norm(uint64_t n, const double* a, const double* b) {
   }
   return worst;
 }
+
+/* ------------------------------------------------------------------ ingest */
+/* fpr::parse_edge_list (edge_list.hpp:39-80).  std::getline lines (split on
+ * '\n', a final unterminated line counts); a line is skipped when empty, when
+ * its FIRST byte is '#' or '%' (:50), or when it holds only " \t\r" (:51);
+ * otherwise two tokens delimited by " \t\r" (:55-69), each parsed by
+ * std::from_chars base 10 over the whole token (:25-30: digits only, no sign,
+ * <= 2^64-1), then nothing but " \t\r" (:71-73).  Dense ids in
+ * first-appearance order, src before dst (:41-45, :74-76): an open-addressing
+ * table stands in for the unordered_map. */
+typedef struct {
+  uint64_t* key;
+  uint64_t* val;
+  unsigned char* used;
+  uint64_t cap, size;
+} fo_idmap;
+
+static uint64_t fo_hash(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  return x;
+}
+
+static int fo_idmap_grow(fo_idmap* mp) {
+  fo_idmap nw;
+  nw.cap = mp->cap ? mp->cap * 2 : 1024;
+  nw.size = mp->size;
+  nw.key = (uint64_t*)malloc(nw.cap * sizeof(uint64_t));
+  nw.val = (uint64_t*)malloc(nw.cap * sizeof(uint64_t));
+  nw.used = (unsigned char*)calloc(nw.cap, 1);
+  if (!nw.key || !nw.val || !nw.used) {
+    free(nw.key);
+    free(nw.val);
+    free(nw.used);
+    return FO_ENOMEM;
+  }
+  for (uint64_t i = 0; i < mp->cap; ++i) {
+    if (!mp->used[i]) continue;
+    uint64_t h = fo_hash(mp->key[i]) & (nw.cap - 1);
+    while (nw.used[h]) h = (h + 1) & (nw.cap - 1);
+    nw.used[h] = 1;
+    nw.key[h] = mp->key[i];
+    nw.val[h] = mp->val[i];
+  }
+  free(mp->key);
+  free(mp->val);
+  free(mp->used);
+  *mp = nw;
+  return FO_OK;
+}
+
+static int fo_dense_id(fo_idmap* mp, uint64_t raw, uint64_t* out) {
+  if (2 * (mp->size + 1) > mp->cap && fo_idmap_grow(mp) != FO_OK) return FO_ENOMEM;
+  uint64_t h = fo_hash(raw) & (mp->cap - 1);
+  while (mp->used[h]) {
+    if (mp->key[h] == raw) {
+      *out = mp->val[h];
+      return FO_OK;
+    }
+    h = (h + 1) & (mp->cap - 1);
+  }
+  mp->used[h] = 1;
+  mp->key[h] = raw;
+  mp->val[h] = mp->size;
+  *out = mp->size++;
+  return FO_OK;
+}
+
+static int fo_is_ws(char c) { return c == ' ' || c == '\t' || c == '\r'; }
+
+int fo_parse_edge_list(const char* text, uint64_t len, uint64_t* n, uint64_t* m, uint64_t* edges,
+                       uint64_t cap, uint64_t* err_line, int* err_kind, uint64_t* tok_off,
+                       uint64_t* tok_len) {
+  fo_idmap mp = {0, 0, 0, 0, 0};
+  uint64_t line = 0, ne = 0, pos = 0;
+  int rc = FO_OK;
+  *err_line = 0;
+  *err_kind = 0;
+  *tok_off = *tok_len = 0;
+  while (pos < len) {
+    uint64_t b = pos, e = pos;
+    while (e < len && text[e] != '\n') ++e;
+    pos = e < len ? e + 1 : len;
+    ++line;
+    if (b == e || text[b] == '#' || text[b] == '%') continue;
+    uint64_t i = b;
+    while (i < e && fo_is_ws(text[i])) ++i;
+    if (i == e) continue;
+    uint64_t v[2];
+    int kind = 0;
+    for (int k = 0; k < 2 && !kind; ++k) {
+      while (i < e && fo_is_ws(text[i])) ++i;
+      if (i == e) {
+        kind = 1;
+        break;
+      }
+      const uint64_t s = i;
+      while (i < e && !fo_is_ws(text[i])) ++i;
+      uint64_t x = 0;
+      for (uint64_t j = s; j < i; ++j) {
+        const unsigned d = (unsigned)(unsigned char)text[j] - (unsigned)'0';
+        if (d > 9u || x > (UINT64_MAX - d) / 10u) {
+          kind = 2;
+          *tok_off = s;
+          *tok_len = i - s;
+          break;
+        }
+        x = x * 10u + d;
+      }
+      v[k] = x;
+    }
+    if (!kind) {
+      while (i < e && fo_is_ws(text[i])) ++i;
+      if (i != e) kind = 3;
+    }
+    if (kind) {
+      *err_line = line;
+      *err_kind = kind;
+      rc = FO_EPARSE;
+      break;
+    }
+    uint64_t ds, dd;
+    if (fo_dense_id(&mp, v[0], &ds) != FO_OK || fo_dense_id(&mp, v[1], &dd) != FO_OK) {
+      rc = FO_ENOMEM;
+      break;
+    }
+    if (edges && ne < cap) {
+      edges[2 * ne] = ds;
+      edges[2 * ne + 1] = dd;
+    }
+    ++ne;
+  }
+  *n = mp.size;
+  *m = ne;
+  free(mp.key);
+  free(mp.val);
+  free(mp.used);
+  if (rc == FO_OK && edges && ne > cap) rc = FO_ERANGE;
+  return rc;
+}
+

@@ -98,6 +98,16 @@ int fo_dense_oracle(uint64_t n, const uint64_t* in_start, const uint64_t* in_src
                     uint64_t max_iterations, double* ranks);
 
 double fo_l1_norm(uint64_t n, const double* a, const double* b);
+
+/* fpr::parse_edge_list (edge_list.hpp:39-80) over a text buffer: n = distinct
+ * ids, m = edge lines; edges (2*cap u64, may be NULL) receive the dense
+ * (src, dst) pairs in input order.  FO_EPARSE: the first malformed line's
+ * 1-based number, kind (1 tokens, 2 bad token, 3 trailing) and, for a bad
+ * token, its byte range.  FO_ERANGE: edges != NULL and cap < m. */
+#define FO_EPARSE 6
+int fo_parse_edge_list(const char* text, uint64_t len, uint64_t* n, uint64_t* m, uint64_t* edges,
+                       uint64_t cap, uint64_t* err_line, int* err_kind, uint64_t* tok_off,
+                       uint64_t* tok_len);
 double fo_linf_norm(uint64_t n, const double* a, const double* b);
 
 #ifdef __cplusplus

@@ -11,6 +11,9 @@
 #include <exception>
 #include <string>
 
+#include <sstream>
+
+#include "fpr/edge_list.hpp"
 #include "fpr/graph.hpp"
 #include "fpr/graph_cache.hpp"
 #include "fpr/layout.hpp"
@@ -45,6 +48,7 @@ struct RefGraph {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+uint64_t ref_last_error_len(void) { return g_err.size(); }
 
 int ref_generate_rmat(uint32_t scale, uint64_t ef, double a, double b, double c, double d,
                       uint64_t seed, uint64_t* src, uint64_t* dst) {
@@ -181,6 +185,33 @@ int ref_load_cache(const char* path, uint64_t* n, uint64_t* m, uint64_t* in_star
     if (in_src) std::memcpy(in_src, g.in_src.data(), g.m * sizeof(uint64_t));
     if (out_degree) std::memcpy(out_degree, g.out_degree.data(), g.n * sizeof(uint64_t));
   });
+}
+
+// fpr::parse_edge_list (edge_list.hpp:39-80) over a text buffer.  Returns 0
+// with *n, *m and (when edges != NULL and cap >= m) the 2*m ids; 3 on
+// fpr::ParseError with *line = line_number and ref_last_error() = what().
+int ref_parse_edge_list(const char* text, uint64_t len, uint64_t* n, uint64_t* m, uint64_t* edges,
+                        uint64_t cap, uint64_t* line) {
+  *line = 0;
+  try {
+    std::istringstream in(std::string(text, len));
+    fpr::EdgeSet es = fpr::parse_edge_list(in);
+    *n = es.n;
+    *m = es.edges.size();
+    if (edges && es.edges.size() <= cap)
+      for (size_t i = 0; i < es.edges.size(); ++i) {
+        edges[2 * i] = es.edges[i].src;
+        edges[2 * i + 1] = es.edges[i].dst;
+      }
+    return 0;
+  } catch (const fpr::ParseError& e) {
+    g_err = e.what();
+    *line = e.line_number;
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
 }
 
 }  // extern "C"

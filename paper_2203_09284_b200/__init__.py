@@ -28,13 +28,13 @@ __all__ = [
     "PageRankConfig", "RankVector", "ConvergenceTrace", "PageRankResult", "Graph", "RmatParams",
     "EngineKind", "DeviceGraph", "B200Error", "pagerank_ec_b200", "pagerank_fused_b200",
     "pagerank_fused_lockstep_b200", "run_engine", "l1_norm", "linf_norm", "to_string",
-    "parse_engine", "lib", "LIB_PATH",
+    "parse_engine", "lib", "LIB_PATH", "EdgeSet", "ParseError", "parse_edge_list",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPR_B200_LIB") or os.path.join(HERE, "libfpr_b200.so")
 
-OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 5
+OK, EINVAL, ECUDA, ENCCL, ENOMEM, ERANGE, EPARSE = 0, 1, 2, 3, 4, 5, 6
 ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2
 NORM_LINF, NORM_L1 = 0, 1
 GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
@@ -45,6 +45,15 @@ class B200Error(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
         self.code = code
+
+
+class ParseError(RuntimeError):
+    """fpr::ParseError (edge_list.hpp:17-21): what() = "line L: ...",
+    line_number = the 1-based line of the first malformed line."""
+
+    def __init__(self, line_number: int, what: str):
+        super().__init__(what)
+        self.line_number = line_number
 
 
 # ----------------------------------------------------------------- C structs
@@ -77,6 +86,11 @@ class _GenParams(C.Structure):
                 ("relabel_bfs", C.c_int32), ("reserved0", C.c_int32), ("bfs_root", C.c_uint64)]
 
 
+class _ParseErr(C.Structure):
+    _fields_ = [("line", C.c_uint64), ("kind", C.c_int32), ("message_len", C.c_uint32),
+                ("message", C.c_char * 256)]
+
+
 EXPORTS = [
     "fpr_b200_options_init", "fpr_b200_config_init", "fpr_b200_last_error", "fpr_b200_version",
     "fpr_b200_graph_create", "fpr_b200_graph_generate", "fpr_b200_graph_destroy",
@@ -84,6 +98,7 @@ EXPORTS = [
     "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank", "fpr_b200_graph_bfs_order",
     "fpr_b200_graph_validate", "fpr_b200_graph_partition", "fpr_b200_part_info",
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
+    "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list",
 ]
 
 _lib = None
@@ -115,11 +130,17 @@ def lib() -> C.CDLL:
         L.fpr_b200_graph_ranks_device.restype = vp
         L.fpr_b200_pagerank.argtypes = [C.POINTER(_GraphView), i32, C.POINTER(_Config),
                                         C.POINTER(_Options), vp, vp, u64, C.POINTER(_Result)]
+        L.fpr_b200_parse_edge_list.argtypes = [vp, u64, C.POINTER(_Options), C.POINTER(u64),
+                                               C.POINTER(u64), vp, u64, C.POINTER(_ParseErr)]
+        L.fpr_b200_graph_from_edge_list.argtypes = [vp, u64, C.POINTER(_Options), C.POINTER(vp),
+                                                    C.POINTER(_ParseErr)]
         _lib = L
     return _lib
 
 
-def _check(rc: int) -> None:
+def _check(rc: int, perr: "_ParseErr | None" = None) -> None:
+    if rc == EPARSE and perr is not None:
+        raise ParseError(int(perr.line), perr.message.decode("latin-1"))
     if rc != OK:
         msg = lib().fpr_b200_last_error().decode()
         if rc in (EINVAL, ERANGE):
@@ -299,6 +320,19 @@ class DeviceGraph:
         gp = _GenParams(GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, n, 0, seed, draws, alpha, kmax)
         return cls._generate(gp, device, norm, wave_count, stream, reorder)
 
+    @classmethod
+    def from_edge_list(cls, text, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False):
+        """build_csr(parse_edge_list(text)) -- parsing, id compaction and the
+        CSR build all on the device (edge_list.hpp:39-80, graph.hpp:35-70)."""
+        ptr, nbytes, keep = _text_arg(text)
+        h = C.c_void_p()
+        perr = _ParseErr()
+        _check(lib().fpr_b200_graph_from_edge_list(ptr, nbytes, C.byref(_options(device, norm, wave_count,
+                                                                                stream, reorder)),
+                                                   C.byref(h), C.byref(perr)), perr)
+        del keep
+        return cls(h.value, device, norm, wave_count)
+
     def validate(self) -> int:
         """0 iff the resident CSR satisfies build_csr's invariants (device check)."""
         f = C.c_uint32()
@@ -423,3 +457,51 @@ def linf_norm(a, b) -> float:
     if a.shape != b.shape:
         raise ValueError("linf_norm: length mismatch")
     return float(np.abs(a - b).max()) if a.size else 0.0
+
+
+# ------------------------------------------------------------ edge-list ingest
+@dataclass
+class EdgeSet:
+    """fpr::EdgeSet (edge_set.hpp): n vertices, edges (m, 2) u64 (src, dst)."""
+
+    n: int
+    edges: np.ndarray
+
+
+def _text_arg(text):
+    """(pointer-compatible object, byte length).  bytes/str are passed as is;
+    a contiguous numpy uint8 array (e.g. a view of pinned memory) by address,
+    so a pinned buffer takes the direct-DMA path."""
+    if isinstance(text, str):
+        text = text.encode("latin-1")
+    if isinstance(text, np.ndarray):
+        a = np.ascontiguousarray(text).view(np.uint8).reshape(-1)
+        return (a.ctypes.data if a.size else None), a.size, a
+    if not isinstance(text, bytes):
+        text = bytes(text)
+    return text, len(text), text
+
+
+def parse_edge_list(text, device: int = -1) -> EdgeSet:
+    """fpr::parse_edge_list (edge_list.hpp:39-80) on the GPU: '#'/'%' comment
+    and blank lines skipped, "src dst" decimal u64 pairs, sparse ids compacted
+    to [0, n) in first-appearance order.  Raises ParseError for the first
+    malformed line, with the reference's line number and message."""
+    ptr, nbytes, keep = _text_arg(text)
+    n, m = C.c_uint64(), C.c_uint64()
+    perr = _ParseErr()
+    opts = _options(device)
+    L = lib()
+    # Upper bound on edges: one per line.  One device pass when it suffices.
+    cap = (nbytes + 3) // 4 + 1 if nbytes < (1 << 28) else 0
+    edges = np.empty((max(cap, 1), 2), np.uint64)
+    rc = L.fpr_b200_parse_edge_list(ptr, nbytes, C.byref(opts), C.byref(n), C.byref(m),
+                                    edges.ctypes.data if cap else None, cap, C.byref(perr))
+    if rc == ERANGE and m.value > cap or (rc == OK and not cap and m.value):
+        edges = np.empty((m.value, 2), np.uint64)
+        rc = L.fpr_b200_parse_edge_list(ptr, nbytes, C.byref(opts), C.byref(n), C.byref(m),
+                                        edges.ctypes.data, m.value, C.byref(perr))
+    _check(rc, perr)
+    del keep
+    return EdgeSet(n.value, edges[: m.value].copy() if cap else edges[: m.value])
+

@@ -128,6 +128,18 @@ struct CsrSource {
   }
 };
 
+// Dense (src, dst) id pairs of a parsed edge list (ingest.cu).
+struct PairSource {
+  const int32_t* ids;  // 2 per edge
+
+  __device__ __forceinline__ bool get(uint64_t e, uint64_t& s, uint64_t& d) const {
+    const int2 p = __ldg(reinterpret_cast<const int2*>(ids) + e);
+    s = (uint32_t)p.x;
+    d = (uint32_t)p.y;
+    return s != d;
+  }
+};
+
 template <class Src>
 __global__ void hist_kernel(Src s, uint64_t count, int fine_shift, unsigned long long* hist) {
   __shared__ unsigned int sh[1 << kFineBits];
@@ -509,6 +521,12 @@ out:
 }
 
 }  // namespace
+
+cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
+                                 const char** msg) {
+  return build_csr_from(PairSource{pairs}, (uint64_t)m, n, g, st, msg);
+}
+
 
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t st, const char** msg) {
   *msg = nullptr;

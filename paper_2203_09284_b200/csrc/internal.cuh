@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace fprb {
@@ -139,5 +140,25 @@ cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_o
 
 // host_narrow.cpp: out[i] = (int32)in[i]; true if any in[i] >= bound.
 bool host_narrow_ids(const uint64_t* in, int32_t* out, int64_t count, uint64_t bound);
+
+// ingest.cu: fpr::parse_edge_list on the device.  `t` = the text (device,
+// len bytes).  On success out.pairs holds 2*out.m int32 dense ids (src, dst
+// per edge, input order; cudaMallocAsync on st, caller frees) and out.n the
+// number of distinct ids.  A malformed line sets err (line > 0) instead.
+struct Ingested {
+  int32_t* pairs = nullptr;
+  int64_t m = 0;
+  uint64_t n = 0;
+};
+struct IngestError {
+  uint64_t line = 0;  // 1-based; 0 = none
+  int kind = 0;       // FPR_B200_PARSE_*
+  std::string token;  // the bad token's bytes
+};
+cudaError_t ingest_edge_list(const unsigned char* t, uint64_t len, bool ends_with_newline, cudaStream_t st,
+                             Ingested& out, IngestError& err, const char** msg);
+// generate.cu: build_csr over m (src, dst) int32 pairs with ids in [0, n).
+cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
+                                 const char** msg);
 
 }  // namespace fprb

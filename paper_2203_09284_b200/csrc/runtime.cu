@@ -171,6 +171,26 @@ bool ring_upload(UploadRing* r, const uint64_t* src, T* dst, int64_t count, uint
   return ok;
 }
 
+// Uploads `len` bytes of PAGEABLE host memory through the ring (parallel
+// memcpy into a pinned buffer while the previous one's DMA is in flight).
+void ring_upload_bytes(UploadRing* r, const char* src, unsigned char* dst, int64_t len, cudaStream_t s,
+                       cudaError_t* e) {
+  int k = 0;
+  for (int64_t off = 0; off < len && *e == cudaSuccess; off += kRingBytes) {
+    const int64_t cnt = std::min<int64_t>(kRingBytes, len - off);
+    if (r->used[k]) *e = cudaEventSynchronize(r->done[k]);
+    if (*e != cudaSuccess) break;
+    char* stage = static_cast<char*>(r->buf[k]);
+    const int64_t piece = 1 << 20;
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < cnt; p += piece) std::memcpy(stage + p, src + off + p, std::min(piece, cnt - p));
+    *e = cudaMemcpyAsync(dst + off, stage, cnt, cudaMemcpyHostToDevice, s);
+    if (*e == cudaSuccess) *e = cudaEventRecord(r->done[k], s);
+    r->used[k] = true;
+    k = (k + 1) % kRingBufs;
+  }
+}
+
 struct Waves {
   int32_t nwaves = 0;
   int32_t* d_task = nullptr;
@@ -1049,9 +1069,154 @@ int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* 
   fpr_b200_graph* h = nullptr;
   if ((rc = fpr_b200_graph_create(view, opts, &h))) return rc;
   rc = fpr_b200_run(h, engine, cfg, ranks_out, errors_out, nullptr, nullptr, errors_cap, result);
-  if (result) result->kernel_launches += 0;
   fpr_b200_graph_destroy(h);
   return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ edge-list ingest
+namespace {
+
+void set_parse_error(fpr_parse_error* err, uint64_t line, int kind, const std::string& what) {
+  if (!err) return;
+  err->line = line;
+  err->kind = kind;
+  // ParseError::what() is a C string: a NUL inside a bad token ends it.
+  const size_t nbytes = std::min(std::strlen(what.c_str()), sizeof(err->message) - 1);
+  err->message_len = (uint32_t)nbytes;
+  std::memcpy(err->message, what.data(), nbytes);
+  err->message[nbytes] = 0;
+}
+
+// Text -> device -> ingest_edge_list.  Returns a status; *ing owns device pairs.
+int ingest_text(fpr_b200_graph* h, const char* text, uint64_t len, Ingested* ing, fpr_parse_error* perr) {
+  set_parse_error(perr, 0, 0, "");
+  if (!text && len) return fail(FPR_B200_EINVAL, "fpr_b200_parse_edge_list: null text");
+  unsigned char* dtext = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&dtext, std::max<uint64_t>(len, 1), h->stream);
+  if (e == cudaSuccess && len) {
+    if (is_pinned(text)) {
+      e = cudaMemcpyAsync(dtext, text, len, cudaMemcpyHostToDevice, h->stream);
+    } else {
+      UploadRing* ring = get_ring(h->device);
+      if (!ring) {
+        cudaFreeAsync(dtext, h->stream);
+        return fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed");
+      }
+      std::lock_guard<std::mutex> lk(ring->mu);
+      ring_upload_bytes(ring, text, dtext, (int64_t)len, h->stream, &e);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // ring reusable once we return
+    }
+  }
+  const char* msg = nullptr;
+  IngestError ie;
+  if (e == cudaSuccess)
+    e = ingest_edge_list(dtext, len, len > 0 && text[len - 1] == '\n', h->stream, *ing, ie, &msg);
+  if (dtext) cudaFreeAsync(dtext, h->stream);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                std::string("fpr_b200_parse_edge_list: ") + cudaGetErrorString(e));
+  if (msg) return fail(FPR_B200_ERANGE, std::string("fpr_b200_parse_edge_list: ") + msg);
+  if (ie.line) {
+    // fpr::ParseError::what() (edge_list.hpp:17-21, 60-72)
+    std::string what = ie.kind == FPR_B200_PARSE_TOKENS      ? std::string("expected two integer tokens")
+                       : ie.kind == FPR_B200_PARSE_BAD_TOKEN ? "bad token '" + ie.token + "'"
+                                                             : std::string("trailing characters after edge");
+    what = "line " + std::to_string(ie.line) + ": " + what;
+    what.resize(std::strlen(what.c_str()));  // what() semantics (C string)
+    set_parse_error(perr, ie.line, ie.kind, what);
+    return fail(FPR_B200_EPARSE, what);
+  }
+  if (ing->n >= (1ull << 31)) {
+    if (ing->pairs) cudaFreeAsync(ing->pairs, h->stream);
+    *ing = Ingested{};
+    return fail(FPR_B200_ERANGE, "fpr_b200: edge list has 2^31 or more distinct ids (int32 vertex ids)");
+  }
+  return FPR_B200_OK;
+}
+
+__global__ void widen_pairs_kernel(const int32_t* in, int64_t count, uint64_t* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+    out[i] = (uint64_t)(uint32_t)in[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int fpr_b200_parse_edge_list(const char* text, uint64_t len, const fpr_b200_options* opts, uint64_t* n_out,
+                             uint64_t* m_out, uint64_t* edges_out, uint64_t edges_cap, fpr_parse_error* err) {
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  Ingested ing;
+  rc = ingest_text(h, text, len, &ing, err);
+  if (rc == FPR_B200_OK) {
+    if (n_out) *n_out = ing.n;
+    if (m_out) *m_out = (uint64_t)ing.m;
+    if (edges_out && (uint64_t)ing.m > edges_cap) {
+      rc = fail(FPR_B200_ERANGE, "fpr_b200_parse_edge_list: edges_cap " + std::to_string(edges_cap) +
+                                     " < m " + std::to_string(ing.m));
+    } else if (edges_out && ing.m > 0) {
+      uint64_t* wide = nullptr;
+      const int64_t cnt = 2 * ing.m;
+      cudaError_t e = cudaMallocAsync((void**)&wide, cnt * sizeof(uint64_t), h->stream);
+      if (e == cudaSuccess) {
+        widen_pairs_kernel<<<(int)std::min<int64_t>((cnt + 255) / 256, 148 * 16), 256, 0, h->stream>>>(
+            ing.pairs, cnt, wide);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(edges_out, wide, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+      if (wide) cudaFreeAsync(wide, h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+      if (e != cudaSuccess)
+        rc = fail(FPR_B200_ECUDA, std::string("fpr_b200_parse_edge_list: ") + cudaGetErrorString(e));
+    }
+  }
+  if (ing.pairs) cudaFreeAsync(ing.pairs, h->stream);
+  destroy_handle(h);
+  return rc;
+}
+
+int fpr_b200_graph_from_edge_list(const char* text, uint64_t len, const fpr_b200_options* opts,
+                                  fpr_b200_graph** out, fpr_parse_error* err) {
+  if (!out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_from_edge_list: null argument");
+  *out = nullptr;
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  Ingested ing;
+  if ((rc = ingest_text(h, text, len, &ing, err))) {
+    destroy_handle(h);
+    return rc;
+  }
+  const char* msg = nullptr;
+  cudaError_t e = build_csr_from_pairs(ing.pairs, ing.m, ing.n, h->g, h->stream, &msg);
+  if (ing.pairs) cudaFreeAsync(ing.pairs, h->stream);
+  if (e != cudaSuccess || msg) {
+    destroy_handle(h);
+    if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200_graph_from_edge_list: ") + msg);
+    return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                std::string("fpr_b200_graph_from_edge_list: ") + cudaGetErrorString(e));
+  }
+  h->allocs.push_back(h->g.row);
+  h->allocs.push_back(h->g.src);
+  h->allocs.push_back(h->g.outdeg);
+  if ((rc = finish_graph(h))) {
+    destroy_handle(h);
+    return rc;
+  }
+  *out = h;
+  return FPR_B200_OK;
 }
 
 }  // extern "C"

@@ -8,6 +8,7 @@ pagerank_{ec,fused}_seq, pagerank_dense_oracle) -- never by this repo's code.
 
     python tests/golden/make_golden.py            # all fixtures
     python tests/golden/make_golden.py --skip-config2
+    python tests/golden/make_golden.py --only edge_list
 
 The fixtures pin the C restatement (oracle/fpr_oracle.c) bit-exactly in
 tests/test_oracle.py, and give the GPU parity tests reference answers that do
@@ -25,6 +26,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 from oracle import Graph, Reference  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -122,11 +124,66 @@ def rmat_fixture(ref: Reference, scale, ef, seed, thresholds, sample=64) -> dict
     return rec
 
 
+def edge_list_fixture(ref: Reference) -> dict:
+    """fpr::parse_edge_list (edge_list.hpp:39-80) on the inputs of the
+    reference's own tests (io_ingest_test.cpp:25-93), edge cases, seeded fuzz
+    texts and a large sparse-id text (digests only)."""
+    from golden_util import fuzz_text, roundtrip_texts, sparse_text_from_edges
+
+    named = [
+        ("SkipsCommentsAndParses", b"# comment\n0 1\n1 2\n"),
+        ("CompactsSparseIds", b"5 9\n9 5\n"),
+        ("RejectsMalformedLine", b"0 x\n"),
+        ("RejectsOverflowingToken", b"0 1\n99999999999999999999999 2\n"),
+        ("RejectsTrailingGarbage", b"0 1 2\n"),
+        ("RejectsShortLine", b"0\n"),
+        ("RejectsNegative", b"0 -1\n"),
+        ("SkipsBlankAndPercentLines", b"% header\n\n   \n0 1\n"),
+        ("empty", b""),
+        ("only_comments", b"# a\n% b\n\n"),
+        ("no_final_newline", b"3 4\n4 5"),
+        ("crlf_tabs", b"1\t2\r\n3 \t 4\r\n"),
+        ("indented_hash_is_a_token", b"  # x\n"),
+        ("u64_max_then_overflow", b"18446744073709551615 0\n18446744073709551616 1\n"),
+        ("vertical_tab_not_whitespace", b"\x0b1 2\n"),
+        ("form_feed_not_whitespace", b"1 2\x0c\n"),
+        ("leading_zeros", b"007 0007\n7 0\n"),
+        ("plus_sign", b"+1 2\n"),
+        ("trailing_whitespace_and_blank_tail", b"1 2 \t\r\n\n\n"),
+        ("self_loops_kept", b"4 4\n4 5\n"),
+        ("first_error_wins", b"1 2\n3\n4 x\n"),
+        ("nul_byte", b"1 2\n3\x004\n"),
+        ("long_line", b"1 " + b"9" * 19 + b"\n" + b"2 " + b" " * 5000 + b"3\n"),
+    ]
+    named += [(f"RenderRoundTrip_{i}", t) for i, t in enumerate(roundtrip_texts())]
+    named += [(f"fuzz_{s}", fuzz_text(s, 1 + s % 60, bad_rate=0.02 if s % 3 == 0 else 0.0))
+              for s in range(120)]
+    cases = []
+    for name, text in named:
+        p = ref.parse_edge_list(text)
+        cases.append({"name": name, "text": text.decode("latin-1"), "n": p.n,
+                      "edges": p.edges.reshape(-1).tolist(), "error_line": p.error_line, "error": p.error})
+    # large: RMAT(12, 16, 7) draws as sparse ids with comment lines
+    _, s, d = ref.generate_rmat(12, 16, seed=7)
+    text = sparse_text_from_edges(s, d)
+    p = ref.parse_edge_list(text)
+    large = {"source": "generate_rmat(12,16,seed=7) draws, raw = id*2654435761+12345, '# block' every 1000",
+             "bytes": len(text), "text_sha256": hashlib.sha256(text).hexdigest(), "n": p.n,
+             "m": int(len(p.edges)), "edges_sha256": sha(p.edges.reshape(-1))}
+    g = ref.build_csr(p.n, p.edges[:, 0], p.edges[:, 1])
+    large["graph"] = graph_digest(g)
+    return {"cases": cases, "large": large}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-config2", action="store_true")
+    ap.add_argument("--only", choices=["edge_list"], help="regenerate one fixture")
     args = ap.parse_args()
     ref = Reference()
+    if args.only == "edge_list":
+        json.dump(edge_list_fixture(ref), open(os.path.join(OUT, "edge_list.json"), "w"), indent=0)
+        return
 
     json.dump(kats(ref), open(os.path.join(OUT, "kat.json"), "w"), indent=1)
     json.dump(corpus(ref), open(os.path.join(OUT, "corpus.json"), "w"))
@@ -138,6 +195,8 @@ def main() -> None:
               open(os.path.join(OUT, "rmat_s12_seed7.json"), "w"), indent=1)
     # BASELINE config 1.
     json.dump(rmat_fixture(ref, 16, 16, 1, [1e-10, 1e-13]), open(os.path.join(OUT, "config1.json"), "w"), indent=1)
+
+    json.dump(edge_list_fixture(ref), open(os.path.join(OUT, "edge_list.json"), "w"), indent=0)
 
     if not args.skip_config2:
         # BASELINE config 2: random_sparse(n=2^22, avg_degree=16, SplitMix64(2)) semantics.

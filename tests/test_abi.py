@@ -39,6 +39,7 @@ int main(void) {{
          sizeof(fpr_b200_options), sizeof(fpr_b200_result), sizeof(fpr_gen_params));
   printf("%zu %zu %zu\\n", offsetof(fpr_b200_options, stream), offsetof(fpr_b200_result, solve_ms),
          offsetof(fpr_gen_params, seed));
+  printf("%zu %zu\\n", sizeof(fpr_parse_error), offsetof(fpr_parse_error, message));
   return 0;
 }}
 """)
@@ -51,6 +52,7 @@ int main(void) {{
     assert sizes[5] == fb._Options.stream.offset
     assert sizes[6] == fb._Result.solve_ms.offset
     assert sizes[7] == fb._GenParams.seed.offset
+    assert sizes[8:10] == [C.sizeof(fb._ParseErr), fb._ParseErr.message.offset]
 
 
 def test_library_is_sm100a_only():

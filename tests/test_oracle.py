@@ -2,6 +2,8 @@
 outputs (tests/golden/, produced by tests/golden/make_golden.py from the
 unmodified reference).  CPU only.  Bit-exact: the restatement must reproduce
 the reference's bytes, not approximate them."""
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -138,3 +140,42 @@ def test_config2_graph(oracle):
     g = oracle.build_csr(n, s, d)
     _graph_matches(g, rec["graph"])
     _run_matches(oracle.pagerank_ec(g, threshold=1e-10), rec["runs"]["ec_seq@1e-10"])
+
+
+# ------------------------------------------------------------ edge-list ingest
+def _check_parsed(p, c):
+    assert p.error_line == c["error_line"], c["name"]
+    assert p.error == c["error"], c["name"]
+    if not c["error_line"]:
+        assert p.n == c["n"], c["name"]
+        assert p.edges.reshape(-1).tolist() == c["edges"], c["name"]
+
+
+def test_oracle_parse_edge_list_golden(oracle):
+    """fo_parse_edge_list == fpr::parse_edge_list on the reference's own test
+    inputs (io_ingest_test.cpp:25-93), edge cases and seeded fuzz texts."""
+    d = load("edge_list.json")
+    assert len(d["cases"]) >= 150
+    for c in d["cases"]:
+        _check_parsed(oracle.parse_edge_list(c["text"].encode("latin-1")), c)
+
+
+def test_oracle_parse_edge_list_large(oracle):
+    from golden_util import sparse_text_from_edges
+
+    big = load("edge_list.json")["large"]
+    _, s, d = oracle.generate_rmat(12, 16, seed=7)
+    text = sparse_text_from_edges(s, d)
+    assert hashlib.sha256(text).hexdigest() == big["text_sha256"]
+    p = oracle.parse_edge_list(text)
+    assert (p.n, len(p.edges)) == (big["n"], big["m"])
+    assert sha(p.edges.reshape(-1)) == big["edges_sha256"]
+
+
+def test_fuzz_generator_is_deterministic():
+    from golden_util import fuzz_text
+
+    d = load("edge_list.json")
+    fz = {c["name"]: c["text"] for c in d["cases"] if c["name"].startswith("fuzz_")}
+    for s in (0, 1, 2, 57, 119):
+        assert fuzz_text(s, 1 + s % 60, bad_rate=0.02 if s % 3 == 0 else 0.0).decode("latin-1") == fz[f"fuzz_{s}"]
