@@ -201,6 +201,64 @@ def cpu_baseline_leg(g_host, gpu_ranks=None, gpu_iters=None) -> dict:
             "sample": "2 EC iterations of config 2 with the C restatement (1 thread)"}
 
 
+def render_fixed(src, dst, width=7) -> np.ndarray:
+    """Bench input for the ingest leg: one "%0{width}d %0{width}d\\n" line per
+    edge (leading zeros are valid from_chars tokens, edge_list.hpp:25-30)."""
+    out = np.empty((len(src), 2 * width + 2), np.uint8)
+    for col, ids in ((0, src), (width + 1, dst)):
+        v = np.asarray(ids, dtype=np.uint64).copy()
+        for k in range(width - 1, -1, -1):
+            out[:, col + k] = (v % np.uint64(10)).astype(np.uint8) + 48
+            v //= np.uint64(10)
+    out[:, width] = 32
+    out[:, 2 * width + 1] = 10
+    return out.reshape(-1)
+
+
+def ingest_leg(fb, g, device) -> dict:
+    """§8(f) edge-list ingest: config 2's edges as text -> resident device CSR
+    through fpr_b200_graph_from_edge_list (pinned host text, H2D inside the
+    timed call), against the reference's parse_edge_list + build_csr on a
+    1/64 sample (single thread: the reference parser is sequential)."""
+    import torch
+
+    dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
+    text = render_fixed(g.in_src, dst)
+    pinned = torch.empty(len(text), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = text
+    buf = pinned.numpy()
+    fb.DeviceGraph.from_edge_list(buf, device=device).close()  # warm-up
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = fb.DeviceGraph.from_edge_list(buf, device=device)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        assert d.m == g.m
+        d.close()
+    dt = float(np.median(times))
+    out = {"workload": f"config-2 edges as '%07d %07d\\n' text ({len(text) / 1e9:.2f} GB, {g.m} lines)",
+           "api": "fpr_b200_graph_from_edge_list (pinned host text -> resident CSR; H2D timed)",
+           "ms": dt * 1e3, "medges_per_s": g.m / dt / 1e6, "text_gb_per_s": len(text) / dt / 1e9,
+           "h2d_bytes": int(len(text))}
+    try:
+        from oracle import load_reference
+
+        ref = load_reference()
+        if ref is not None:
+            sample = text[: (len(text) // 64 // 16) * 16].tobytes()
+            t0 = time.perf_counter()
+            p = ref.parse_edge_list(sample)
+            ref.build_csr(p.n, p.edges[:, 0], p.edges[:, 1])
+            rdt = time.perf_counter() - t0
+            out["reference"] = {"medges_per_s": len(p.edges) / rdt / 1e6, "kind": "reference", "cores": 1,
+                                "sample": f"parse_edge_list + build_csr of the first {len(p.edges)} lines"}
+    except Exception as ex:  # reference arm is informative only
+        out["reference"] = {"unavailable": str(ex)}
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -209,6 +267,7 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ingest", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the multi-GPU partitioned path even at N=1 (NCCL world of 1)")
     args = ap.parse_args()
@@ -300,6 +359,11 @@ def main() -> None:
     if not args.no_e2e:
         g_host = dg.download()
         e2e = e2e_leg(fb, g_host, local, args, iters)
+    ingest = None
+    if rank == 0 and ws == 1 and not args.no_ingest:
+        if g_host is None:
+            g_host = dg.download()
+        ingest = ingest_leg(fb, g_host, local)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         if g_host is None:
@@ -329,6 +393,7 @@ def main() -> None:
             "fused": fused,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "ingest": ingest,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
         }

@@ -8,6 +8,8 @@ Graph sources:
   --rmat-bfs SCALE:EF:SEED    ... relabelled in BFS crawl order (config 3)
   --uniform N:DEG:SEED        testutil::random_sparse semantics (config 2)
   --chunglu N:DRAWS:SEED      config 4
+  --edges PATH                SNAP edge-list text, parsed on the device
+                              (build_csr(parse_edge_list(file)), edge_list.hpp)
 
 Engines: ec_b200, fused_b200, fused_lockstep_b200.  The L1 reference column
 (l1_vs_seq_ec) is taken from ec_b200, which equals the reference's ec_seq
@@ -24,7 +26,7 @@ import time
 
 import numpy as np
 
-from . import (DeviceGraph, EngineKind, NORM_L1, NORM_LINF, PageRankConfig, RmatParams,
+from . import (DeviceGraph, EngineKind, NORM_L1, NORM_LINF, PageRankConfig, ParseError, RmatParams,
                l1_norm, parse_engine, ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP)
 from .cache import CacheError, load_cache, save_cache
 
@@ -48,14 +50,18 @@ def _triple(text: str, name: str) -> tuple[int, int, int]:
 
 
 def open_graph(args, norm=NORM_LINF) -> tuple[DeviceGraph, str]:
-    given = [k for k in ("graph", "rmat", "rmat_bfs", "uniform", "chunglu") if getattr(args, k, None)]
+    given = [k for k in ("graph", "rmat", "rmat_bfs", "uniform", "chunglu", "edges") if getattr(args, k, None)]
     if len(given) != 1:
-        raise UsageError("exactly one graph source is required (--graph/--rmat/--rmat-bfs/--uniform/--chunglu)")
+        raise UsageError("exactly one graph source is required "
+                         "(--graph/--rmat/--rmat-bfs/--uniform/--chunglu/--edges)")
     k = given[0]
     v = getattr(args, k)
     if k == "graph":
         g = load_cache(v)  # CacheError -> I/O exit code
         return DeviceGraph.from_graph(g, norm=norm), v
+    if k == "edges":
+        text = np.fromfile(v, dtype=np.uint8)  # OSError -> I/O exit code
+        return DeviceGraph.from_edge_list(text, norm=norm), v
     a, b, c = _triple(v, k.replace("_", "-"))
     if k in ("rmat", "rmat_bfs"):
         return DeviceGraph.generate_rmat(RmatParams(scale=a, edge_factor=b, seed=c), norm=norm,
@@ -164,6 +170,7 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--rmat-bfs", dest="rmat_bfs")
         p.add_argument("--uniform")
         p.add_argument("--chunglu")
+        p.add_argument("--edges")
         p.add_argument("--damping", type=float, default=0.85)
         p.add_argument("--threshold", type=float, default=1e-15)
         p.add_argument("--threads", type=int, default=1)
@@ -208,7 +215,7 @@ def main(argv=None, out=None) -> int:
     except UsageError as e:
         sys.stderr.write(f"fpr-b200: {e}\n")
         return EXIT_USAGE
-    except (CacheError, OSError) as e:
+    except (CacheError, OSError, ParseError) as e:  # a malformed input file is an I/O error
         sys.stderr.write(f"fpr-b200: {e}\n")
         return EXIT_IO
     except ValueError as e:  # reference validation messages (invalid_argument)

@@ -7,6 +7,9 @@
 #include <stdexcept>
 #include <string>
 
+#include <sstream>
+
+#include "fpr/edge_list_b200.hpp"
 #include "fpr/metrics.hpp"
 #include "fpr/pagerank_b200.hpp"
 #include "fpr/rmat.hpp"
@@ -74,6 +77,38 @@ int main() {
   capped.max_iterations = 3;
   const fpr::PageRankResult nc = fpr::pagerank_ec_b200(g, capped);
   CHECK(nc.trace.iterations == 3 && !nc.trace.converged, "non-convergence is a result");
+
+  // edge-list ingest: the reference's parse_edge_list vs the device parser
+  {
+    std::ostringstream text;
+    fpr::write_edge_list(text, fpr::generate_rmat(p), {"drop-in ingest"});
+    std::string t = text.str() + "% tail comment\r\n\n  \t\n77777777777 5\n";
+    std::istringstream a(t), b(t);
+    const fpr::EdgeSet ea = fpr::parse_edge_list(a);
+    const fpr::EdgeSet eb = fpr::parse_edge_list_b200(b);
+    CHECK(ea == eb, "EdgeSet differs (n %llu vs %llu, m %zu vs %zu)", (unsigned long long)ea.n,
+          (unsigned long long)eb.n, ea.edges.size(), eb.edges.size());
+    CHECK(fpr::build_csr(ea).in_src == fpr::build_csr(eb).in_src, "build_csr differs");
+    const std::string badtext = t + "1 2 3\n4 x\n";
+    std::string want, got;
+    std::uint64_t wl = 0, gl = 0;
+    try {
+      std::istringstream in(badtext);
+      fpr::parse_edge_list(in);
+    } catch (const fpr::ParseError& e) {
+      want = e.what();
+      wl = e.line_number;
+    }
+    try {
+      std::istringstream in(badtext);
+      fpr::parse_edge_list_b200(in);
+    } catch (const fpr::ParseError& e) {
+      got = e.what();
+      gl = e.line_number;
+    }
+    CHECK(wl > 0 && wl == gl && want == got, "ParseError '%s'@%llu vs '%s'@%llu", want.c_str(),
+          (unsigned long long)wl, got.c_str(), (unsigned long long)gl);
+  }
 
   std::printf("%s: ec %llu it, fused %llu it (ref fused_seq %llu)\n", failures ? "FAILED" : "OK",
               (unsigned long long)gpu.trace.iterations, (unsigned long long)fgpu.trace.iterations,
