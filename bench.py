@@ -268,6 +268,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ingest", action="store_true")
+    ap.add_argument("--copy-exchange", action="store_true",
+                    help="N>1: NCCL all-gather of slices instead of the fused P2P-store exchange")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the multi-GPU partitioned path even at N=1 (NCCL world of 1)")
     args = ap.parse_args()
@@ -409,7 +411,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     iteration (paper_2203_09284_b200/dist.py)."""
     import torch
 
-    from paper_2203_09284_b200.dist import B200Part, TorchExchange, solve_partitioned
+    from paper_2203_09284_b200.dist import B200Part, PartitionedSolver, TorchExchange
 
     sptr = fb.torch_stream_handle()
     full = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
@@ -419,8 +421,11 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     ex = TorchExchange()
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     dev = f"cuda:{local}"
+    # fused exchange: the sweep stores its slice into the peers' replicas
+    # (CUDA IPC / NVLink P2P); NCCL carries only the 16-B residual pair
+    solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1)
     for _ in range(args.warmup):
-        r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=False)
+        r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=False)
     iters = r.iterations
 
     def barrier():
@@ -433,17 +438,20 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            r = solve_partitioned(part, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=False)
+            r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=False)
             assert r.iterations == iters
         ev1.record(stream)
         barrier()
     t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    fr = solve_partitioned(part, ex, fb.ENGINE_FUSED, cfg, device=dev, want_ranks=False)
+    fr = solver.solve(fb.ENGINE_FUSED, cfg, want_ranks=False)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_multi(args, fb, dist, part, ex, cfg, dev, local, iters)
+        e2e = e2e_multi(args, fb, dist, solver, cfg, dev, local, iters)
+    exchange = ("fused: sweep epilogue P2P-stores each slice into the peers' replicas (CUDA IPC over NVLink); "
+                "NCCL all-gather of the 16-B residual pair" if solver.fused_exchange else
+                "NCCL all-gather of contribution slices + residual pair")
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -453,7 +461,8 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
             "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
                        "norm": "linf", "step": "1 full EC solve (time-to-converge)",
-                       "parallelism": f"dst-range partition x{ws}, NCCL all-gather per iteration",
+                       "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
+                       "exchange_fallback": solver.fallback,
                        "slice": part.slice, "l2": "inputs larger than L2; no flush"},
             "time_to_converge_ms": ms_step,
             "fused": {"engine": "fused_b200", "iterations": fr.iterations},
@@ -461,16 +470,17 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "gpu_launches": int(args.steps * iters), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    solver.close()
     part.close()
 
 
-def e2e_multi(args, fb, dist, part, ex, cfg, dev, local, iters) -> dict:
+def e2e_multi(args, fb, dist, solver, cfg, dev, local, iters) -> dict:
     """N GPUs end to end through the public API: every rank uploads the pinned
     host CSR (fpr_b200_graph_create), partitions it on its device, solves with
     the NCCL exchange and downloads its rank slice.  Max over ranks."""
     import torch
 
-    from paper_2203_09284_b200.dist import B200Part, solve_partitioned
+    from paper_2203_09284_b200.dist import B200Part
 
     g = None
     with fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local,
@@ -490,7 +500,10 @@ def e2e_multi(args, fb, dist, part, ex, cfg, dev, local, iters) -> dict:
     def call():
         with fb.DeviceGraph.from_graph(hg, device=local, stream=fb.torch_stream_handle()) as full_g:
             p = B200Part(full_g, ws, rank, device=local, stream=fb.torch_stream_handle())
-        r = solve_partitioned(p, ex, fb.ENGINE_EC, cfg, device=dev, want_ranks=True)
+        old = solver.local
+        solver.rebind(p)  # exchange buffers / peer replicas are persistent state
+        r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=True)
+        solver.rebind(old)
         p.close()
         return r
 

@@ -189,6 +189,26 @@ int fpr_b200_part_sweep(fpr_b200_graph* g, int engine, const fpr_config* cfg,
                         const double* exch_read, double* exch_write, double* pair_out);
 int fpr_b200_part_ranks(fpr_b200_graph* g, double* ranks_out);
 
+/* Fused exchange: part_sweep whose epilogue also stores every updated
+ * contribution into the other parts' exchange vectors -- peer_write[q] is
+ * part q's write vector (base of the whole padded exchange space) mapped into
+ * this device (fpr_b200_ipc_import for another process/GPU; a plain device
+ * pointer within one process), peer_write[part] is ignored, npeer_bufs must
+ * equal nparts (<= 8).  The sweep thereby performs the all-gather over NVLink
+ * P2P stores, tile by tile as rows finalize; only the 16-B residual pair is
+ * left for a collective, and that collective doubles as the barrier. */
+int fpr_b200_part_sweep_peers(fpr_b200_graph* g, int engine, const fpr_config* cfg,
+                              const double* exch_read, double* exch_write,
+                              double* const* peer_write, uint32_t npeer_bufs, double* pair_out);
+
+/* CUDA IPC of exchange buffers between the per-GPU processes.  A handle is
+ * the cudaIpcMemHandle of the allocation holding dev_ptr plus dev_ptr's
+ * offset in it (buffers from caching allocators are sub-allocations). */
+#define FPR_B200_IPC_HANDLE_BYTES 72
+int fpr_b200_ipc_export(const void* dev_ptr, void* handle_out /* 72 B */);
+int fpr_b200_ipc_import(const void* handle /* 72 B */, int device, void** dev_ptr_out);
+int fpr_b200_ipc_close(void* dev_ptr);
+
 /* Edge-list text ingest (SNAP style, edge_list.hpp:33-80): '#'/'%' comment
  * lines and blank/whitespace-only lines skipped, every other line exactly two
  * decimal u64 tokens separated by ' ', '\t' or '\r'; ids compacted to [0, n)

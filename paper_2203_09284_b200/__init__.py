@@ -98,7 +98,8 @@ EXPORTS = [
     "fpr_b200_run", "fpr_b200_graph_ranks_device", "fpr_b200_pagerank", "fpr_b200_graph_bfs_order",
     "fpr_b200_graph_validate", "fpr_b200_graph_partition", "fpr_b200_part_info",
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
-    "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list",
+    "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
+    "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close",
 ]
 
 _lib = None

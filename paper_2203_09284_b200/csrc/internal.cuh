@@ -54,6 +54,8 @@ struct Partition {
 };
 
 // Everything the persistent solve kernel needs (passed by value).
+constexpr int kMaxPeers = 7;  // parts - 1 on one NVSwitch node of 8 GPUs
+
 struct SolveParams {
   int32_t n;
   const int64_t* row;
@@ -86,6 +88,11 @@ struct SolveParams {
   GridBar* bar;
   unsigned int* out_iters;
   int* out_stop;
+  // Fused exchange (multi-GPU): every finalized contribution is also stored
+  // into each peer's replica (peer[q] = that replica at this part's slice,
+  // P2P-mapped), so the sweep itself performs the all-gather over NVLink.
+  int32_t npeers;
+  double* peer[kMaxPeers];
 };
 
 enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };

@@ -245,7 +245,9 @@ __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_
                  : "+d"(v)
                  : "l"(addr), "r"((int)valid)
                  : "memory");
-  } else {  // L2 only: random 8-B gathers have no L1 reuse
+  } else {
+    // L2 only: random 8-B gathers have no L1 reuse (an L1-allocating ld.ca
+    // variant measured no faster even on R-MAT hubs)
     asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cg.f64 %0, [%1]; }"
                  : "+d"(v)
                  : "l"(addr), "r"((int)valid));
@@ -407,6 +409,8 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
           st_relaxed_f64(cur + r, c);
         else
           cur[r] = c;
+        // fused exchange: the same (coalesced) store into every peer replica
+        for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
       }
       const double d = fabs(nv - ov);
       lmax = fmax(lmax, d);
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
         *p.out_iters = it + 1;
         *p.out_stop = crit <= p.threshold ? 1 : 0;
       }
+      if (p.npeers) __threadfence_system();  // peer-replica stores performed before exit
       return;
     }
   }

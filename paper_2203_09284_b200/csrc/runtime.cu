@@ -986,8 +986,19 @@ int fpr_b200_part_init(fpr_b200_graph* h, double* exchange) {
 
 int fpr_b200_part_sweep(fpr_b200_graph* h, int engine, const fpr_config* cfg,
                         const double* exch_read, double* exch_write, double* pair_out) {
+  return fpr_b200_part_sweep_peers(h, engine, cfg, exch_read, exch_write, nullptr, 0, pair_out);
+}
+
+int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* cfg,
+                              const double* exch_read, double* exch_write,
+                              double* const* peer_write, uint32_t npeer_bufs, double* pair_out) {
   if (!h || !cfg || !exch_read || !exch_write || !pair_out)
     return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: null argument");
+  if (npeer_bufs && (!peer_write || npeer_bufs != (uint32_t)h->nparts))
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: need one exchange pointer per part");
+  if (npeer_bufs && h->nparts - 1 > kMaxPeers)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: at most " + std::to_string(kMaxPeers + 1) +
+                                     " parts");
   int rc = validate_config(cfg);
   if (rc) return rc;
   if (engine != kEC && engine != kFused)
@@ -1034,6 +1045,12 @@ int fpr_b200_part_sweep(fpr_b200_graph* h, int engine, const fpr_config* cfg,
   p.bar = h->bar;
   p.out_iters = h->d_iters;
   p.out_stop = h->d_stop;
+  p.npeers = 0;
+  for (uint32_t q = 0; q < npeer_bufs; ++q) {
+    if ((int)q == h->part_id) continue;
+    if (!peer_write[q]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: null peer pointer");
+    p.peer[p.npeers++] = peer_write[q] + p.write_off;  // this part's slice in part q's replica
+  }
   CK(launch_solve(engine, grid, p, h->stream));
   CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
@@ -1220,3 +1237,83 @@ int fpr_b200_graph_from_edge_list(const char* text, uint64_t len, const fpr_b200
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ CUDA IPC (fused exchange)
+namespace {
+std::map<void*, void*> g_ipc_offsets;  // imported pointer -> mapped allocation base
+std::mutex g_ipc_mu;
+}  // namespace
+
+extern "C" {
+
+// A handle is the 64-B cudaIpcMemHandle of the ALLOCATION containing dev_ptr
+// (caching allocators such as torch's sub-allocate) plus dev_ptr's byte
+// offset inside it; the importer maps the allocation and adds the offset.
+namespace {
+using GetAddressRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+cudaError_t allocation_base(const void* p, uintptr_t* base) {
+  static GetAddressRangeFn fn = nullptr;
+  if (!fn) {
+    void* sym = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &sym, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !sym) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    fn = reinterpret_cast<GetAddressRangeFn>(sym);
+  }
+  unsigned long long b = 0;
+  size_t size = 0;
+  if (fn(&b, &size, (unsigned long long)(uintptr_t)p) != 0) return cudaErrorInvalidValue;
+  *base = (uintptr_t)b;
+  return cudaSuccess;
+}
+}  // namespace
+
+int fpr_b200_ipc_export(const void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return fail(FPR_B200_EINVAL, "fpr_b200_ipc_export: null argument");
+  cudaIpcMemHandle_t hd;
+  uintptr_t base = 0;
+  cudaError_t e = allocation_base(dev_ptr, &base);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(FPR_B200_ECUDA, std::string("fpr_b200_ipc_export: ") + cudaGetErrorString(e));
+  static_assert(sizeof(hd) + sizeof(uint64_t) == FPR_B200_IPC_HANDLE_BYTES, "IPC handle size");
+  const uint64_t off = (uint64_t)((uintptr_t)dev_ptr - base);
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  std::memcpy(static_cast<char*>(handle_out) + sizeof(hd), &off, sizeof(off));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_ipc_import(const void* handle, int device, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(FPR_B200_EINVAL, "fpr_b200_ipc_import: null argument");
+  *dev_ptr_out = nullptr;
+  cudaIpcMemHandle_t hd;
+  uint64_t off = 0;
+  std::memcpy(&hd, handle, sizeof(hd));
+  std::memcpy(&off, static_cast<const char*>(handle) + sizeof(hd), sizeof(off));
+  void* base = nullptr;
+  cudaError_t e = device >= 0 ? cudaSetDevice(device) : cudaSuccess;
+  // LazyEnablePeerAccess: a buffer on another GPU is reached over NVLink P2P
+  if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(FPR_B200_ECUDA, std::string("fpr_b200_ipc_import: ") + cudaGetErrorString(e));
+  *dev_ptr_out = static_cast<char*>(base) + off;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_offsets[*dev_ptr_out] = base;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return FPR_B200_OK;
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_offsets.find(dev_ptr);
+    if (it == g_ipc_offsets.end()) return fail(FPR_B200_EINVAL, "fpr_b200_ipc_close: not an imported pointer");
+    base = it->second;
+    g_ipc_offsets.erase(it);
+  }
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return fail(FPR_B200_ECUDA, std::string("fpr_b200_ipc_close: ") + cudaGetErrorString(e));
+  return FPR_B200_OK;
+}
+
+}  // extern "C"
+

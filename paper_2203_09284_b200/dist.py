@@ -23,6 +23,13 @@ C ABI (``fpr_b200_part_*``); the gloo CPU tests plug in a numpy restatement.
 The exchange is pluggable too: ``TorchExchange`` (torch.distributed, one
 process per GPU) or ``EmulatedExchange`` (all parts in one process, slices
 copied -- for single-GPU validation of the partitioned path).
+
+Fused exchange (``fused_exchange=True``): instead of an all-gather after the
+sweep, the sweep kernel's epilogue stores every finalized contribution into
+each peer's replica as well (``fpr_b200_part_sweep_peers``; replicas mapped
+with CUDA IPC, i.e. NVLink P2P stores through NVSwitch), so the exchange
+overlaps the sweep row tile by row tile and only the 16-B residual pair
+remains a collective -- which doubles as the inter-iteration barrier.
 """
 from __future__ import annotations
 
@@ -112,6 +119,12 @@ class B200Part:
     """This rank's part on its GPU, driven through the C ABI."""
 
     def __init__(self, full: DeviceGraph, nparts: int, part: int, device: int = 0, stream=None):
+        # The exchange runs on torch's stream (NCCL / copies / .cpu()), so the
+        # sweeps must too: default to torch's current stream, not a private one.
+        if stream is None:
+            from . import torch_stream_handle
+
+            stream = torch_stream_handle()
         self.nparts, self.part = nparts, part
         bounds = np.empty(nparts + 1, np.uint64)
         sl = C.c_uint64()
@@ -140,6 +153,18 @@ class B200Part:
         _check(lib().fpr_b200_part_sweep(self.graph._h, engine, C.byref(c), read.data_ptr(),
                                          write.data_ptr(), pair.data_ptr()))
 
+    def sweep_peers(self, engine: int, cfg: PageRankConfig, read, write, peer_ptrs, pair) -> None:
+        """Fused exchange: the sweep also stores this part's slice straight into
+        every other part's write vector (peer_ptrs[q], device addresses mapped
+        into this process)."""
+        c = cfg._c()
+        arr = (C.c_void_p * len(peer_ptrs))(*peer_ptrs)
+        L = lib()
+        L.fpr_b200_part_sweep_peers.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Config), C.c_void_p,
+                                                C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]
+        _check(L.fpr_b200_part_sweep_peers(self.graph._h, engine, C.byref(c), read.data_ptr(),
+                                           write.data_ptr(), arr, len(peer_ptrs), pair.data_ptr()))
+
     def ranks(self) -> np.ndarray:
         out = np.empty(max(self.n_local, 1), np.float64)
         _check(lib().fpr_b200_part_ranks(self.graph._h, out.ctypes.data))
@@ -147,6 +172,65 @@ class B200Part:
 
     def close(self):
         self.graph.close()
+
+
+# ------------------------------------------------------------ fused exchange
+IPC_HANDLE_BYTES = 72  # FPR_B200_IPC_HANDLE_BYTES
+
+
+def ipc_export(ptr: int) -> bytes:
+    h = (C.c_char * IPC_HANDLE_BYTES)()
+    L = lib()
+    L.fpr_b200_ipc_export.argtypes = [C.c_void_p, C.c_void_p]
+    _check(L.fpr_b200_ipc_export(ptr, h))
+    return bytes(h.raw)
+
+
+def ipc_import(handle: bytes, device: int) -> int:
+    out = C.c_void_p()
+    L = lib()
+    L.fpr_b200_ipc_import.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+    _check(L.fpr_b200_ipc_import(handle, device, C.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int) -> None:
+    L = lib()
+    L.fpr_b200_ipc_close.argtypes = [C.c_void_p]
+    _check(L.fpr_b200_ipc_close(ptr))
+
+
+class PeerReplicas:
+    """Every part's exchange vectors mapped into this process, for the fused
+    exchange: ptrs[k][q] = device address of part q's buffer k (its own buffer
+    for q == rank, a CUDA-IPC mapping -- NVLink P2P on another GPU -- else).
+    Handles travel over the process group (all_gather_object)."""
+
+    def __init__(self, bufs, group=None, device: int = 0):
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        mine = [ipc_export(b.data_ptr()) for b in bufs]
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []
+        self.ptrs = []
+        for k, b in enumerate(bufs):
+            row = []
+            for q in range(world):
+                if q == self.rank:
+                    row.append(b.data_ptr())
+                else:
+                    ptr = ipc_import(everyone[q][k], device)
+                    self._opened.append(ptr)
+                    row.append(ptr)
+            self.ptrs.append(row)
+
+    def close(self):
+        for ptr in self._opened:
+            ipc_close(ptr)
+        self._opened = []
 
 
 @dataclass
@@ -167,45 +251,108 @@ def _reduce_pairs(pairs: np.ndarray) -> tuple[float, float]:
     return mx, sm
 
 
+class PartitionedSolver:
+    """This rank's solver state, built once and reused across solves: the
+    exchange vectors (two for EC's ping-pong; FUSED updates the first in
+    place), the residual pair and -- with fused_exchange -- the peers'
+    replicas mapped through CUDA IPC.  If the replicas cannot be mapped
+    (no P2P path), it falls back to the all-gather and says why in
+    `fallback`."""
+
+    def __init__(self, local, exchange: TorchExchange, device="cuda", fused_exchange: bool = False,
+                 pairs_on_host: bool = False):
+        import torch
+
+        self.local, self.exchange, self.pairs_on_host = local, exchange, pairs_on_host
+        P, S = exchange.world, local.slice
+        self.bufs = [torch.zeros(P * S, dtype=torch.float64, device=device) for _ in range(2)]
+        self.pair = torch.zeros(2, dtype=torch.float64, device=device)
+        self.reps, self.fallback = None, None
+        if fused_exchange:
+            dev = self.bufs[0].device.index or 0
+            try:
+                self.reps = PeerReplicas(self.bufs, exchange.group, dev)
+            except B200Error as e:
+                self.fallback = f"fused exchange unavailable ({e}); NCCL all-gather used"
+
+    def rebind(self, local) -> None:
+        """Reuse buffers and replicas for a re-created part of the same shape."""
+        if local.slice != self.local.slice:
+            raise ValueError("rebind: part slice differs")
+        self.local = local
+
+    @property
+    def fused_exchange(self) -> bool:
+        return self.reps is not None
+
+    def solve(self, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF,
+              want_ranks: bool = True) -> PartResult:
+        if engine not in (ENGINE_EC, ENGINE_FUSED):
+            raise ValueError("multi-GPU engines: EC or FUSED")
+        local, exchange, S = self.local, self.exchange, self.local.slice
+        ri = 0  # index of the buffer read this iteration
+        local.init(self.bufs[0])
+        exchange.allgather_slices(self.bufs[0], S)
+        res = PartResult(np.empty(0))
+        for it in range(int(cfg.max_iterations)):
+            t0 = time.perf_counter()
+            wi = 1 - ri if engine == ENGINE_EC else ri
+            read, write = self.bufs[ri], self.bufs[wi]
+            if self.reps is not None:
+                # the sweep's epilogue stores into every peer replica (P2P)
+                local.sweep_peers(engine, cfg, read, write, self.reps.ptrs[wi], self.pair)
+            else:
+                local.sweep(engine, cfg, read, write, self.pair)
+                exchange.allgather_slices(write, S)
+            # the residual all-gather is also the barrier that keeps a fast
+            # rank from writing a replica a slower peer is still reading
+            pr = self.pair.cpu() if self.pairs_on_host else self.pair
+            err, l1 = _reduce_pairs(exchange.allgather_pairs(pr).cpu().numpy())
+            res.iter_seconds.append(time.perf_counter() - t0)
+            res.errors.append(err)
+            res.l1_errors.append(l1)
+            res.iterations = it + 1
+            ri = wi
+            if (l1 if norm == NORM_L1 else err) <= cfg.threshold:
+                break
+        crit = res.l1_errors[-1] if norm == NORM_L1 else res.errors[-1]
+        res.converged = crit <= cfg.threshold
+        if want_ranks:
+            res.ranks = local.ranks()
+        return res
+
+    def close(self):
+        if self.reps is not None:
+            import torch
+
+            torch.cuda.synchronize()
+            self.exchange.dist.barrier(group=self.exchange.group)  # no peer still writes into ours
+            self.reps.close()
+            self.reps = None
+
+
 def solve_partitioned(local, exchange: TorchExchange, engine: int, cfg: PageRankConfig,
-                      norm: int = NORM_LINF, device="cuda", want_ranks: bool = True) -> PartResult:
-    """Run `engine` to convergence on this rank's part (one process per GPU).
-    want_ranks=False leaves the part's ranks on the device (benchmarking)."""
-    import torch
-
-    if engine not in (ENGINE_EC, ENGINE_FUSED):
-        raise ValueError("multi-GPU engines: EC or FUSED")
-    P, S = exchange.world, local.slice
-    a = torch.zeros(P * S, dtype=torch.float64, device=device)
-    b = torch.zeros_like(a) if engine == ENGINE_EC else a
-    pair = torch.zeros(2, dtype=torch.float64, device=device)
-    local.init(a)
-    exchange.allgather_slices(a, S)
-    res = PartResult(np.empty(0))
-    for it in range(int(cfg.max_iterations)):
-        t0 = time.perf_counter()
-        local.sweep(engine, cfg, a, b, pair)
-        exchange.allgather_slices(b, S)
-        pairs = exchange.allgather_pairs(pair).cpu().numpy()
-        err, l1 = _reduce_pairs(pairs)
-        res.iter_seconds.append(time.perf_counter() - t0)
-        res.errors.append(err)
-        res.l1_errors.append(l1)
-        res.iterations = it + 1
-        if engine == ENGINE_EC:
-            a, b = b, a
-        if (l1 if norm == NORM_L1 else err) <= cfg.threshold:
-            break
-    crit = res.l1_errors[-1] if norm == NORM_L1 else res.errors[-1]
-    res.converged = crit <= cfg.threshold
-    if want_ranks:
-        res.ranks = local.ranks()
-    return res
+                      norm: int = NORM_LINF, device="cuda", want_ranks: bool = True,
+                      fused_exchange: bool = False, pairs_on_host: bool = False) -> PartResult:
+    """Run `engine` to convergence on this rank's part (one process per GPU);
+    a one-shot PartitionedSolver.  want_ranks=False leaves the part's ranks on
+    the device (benchmarking).  fused_exchange=True replaces the per-iteration
+    all-gather of contribution slices by the sweep's own P2P stores into the
+    peers' replicas.  pairs_on_host moves the 16-B pair through host memory
+    (gloo groups)."""
+    s = PartitionedSolver(local, exchange, device, fused_exchange, pairs_on_host)
+    try:
+        return s.solve(engine, cfg, norm, want_ranks)
+    finally:
+        s.close()
 
 
-def solve_emulated(parts, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF) -> PartResult:
+def solve_emulated(parts, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF,
+                   fused_exchange: bool = False) -> PartResult:
     """All parts in one process on one GPU (EmulatedExchange): returns the
-    concatenated global rank vector."""
+    concatenated global rank vector.  fused_exchange=True has each part's
+    sweep store its slice into the other parts' vectors (the P2P-store path
+    with local pointers) instead of the copy exchange."""
     import torch
 
     P, S = len(parts), parts[0].slice
@@ -220,9 +367,13 @@ def solve_emulated(parts, engine: int, cfg: PageRankConfig, norm: int = NORM_LIN
     res = PartResult(np.empty(0))
     for it in range(int(cfg.max_iterations)):
         for r in range(P):
-            parts[r].sweep(engine, cfg, A[r], B[r], pairs[r])
+            if fused_exchange:
+                parts[r].sweep_peers(engine, cfg, A[r], B[r], [x.data_ptr() for x in B], pairs[r])
+            else:
+                parts[r].sweep(engine, cfg, A[r], B[r], pairs[r])
         torch.cuda.synchronize()
-        ex.allgather_slices_all(B, S)
+        if not fused_exchange:
+            ex.allgather_slices_all(B, S)
         err, l1 = _reduce_pairs(torch.cat(pairs).cpu().numpy())
         res.errors.append(err)
         res.l1_errors.append(l1)

@@ -29,3 +29,98 @@ def test_partitioned_ec_matches_oracle(oracle, P):
     assert fu.converged and oracle.l1_norm(fu.ranks, xstar) <= g.n * 1e-10 * 0.85 / 0.15
     for p in parts:
         p.close()
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_fused_exchange_matches_copy_exchange(oracle, P):
+    """The fused exchange (sweep epilogue stores into the other parts'
+    vectors, fpr_b200_part_sweep_peers) exchanges exactly the values the copy
+    all-gather would: EC is bit-identical to the copy path; FusEd (in place,
+    peers see fresher values) converges within the L-inf-threshold bound."""
+    n, s, d = oracle.generate_rmat(16, 16, seed=1)
+    g = oracle.build_csr(n, s, d)
+    stream = fb.torch_stream_handle()
+    with fb.DeviceGraph.from_graph(fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)) as full:
+        parts = [B200Part(full, P, r, stream=stream) for r in range(P)]
+    cfg = fb.PageRankConfig(threshold=1e-10)
+    copy = solve_emulated(parts, fb.ENGINE_EC, cfg)
+    fused = solve_emulated(parts, fb.ENGINE_EC, cfg, fused_exchange=True)
+    assert fused.iterations == copy.iterations
+    np.testing.assert_array_equal(fused.ranks, copy.ranks)
+    assert fused.errors == copy.errors
+    fu = solve_emulated(parts, fb.ENGINE_FUSED, cfg, fused_exchange=True)
+    xstar = oracle.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
+    assert fu.converged and oracle.l1_norm(fu.ranks, xstar) <= g.n * 1e-10 * 0.85 / 0.15
+    for p in parts:
+        p.close()
+
+
+def _ipc_worker(rank, world, port, path, q):
+    """One of two processes on the SAME GPU: CUDA-IPC replicas + fused
+    exchange, gloo for handles/pairs.  The processes' sweep kernels never wait
+    on each other; the host barrier (pair all-gather) orders the iterations."""
+    import os
+    import sys
+
+    sys.path.insert(0, path)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import paper_2203_09284_b200 as fbw
+    from oracle import Oracle
+    from paper_2203_09284_b200.dist import B200Part as Part, TorchExchange, solve_partitioned
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        n, s, d = o.generate_rmat(14, 16, seed=3)
+        g = o.build_csr(n, s, d)
+        with fbw.DeviceGraph.from_graph(fbw.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)) as full:
+            part = Part(full, world, rank)
+        ex = TorchExchange()
+
+        class HostGather(TorchExchange):  # gloo: slices through host memory for the one initial exchange
+            def allgather_slices(self, buf, slice_):
+                import torch
+
+                h = buf.cpu()
+                mine = h[self.rank * slice_:(self.rank + 1) * slice_].clone()
+                self.dist.all_gather_into_tensor(h, mine)
+                buf.copy_(h)
+
+        res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, fbw.PageRankConfig(threshold=1e-10),
+                                fused_exchange=True, pairs_on_host=True)
+        out = [None] * world
+        dist.all_gather_object(out, (res.iterations, res.ranks.tolist()))
+        if rank == 0:
+            ref = o.pagerank_ec(g, threshold=1e-10)
+            ranks = np.concatenate([np.array(x[1]) for x in out])
+            q.put((out[0][0], ref.iterations, float(np.max(np.abs(ranks - ref.ranks) / ref.ranks))))
+        part.close()
+        del ex
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_exchange_two_processes_cuda_ipc():
+    import multiprocessing as mp
+    import os
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, root, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    it, ref_it, rel = q.get(timeout=5)
+    assert it == ref_it and rel <= 1e-12
