@@ -316,7 +316,7 @@ __device__ __forceinline__ double task_sums(const double (&v)[8], unsigned bits8
   return acc;
 }
 
-template <bool ASYNC>
+template <bool ASYNC, bool PEERS>
 __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const TaskMeta& m,
                                             double acc, unsigned bits8, const RowPre& rp,
                                             double* cur, WarpSmem& ws, int lane, double& lmax,
@@ -410,7 +410,8 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         else
           cur[r] = c;
         // fused exchange: the same (coalesced) store into every peer replica
-        for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
+        if (PEERS)
+          for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
       }
       const double d = fabs(nv - ov);
       lmax = fmax(lmax, d);
@@ -429,7 +430,7 @@ __device__ __forceinline__ unsigned load_bits8(const SolveParams& p, int t, int 
   return (__ldg(p.task_bits + 8 * (int64_t)t + (lane >> 2)) >> ((lane & 3) * 8)) & 0xffu;
 }
 
-template <bool ASYNC>
+template <bool ASYNC, bool PEERS>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
                                           double* cur, WarpSmem& ws, int lane,
@@ -467,7 +468,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
         if (tn + 2 * nwarps < te) mnnn = load_meta(p, tn + 2 * nwarps);
       }
     }
-    task_finish<ASYNC>(p, t, m, acc, bits, rp, cur, ws, lane, lmax, lsum);
+    task_finish<ASYNC, PEERS>(p, t, m, acc, bits, rp, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;
@@ -482,7 +483,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
 // ------------------------------------------------------ persistent solver
 // ASYNC=false: Jacobi (nwaves == 1, EC) or wave-lockstep Gauss-Seidel.
 // ASYNC=true : block-asynchronous Gauss-Seidel, in-place contributions.
-template <bool ASYNC, int BT, int MB>
+template <bool ASYNC, int BT, int MB, bool PEERS>
 __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
   constexpr int kWPB = BT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -499,13 +500,13 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
     double lmax = 0.0, lsum = 0.0;
     if (ASYNC) {
       // in place: reads through the full vector, writes to this part's slice
-      run_tasks<true>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0 + p.write_off, ws, lane, pol,
+      run_tasks<true, PEERS>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0 + p.write_off, ws, lane, pol,
                       lmax, lsum);
     } else {
       const double* prev = par ? p.contrib1 : p.contrib0;
       double* cur = (par ? p.contrib0 : p.contrib1) + p.write_off;
       for (int w = 0; w < p.nwaves; ++w) {
-        run_tasks<false>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
+        run_tasks<false, PEERS>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
                          __ldg(p.wave_row + w), prev, cur, ws, lane, pol, lmax, lsum);
         if (w + 1 < p.nwaves) grid_sync(p.bar);
       }
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
         *p.out_iters = it + 1;
         *p.out_stop = crit <= p.threshold ? 1 : 0;
       }
-      if (p.npeers) __threadfence_system();  // peer-replica stores performed before exit
+      if (PEERS) __threadfence_system();  // peer-replica stores performed before exit
       return;
     }
   }
@@ -765,30 +766,40 @@ struct SolveShape {
   int smem;
 };
 
-static SolveShape solve_shape(int engine) {
+// PEERS: the fused-exchange instantiation (peer-replica stores in the
+// epilogue); the plain one carries no trace of it.
+static SolveShape solve_shape(int engine, bool peers) {
   if (engine == kFused)
-    return {(const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB>, FPR_ASYNC_BLOCK,
-            solve_smem_bytes<FPR_ASYNC_BLOCK>()};
-  return {(const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB>, FPR_EC_BLOCK,
-          solve_smem_bytes<FPR_EC_BLOCK>()};
+    return {peers ? (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, true>
+                  : (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, false>,
+            FPR_ASYNC_BLOCK, solve_smem_bytes<FPR_ASYNC_BLOCK>()};
+  return {peers ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, true>
+                : (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, false>,
+          FPR_EC_BLOCK, solve_smem_bytes<FPR_EC_BLOCK>()};
 }
 
-int solve_block_threads(int engine) { return solve_shape(engine).block; }
+int solve_block_threads(int engine) { return solve_shape(engine, false).block; }
 
+// Co-resident grid for the engine: the smaller of the two instantiations'
+// occupancy, so either can be launched cooperatively with it.
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
-  const SolveShape sh = solve_shape(engine);
-  cudaError_t e = cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.block, sh.smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  *grid_out = per_sm * num_sms;
+  int best = 1 << 30;
+  for (bool peers : {false, true}) {
+    const SolveShape sh = solve_shape(engine, peers);
+    cudaError_t e = cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sh.fn, sh.block, sh.smem);
+    if (e != cudaSuccess) return e;
+    best = std::min(best, per_sm);
+  }
+  if (best < 1) return cudaErrorInvalidConfiguration;
+  *grid_out = best * num_sms;
   return cudaSuccess;
 }
 
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s) {
-  const SolveShape sh = solve_shape(engine);
+  const SolveShape sh = solve_shape(engine, p.npeers > 0);
   SolveParams copy = p;
   void* args[] = {&copy};
   return cudaLaunchCooperativeKernel(sh.fn, dim3(grid), dim3(sh.block), args, sh.smem, s);
