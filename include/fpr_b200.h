@@ -84,6 +84,11 @@ typedef struct fpr_config {
 #define FPR_B200_OPT_REORDER 1u /* renumber vertices by descending out-degree inside
                                   the library (locality for contrib gathers); ranks
                                   and traces are reported in the caller's ids */
+#define FPR_B200_OPT_BLOCKED 2u /* EC engine: source-blocked sweeps (column blocks of
+                                  2^24 vertices, FPR_B200_BLOCK_SHIFT overrides) so the
+                                  gathers of a block pass stay near L2; only for graphs
+                                  whose contribution vector far exceeds L2 (configs 4/5
+                                  in natural order) */
 
 typedef struct fpr_b200_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */

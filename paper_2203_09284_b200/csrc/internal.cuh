@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace fprb {
@@ -93,6 +94,10 @@ struct SolveParams {
   // P2P-mapped), so the sweep itself performs the all-gather over NVLink.
   int32_t npeers;
   double* peer[kMaxPeers];
+  // Source-blocked EC pass (kModeAccum): local row r is global row brow_ids[r];
+  // its in-block sum is added to partial[brow_ids[r]].
+  const int32_t* brow_ids;
+  double* partial;
 };
 
 enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
@@ -167,5 +172,31 @@ cudaError_t ingest_edge_list(const unsigned char* t, uint64_t len, bool ends_wit
 // generate.cu: build_csr over m (src, dst) int32 pairs with ids in [0, n).
 cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
                                  const char** msg);
+
+// blocked.cu: the source-blocked layout of a graph (FPR_B200_OPT_BLOCKED).
+struct BlockSet {
+  struct Block {
+    DevGraph view;          // local rows (compacted), row_ptr, edges in the block
+    int32_t* ids = nullptr; // local row -> global row
+    Partition part;
+    int32_t* waves = nullptr;  // {0, ntasks, 0, 0}: wave_task / wave_row of a one-wave sweep
+  };
+  int nblocks = 0;
+  int shift = 0;
+  std::vector<Block> blocks;
+  int32_t* src_pool = nullptr;
+  double* partial = nullptr;       // n: per-row sum over the blocks swept so far
+  double* tail_partial = nullptr;  // max_ntasks: split-row pieces (NaN = not ready)
+  double* cta_pairs = nullptr;     // apply pass: per-CTA (max, sum)
+  double* scratch = nullptr;       // per-pass residual slots the accumulate kernel writes
+  int apply_grid = 0;
+  int64_t max_ntasks = 0;
+  int64_t pairs = 0;               // (row, block) pairs = sum of local rows
+  std::vector<void*> allocs;
+};
+cudaError_t build_blocks(const DevGraph& g, int shift, cudaStream_t st, BlockSet& bs, const char** msg);
+void free_blocks(BlockSet& bs, cudaStream_t st);
+cudaError_t launch_apply(const BlockSet& bs, int32_t n, const int32_t* outdeg, double* pr, double* cur,
+                         double base, double damping, double* err, double* l1, cudaStream_t st);
 
 }  // namespace fprb

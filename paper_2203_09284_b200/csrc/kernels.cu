@@ -254,6 +254,14 @@ __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_
   }
 }
 
+// Finalize mode of a solve instantiation:
+//   kModeFinal : rank update + contribution store (single GPU);
+//   kModePeers : ... plus the store into every peer replica (fused exchange);
+//   kModeAccum : source-blocked EC pass: the task's rows are
+//                a column block's compacted rows; each adds its in-block sum
+//                to partial[brow_ids[r]] and the apply pass finishes the row.
+constexpr int kModeFinal = 0, kModePeers = 1, kModeAccum = 2;
+
 // Row metadata of a task's first 32 rows (i0 .. i0+31, including the open
 // row i1 when it falls in that window), prefetched one task ahead, with the
 // row bounds already relative to the task's first edge j0.
@@ -263,6 +271,7 @@ struct RowPre {
   int od;     // outdeg[r] (finalized rows only)
   double ov;  // pr[r]     (finalized rows only)
 };
+template <int MODE>
 __device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMeta& m, int lane) {
   RowPre r{0, 0, 0, 0.0};
   const int row = m.i0 + lane;
@@ -270,8 +279,14 @@ __device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMe
     const int64_t a = __ldg(p.row + row), b = __ldg(p.row + row + 1);
     r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
     r.hi = (int)(b - m.j0);
-    r.od = __ldg(p.outdeg + row);
-    r.ov = p.pr[row];
+    if (MODE != kModeAccum) {
+      r.od = __ldg(p.outdeg + row);
+      r.ov = p.pr[row];
+    } else {  // accumulate pass: od = global row, ov = its running partial (prefetched:
+              // only this task writes that slot during the pass)
+      r.od = __ldg(p.brow_ids + row);
+      r.ov = p.partial[r.od];
+    }
   } else if (row == m.i1 && row < p.n) {
     const int64_t a = __ldg(p.row + row);
     r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
@@ -316,7 +331,7 @@ __device__ __forceinline__ double task_sums(const double (&v)[8], unsigned bits8
   return acc;
 }
 
-template <bool ASYNC, bool PEERS>
+template <bool ASYNC, int MODE>
 __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const TaskMeta& m,
                                             double acc, unsigned bits8, const RowPre& rp,
                                             double* cur, WarpSmem& ws, int lane, double& lmax,
@@ -391,8 +406,10 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
       if (rb != i0) {
         lo = (int)(__ldg(p.row + r) - j0);
         hi = (int)(__ldg(p.row + r + 1) - j0);
-        od = __ldg(p.outdeg + r);
-        ov = p.pr[r];
+        if (MODE != kModeAccum) {
+          od = __ldg(p.outdeg + r);
+          ov = p.pr[r];
+        }
       }
       double sum = 0.0;
       if (lo < hi) {
@@ -401,6 +418,12 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         if (lo + off < (e & ~7)) sum = ws.carry[e >> 3] + sum;
       }
       if (r == i0 && has_head) sum = head_extra + sum;
+      if (MODE == kModeAccum) {  // blocks run in order: one writer per (row, block)
+        const int gid = rb == i0 ? rp.od : __ldg(p.brow_ids + r);
+        const double before = rb == i0 ? rp.ov : p.partial[gid];
+        p.partial[gid] = before + sum;
+        continue;
+      }
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
       p.pr[r] = nv;
       if (od > 0) {
@@ -410,7 +433,7 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         else
           cur[r] = c;
         // fused exchange: the same (coalesced) store into every peer replica
-        if (PEERS)
+        if (MODE == kModePeers)
           for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
       }
       const double d = fabs(nv - ov);
@@ -430,7 +453,7 @@ __device__ __forceinline__ unsigned load_bits8(const SolveParams& p, int t, int 
   return (__ldg(p.task_bits + 8 * (int64_t)t + (lane >> 2)) >> ((lane & 3) * 8)) & 0xffu;
 }
 
-template <bool ASYNC, bool PEERS>
+template <bool ASYNC, int MODE>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
                                           double* cur, WarpSmem& ws, int lane,
@@ -443,7 +466,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
     const Src8 sx = load_src8(p, m, lane, pol);
     issue_gathers8<ASYNC>(m, sx, lane, fresh_below, prev, cur, v);
   }
-  RowPre rp = load_rowpre(p, m, lane);
+  RowPre rp = load_rowpre<MODE>(p, m, lane);
   unsigned bits = load_bits8(p, t, lane);
   TaskMeta mn{0, 0, 0, 0}, mnn{0, 0, 0, 0};
   Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
@@ -461,14 +484,14 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
     TaskMeta mnnn{0, 0, 0, 0};
     if (tn < te) {
       issue_gathers8<ASYNC>(mn, sn, lane, fresh_below, prev, cur, v);
-      rpn = load_rowpre(p, mn, lane);
+      rpn = load_rowpre<MODE>(p, mn, lane);
       bitsn = load_bits8(p, tn, lane);
       if (tn + nwarps < te) {
         snn = load_src8(p, mnn, lane, pol);
         if (tn + 2 * nwarps < te) mnnn = load_meta(p, tn + 2 * nwarps);
       }
     }
-    task_finish<ASYNC, PEERS>(p, t, m, acc, bits, rp, cur, ws, lane, lmax, lsum);
+    task_finish<ASYNC, MODE>(p, t, m, acc, bits, rp, cur, ws, lane, lmax, lsum);
     if (tn >= te) break;
     t = tn;
     m = mn;
@@ -483,7 +506,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
 // ------------------------------------------------------ persistent solver
 // ASYNC=false: Jacobi (nwaves == 1, EC) or wave-lockstep Gauss-Seidel.
 // ASYNC=true : block-asynchronous Gauss-Seidel, in-place contributions.
-template <bool ASYNC, int BT, int MB, bool PEERS>
+template <bool ASYNC, int BT, int MB, int MODE>
 __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
   constexpr int kWPB = BT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -500,13 +523,13 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
     double lmax = 0.0, lsum = 0.0;
     if (ASYNC) {
       // in place: reads through the full vector, writes to this part's slice
-      run_tasks<true, PEERS>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0 + p.write_off, ws, lane, pol,
+      run_tasks<true, MODE>(p, 0, p.ntasks, gwarp, nwarps, 0, p.contrib0, p.contrib0 + p.write_off, ws, lane, pol,
                       lmax, lsum);
     } else {
       const double* prev = par ? p.contrib1 : p.contrib0;
       double* cur = (par ? p.contrib0 : p.contrib1) + p.write_off;
       for (int w = 0; w < p.nwaves; ++w) {
-        run_tasks<false, PEERS>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
+        run_tasks<false, MODE>(p, __ldg(p.wave_task + w), __ldg(p.wave_task + w + 1), gwarp, nwarps,
                          __ldg(p.wave_row + w), prev, cur, ws, lane, pol, lmax, lsum);
         if (w + 1 < p.nwaves) grid_sync(p.bar);
       }
@@ -526,7 +549,7 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
         *p.out_iters = it + 1;
         *p.out_stop = crit <= p.threshold ? 1 : 0;
       }
-      if (PEERS) __threadfence_system();  // peer-replica stores performed before exit
+      if (MODE == kModePeers) __threadfence_system();  // peer-replica stores performed before exit
       return;
     }
   }
@@ -766,26 +789,27 @@ struct SolveShape {
   int smem;
 };
 
-// PEERS: the fused-exchange instantiation (peer-replica stores in the
-// epilogue); the plain one carries no trace of it.
-static SolveShape solve_shape(int engine, bool peers) {
+// One instantiation per finalize mode; the plain one carries no trace of the
+// others.  (The async engine has no accumulate mode.)
+static SolveShape solve_shape(int engine, int mode) {
   if (engine == kFused)
-    return {peers ? (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, true>
-                  : (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, false>,
+    return {mode == kModePeers ? (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModePeers>
+                               : (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModeFinal>,
             FPR_ASYNC_BLOCK, solve_smem_bytes<FPR_ASYNC_BLOCK>()};
-  return {peers ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, true>
-                : (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, false>,
-          FPR_EC_BLOCK, solve_smem_bytes<FPR_EC_BLOCK>()};
+  const void* fn = mode == kModePeers   ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModePeers>
+                   : mode == kModeAccum ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModeAccum>
+                                        : (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModeFinal>;
+  return {fn, FPR_EC_BLOCK, solve_smem_bytes<FPR_EC_BLOCK>()};
 }
 
-int solve_block_threads(int engine) { return solve_shape(engine, false).block; }
+int solve_block_threads(int engine) { return solve_shape(engine, kModeFinal).block; }
 
-// Co-resident grid for the engine: the smaller of the two instantiations'
+// Co-resident grid for the engine: the smallest of its instantiations'
 // occupancy, so either can be launched cooperatively with it.
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
   int best = 1 << 30;
-  for (bool peers : {false, true}) {
-    const SolveShape sh = solve_shape(engine, peers);
+  for (int mode : {kModeFinal, kModePeers, kModeAccum}) {
+    const SolveShape sh = solve_shape(engine, mode);
     cudaError_t e = cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -799,7 +823,7 @@ cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
 }
 
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s) {
-  const SolveShape sh = solve_shape(engine, p.npeers > 0);
+  const SolveShape sh = solve_shape(engine, p.brow_ids ? kModeAccum : (p.npeers > 0 ? kModePeers : kModeFinal));
   SolveParams copy = p;
   void* args[] = {&copy};
   return cudaLaunchCooperativeKernel(sh.fn, dim3(grid), dim3(sh.block), args, sh.smem, s);

@@ -239,6 +239,7 @@ struct fpr_b200_graph {
   uint32_t nparts = 1, part_id = 0;
   uint32_t flags = 0;
   int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
+  BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
   double* ranks_tmp = nullptr;    // reordered ranks gathered back to caller order
   uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
@@ -268,6 +269,11 @@ void destroy_handle(fpr_b200_graph* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
+  if (h->blk) {
+    free_blocks(*h->blk, h->stream);
+    delete h->blk;
+    h->blk = nullptr;
+  }
   if (h->stream) cudaStreamSynchronize(h->stream);
   release_staging(h->hs);
   for (auto& e : h->ev)
@@ -774,6 +780,130 @@ int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t*
 
 const double* fpr_b200_graph_ranks_device(const fpr_b200_graph* h) { return h ? h->pr : nullptr; }
 
+namespace {
+// The EC solve over the source-blocked layout: per iteration, one accumulate
+// pass of the solve kernel per column block (in block order), then the apply
+// pass and its fixed-order residual reduction; the stop rule is checked on
+// the host after each iteration (pagerank.hpp:141), so the iteration count is
+// the reference's.
+int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* errors_out,
+                double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
+  const DevGraph& g = h->g;
+  float setup_ms = 0.f, solve_ms = 0.f;
+  uint64_t launches = 0;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  if (!h->blk) {
+    // 2^24-vertex blocks (128 MB of contributions) measured best on configs
+    // 4/5; FPR_B200_BLOCK_SHIFT overrides.
+    int shift = 24;
+    if (const char* s = std::getenv("FPR_B200_BLOCK_SHIFT")) shift = std::max(10, std::min(30, std::atoi(s)));
+    while ((((int64_t)g.n + (1ll << shift) - 1) >> shift) > 256) ++shift;
+    auto* bs = new BlockSet;
+    const char* msg = nullptr;
+    cudaError_t e = build_blocks(g, shift, h->stream, *bs, &msg);
+    if (e != cudaSuccess || msg) {
+      delete bs;
+      if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200 blocked layout: ") + msg);
+      return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                  std::string("fpr_b200 blocked layout: ") + cudaGetErrorString(e));
+    }
+    h->blk = bs;
+  }
+  BlockSet& bs = *h->blk;
+  CK(launch_init(g, h->pr, h->contrib[0], h->stream));
+  ++launches;
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  const int wpb = solve_block_threads(kEC) / 32;
+  SolveParams p{};
+  p.pr = h->pr;
+  p.damping = cfg->damping;
+  p.base = (1.0 - cfg->damping) / (double)g.n;
+  p.threshold = 0.0;
+  p.norm = h->norm;
+  p.max_iters = 1;
+  p.parity0 = 0;
+  p.nwaves = 1;
+  p.tail_partial = bs.tail_partial;
+  p.partial = bs.partial;
+  p.errors = bs.scratch;
+  p.l1errors = bs.scratch + 1;
+  p.iter_ns = reinterpret_cast<unsigned long long*>(bs.scratch + 2);
+  p.partials = h->partials;
+  p.totals = h->totals;
+  p.bar = h->bar;
+  p.out_iters = h->d_iters;
+  p.out_stop = h->d_stop;
+  uint64_t total = 0;
+  int par = 0;
+  double last_err = 1.0, last_l1 = 1.0;
+  while (total < cfg->max_iterations) {
+    double* prev = h->contrib[par];
+    double* cur = h->contrib[par ^ 1];
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    for (const BlockSet::Block& B : bs.blocks) {
+      if (B.view.n == 0) continue;
+      SolveParams q = p;
+      q.n = B.view.n;
+      q.row = B.view.row;
+      q.src = B.view.src;
+      q.task_row = B.part.task_row;
+      q.task_edge = B.part.task_edge;
+      q.head_first = B.part.head_first;
+      q.task_bits = B.part.task_bits;
+      q.ntasks = B.part.ntasks;
+      q.wave_task = B.waves;
+      q.wave_row = B.waves + 2;
+      q.brow_ids = B.ids;
+      q.contrib0 = prev;
+      q.contrib1 = cur;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[0], (B.part.ntasks + wpb - 1) / wpb));
+      CK(launch_solve(kEC, grid, q, h->stream));
+      ++launches;
+    }
+    CK(launch_apply(bs, g.n, g.outdeg, h->pr, cur, p.base, p.damping, h->d_errors, h->d_l1, h->stream));
+    launches += 2;
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    CK(cudaMemcpyAsync(h->h_errors, h->d_errors, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->h_l1, h->d_l1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (total == 0) cudaEventElapsedTime(&setup_ms, h->ev[0], h->ev[1]);
+    float it_ms = 0.f;
+    cudaEventElapsedTime(&it_ms, h->ev[1], h->ev[2]);
+    solve_ms += it_ms;
+    if (errors_out && errors_cap < total + 1)
+      return fail(FPR_B200_EINVAL, "fpr_b200_run: errors buffer holds " + std::to_string(errors_cap) +
+                                       " entries, need " + std::to_string(total + 1));
+    last_err = h->h_errors[0];
+    last_l1 = h->h_l1[0];
+    if (errors_out) errors_out[total] = last_err;
+    if (l1_out) l1_out[total] = last_l1;
+    if (iter_ns_out) iter_ns_out[total] = (uint64_t)(it_ms * 1e6);
+    ++total;
+    par ^= 1;
+    if ((h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err) <= cfg->threshold) break;
+  }
+  if (ranks_out) {
+    const double* src = h->pr;
+    if (h->new_of_old) {
+      CK(launch_gather_ranks(h->pr, h->new_of_old, g.n, h->ranks_tmp, h->stream));
+      src = h->ranks_tmp;
+    }
+    CK(cudaMemcpyAsync(ranks_out, src, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  if (result) {
+    result->iterations = total;
+    const double crit = h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err;
+    result->converged = (total > 0 && crit <= cfg->threshold) ? 1 : 0;
+    result->final_error = total > 0 ? last_err : 1.0;
+    result->setup_ms = setup_ms;
+    result->solve_ms = solve_ms;
+    result->kernel_launches = launches;
+  }
+  return FPR_B200_OK;
+}
+}  // namespace
+
 int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* ranks_out,
                  double* errors_out, double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap,
                  fpr_b200_result* result) {
@@ -784,6 +914,8 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   if (engine != kEC && engine != kFused && engine != kLockstep)
     return fail(FPR_B200_EINVAL, "fpr_b200: unknown engine " + std::to_string(engine));
   CK(cudaSetDevice(h->device));
+  if (engine == kEC && (h->flags & FPR_B200_OPT_BLOCKED) && h->nparts <= 1)
+    return run_blocked(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
 
   // Jacobi = one wave; lockstep = the cached wave schedule; async = all tasks.
   const Waves* wv = nullptr;

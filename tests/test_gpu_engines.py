@@ -244,3 +244,24 @@ def test_pinned_upload_split(config1, share, monkeypatch):
                 fb.DeviceGraph.from_graph(pg)
         finally:
             src[pos] = old
+
+
+@pytest.mark.parametrize("shift,reorder", [(12, False), (14, False), (12, True), (22, False)])
+def test_blocked_ec_matches_oracle(config1, oracle, shift, reorder, monkeypatch):
+    """FPR_B200_OPT_BLOCKED: source-blocked EC sweeps (accumulate passes per
+    column block + apply pass) give the reference's per-iteration ranks within
+    1e-12 relative and its iteration count, for 1..16 blocks."""
+    rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_BLOCK_SHIFT", str(shift))
+    ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
+    with fb.DeviceGraph.from_graph(to_fb(g), blocked=True, reorder=reorder) as d2:
+        r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=1))
+        assert rel(r1.ranks.values, ref.history[0]) <= EC_RTOL
+        r3 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
+        assert rel(r3.ranks.values, ref.history[2]) <= EC_RTOL
+        r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))  # unblocked engines still work
+    assert r.trace.iterations == ref.iterations and r.trace.converged
+    assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
+    assert np.max(np.abs(r.trace.errors - ref.errors)) <= EC_RTOL * float(ref.ranks.max())
+    assert fu.trace.converged
