@@ -101,6 +101,10 @@ struct SolveParams {
 };
 
 enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
+// Launch-shape id of the async engine on graphs whose contributions exceed
+// ~64 MB (20 warps/SM instead of 16: more gathers in flight for DRAM-bound
+// sweeps; measured).  Internal only.
+constexpr int kFusedWide = 3;
 
 // kernels.cu
 cudaError_t launch_partition(const DevGraph& g, Partition& p, cudaStream_t s);

@@ -241,10 +241,17 @@ __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_
   const double* basep = ASYNC ? prev : ((s < fresh_below) ? cur : prev);
   const double* addr = basep + s;
   if (ASYNC) {  // value-atomic live read (pagerank.hpp:305)
+#ifdef FPR_ASYNC_CG
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cg.f64 %0, [%1]; }"
+                 : "+d"(v)
+                 : "l"(addr), "r"((int)valid)
+                 : "memory");
+#else
     asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.relaxed.gpu.global.f64 %0, [%1]; }"
                  : "+d"(v)
                  : "l"(addr), "r"((int)valid)
                  : "memory");
+#endif
   } else {
     // L2 only: random 8-B gathers have no L1 reuse (an L1-allocating ld.ca
     // variant measured no faster even on R-MAT hubs)
@@ -792,6 +799,10 @@ struct SolveShape {
 // One instantiation per finalize mode; the plain one carries no trace of the
 // others.  (The async engine has no accumulate mode.)
 static SolveShape solve_shape(int engine, int mode) {
+  if (engine == kFusedWide)
+    return {mode == kModePeers ? (const void*)solve_kernel<true, FPR_EC_BLOCK, FPR_EC_MINB, kModePeers>
+                               : (const void*)solve_kernel<true, FPR_EC_BLOCK, FPR_EC_MINB, kModeFinal>,
+            FPR_EC_BLOCK, solve_smem_bytes<FPR_EC_BLOCK>()};
   if (engine == kFused)
     return {mode == kModePeers ? (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModePeers>
                                : (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModeFinal>,

@@ -213,6 +213,7 @@ struct fpr_b200_graph {
   double* contrib[2] = {nullptr, nullptr};
   double* tail_partial = nullptr;
   int grid_full[2] = {0, 0};  // [0]=Jacobi/lockstep kernel, [1]=async kernel
+  int async_shape = kFused;   // kFusedWide when the contributions exceed ~64 MB
   double* partials = nullptr;
   double* totals = nullptr;
   GridBar* bar = nullptr;
@@ -374,7 +375,8 @@ int finish_graph(fpr_b200_graph* h) {
   // tail partials start "not ready" (NaN); each consumer re-arms what it reads.
   CK(cudaMemsetAsync(h->tail_partial, 0xFF, (nt + 1) * sizeof(double), h->stream));
   CK(solve_grid(kEC, h->num_sms, &h->grid_full[0]));
-  CK(solve_grid(kFused, h->num_sms, &h->grid_full[1]));
+  h->async_shape = (int64_t)g.n * (int64_t)sizeof(double) > (64ll << 20) ? kFusedWide : kFused;
+  CK(solve_grid(h->async_shape, h->num_sms, &h->grid_full[1]));
   const int gmax = std::max(h->grid_full[0], h->grid_full[1]);
   if ((rc = dalloc_n(h, &h->partials, 2 * gmax)) || (rc = dalloc_n(h, &h->totals, 2)) ||
       (rc = dalloc_n(h, &h->bar, 1)) || (rc = dalloc_n(h, &h->d_iters, 1)) ||
@@ -924,7 +926,8 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     return fail(FPR_B200_ECUDA, "fpr_b200: internal error (EC wave schedule)");
   }
   const int variant = engine == kFused ? 1 : 0;
-  const int wpb = solve_block_threads(engine) / 32;
+  const int shape = engine == kFused ? h->async_shape : engine;
+  const int wpb = solve_block_threads(shape) / 32;
   const int64_t want = (h->part.ntasks + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
 
@@ -978,7 +981,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     p.max_iters = (uint32_t)chunk;
     p.parity0 = parity;
     CK(cudaEventRecord(h->ev[1], h->stream));
-    CK(launch_solve(engine, grid, p, h->stream));
+    CK(launch_solve(shape, grid, p, h->stream));
     CK(cudaEventRecord(h->ev[2], h->stream));
     ++launches;
     CK(cudaMemcpyAsync(h->h_iters, h->d_iters, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
@@ -1141,7 +1144,8 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   const Waves* wv = nullptr;
   if ((rc = get_waves(h, 1u, &wv))) return rc;
   const int variant = engine == kFused ? 1 : 0;
-  const int wpb = solve_block_threads(engine) / 32;
+  const int shape = engine == kFused ? h->async_shape : engine;
+  const int wpb = solve_block_threads(shape) / 32;
   const int64_t want = (h->part.ntasks + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
   const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
@@ -1183,7 +1187,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
     if (!peer_write[q]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: null peer pointer");
     p.peer[p.npeers++] = peer_write[q] + p.write_off;  // this part's slice in part q's replica
   }
-  CK(launch_solve(engine, grid, p, h->stream));
+  CK(launch_solve(shape, grid, p, h->stream));
   CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   return FPR_B200_OK;
