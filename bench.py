@@ -259,6 +259,39 @@ def ingest_leg(fb, g, device) -> dict:
     return out
 
 
+def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
+    """BASELINE configs 3-5 on one GPU, generated on the device (untimed):
+    EC and FusEd time-to-converge at L-inf 1e-10, ms per sweep, GTEPS and
+    the HBM-roofline fraction (12 m + 36 n bytes per sweep).  Not the
+    headline metric; reported beside it.  Solve times are CUDA-event times
+    of the persistent solve launches (resident graph)."""
+    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
+    peak, _ = peaks()
+    out = {}
+    for c in which:
+        if c == "3":
+            dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(24, 16, seed=3), relabel_bfs=True, device=device)
+            name = "config3: RMAT s24 ef16 seed 3, BFS crawl-order relabel"
+        elif c == "4":
+            dg = fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, device=device)
+            name = "config4: Chung-Lu n=2^26, 1.2e9 draws, alpha 2.1, seed 4, random order"
+        else:
+            dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device,
+                                              reorder=c.endswith("r"))
+            name = "config5: RMAT s28 ef16 seed 5" + (" + FPR_B200_OPT_REORDER" if c.endswith("r") else "")
+        with dg:
+            rec = {"workload": name, "n": dg.n, "m": dg.m}
+            for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED, "fused")):
+                r = dg.run(eng, cfg, copy_ranks=False, copy_trace=False)
+                ms_it = r.solve_ms / r.trace.iterations
+                rec[tag] = {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
+                            "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it,
+                            "gteps": dg.m / ms_it / 1e6,
+                            "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
+            out["config" + c] = rec
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -268,6 +301,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ingest", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip configs 3-5 (about 1 min)")
     ap.add_argument("--copy-exchange", action="store_true",
                     help="N>1: NCCL all-gather of slices instead of the fused P2P-store exchange")
     ap.add_argument("--partitioned", action="store_true",
@@ -349,6 +383,8 @@ def main() -> None:
     fused = {}
     fr = [dg.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False) for _ in range(max(3, args.steps // 4))]
     fused = {"engine": "fused_b200", "iterations": fr[-1].trace.iterations,
+             "roofline_frac": algorithmic_bytes(n, m) * fr[-1].trace.iterations
+             / (float(np.mean([x.solve_ms for x in fr])) * 1e-3) / 1e9 / peaks()[0],
              "iterations_min_max": [min(x.trace.iterations for x in fr), max(x.trace.iterations for x in fr)],
              "ms_per_solve": float(np.mean([x.solve_ms for x in fr])),
              "gteps": float(np.mean([m * x.trace.iterations / x.solve_ms / 1e6 for x in fr]))}
@@ -366,6 +402,9 @@ def main() -> None:
         if g_host is None:
             g_host = dg.download()
         ingest = ingest_leg(fb, g_host, local)
+    large = None
+    if rank == 0 and ws == 1 and not args.no_large:
+        large = large_configs_leg(fb, local)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         if g_host is None:
@@ -396,6 +435,7 @@ def main() -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ingest": ingest,
+            "configs_3_5": large,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
         }

@@ -1,6 +1,6 @@
 # Round profile artefacts for the bench command: plain run, ncu launch list, one full capture.
 T=${1:-r1}
-CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-ingest"
+CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-ingest --no-large"
 timeout -s KILL 300 $CMD > gpurun_out/plain_bench_$T.json 2> gpurun_out/plain_bench_$T.err && \
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches_$T.csv $CMD > gpurun_out/ncu_launch_$T.log 2>&1
