@@ -88,14 +88,20 @@ def _ipc_worker(rank, world, port, path, q):
                 self.dist.all_gather_into_tensor(h, mine)
                 buf.copy_(h)
 
-        res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, fbw.PageRankConfig(threshold=1e-10),
-                                fused_exchange=True, pairs_on_host=True)
+        cfg = fbw.PageRankConfig(threshold=1e-10)
+        res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, cfg, fused_exchange=True, pairs_on_host=True)
+        # FusEd in place: peers' P2P stores land in the vector this rank is sweeping
+        fres = solve_partitioned(part, HostGather(), fbw.ENGINE_FUSED, cfg, fused_exchange=True,
+                                 pairs_on_host=True)
         out = [None] * world
-        dist.all_gather_object(out, (res.iterations, res.ranks.tolist()))
+        dist.all_gather_object(out, (res.iterations, res.ranks.tolist(), fres.converged, fres.ranks.tolist()))
         if rank == 0:
             ref = o.pagerank_ec(g, threshold=1e-10)
+            xstar = o.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
             ranks = np.concatenate([np.array(x[1]) for x in out])
-            q.put((out[0][0], ref.iterations, float(np.max(np.abs(ranks - ref.ranks) / ref.ranks))))
+            franks = np.concatenate([np.array(x[3]) for x in out])
+            q.put((out[0][0], ref.iterations, float(np.max(np.abs(ranks - ref.ranks) / ref.ranks)),
+                   all(x[2] for x in out), o.l1_norm(franks, xstar), g.n * 1e-10 * 0.85 / 0.15))
         part.close()
         del ex
     finally:
@@ -122,5 +128,6 @@ def test_fused_exchange_two_processes_cuda_ipc():
         if p.is_alive():
             p.kill()
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    it, ref_it, rel = q.get(timeout=5)
+    it, ref_it, rel, fconv, fl1, bound = q.get(timeout=5)
     assert it == ref_it and rel <= 1e-12
+    assert fconv and fl1 <= bound
