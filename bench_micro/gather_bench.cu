@@ -49,8 +49,20 @@ float run(const int* idx, const double* vals, long long m, double* out, int bloc
   return ms / 5;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // "one": a single config-2-shaped launch (n = 2^22, 8 CTAs/SM, U=8, ld.cg) for ncu
+    const long long m1 = 1ll << 26;
+    const int n1 = 1 << 22;
+    int* idx1; double* vals1; double* out1;
+    cudaMalloc(&idx1, m1 * 4); cudaMalloc(&out1, 8); cudaMalloc(&vals1, (size_t)n1 * 8);
+    cudaMemset(vals1, 0, (size_t)n1 * 8);
+    fill_idx<<<1024, 256>>>(idx1, m1, n1, 0);
+    cudaDeviceSynchronize();
+    const float t = run<8, 1>(idx1, vals1, m1, out1, sms * 8, 256);
+    printf("n=%d: %.1f G gathers/s (%.3f ms per 2^26 gathers)\n", n1, m1 / t / 1e6, t);
+    return 0;
+  }
   const long long m = 1ll << 26;
   int* idx; double* vals; double* out;
   cudaMalloc(&idx, m * 4); cudaMalloc(&out, 8);
