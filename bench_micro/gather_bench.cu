@@ -61,6 +61,13 @@ int main(int argc, char** argv) {
     cudaDeviceSynchronize();
     const float t = run<8, 1>(idx1, vals1, m1, out1, sms * 8, 256);
     printf("n=%d: %.1f G gathers/s (%.3f ms per 2^26 gathers)\n", n1, m1 / t / 1e6, t);
+    if (argc > 2) {  // "one all": the load flavours side by side
+      const float tl = run<8, 0>(idx1, vals1, m1, out1, sms * 8, 256);
+      const float tg = run<8, 3>(idx1, vals1, m1, out1, sms * 8, 256);
+      const float t20 = run<8, 1>(idx1, vals1, m1, out1, sms * 5, 128);
+      printf("ld.ca %.1f  ld.nc(__ldg) %.1f  ld.cg at 20 warps/SM %.1f G/s\n", m1 / tl / 1e6, m1 / tg / 1e6,
+             m1 / t20 / 1e6);
+    }
     return 0;
   }
   const long long m = 1ll << 26;
