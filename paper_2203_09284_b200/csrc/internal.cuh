@@ -57,6 +57,13 @@ struct Partition {
 // Everything the persistent solve kernel needs (passed by value).
 constexpr int kMaxPeers = 7;  // parts - 1 on one NVSwitch node of 8 GPUs
 
+// Per-launch result the host reads back in ONE copy (pinned mirror).
+struct SolveStatus {
+  unsigned int iters;
+  int stop;
+  double last[2];
+};
+
 struct SolveParams {
   int32_t n;
   const int64_t* row;
@@ -89,6 +96,7 @@ struct SolveParams {
   GridBar* bar;
   unsigned int* out_iters;
   int* out_stop;
+  double* out_last;  // [2]: residual (max, sum) of the launch's last sweep
   // Fused exchange (multi-GPU): every finalized contribution is also stored
   // into each peer's replica (peer[q] = that replica at this part's slice,
   // P2P-mapped), so the sweep itself performs the all-gather over NVLink.

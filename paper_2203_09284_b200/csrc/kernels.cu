@@ -555,6 +555,8 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         *p.out_iters = it + 1;
         *p.out_stop = crit <= p.threshold ? 1 : 0;
+        p.out_last[0] = tmax;
+        p.out_last[1] = tsum;
       }
       if (MODE == kModePeers) __threadfence_system();  // peer-replica stores performed before exit
       return;

@@ -47,6 +47,7 @@ constexpr uint32_t kChunkIters = 1u << 16;  // device trace capacity per launch
 // Pinned host staging for the per-launch trace readback, pooled process-wide so
 // a one-shot fpr_b200_pagerank() does not pay cudaMallocHost on every call.
 struct HostStaging {
+  SolveStatus* status = nullptr;
   unsigned int* iters = nullptr;
   int* stop = nullptr;
   double* errors = nullptr;
@@ -66,12 +67,14 @@ HostStaging* acquire_staging() {
     }
   }
   auto* s = new HostStaging;
-  if (cudaMallocHost(&s->iters, sizeof(unsigned)) != cudaSuccess ||
+  if (cudaMallocHost(&s->status, sizeof(SolveStatus)) != cudaSuccess ||
+      cudaMallocHost(&s->iters, sizeof(unsigned)) != cudaSuccess ||
       cudaMallocHost(&s->stop, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&s->errors, kChunkIters * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&s->l1, kChunkIters * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&s->ns, (kChunkIters + 1) * sizeof(unsigned long long)) != cudaSuccess) {
-    for (void* p : {(void*)s->iters, (void*)s->stop, (void*)s->errors, (void*)s->l1, (void*)s->ns})
+    for (void* p : {(void*)s->status, (void*)s->iters, (void*)s->stop, (void*)s->errors, (void*)s->l1,
+                    (void*)s->ns})
       if (p) cudaFreeHost(p);
     delete s;
     return nullptr;
@@ -217,8 +220,7 @@ struct fpr_b200_graph {
   double* partials = nullptr;
   double* totals = nullptr;
   GridBar* bar = nullptr;
-  unsigned int* d_iters = nullptr;
-  int* d_stop = nullptr;
+  SolveStatus* d_status = nullptr;  // iters, stop, last residual pair: one readback per launch
   double* d_errors = nullptr;
   double* d_l1 = nullptr;
   unsigned long long* d_ns = nullptr;
@@ -379,8 +381,8 @@ int finish_graph(fpr_b200_graph* h) {
   CK(solve_grid(h->async_shape, h->num_sms, &h->grid_full[1]));
   const int gmax = std::max(h->grid_full[0], h->grid_full[1]);
   if ((rc = dalloc_n(h, &h->partials, 2 * gmax)) || (rc = dalloc_n(h, &h->totals, 2)) ||
-      (rc = dalloc_n(h, &h->bar, 1)) || (rc = dalloc_n(h, &h->d_iters, 1)) ||
-      (rc = dalloc_n(h, &h->d_stop, 1)) || (rc = dalloc_n(h, &h->d_errors, kChunkIters)) ||
+      (rc = dalloc_n(h, &h->bar, 1)) || (rc = dalloc_n(h, &h->d_status, 1)) ||
+      (rc = dalloc_n(h, &h->d_errors, kChunkIters)) ||
       (rc = dalloc_n(h, &h->d_l1, kChunkIters)) || (rc = dalloc_n(h, &h->d_ns, kChunkIters + 1)))
     return rc;
   CK(cudaMemsetAsync(h->bar, 0, sizeof(GridBar), h->stream));
@@ -833,8 +835,9 @@ int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, dou
   p.partials = h->partials;
   p.totals = h->totals;
   p.bar = h->bar;
-  p.out_iters = h->d_iters;
-  p.out_stop = h->d_stop;
+  p.out_iters = &h->d_status->iters;
+  p.out_stop = &h->d_status->stop;
+  p.out_last = h->d_status->last;
   uint64_t total = 0;
   int par = 0;
   double last_err = 1.0, last_l1 = 1.0;
@@ -969,8 +972,9 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.partials = h->partials;
   p.totals = h->totals;
   p.bar = h->bar;
-  p.out_iters = h->d_iters;
-  p.out_stop = h->d_stop;
+  p.out_iters = &h->d_status->iters;
+  p.out_stop = &h->d_status->stop;
+  p.out_last = h->d_status->last;
 
   uint64_t total = 0;
   int parity = 0;
@@ -984,8 +988,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     CK(launch_solve(shape, grid, p, h->stream));
     CK(cudaEventRecord(h->ev[2], h->stream));
     ++launches;
-    CK(cudaMemcpyAsync(h->h_iters, h->d_iters, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(h->h_stop, h->d_stop, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->hs->status, h->d_status, sizeof(SolveStatus), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (!setup_timed) {
       cudaEventElapsedTime(&setup_ms, h->ev[0], h->ev[1]);
@@ -994,26 +997,30 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     float chunk_ms = 0.f;
     cudaEventElapsedTime(&chunk_ms, h->ev[1], h->ev[2]);
     solve_ms += chunk_ms;
-    const uint64_t done = *h->h_iters;
-    stop = *h->h_stop;
+    const uint64_t done = h->hs->status->iters;
+    stop = h->hs->status->stop;
     if (done == 0 || done > chunk) return fail(FPR_B200_ECUDA, "fpr_b200: solver reported bad count");
     if (errors_out && errors_cap < total + done)
       return fail(FPR_B200_EINVAL, "fpr_b200_run: errors buffer holds " +
                                        std::to_string(errors_cap) + " entries, need " +
                                        std::to_string(total + done));
-    CK(cudaMemcpyAsync(h->h_errors, h->d_errors, done * sizeof(double), cudaMemcpyDeviceToHost,
-                       h->stream));
-    CK(cudaMemcpyAsync(h->h_l1, h->d_l1, done * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    if (iter_ns_out)
-      CK(cudaMemcpyAsync(h->h_ns, h->d_ns, (done + 1) * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (errors_out) std::memcpy(errors_out + total, h->h_errors, done * sizeof(double));
-    if (l1_out) std::memcpy(l1_out + total, h->h_l1, done * sizeof(double));
-    if (iter_ns_out)
-      for (uint64_t k = 0; k < done; ++k) iter_ns_out[total + k] = h->h_ns[k + 1] - h->h_ns[k];
-    last_err = h->h_errors[done - 1];
-    last_l1 = h->h_l1[done - 1];
+    if (errors_out || l1_out || iter_ns_out) {  // the trace: a second copy only when asked for
+      if (errors_out)
+        CK(cudaMemcpyAsync(h->h_errors, h->d_errors, done * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream));
+      if (l1_out)
+        CK(cudaMemcpyAsync(h->h_l1, h->d_l1, done * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      if (iter_ns_out)
+        CK(cudaMemcpyAsync(h->h_ns, h->d_ns, (done + 1) * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      if (errors_out) std::memcpy(errors_out + total, h->h_errors, done * sizeof(double));
+      if (l1_out) std::memcpy(l1_out + total, h->h_l1, done * sizeof(double));
+      if (iter_ns_out)
+        for (uint64_t k = 0; k < done; ++k) iter_ns_out[total + k] = h->h_ns[k + 1] - h->h_ns[k];
+    }
+    last_err = h->hs->status->last[0];
+    last_l1 = h->hs->status->last[1];
     total += done;
     parity ^= (int)(done & 1);
     if (stop) break;
@@ -1179,8 +1186,9 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.partials = h->partials;
   p.totals = h->totals;
   p.bar = h->bar;
-  p.out_iters = h->d_iters;
-  p.out_stop = h->d_stop;
+  p.out_iters = &h->d_status->iters;
+  p.out_stop = &h->d_status->stop;
+  p.out_last = h->d_status->last;
   p.npeers = 0;
   for (uint32_t q = 0; q < npeer_bufs; ++q) {
     if ((int)q == h->part_id) continue;
