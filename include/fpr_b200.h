@@ -140,6 +140,8 @@ int fpr_b200_graph_create(const fpr_graph_view* view, const fpr_b200_options* op
 int fpr_b200_graph_generate(const fpr_gen_params* params, const fpr_b200_options* opts,
                             fpr_b200_graph** out);
 void fpr_b200_graph_destroy(fpr_b200_graph* g);
+/* Lockstep engine: waves per sweep for later runs (0 = auto). */
+int fpr_b200_graph_set_wave_count(fpr_b200_graph* g, uint32_t wave_count);
 int fpr_b200_graph_info(const fpr_b200_graph* g, uint64_t* n, uint64_t* m, uint64_t* ntasks);
 /* Downloads the CSR as fpr::Graph arrays (u64).  EINVAL for a graph created
  * with FPR_B200_OPT_REORDER (its resident CSR is in internal ids). */

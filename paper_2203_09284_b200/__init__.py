@@ -100,7 +100,7 @@ EXPORTS = [
     "fpr_b200_graph_validate", "fpr_b200_graph_partition", "fpr_b200_part_info",
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
     "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
-    "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close",
+    "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
 ]
 
 _lib = None
@@ -337,6 +337,12 @@ class DeviceGraph:
                                                    C.byref(h), C.byref(perr)), perr)
         del keep
         return cls(h.value, device, norm, wave_count)
+
+    def set_wave_count(self, waves: int) -> None:
+        """Lockstep engine: waves per sweep for later runs (0 = auto)."""
+        L = lib()
+        L.fpr_b200_graph_set_wave_count.argtypes = [C.c_void_p, C.c_uint32]
+        _check(L.fpr_b200_graph_set_wave_count(self._h, waves))
 
     def validate(self) -> int:
         """0 iff the resident CSR satisfies build_csr's invariants (device check)."""

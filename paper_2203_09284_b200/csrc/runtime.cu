@@ -396,12 +396,13 @@ int get_waves(fpr_b200_graph* h, uint32_t wave_count, const Waves** out) {
   const int64_t items = (int64_t)h->g.n + h->g.m;
   uint32_t S = wave_count;
   if (S == 0) {
-    // Auto: one wave per ~16M items keeps the per-wave barrier + pipeline
-    // refill (~10 us) near 10% of a sweep; 2..16 waves recover most of the
-    // Gauss-Seidel gain (RMAT s20: 1/2/4/8/16 waves -> 69/60/52/48/46 sweeps,
-    // fused_seq 45).
-    const int64_t want = (items + (1 << 24) - 1) >> 24;
-    S = (uint32_t)std::min<int64_t>(16, std::max<int64_t>(2, want));
+    // Auto: one wave per ~32M merge items.  Each wave costs a grid barrier
+    // plus a pipeline drain/refill (8-25 us); more waves recover more of the
+    // Gauss-Seidel gain.  Measured time-to-converge optima (scripts/
+    // wave_probe.py): config 2 (71M items) 2 waves, config 3 (280M) 8,
+    // config 4 (1.2G) 16-32, config 5 (4.5G) 16-32.
+    const int64_t want = items >> 25;
+    S = (uint32_t)std::min<int64_t>(32, std::max<int64_t>(2, want));
   }
   auto it = h->waves.find(S);
   if (it != h->waves.end()) {
@@ -684,6 +685,12 @@ int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* o
 }
 
 void fpr_b200_graph_destroy(fpr_b200_graph* h) { destroy_handle(h); }
+
+int fpr_b200_graph_set_wave_count(fpr_b200_graph* h, uint32_t wave_count) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_set_wave_count: null graph");
+  h->wave_count = wave_count;  // schedules are cached per wave count (get_waves)
+  return FPR_B200_OK;
+}
 
 int fpr_b200_graph_info(const fpr_b200_graph* h, uint64_t* n, uint64_t* m, uint64_t* ntasks) {
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_info: null graph");
