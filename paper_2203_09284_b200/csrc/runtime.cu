@@ -1198,7 +1198,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.out_last = h->d_status->last;
   p.npeers = 0;
   for (uint32_t q = 0; q < npeer_bufs; ++q) {
-    if ((int)q == h->part_id) continue;
+    if (q == (uint32_t)h->part_id) continue;
     if (!peer_write[q]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: null peer pointer");
     p.peer[p.npeers++] = peer_write[q] + p.write_off;  // this part's slice in part q's replica
   }
