@@ -292,6 +292,51 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
     return out
 
 
+def build_csr_leg(fb, g, device) -> dict:
+    """Graph loading (§8(a) a12): fpr::build_csr(EdgeSet) of config 2's edges
+    (pinned host u64 src/dst, H2D + narrowing + device sort/dedup/scan timed)
+    through fpr_b200_graph_from_edges, against the reference's build_csr on a
+    1/16 sample of the same edges (single thread, as the reference runs)."""
+    import torch
+
+    dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
+    ts = torch.empty(g.m, dtype=torch.int64, pin_memory=True)
+    td = torch.empty(g.m, dtype=torch.int64, pin_memory=True)
+    s, d = ts.numpy().view(np.uint64), td.numpy().view(np.uint64)
+    s[:] = g.in_src
+    d[:] = dst
+    fb.DeviceGraph.from_edges(g.n, s, d, device=device).close()  # warm-up
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dg = fb.DeviceGraph.from_edges(g.n, s, d, device=device)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        assert dg.m == g.m
+        dg.close()
+    dt = float(np.median(times))
+    out = {"workload": f"config-2 edges as an EdgeSet (n={g.n}, {g.m} edges)",
+           "api": "fpr_b200_graph_from_edges (pinned host u64 src/dst -> resident CSR + partition)",
+           "ms": dt * 1e3, "medges_per_s": g.m / dt / 1e6, "h2d_bytes": int(16 * g.m)}
+    try:
+        from oracle import load_reference
+
+        ref = load_reference()
+        if ref is not None:
+            k = g.m // 16
+            rng = np.random.default_rng(0)
+            pick = np.sort(rng.choice(g.m, size=k, replace=False))
+            t0 = time.perf_counter()
+            ref.build_csr(g.n, s[pick].copy(), d[pick].copy())
+            rdt = time.perf_counter() - t0
+            out["reference"] = {"medges_per_s": k / rdt / 1e6, "kind": "reference", "cores": 1,
+                                "sample": f"build_csr of a random 1/16 of the edges ({k}), n = {g.n}"}
+    except Exception as ex:
+        out["reference"] = {"unavailable": str(ex)}
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,6 +447,11 @@ def main() -> None:
         if g_host is None:
             g_host = dg.download()
         ingest = ingest_leg(fb, g_host, local)
+    csr = None
+    if rank == 0 and ws == 1 and not args.no_ingest:
+        if g_host is None:
+            g_host = dg.download()
+        csr = build_csr_leg(fb, g_host, local)
     large = None
     if rank == 0 and ws == 1 and not args.no_large:
         large = large_configs_leg(fb, local)
@@ -435,6 +485,7 @@ def main() -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ingest": ingest,
+            "build_csr": csr,
             "configs_3_5": large,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),

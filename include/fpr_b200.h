@@ -22,6 +22,7 @@
  *                              (rmat.hpp:42, graph.hpp:35) and
  *                              testutil::random_sparse (tests/test_util.hpp:49)
  *   fpr_b200_graph_download_csr -> the fpr::Graph arrays of build_csr
+ *   fpr_b200_graph_from_edges   -> fpr::build_csr(EdgeSet)  (graph.hpp:35-70)
  *   fpr_b200_parse_edge_list -> fpr::parse_edge_list     (edge_list.hpp:39-80)
  *   fpr_b200_graph_from_edge_list
  *                           -> fpr::build_csr(fpr::parse_edge_list(in))
@@ -139,6 +140,11 @@ int fpr_b200_graph_create(const fpr_graph_view* view, const fpr_b200_options* op
  * build_csr(generate_rmat(p)) / build_csr(random_sparse(...)). */
 int fpr_b200_graph_generate(const fpr_gen_params* params, const fpr_b200_options* opts,
                             fpr_b200_graph** out);
+/* fpr::build_csr(EdgeSet{n, edges}) (graph.hpp:35-70) on the device: m edges
+ * as two u64 arrays (host or pinned memory).  EINVAL names the first edge
+ * with an endpoint outside [0, n), in build_csr's words. */
+int fpr_b200_graph_from_edges(uint64_t n, uint64_t m, const uint64_t* src, const uint64_t* dst,
+                              const fpr_b200_options* opts, fpr_b200_graph** out);
 void fpr_b200_graph_destroy(fpr_b200_graph* g);
 /* Lockstep engine: waves per sweep for later runs (0 = auto). */
 int fpr_b200_graph_set_wave_count(fpr_b200_graph* g, uint32_t wave_count);

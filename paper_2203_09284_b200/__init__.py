@@ -28,7 +28,7 @@ __all__ = [
     "PageRankConfig", "RankVector", "ConvergenceTrace", "PageRankResult", "Graph", "RmatParams",
     "EngineKind", "DeviceGraph", "B200Error", "pagerank_ec_b200", "pagerank_fused_b200",
     "pagerank_fused_lockstep_b200", "run_engine", "l1_norm", "linf_norm", "to_string",
-    "parse_engine", "lib", "LIB_PATH", "EdgeSet", "ParseError", "parse_edge_list",
+    "parse_engine", "lib", "LIB_PATH", "EdgeSet", "ParseError", "parse_edge_list", "build_csr",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -101,6 +101,7 @@ EXPORTS = [
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
     "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
+    "fpr_b200_graph_from_edges",
 ]
 
 _lib = None
@@ -326,6 +327,25 @@ class DeviceGraph:
         return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked)
 
     @classmethod
+    def from_edges(cls, n: int, src, dst, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
+                   blocked=False):
+        """fpr::build_csr(EdgeSet{n, (src, dst)}) on the device (graph.hpp:35-70):
+        duplicates and self-loops dropped, in-segments ascending; ValueError
+        names the first out-of-range edge as build_csr does."""
+        s_, d_ = _u64(src), _u64(dst)
+        if len(s_) != len(d_):
+            raise ValueError("from_edges: src and dst lengths differ")
+        h = C.c_void_p()
+        L = lib()
+        L.fpr_b200_graph_from_edges.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                C.POINTER(_Options), C.POINTER(C.c_void_p)]
+        _check(L.fpr_b200_graph_from_edges(n, len(s_), s_.ctypes.data if len(s_) else None,
+                                           d_.ctypes.data if len(d_) else None,
+                                           C.byref(_options(device, norm, wave_count, stream, reorder, blocked)),
+                                           C.byref(h)))
+        return cls(h.value, device, norm, wave_count)
+
+    @classmethod
     def from_edge_list(cls, text, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False):
         """build_csr(parse_edge_list(text)) -- parsing, id compaction and the
         CSR build all on the device (edge_list.hpp:39-80, graph.hpp:35-70)."""
@@ -515,4 +535,10 @@ def parse_edge_list(text, device: int = -1) -> EdgeSet:
     _check(rc, perr)
     del keep
     return EdgeSet(n.value, edges[: m.value].copy() if cap else edges[: m.value])
+
+
+def build_csr(n: int, src, dst, device: int = -1) -> Graph:
+    """fpr::build_csr on the GPU, returned as host u64 arrays (fpr::Graph)."""
+    with DeviceGraph.from_edges(n, src, dst, device=device) as dg:
+        return dg.download()
 

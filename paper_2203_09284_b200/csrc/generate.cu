@@ -128,6 +128,18 @@ struct CsrSource {
   }
 };
 
+// Two separate id arrays (a host EdgeSet uploaded and narrowed).
+struct ArraySource {
+  const int32_t* s;
+  const int32_t* d;
+
+  __device__ __forceinline__ bool get(uint64_t e, uint64_t& src, uint64_t& dst) const {
+    src = (uint32_t)__ldg(s + e);
+    dst = (uint32_t)__ldg(d + e);
+    return src != dst;
+  }
+};
+
 // Dense (src, dst) id pairs of a parsed edge list (ingest.cu).
 struct PairSource {
   const int32_t* ids;  // 2 per edge
@@ -525,6 +537,11 @@ out:
 cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
                                  const char** msg) {
   return build_csr_from(PairSource{pairs}, (uint64_t)m, n, g, st, msg);
+}
+
+cudaError_t build_csr_from_arrays(const int32_t* src, const int32_t* dst, int64_t m, uint64_t n, DevGraph& g,
+                                  cudaStream_t st, const char** msg) {
+  return build_csr_from(ArraySource{src, dst}, (uint64_t)m, n, g, st, msg);
 }
 
 

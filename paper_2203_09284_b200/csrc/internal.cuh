@@ -181,6 +181,9 @@ struct IngestError {
 };
 cudaError_t ingest_edge_list(const unsigned char* t, uint64_t len, bool ends_with_newline, cudaStream_t st,
                              Ingested& out, IngestError& err, const char** msg);
+// generate.cu: build_csr over m edges given as two int32 arrays, ids in [0, n).
+cudaError_t build_csr_from_arrays(const int32_t* src, const int32_t* dst, int64_t m, uint64_t n, DevGraph& g,
+                                  cudaStream_t st, const char** msg);
 // generate.cu: build_csr over m (src, dst) int32 pairs with ids in [0, n).
 cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
                                  const char** msg);

@@ -684,6 +684,98 @@ int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* o
   return FPR_B200_OK;
 }
 
+// fpr::build_csr(EdgeSet) (graph.hpp:35-70) on the device: the endpoints are
+// narrowed to int32 with a range check while they upload (host threads through
+// the pinned ring, or DMA + device narrowing for pinned input), then the K4
+// build (sort by (dst, src), dedup, drop self-loops, degree scans).
+int fpr_b200_graph_from_edges(uint64_t n, uint64_t m, const uint64_t* src, const uint64_t* dst,
+                              const fpr_b200_options* opts, fpr_b200_graph** out) {
+  if (!out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_from_edges: null argument");
+  *out = nullptr;
+  if (m && (!src || !dst)) return fail(FPR_B200_EINVAL, "fpr_b200_graph_from_edges: null edge arrays");
+  if (n >= (1ull << 31)) return fail(FPR_B200_ERANGE, "fpr_b200: n >= 2^31 exceeds the int32 vertex-id range");
+  if (m >= (1ull << 40)) return fail(FPR_B200_ERANGE, "fpr_b200: too many edges");
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  // temporaries (freed once the CSR is built)
+  int32_t* ds = nullptr;
+  int32_t* dd = nullptr;
+  unsigned int* bad = nullptr;
+  uint64_t* stage = nullptr;
+  auto bail = [&](int code) {
+    for (void* p : {(void*)ds, (void*)dd, (void*)bad, (void*)stage})
+      if (p) cudaFreeAsync(p, h->stream);
+    destroy_handle(h);
+    return code;
+  };
+  cudaError_t e = cudaMallocAsync((void**)&ds, (m + 1) * sizeof(int32_t), h->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&dd, (m + 1) * sizeof(int32_t), h->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&bad, sizeof(unsigned), h->stream);
+  if (e != cudaSuccess) return bail(fail(FPR_B200_ENOMEM, "fpr_b200_graph_from_edges: device allocation failed"));
+  e = cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream);
+  bool ok = true;
+  if (e == cudaSuccess && m > 0) {
+    if (is_pinned(src) && is_pinned(dst)) {
+      const int64_t chunk = std::min<int64_t>((int64_t)m, 1 << 24);
+      if (cudaMallocAsync((void**)&stage, chunk * sizeof(uint64_t), h->stream) != cudaSuccess)
+        return bail(fail(FPR_B200_ENOMEM, "fpr_b200_graph_from_edges: device allocation failed"));
+      for (int side = 0; side < 2 && e == cudaSuccess; ++side) {
+        const uint64_t* host = side ? dst : src;
+        int32_t* dev = side ? dd : ds;
+        for (int64_t off = 0; off < (int64_t)m && e == cudaSuccess; off += chunk) {
+          const int64_t cnt = std::min<int64_t>(chunk, (int64_t)m - off);
+          e = cudaMemcpyAsync(stage, host + off, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream);
+          if (e == cudaSuccess) e = launch_narrow_ids(stage, dev + off, cnt, n, bad, h->stream);
+        }
+      }
+    } else {
+      UploadRing* ring = get_ring(h->device);
+      if (!ring) return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
+      std::lock_guard<std::mutex> lk(ring->mu);
+      int k = 0;
+      ok = ring_upload<int32_t>(ring, src, ds, (int64_t)m, n, h->stream, k, &e);
+      ok = ring_upload<int32_t>(ring, dst, dd, (int64_t)m, n, h->stream, k, &e) && ok;
+    }
+  }
+  unsigned hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->h_iters, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess)
+    return bail(fail(FPR_B200_ECUDA, std::string("fpr_b200_graph_from_edges: ") + cudaGetErrorString(e)));
+  hbad = *h->h_iters;
+  if (!ok || hbad) {
+    // The device saw an endpoint outside [0, n); name the first one the way
+    // build_csr does (graph.hpp:39-43).  Error path only.
+    for (uint64_t i = 0; i < m; ++i)
+      if (src[i] >= n || dst[i] >= n)
+        return bail(fail(FPR_B200_EINVAL, "build_csr: edge #" + std::to_string(i) + " (" + std::to_string(src[i]) +
+                                              "," + std::to_string(dst[i]) + ") has endpoint outside [0," +
+                                              std::to_string(n) + ")"));
+  }
+  const char* msg = nullptr;
+  e = build_csr_from_arrays(ds, dd, (int64_t)m, n, h->g, h->stream, &msg);
+  for (void* p : {(void*)ds, (void*)dd, (void*)bad, (void*)stage})
+    if (p) cudaFreeAsync(p, h->stream);
+  ds = dd = nullptr;
+  bad = nullptr;
+  stage = nullptr;
+  if (e != cudaSuccess || msg) {
+    if (msg) return bail(fail(FPR_B200_ENOMEM, std::string("fpr_b200_graph_from_edges: ") + msg));
+    return bail(fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                     std::string("fpr_b200_graph_from_edges: ") + cudaGetErrorString(e)));
+  }
+  h->allocs.push_back(h->g.row);
+  h->allocs.push_back(h->g.src);
+  h->allocs.push_back(h->g.outdeg);
+  if ((rc = finish_graph(h))) return bail(rc);
+  *out = h;
+  return FPR_B200_OK;
+}
+
 void fpr_b200_graph_destroy(fpr_b200_graph* h) { destroy_handle(h); }
 
 int fpr_b200_graph_set_wave_count(fpr_b200_graph* h, uint32_t wave_count) {

@@ -10,6 +10,7 @@
 #include <sstream>
 
 #include "fpr/edge_list_b200.hpp"
+#include "fpr/graph_b200.hpp"
 #include "fpr/metrics.hpp"
 #include "fpr/pagerank_b200.hpp"
 #include "fpr/rmat.hpp"
@@ -77,6 +78,28 @@ int main() {
   capped.max_iterations = 3;
   const fpr::PageRankResult nc = fpr::pagerank_ec_b200(g, capped);
   CHECK(nc.trace.iterations == 3 && !nc.trace.converged, "non-convergence is a result");
+
+  // build_csr on the device vs the reference's build_csr (graph.hpp:35-70)
+  {
+    const fpr::EdgeSet raw = fpr::generate_rmat(p);
+    const fpr::Graph a = fpr::build_csr(raw), b = fpr::build_csr_b200(raw);
+    CHECK(a.n == b.n && a.m == b.m && a.in_start == b.in_start && a.in_src == b.in_src &&
+              a.out_degree == b.out_degree,
+          "build_csr_b200 differs (m %llu vs %llu)", (unsigned long long)a.m, (unsigned long long)b.m);
+    fpr::EdgeSet bad{2, {{0, 1}, {0, 2}}};
+    std::string want, got;
+    try {
+      fpr::build_csr(bad);
+    } catch (const std::invalid_argument& e) {
+      want = e.what();
+    }
+    try {
+      fpr::build_csr_b200(bad);
+    } catch (const std::invalid_argument& e) {
+      got = e.what();
+    }
+    CHECK(!want.empty() && want == got, "build_csr error '%s' vs '%s'", want.c_str(), got.c_str());
+  }
 
   // edge-list ingest: the reference's parse_edge_list vs the device parser
   {
