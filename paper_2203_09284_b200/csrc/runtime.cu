@@ -494,6 +494,90 @@ const char* fpr_b200_last_error(void) { return g_last_error.c_str(); }
 
 int fpr_b200_version(void) { return 1; }
 
+// Pinned u64 id arrays -> int32 device arrays, range-checked against `bound`
+// (a failure sets *bad).  The link is the bound at 8 B per id, so for arrays
+// marked `split` host threads narrow the last host_narrow_share() to 4 B per
+// id through the pinned ring (ring stream) while the DMA engine moves the rest
+// raw into two device staging buffers that the main stream narrows, chunk i
+// copying while chunk i-1 narrows (e2e).  An optional raw blob
+// (in_start) goes first on the copy stream.  Ordered before later work on
+// h->stream; returns a status code, CUDA errors in *e.
+struct IdUpload {
+  const uint64_t* host;
+  int32_t* dev;
+  int64_t count;
+  bool split;
+};
+
+int upload_ids_pinned(fpr_b200_graph* h, const std::vector<IdUpload>& arrays, uint64_t bound, unsigned int* bad,
+                      const void* raw_host, void* raw_dev, size_t raw_bytes, cudaError_t* e) {
+  const int64_t chunk = 1 << 24;
+  struct Piece {
+    const uint64_t* host;
+    int32_t* dst;
+    int64_t count;
+  };
+  std::vector<Piece> pieces;
+  struct HostPart {
+    const uint64_t* host;
+    int32_t* dst;
+    int64_t count;
+  };
+  std::vector<HostPart> host_parts;
+  const double share = host_narrow_share();
+  int64_t most = 0;
+  for (const IdUpload& a : arrays) {
+    const int64_t nh = a.split ? (int64_t)((double)a.count * share) : 0;
+    const int64_t nd = a.count - nh;
+    for (int64_t off = 0; off < nd; off += chunk) pieces.push_back({a.host + off, a.dev + off, std::min(chunk, nd - off)});
+    if (nh > 0) host_parts.push_back({a.host + nd, a.dev + nd, nh});
+    most = std::max(most, std::min(chunk, nd));
+  }
+  UploadRing* ring = host_parts.empty() ? nullptr : get_ring(h->device);
+  if (!host_parts.empty() && !ring) return fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed");
+  uint64_t* stage = nullptr;
+  if (*e == cudaSuccess && most > 0) *e = cudaMallocAsync((void**)&stage, 2 * most * sizeof(uint64_t), h->stream);
+  if (*e == cudaSuccess && !h->copy_stream) *e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+  for (auto& ev : h->up_ev)
+    if (*e == cudaSuccess && !ev) *e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (*e == cudaSuccess) *e = cudaEventRecord(h->up_ev[2], h->stream);  // destinations + staging allocated
+  if (*e == cudaSuccess) *e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2], 0);
+  if (*e == cudaSuccess && raw_bytes)
+    *e = cudaMemcpyAsync(raw_dev, raw_host, raw_bytes, cudaMemcpyHostToDevice, h->copy_stream);
+  for (size_t i = 0; *e == cudaSuccess && i < pieces.size(); ++i) {
+    const int k = (int)(i & 1);
+    uint64_t* buf = stage + k * most;
+    if (i >= 2) *e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2 + k], 0);  // buf drained
+    if (*e == cudaSuccess)
+      *e = cudaMemcpyAsync(buf, pieces[i].host, pieces[i].count * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           h->copy_stream);
+    if (*e == cudaSuccess) *e = cudaEventRecord(h->up_ev[k], h->copy_stream);
+    if (*e == cudaSuccess) *e = cudaStreamWaitEvent(h->stream, h->up_ev[k], 0);
+    if (*e == cudaSuccess) *e = launch_narrow_ids(buf, pieces[i].dst, pieces[i].count, bound, bad, h->stream);
+    if (*e == cudaSuccess) *e = cudaEventRecord(h->up_ev[2 + k], h->stream);
+  }
+  if (*e == cudaSuccess && raw_bytes && pieces.empty()) {  // raw blob alone: order it before later work
+    *e = cudaEventRecord(h->up_ev[0], h->copy_stream);
+    if (*e == cudaSuccess) *e = cudaStreamWaitEvent(h->stream, h->up_ev[0], 0);
+  }
+  if (*e == cudaSuccess && !host_parts.empty()) {
+    if (!h->ring_stream) *e = cudaStreamCreateWithFlags(&h->ring_stream, cudaStreamNonBlocking);
+    if (*e == cudaSuccess && !h->ring_ev) *e = cudaEventCreateWithFlags(&h->ring_ev, cudaEventDisableTiming);
+    if (*e == cudaSuccess) *e = cudaEventRecord(h->ring_ev, h->stream);
+    if (*e == cudaSuccess) *e = cudaStreamWaitEvent(h->ring_stream, h->ring_ev, 0);
+    std::lock_guard<std::mutex> lk(ring->mu);
+    int k = 0;
+    bool ok = true;
+    for (const HostPart& hp : host_parts)
+      if (*e == cudaSuccess) ok = ring_upload<int32_t>(ring, hp.host, hp.dst, hp.count, bound, h->ring_stream, k, e) && ok;
+    if (*e == cudaSuccess) *e = cudaEventRecord(h->ring_ev, h->ring_stream);
+    if (*e == cudaSuccess) *e = cudaStreamWaitEvent(h->stream, h->ring_ev, 0);
+    if (*e == cudaSuccess && !ok) *e = cudaMemsetAsync(bad, 1, 1, h->stream);  // reported with the device check
+  }
+  if (stage) cudaFreeAsync(stage, h->stream);  // after the last narrow on h->stream
+  return FPR_B200_OK;
+}
+
 int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
                           fpr_b200_graph** out) {
   if (!v || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_create: null argument");
@@ -539,69 +623,12 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
       return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_src/out_degree value outside [0," +
                                             std::to_string(v->n) + ")"));
   }
-  // Pinned source: u64 -> int32 through two device staging buffers: chunk i is
-  // copied on the copy stream while chunk i-1 is narrowed on the main one.
-  const int64_t chunk = 1 << 24;
-  uint64_t* stage = nullptr;
-  const int64_t need = std::min<int64_t>(chunk, std::max<int64_t>(g.m, g.n));
-  if (e == cudaSuccess && need > 0 && pinned) {
-    if ((rc = dalloc_n(h, &stage, 2 * need))) return bail(rc);
-    if (!h->copy_stream) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
-    for (auto& ev : h->up_ev)
-      if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    struct Piece {
-      const uint64_t* host;
-      int32_t* dst;
-      int64_t count;
-    };
-    // The link is the bound (8 B per edge raw).  Host threads narrow the
-    // last `host_share` of in_src to 4 B per edge through the pinned ring,
-    // concurrently with the raw DMA of the rest, so the link carries fewer
-    // bytes while both halves finish together (e2e).
-    const int64_t m_host = (int64_t)((double)g.m * host_narrow_share());
-    const int64_t m_dev = g.m - m_host;
-    UploadRing* ring = m_host > 0 ? get_ring(h->device) : nullptr;
-    if (m_host > 0 && !ring)
-      return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
-    std::vector<Piece> pieces;
-    for (int64_t off = 0; off < m_dev; off += chunk)
-      pieces.push_back({v->in_src + off, g.src + off, std::min<int64_t>(chunk, m_dev - off)});
-    for (int64_t off = 0; off < g.n; off += chunk)
-      pieces.push_back({v->out_degree + off, g.outdeg + off, std::min<int64_t>(chunk, g.n - off)});
-    if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2], h->stream);  // staging allocated
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2], 0);
-    // in_start first on the copy stream; the main stream's wait on the last
-    // piece's copy event orders it before check_offsets / partitioning.
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(g.row, v->in_start, (g.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                          h->copy_stream);
-    for (size_t i = 0; e == cudaSuccess && i < pieces.size(); ++i) {
-      const int k = (int)(i & 1);
-      uint64_t* buf = stage + k * need;
-      if (i >= 2) e = cudaStreamWaitEvent(h->copy_stream, h->up_ev[2 + k], 0);  // buf drained
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(buf, pieces[i].host, pieces[i].count * sizeof(uint64_t),
-                            cudaMemcpyHostToDevice, h->copy_stream);
-      if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[k], h->copy_stream);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->up_ev[k], 0);
-      if (e == cudaSuccess)
-        e = launch_narrow_ids(buf, pieces[i].dst, pieces[i].count, v->n, bad, h->stream);
-      if (e == cudaSuccess) e = cudaEventRecord(h->up_ev[2 + k], h->stream);
-    }
-    if (e == cudaSuccess && m_host > 0) {
-      if (!h->ring_stream) e = cudaStreamCreateWithFlags(&h->ring_stream, cudaStreamNonBlocking);
-      if (e == cudaSuccess && !h->ring_ev) e = cudaEventCreateWithFlags(&h->ring_ev, cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventRecord(h->ring_ev, h->stream);  // g.src allocated
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->ring_stream, h->ring_ev, 0);
-      std::lock_guard<std::mutex> lk(ring->mu);
-      int k = 0;
-      bool ok = e == cudaSuccess &&
-                ring_upload<int32_t>(ring, v->in_src + m_dev, g.src + m_dev, m_host, v->n, h->ring_stream, k, &e);
-      if (e == cudaSuccess) e = cudaEventRecord(h->ring_ev, h->ring_stream);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->ring_ev, 0);
-      if (e == cudaSuccess && !ok)
-        e = cudaMemsetAsync(bad, 1, 1, h->stream);  // reported with the device-side range check
-    }
+  if (e == cudaSuccess && g.n > 0 && pinned) {
+    // in_src split between raw DMA and host narrowing; out_degree raw;
+    // in_start (int64 as is) first on the copy stream.
+    const std::vector<IdUpload> arrays = {{v->in_src, g.src, g.m, true}, {v->out_degree, g.outdeg, g.n, false}};
+    if ((rc = upload_ids_pinned(h, arrays, v->n, bad, v->in_start, g.row, (g.n + 1) * sizeof(int64_t), &e)))
+      return bail(rc);
   }
   if (e == cudaSuccess && g.n > 0) e = launch_check_offsets(g.row, g.n, g.m, bad, h->stream);
   unsigned hbad = 0;
@@ -705,9 +732,8 @@ int fpr_b200_graph_from_edges(uint64_t n, uint64_t m, const uint64_t* src, const
   int32_t* ds = nullptr;
   int32_t* dd = nullptr;
   unsigned int* bad = nullptr;
-  uint64_t* stage = nullptr;
   auto bail = [&](int code) {
-    for (void* p : {(void*)ds, (void*)dd, (void*)bad, (void*)stage})
+    for (void* p : {(void*)ds, (void*)dd, (void*)bad})
       if (p) cudaFreeAsync(p, h->stream);
     destroy_handle(h);
     return code;
@@ -720,18 +746,8 @@ int fpr_b200_graph_from_edges(uint64_t n, uint64_t m, const uint64_t* src, const
   bool ok = true;
   if (e == cudaSuccess && m > 0) {
     if (is_pinned(src) && is_pinned(dst)) {
-      const int64_t chunk = std::min<int64_t>((int64_t)m, 1 << 24);
-      if (cudaMallocAsync((void**)&stage, chunk * sizeof(uint64_t), h->stream) != cudaSuccess)
-        return bail(fail(FPR_B200_ENOMEM, "fpr_b200_graph_from_edges: device allocation failed"));
-      for (int side = 0; side < 2 && e == cudaSuccess; ++side) {
-        const uint64_t* host = side ? dst : src;
-        int32_t* dev = side ? dd : ds;
-        for (int64_t off = 0; off < (int64_t)m && e == cudaSuccess; off += chunk) {
-          const int64_t cnt = std::min<int64_t>(chunk, (int64_t)m - off);
-          e = cudaMemcpyAsync(stage, host + off, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream);
-          if (e == cudaSuccess) e = launch_narrow_ids(stage, dev + off, cnt, n, bad, h->stream);
-        }
-      }
+      const std::vector<IdUpload> arrays = {{src, ds, (int64_t)m, true}, {dst, dd, (int64_t)m, true}};
+      if ((rc = upload_ids_pinned(h, arrays, n, bad, nullptr, nullptr, 0, &e))) return bail(rc);
     } else {
       UploadRing* ring = get_ring(h->device);
       if (!ring) return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
@@ -758,11 +774,10 @@ int fpr_b200_graph_from_edges(uint64_t n, uint64_t m, const uint64_t* src, const
   }
   const char* msg = nullptr;
   e = build_csr_from_arrays(ds, dd, (int64_t)m, n, h->g, h->stream, &msg);
-  for (void* p : {(void*)ds, (void*)dd, (void*)bad, (void*)stage})
+  for (void* p : {(void*)ds, (void*)dd, (void*)bad})
     if (p) cudaFreeAsync(p, h->stream);
   ds = dd = nullptr;
   bad = nullptr;
-  stage = nullptr;
   if (e != cudaSuccess || msg) {
     if (msg) return bail(fail(FPR_B200_ENOMEM, std::string("fpr_b200_graph_from_edges: ") + msg));
     return bail(fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
