@@ -28,7 +28,8 @@ __all__ = [
     "PageRankConfig", "RankVector", "ConvergenceTrace", "PageRankResult", "Graph", "RmatParams",
     "EngineKind", "DeviceGraph", "B200Error", "pagerank_ec_b200", "pagerank_fused_b200",
     "pagerank_fused_lockstep_b200", "run_engine", "l1_norm", "linf_norm", "to_string",
-    "parse_engine", "lib", "LIB_PATH", "EdgeSet", "ParseError", "parse_edge_list", "build_csr",
+    "parse_engine", "lib", "LIB_PATH", "EdgeSet", "ParseError", "parse_edge_list", "write_edge_list",
+    "build_csr",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -535,6 +536,18 @@ def parse_edge_list(text, device: int = -1) -> EdgeSet:
     _check(rc, perr)
     del keep
     return EdgeSet(n.value, edges[: m.value].copy() if cap else edges[: m.value])
+
+
+def write_edge_list(es: EdgeSet, header=()) -> bytes:
+    """fpr::write_edge_list (edge_list.hpp:84-89): '# ' + each header line,
+    then one "src dst" line per edge.  Host-side formatting (vectorised), the
+    inverse of parse_edge_list for densely labelled inputs."""
+    head = "".join(f"# {h}\n" for h in header).encode()
+    e = np.asarray(es.edges, dtype=np.uint64).reshape(-1, 2)
+    if len(e) == 0:
+        return head
+    body = np.char.add(np.char.add(e[:, 0].astype(str), " "), e[:, 1].astype(str))
+    return head + ("\n".join(body.tolist()) + "\n").encode()
 
 
 def build_csr(n: int, src, dst, device: int = -1) -> Graph:

@@ -136,7 +136,15 @@ def cmd_gen(args, out) -> int:
     dg, label = open_graph(args)
     with dg:
         g = dg.download()
-    save_cache(g, args.out)  # FPRG (graph_cache.hpp); CacheError -> I/O
+    if args.format == "edges":  # SNAP text (edge_list.hpp:84-89) of the normalised graph
+        from . import EdgeSet, write_edge_list
+
+        dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
+        text = write_edge_list(EdgeSet(g.n, np.stack([g.in_src, dst], axis=1)), [f"{label} n={g.n} m={g.m}"])
+        with open(args.out, "wb") as f:
+            f.write(text)
+    else:
+        save_cache(g, args.out)  # FPRG (graph_cache.hpp); CacheError -> I/O
     out.write(f"wrote {args.out}: {label} n={g.n} m={g.m}\n")
     return EXIT_OK
 
@@ -190,6 +198,7 @@ def build_parser() -> argparse.ArgumentParser:
     p = sub.add_parser("gen")
     common(p)
     p.add_argument("--out", required=True)
+    p.add_argument("--format", choices=["fprg", "edges"], default="fprg")
     p = sub.add_parser("compare")
     common(p)
     return ap
