@@ -437,6 +437,17 @@ def main() -> None:
     fused["lockstep"] = {"iterations": lr.trace.iterations, "ms_per_solve": lr.solve_ms,
                          "waves": int(len(dg.wave_starts()) - 1)}
 
+    # BASELINE.json words the stop rule as an L1 delta; the reference stops on
+    # L-inf (the headline).  Same graph, L1 rule, reported beside it.
+    l1_stop = {}
+    with fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr,
+                                         norm=fb.NORM_L1) as dl1:
+        for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED_LOCKSTEP, "fused_lockstep"),
+                         (fb.ENGINE_FUSED, "fused")):
+            dl1.run(eng, cfg, copy_ranks=False, copy_trace=False)
+            r1 = dl1.run(eng, cfg, copy_ranks=False, copy_trace=False)
+            l1_stop[tag] = {"iterations": r1.trace.iterations, "time_to_converge_ms": r1.solve_ms,
+                            "converged": bool(r1.trace.converged)}
     g_host = None
     e2e = None
     if not args.no_e2e:
@@ -482,6 +493,7 @@ def main() -> None:
                          "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": algorithmic_bytes(n, m) * iters},
             "fused": fused,
+            "l1_stop_rule": l1_stop,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ingest": ingest,
