@@ -101,6 +101,7 @@ struct SolveParams {
   // into each peer's replica (peer[q] = that replica at this part's slice,
   // P2P-mapped), so the sweep itself performs the all-gather over NVLink.
   int32_t npeers;
+  int32_t peer_skip_empty;  // peers already hold the constant contribution of rows without in-edges
   double* peer[kMaxPeers];
   // Source-blocked EC pass (kModeAccum): local row r is global row brow_ids[r];
   // its in-block sum is added to partial[brow_ids[r]].

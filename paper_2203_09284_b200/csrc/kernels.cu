@@ -440,7 +440,7 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         else
           cur[r] = c;
         // fused exchange: the same (coalesced) store into every peer replica
-        if (MODE == kModePeers)
+        if (MODE == kModePeers && !(p.peer_skip_empty && lo == hi && !(r == i0 && has_head)))
           for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
       }
       const double d = fabs(nv - ov);

@@ -243,6 +243,7 @@ struct fpr_b200_graph {
   uint32_t flags = 0;
   int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
   BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
+  uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
   double* ranks_tmp = nullptr;    // reordered ranks gathered back to caller order
   uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
@@ -1237,6 +1238,7 @@ int fpr_b200_part_init(fpr_b200_graph* h, double* exchange) {
   const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
   CK(launch_part_init(h->g, 1.0 / (double)ng, h->pr, exchange + (uint64_t)h->part_id * h->slice,
                       h->stream));
+  h->part_sweeps = 0;
   return FPR_B200_OK;
 }
 
@@ -1304,6 +1306,11 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.out_stop = &h->d_status->stop;
   p.out_last = h->d_status->last;
   p.npeers = 0;
+  // Rows without in-edges have a constant contribution after the first sweep;
+  // once both ping-pong replicas hold it (2 sweeps after part_init) peers
+  // are not sent it again (SURVEY §8(e) exchange compaction).
+  p.peer_skip_empty = h->part_sweeps >= 2 ? 1 : 0;
+  ++h->part_sweeps;
   for (uint32_t q = 0; q < npeer_bufs; ++q) {
     if (q == (uint32_t)h->part_id) continue;
     if (!peer_write[q]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: null peer pointer");
