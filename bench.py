@@ -526,7 +526,10 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     dev = f"cuda:{local}"
     # fused exchange: the sweep stores its slice into the peers' replicas
     # (CUDA IPC / NVLink P2P); NCCL carries only the 16-B residual pair
-    solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1)
+    # Speculation costs one extra sweep per solve and saves a host round trip
+    # per iteration: a win once the sweep is short (N > 1), a loss at N = 1.
+    solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1,
+                               speculate=ws > 1)
     for _ in range(args.warmup):
         r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=False)
     iters = r.iterations
@@ -565,6 +568,8 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
                        "norm": "linf", "step": "1 full EC solve (time-to-converge)",
                        "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
+                       "host_loop": ("speculative: sweep k+1 enqueued before iteration k's residual is read"
+                                     if ws > 1 else "synchronous"),
                        "exchange_fallback": solver.fallback,
                        "slice": part.slice, "l2": "inputs larger than L2; no flush"},
             "time_to_converge_ms": ms_step,

@@ -201,6 +201,9 @@ int fpr_b200_part_init(fpr_b200_graph* g, double* exchange);
 int fpr_b200_part_sweep(fpr_b200_graph* g, int engine, const fpr_config* cfg,
                         const double* exch_read, double* exch_write, double* pair_out);
 int fpr_b200_part_ranks(fpr_b200_graph* g, double* ranks_out);
+/* The part's ranks one sweep before the latest (a speculative driver that ran
+ * one sweep past the stopping iteration reports these). */
+int fpr_b200_part_ranks_prev(fpr_b200_graph* g, double* ranks_out);
 
 /* Fused exchange: part_sweep whose epilogue also stores every updated
  * contribution into the other parts' exchange vectors -- peer_write[q] is
@@ -209,7 +212,10 @@ int fpr_b200_part_ranks(fpr_b200_graph* g, double* ranks_out);
  * pointer within one process), peer_write[part] is ignored, npeer_bufs must
  * equal nparts (<= 8).  The sweep thereby performs the all-gather over NVLink
  * P2P stores, tile by tile as rows finalize; only the 16-B residual pair is
- * left for a collective, and that collective doubles as the barrier. */
+ * left for a collective, and that collective doubles as the barrier.  Rows
+ * without in-edges (constant contribution) are sent only in the first 3
+ * sweeps after fpr_b200_part_init: a driver may rotate through up to 3
+ * exchange vectors. */
 int fpr_b200_part_sweep_peers(fpr_b200_graph* g, int engine, const fpr_config* cfg,
                               const double* exch_read, double* exch_write,
                               double* const* peer_write, uint32_t npeer_bufs, double* pair_out);

@@ -102,7 +102,7 @@ EXPORTS = [
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
     "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
-    "fpr_b200_graph_from_edges",
+    "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev",
 ]
 
 _lib = None

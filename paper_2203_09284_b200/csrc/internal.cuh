@@ -77,7 +77,8 @@ struct SolveParams {
   const int32_t* wave_task;  // nwaves+1
   const int32_t* wave_row;   // nwaves+1
   int32_t nwaves;
-  double* pr;
+  double* pr;      // ranks read (old value of each row)
+  double* pr_out;  // ranks written: == pr except in multi-GPU part sweeps (ping-pong)
   double* contrib0;
   double* contrib1;
   int32_t parity0;  // contrib buffer holding the previous sweep at local iteration 0

@@ -432,7 +432,7 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         continue;
       }
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
-      p.pr[r] = nv;
+      p.pr_out[r] = nv;
       if (od > 0) {
         const double c = __ddiv_rn(nv, (double)od);
         if (ASYNC)

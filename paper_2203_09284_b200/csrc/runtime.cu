@@ -244,6 +244,8 @@ struct fpr_b200_graph {
   int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
   BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
   uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
+  double* part_pr[2] = {nullptr, nullptr};  // part ranks ping-pong ([0] = pr)
+  int part_pr_cur = 0;                       // buffer holding the latest sweep
   double* ranks_tmp = nullptr;    // reordered ranks gathered back to caller order
   uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
@@ -935,6 +937,7 @@ int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, dou
   const int wpb = solve_block_threads(kEC) / 32;
   SolveParams p{};
   p.pr = h->pr;
+  p.pr_out = h->pr;
   p.damping = cfg->damping;
   p.base = (1.0 - cfg->damping) / (double)g.n;
   p.threshold = 0.0;
@@ -1073,6 +1076,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.wave_row = wv->d_row;
   p.nwaves = wv->nwaves;
   p.pr = h->pr;
+  p.pr_out = h->pr;
   p.contrib0 = h->contrib[0];
   p.contrib1 = h->contrib[1];
   p.tail_partial = h->tail_partial;
@@ -1236,6 +1240,10 @@ int fpr_b200_part_init(fpr_b200_graph* h, double* exchange) {
   if (!h || !exchange) return fail(FPR_B200_EINVAL, "fpr_b200_part_init: null argument");
   CK(cudaSetDevice(h->device));
   const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
+  int rc = 0;
+  if (!h->part_pr[1] && (rc = dalloc_n(h, &h->part_pr[1], std::max<int64_t>(h->g.n, 1)))) return rc;
+  h->part_pr[0] = h->pr;
+  h->part_pr_cur = 0;
   CK(launch_part_init(h->g, 1.0 / (double)ng, h->pr, exchange + (uint64_t)h->part_id * h->slice,
                       h->stream));
   h->part_sweeps = 0;
@@ -1252,6 +1260,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
                               double* const* peer_write, uint32_t npeer_bufs, double* pair_out) {
   if (!h || !cfg || !exch_read || !exch_write || !pair_out)
     return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: null argument");
+  if (!h->part_pr[0]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: call fpr_b200_part_init first");
   if (npeer_bufs && (!peer_write || npeer_bufs != (uint32_t)h->nparts))
     return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: need one exchange pointer per part");
   if (npeer_bufs && h->nparts - 1 > kMaxPeers)
@@ -1285,7 +1294,10 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.wave_task = wv->d_task;
   p.wave_row = wv->d_row;
   p.nwaves = wv->nwaves;
-  p.pr = h->pr;
+  // ranks ping-pong between two buffers, so the state before the latest
+  // sweep stays readable (fpr_b200_part_ranks_prev: speculative drivers)
+  p.pr = h->part_pr[h->part_pr_cur];
+  p.pr_out = h->part_pr[h->part_pr_cur ^ 1];
   p.contrib0 = const_cast<double*>(exch_read);
   p.contrib1 = exch_write;
   p.parity0 = 0;
@@ -1307,9 +1319,10 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.out_last = h->d_status->last;
   p.npeers = 0;
   // Rows without in-edges have a constant contribution after the first sweep;
-  // once both ping-pong replicas hold it (2 sweeps after part_init) peers
-  // are not sent it again (SURVEY §8(e) exchange compaction).
-  p.peer_skip_empty = h->part_sweeps >= 2 ? 1 : 0;
+  // once every rotating exchange vector holds it (3 sweeps after part_init:
+  // drivers rotate through 2, or 3 when speculating) peers are not sent it
+  // again (SURVEY §8(e) exchange compaction).
+  p.peer_skip_empty = h->part_sweeps >= 3 ? 1 : 0;
   ++h->part_sweeps;
   for (uint32_t q = 0; q < npeer_bufs; ++q) {
     if (q == (uint32_t)h->part_id) continue;
@@ -1317,6 +1330,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
     p.peer[p.npeers++] = peer_write[q] + p.write_off;  // this part's slice in part q's replica
   }
   CK(launch_solve(shape, grid, p, h->stream));
+  h->part_pr_cur ^= 1;
   CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   return FPR_B200_OK;
@@ -1336,7 +1350,19 @@ int fpr_b200_part_info(const fpr_b200_graph* h, uint64_t* n_global, uint64_t* ro
 int fpr_b200_part_ranks(fpr_b200_graph* h, double* ranks_out) {
   if (!h || !ranks_out) return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks: null argument");
   CK(cudaSetDevice(h->device));
-  CK(cudaMemcpyAsync(ranks_out, h->pr, h->g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  const double* src = h->part_pr[0] ? h->part_pr[h->part_pr_cur] : h->pr;
+  CK(cudaMemcpyAsync(ranks_out, src, h->g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_ranks_prev(fpr_b200_graph* h, double* ranks_out) {
+  if (!h || !ranks_out) return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_prev: null argument");
+  if (!h->part_pr[0] || h->part_sweeps == 0)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_prev: no sweep since fpr_b200_part_init");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(ranks_out, h->part_pr[h->part_pr_cur ^ 1], h->g.n * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return FPR_B200_OK;
 }

@@ -165,9 +165,13 @@ class B200Part:
         _check(L.fpr_b200_part_sweep_peers(self.graph._h, engine, C.byref(c), read.data_ptr(),
                                            write.data_ptr(), arr, len(peer_ptrs), pair.data_ptr()))
 
-    def ranks(self) -> np.ndarray:
+    def ranks(self, back: int = 0) -> np.ndarray:
+        """This part's ranks after the latest sweep, or (back=1) one sweep earlier."""
         out = np.empty(max(self.n_local, 1), np.float64)
-        _check(lib().fpr_b200_part_ranks(self.graph._h, out.ctypes.data))
+        L = lib()
+        fn = L.fpr_b200_part_ranks_prev if back else L.fpr_b200_part_ranks
+        fn.argtypes = [C.c_void_p, C.c_void_p]
+        _check(fn(self.graph._h, out.ctypes.data))
         return out[: self.n_local]
 
     def close(self):
@@ -253,20 +257,28 @@ def _reduce_pairs(pairs: np.ndarray) -> tuple[float, float]:
 
 class PartitionedSolver:
     """This rank's solver state, built once and reused across solves: the
-    exchange vectors (two for EC's ping-pong; FUSED updates the first in
-    place), the residual pair and -- with fused_exchange -- the peers'
-    replicas mapped through CUDA IPC.  If the replicas cannot be mapped
-    (no P2P path), it falls back to the all-gather and says why in
-    `fallback`."""
+    exchange vectors (two for EC's ping-pong, three when speculating; FUSED
+    updates the first in place), the residual pairs and -- with
+    fused_exchange -- the peers' replicas mapped through CUDA IPC.  If the
+    replicas cannot be mapped (no P2P path), it falls back to the all-gather
+    and says why in `fallback`.
+
+    speculate=True (EC): sweep k+1 is enqueued before the host has read
+    iteration k's residual, so the GPU never idles on the host round trip.
+    Triple-buffered exchange vectors keep the extra sweep from touching
+    anything iteration k needs; if k was the stopping iteration the part's
+    ranks are read one sweep back (fpr_b200_part_ranks_prev), so results and
+    the iteration count are the non-speculative ones."""
 
     def __init__(self, local, exchange: TorchExchange, device="cuda", fused_exchange: bool = False,
-                 pairs_on_host: bool = False):
+                 pairs_on_host: bool = False, speculate: bool = False):
         import torch
 
         self.local, self.exchange, self.pairs_on_host = local, exchange, pairs_on_host
+        self.speculate = speculate
         P, S = exchange.world, local.slice
-        self.bufs = [torch.zeros(P * S, dtype=torch.float64, device=device) for _ in range(2)]
-        self.pair = torch.zeros(2, dtype=torch.float64, device=device)
+        self.bufs = [torch.zeros(P * S, dtype=torch.float64, device=device) for _ in range(3 if speculate else 2)]
+        self.pairs = [torch.zeros(2, dtype=torch.float64, device=device) for _ in range(2)]
         self.reps, self.fallback = None, None
         if fused_exchange:
             dev = self.bufs[0].device.index or 0
@@ -285,40 +297,72 @@ class PartitionedSolver:
     def fused_exchange(self) -> bool:
         return self.reps is not None
 
+    def _launch(self, j: int, engine: int, cfg: PageRankConfig):
+        """Enqueue sweep j and its residual all-gather; returns a token for _wait."""
+        import torch
+
+        nb = len(self.bufs)
+        ri, wi = (j % nb, (j + 1) % nb) if engine == ENGINE_EC else (0, 0)
+        read, write = self.bufs[ri], self.bufs[wi]
+        pair = self.pairs[j % 2]
+        if self.reps is not None:
+            # the sweep's epilogue stores into every peer replica (P2P)
+            self.local.sweep_peers(engine, cfg, read, write, self.reps.ptrs[wi], pair)
+        else:
+            self.local.sweep(engine, cfg, read, write, pair)
+            self.exchange.allgather_slices(write, self.local.slice)
+        # the residual all-gather is also the barrier that keeps a fast rank
+        # from writing a replica a slower peer is still reading
+        out = self.exchange.allgather_pairs(pair.cpu() if self.pairs_on_host else pair)
+        if out.is_cuda:
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            return host, ev
+        return out, None
+
+    @staticmethod
+    def _wait(tok) -> np.ndarray:
+        host, ev = tok
+        if ev is not None:
+            ev.synchronize()
+        return host.numpy()
+
     def solve(self, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF,
               want_ranks: bool = True) -> PartResult:
         if engine not in (ENGINE_EC, ENGINE_FUSED):
             raise ValueError("multi-GPU engines: EC or FUSED")
-        local, exchange, S = self.local, self.exchange, self.local.slice
-        ri = 0  # index of the buffer read this iteration
+        spec = self.speculate and engine == ENGINE_EC
+        local, exchange = self.local, self.exchange
         local.init(self.bufs[0])
-        exchange.allgather_slices(self.bufs[0], S)
+        exchange.allgather_slices(self.bufs[0], local.slice)
         res = PartResult(np.empty(0))
-        for it in range(int(cfg.max_iterations)):
-            t0 = time.perf_counter()
-            wi = 1 - ri if engine == ENGINE_EC else ri
-            read, write = self.bufs[ri], self.bufs[wi]
-            if self.reps is not None:
-                # the sweep's epilogue stores into every peer replica (P2P)
-                local.sweep_peers(engine, cfg, read, write, self.reps.ptrs[wi], self.pair)
-            else:
-                local.sweep(engine, cfg, read, write, self.pair)
-                exchange.allgather_slices(write, S)
-            # the residual all-gather is also the barrier that keeps a fast
-            # rank from writing a replica a slower peer is still reading
-            pr = self.pair.cpu() if self.pairs_on_host else self.pair
-            err, l1 = _reduce_pairs(exchange.allgather_pairs(pr).cpu().numpy())
-            res.iter_seconds.append(time.perf_counter() - t0)
+        max_it = int(cfg.max_iterations)
+        t0 = time.perf_counter()
+        pend = self._launch(0, engine, cfg)
+        ahead = None
+        it = 0
+        while True:
+            nxt = self._launch(it + 1, engine, cfg) if spec and it + 1 < max_it else None
+            err, l1 = _reduce_pairs(self._wait(pend))
+            t1 = time.perf_counter()
+            res.iter_seconds.append(t1 - t0)
+            t0 = t1
             res.errors.append(err)
             res.l1_errors.append(l1)
             res.iterations = it + 1
-            ri = wi
-            if (l1 if norm == NORM_L1 else err) <= cfg.threshold:
+            if (l1 if norm == NORM_L1 else err) <= cfg.threshold or it + 1 >= max_it:
+                ahead = nxt
                 break
+            pend = nxt if nxt is not None else self._launch(it + 1, engine, cfg)
+            it += 1
+        if ahead is not None:
+            self._wait(ahead)  # the extra sweep has finished everywhere before buffers are reused
         crit = res.l1_errors[-1] if norm == NORM_L1 else res.errors[-1]
         res.converged = crit <= cfg.threshold
         if want_ranks:
-            res.ranks = local.ranks()
+            res.ranks = local.ranks(back=1) if ahead is not None else local.ranks()
         return res
 
     def close(self):
@@ -333,14 +377,15 @@ class PartitionedSolver:
 
 def solve_partitioned(local, exchange: TorchExchange, engine: int, cfg: PageRankConfig,
                       norm: int = NORM_LINF, device="cuda", want_ranks: bool = True,
-                      fused_exchange: bool = False, pairs_on_host: bool = False) -> PartResult:
+                      fused_exchange: bool = False, pairs_on_host: bool = False,
+                      speculate: bool = False) -> PartResult:
     """Run `engine` to convergence on this rank's part (one process per GPU);
     a one-shot PartitionedSolver.  want_ranks=False leaves the part's ranks on
     the device (benchmarking).  fused_exchange=True replaces the per-iteration
     all-gather of contribution slices by the sweep's own P2P stores into the
     peers' replicas.  pairs_on_host moves the 16-B pair through host memory
     (gloo groups)."""
-    s = PartitionedSolver(local, exchange, device, fused_exchange, pairs_on_host)
+    s = PartitionedSolver(local, exchange, device, fused_exchange, pairs_on_host, speculate)
     try:
         return s.solve(engine, cfg, norm, want_ranks)
     finally:

@@ -45,17 +45,17 @@ class NumpyPart:
             sums[nz] = red
         nv = (1 - cfg.damping) / self.n_global + cfg.damping * sums
         d = np.abs(nv - self.pr)
-        self.pr = nv
+        self.prev, self.pr = self.pr, nv
         off = self.part * self.slice
         wr[off:off + self.n_local] = np.where(self.outdeg > 0, nv / np.maximum(self.outdeg, 1), 0.0)
         p = pair.numpy()
         p[0], p[1] = (d.max() if d.size else 0.0), d.sum()
 
-    def ranks(self):
-        return self.pr
+    def ranks(self, back=0):
+        return self.prev if back else self.pr
 
 
-def _worker(rank, world, port, engine, threshold, out_dir):
+def _worker(rank, world, port, engine, threshold, out_dir, speculate=False):
     import torch.distributed as dist
 
     from oracle import Oracle
@@ -69,7 +69,7 @@ def _worker(rank, world, port, engine, threshold, out_dir):
     bounds = partition_bounds(g.in_start, world)
     local = NumpyPart(g, bounds, rank)
     res = solve_partitioned(local, TorchExchange(), engine, PageRankConfig(threshold=threshold),
-                            device="cpu")
+                            device="cpu", speculate=speculate)
     np.save(os.path.join(out_dir, f"r{rank}.npy"), res.ranks)
     np.save(os.path.join(out_dir, f"e{rank}.npy"), np.array(res.errors))
     dist.destroy_process_group()
@@ -81,8 +81,8 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _run(engine, threshold, tmp_path):
-    mp.spawn(_worker, args=(2, _free_port(), engine, threshold, str(tmp_path)), nprocs=2, join=True)
+def _run(engine, threshold, tmp_path, speculate=False):
+    mp.spawn(_worker, args=(2, _free_port(), engine, threshold, str(tmp_path), speculate), nprocs=2, join=True)
     ranks = np.concatenate([np.load(tmp_path / f"r{r}.npy") for r in range(2)])
     errs = [np.load(tmp_path / f"e{r}.npy") for r in range(2)]
     return ranks, errs
@@ -102,8 +102,12 @@ def test_partition_bounds_balanced(oracle):
         assert np.array_equal(b[part] + rm % sl, g.in_src.astype(np.int64))
 
 
-def test_gloo_ec_matches_oracle(oracle, tmp_path):
-    ranks, errs = _run(ENGINE_EC, 1e-10, tmp_path)
+@pytest.mark.parametrize("speculate", [False, True])
+def test_gloo_ec_matches_oracle(oracle, tmp_path, speculate):
+    """speculate=True enqueues sweep k+1 before reading iteration k's residual
+    and reads the ranks one sweep back after the stop: same iteration count
+    and ranks as the non-speculative driver."""
+    ranks, errs = _run(ENGINE_EC, 1e-10, tmp_path, speculate)
     n, s, d = oracle.generate_rmat(11, 16, seed=7)
     ref = oracle.pagerank_ec(oracle.build_csr(n, s, d), threshold=1e-10)
     assert len(errs[0]) == len(errs[1]) == ref.iterations  # same stop decision everywhere

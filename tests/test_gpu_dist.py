@@ -89,7 +89,8 @@ def _ipc_worker(rank, world, port, path, q):
                 buf.copy_(h)
 
         cfg = fbw.PageRankConfig(threshold=1e-10)
-        res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, cfg, fused_exchange=True, pairs_on_host=True)
+        res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, cfg, fused_exchange=True, pairs_on_host=True,
+                                speculate=True)
         # FusEd in place: peers' P2P stores land in the vector this rank is sweeping
         fres = solve_partitioned(part, HostGather(), fbw.ENGINE_FUSED, cfg, fused_exchange=True,
                                  pairs_on_host=True)
