@@ -583,9 +583,9 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
 
 
 def e2e_multi(args, fb, dist, solver, cfg, dev, local, iters) -> dict:
-    """N GPUs end to end through the public API: every rank uploads the pinned
-    host CSR (fpr_b200_graph_create), partitions it on its device, solves with
-    the NCCL exchange and downloads its rank slice.  Max over ranks."""
+    """N GPUs end to end through the public API: every rank uploads only its
+    own rows of the pinned host CSR (fpr_b200_part_create), solves with the
+    partitioned driver and downloads its rank slice.  Max over ranks."""
     import torch
 
     from paper_2203_09284_b200.dist import B200Part
@@ -605,12 +605,14 @@ def e2e_multi(args, fb, dist, solver, cfg, dev, local, iters) -> dict:
     hg = fb.Graph(g.n, g.m, keep[0][1], keep[1][1], keep[2][1])
     ws, rank = dist.get_world_size(), dist.get_rank()
 
+    ranks_host = torch.empty(g.n, dtype=torch.float64, pin_memory=True).numpy()  # >= any part's rows
+
     def call():
-        with fb.DeviceGraph.from_graph(hg, device=local, stream=fb.torch_stream_handle()) as full_g:
-            p = B200Part(full_g, ws, rank, device=local, stream=fb.torch_stream_handle())
+        # each rank uploads only its own rows (fpr_b200_part_create)
+        p = B200Part.from_view(hg, ws, rank, device=local, stream=fb.torch_stream_handle())
         old = solver.local
         solver.rebind(p)  # exchange buffers / peer replicas are persistent state
-        r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=True)
+        r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=True, ranks_out=ranks_host)
         solver.rebind(old)
         p.close()
         return r
@@ -630,7 +632,7 @@ def e2e_multi(args, fb, dist, solver, cfg, dev, local, iters) -> dict:
     d2h = 8 * len(r.ranks) + 16 * ws * r.iterations
     return {"value": g.m * r.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
-            "api": "fpr_b200_graph_create + fpr_b200_graph_partition + fpr_b200_part_* (pinned host u64 CSR, per rank)"}
+            "api": "fpr_b200_part_create + fpr_b200_part_* (pinned host u64 CSR, each rank uploads its rows)"}
 
 
 def e2e_leg(fb, g, device, args, iters) -> dict:

@@ -193,6 +193,13 @@ int fpr_b200_graph_partition(const fpr_b200_graph* full, uint32_t nparts, uint32
 int fpr_b200_part_info(const fpr_b200_graph* g, uint64_t* n_global, uint64_t* row_begin,
                        uint64_t* slice, uint32_t* nparts, uint32_t* part);
 /* pr = 1/n_global for the part's rows; their contributions into exchange's slice. */
+/* Part `part` of `nparts` straight from a host view: the same destination-
+ * range bounds and slice as fpr_b200_graph_partition (computed on the host),
+ * but only this part's rows, in-edges and out-degrees are uploaded -- each
+ * rank of a multi-GPU job moves ~1/nparts of the graph over its own link. */
+int fpr_b200_part_create(const fpr_graph_view* view, uint32_t nparts, uint32_t part,
+                         const fpr_b200_options* opts, uint64_t* bounds_out, uint64_t* slice_out,
+                         fpr_b200_graph** out);
 int fpr_b200_part_init(fpr_b200_graph* g, double* exchange);
 /* One sweep on the part's stream, reading sources through exch_read and
  * writing the part's contributions into exch_write's slice (EC: distinct

@@ -102,7 +102,7 @@ EXPORTS = [
     "fpr_b200_part_init", "fpr_b200_part_sweep", "fpr_b200_part_ranks",
     "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
-    "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev",
+    "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev", "fpr_b200_part_create",
 ]
 
 _lib = None
@@ -134,6 +134,25 @@ def lib() -> C.CDLL:
         L.fpr_b200_graph_ranks_device.restype = vp
         L.fpr_b200_pagerank.argtypes = [C.POINTER(_GraphView), i32, C.POINTER(_Config),
                                         C.POINTER(_Options), vp, vp, u64, C.POINTER(_Result)]
+        # Every pointer-taking entry point gets its argtypes here, once: an
+        # unset argtype makes ctypes pass a Python int as a 32-bit C int.
+        u32 = C.c_uint32
+        L.fpr_b200_graph_partition.argtypes = [vp, u32, u32, C.POINTER(_Options), vp, C.POINTER(u64),
+                                               C.POINTER(vp)]
+        L.fpr_b200_part_create.argtypes = [C.POINTER(_GraphView), u32, u32, C.POINTER(_Options), vp,
+                                           C.POINTER(u64), C.POINTER(vp)]
+        L.fpr_b200_part_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(u32),
+                                         C.POINTER(u32)]
+        L.fpr_b200_part_init.argtypes = [vp, vp]
+        L.fpr_b200_part_sweep.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp]
+        L.fpr_b200_part_sweep_peers.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, u32, vp]
+        L.fpr_b200_part_ranks.argtypes = [vp, vp]
+        L.fpr_b200_part_ranks_prev.argtypes = [vp, vp]
+        L.fpr_b200_ipc_export.argtypes = [vp, vp]
+        L.fpr_b200_ipc_import.argtypes = [C.c_char_p, i32, C.POINTER(vp)]
+        L.fpr_b200_ipc_close.argtypes = [vp]
+        L.fpr_b200_graph_set_wave_count.argtypes = [vp, u32]
+        L.fpr_b200_graph_from_edges.argtypes = [u64, u64, vp, vp, C.POINTER(_Options), C.POINTER(vp)]
         L.fpr_b200_parse_edge_list.argtypes = [vp, u64, C.POINTER(_Options), C.POINTER(u64),
                                                C.POINTER(u64), vp, u64, C.POINTER(_ParseErr)]
         L.fpr_b200_graph_from_edge_list.argtypes = [vp, u64, C.POINTER(_Options), C.POINTER(vp),
@@ -338,8 +357,6 @@ class DeviceGraph:
             raise ValueError("from_edges: src and dst lengths differ")
         h = C.c_void_p()
         L = lib()
-        L.fpr_b200_graph_from_edges.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
-                                                C.POINTER(_Options), C.POINTER(C.c_void_p)]
         _check(L.fpr_b200_graph_from_edges(n, len(s_), s_.ctypes.data if len(s_) else None,
                                            d_.ctypes.data if len(d_) else None,
                                            C.byref(_options(device, norm, wave_count, stream, reorder, blocked)),
@@ -361,9 +378,7 @@ class DeviceGraph:
 
     def set_wave_count(self, waves: int) -> None:
         """Lockstep engine: waves per sweep for later runs (0 = auto)."""
-        L = lib()
-        L.fpr_b200_graph_set_wave_count.argtypes = [C.c_void_p, C.c_uint32]
-        _check(L.fpr_b200_graph_set_wave_count(self._h, waves))
+        _check(lib().fpr_b200_graph_set_wave_count(self._h, waves))
 
     def validate(self) -> int:
         """0 iff the resident CSR satisfies build_csr's invariants (device check)."""

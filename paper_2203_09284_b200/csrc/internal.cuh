@@ -130,6 +130,9 @@ cudaError_t launch_part_bounds(const DevGraph& g, uint32_t nparts, int64_t* boun
 cudaError_t launch_part_extract(const DevGraph& g, const int64_t* bounds, uint32_t nparts,
                                 uint32_t part, int64_t slice, int64_t nloc, int64_t mloc,
                                 DevGraph& out, cudaStream_t s);
+cudaError_t launch_offset_shift(int64_t* row, int64_t count, int64_t e0, cudaStream_t s);
+cudaError_t launch_part_remap(int32_t* src, int64_t m, const int64_t* bounds, uint32_t nparts, int64_t slice,
+                              cudaStream_t s);
 cudaError_t launch_part_init(const DevGraph& g, double init, double* pr, double* contrib_slice,
                              cudaStream_t s);
 cudaError_t launch_validate(const DevGraph& g, int32_t* recount, unsigned int* bad, cudaStream_t s);

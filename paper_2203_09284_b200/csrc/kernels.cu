@@ -719,6 +719,32 @@ __global__ void part_extract_kernel(const int64_t* row, const int32_t* src, cons
   }
 }
 
+// In-place variants for a part uploaded directly from the host (part_create):
+// row offsets made local, global source ids remapped into the exchange space.
+__global__ void offset_shift_kernel(int64_t* row, int64_t count, int64_t e0) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) row[i] -= e0;
+}
+
+__global__ void part_remap_kernel(int32_t* src, int64_t m, const int64_t* bounds, uint32_t nparts, int64_t slice) {
+  __shared__ int64_t sb[65];
+  for (uint32_t i = threadIdx.x; i <= nparts; i += blockDim.x) sb[i] = bounds[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    const int32_t s = src[e];
+    uint32_t lo = 0, hi = nparts;  // last part with bounds[part] <= s
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sb[mid] <= s)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    src[e] = (int32_t)((int64_t)lo * slice + (s - sb[lo]));
+  }
+}
+
 __global__ void part_init_kernel(int32_t n, const int32_t* outdeg, double init, double* pr,
                                  double* contrib_slice) {
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
@@ -865,6 +891,17 @@ cudaError_t launch_part_extract(const DevGraph& g, const int64_t* bounds, uint32
                                 DevGraph& out, cudaStream_t s) {
   part_extract_kernel<<<grid_for(nloc > mloc ? nloc : mloc), 256, 0, s>>>(
       g.row, g.src, g.outdeg, bounds, nparts, part, slice, out.row, out.src, out.outdeg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_offset_shift(int64_t* row, int64_t count, int64_t e0, cudaStream_t s) {
+  if (count > 0) offset_shift_kernel<<<grid_for(count), 256, 0, s>>>(row, count, e0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_remap(int32_t* src, int64_t m, const int64_t* bounds, uint32_t nparts, int64_t slice,
+                              cudaStream_t s) {
+  if (m > 0) part_remap_kernel<<<grid_for(m), 256, 0, s>>>(src, m, bounds, nparts, slice);
   return cudaGetLastError();
 }
 

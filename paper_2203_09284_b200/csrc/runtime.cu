@@ -1236,6 +1236,124 @@ int fpr_b200_graph_partition(const fpr_b200_graph* fullc, uint32_t nparts, uint3
   return FPR_B200_OK;
 }
 
+// Host restatement of part_bounds_kernel / merge_path (same integer steps), so
+// every rank derives the same bounds from its own copy of in_start.
+namespace {
+std::vector<int64_t> host_part_bounds(const uint64_t* in_start, int64_t n, int64_t m, uint32_t nparts) {
+  std::vector<int64_t> b(nparts + 1);
+  const int64_t total = n + m;
+  for (uint32_t r = 0; r <= nparts; ++r) {
+    if (r == nparts) {
+      b[r] = n;
+      continue;
+    }
+    const int64_t diag = (int64_t)((__int128)total * r / nparts);
+    int64_t lo = diag - m > 0 ? diag - m : 0;
+    int64_t hi = diag < n ? diag : n;
+    while (lo < hi) {
+      const int64_t pivot = (lo + hi) >> 1;
+      if ((int64_t)in_start[pivot + 1] <= diag - pivot - 1)
+        lo = pivot + 1;
+      else
+        hi = pivot;
+    }
+    b[r] = lo;
+  }
+  return b;
+}
+}  // namespace
+
+int fpr_b200_part_create(const fpr_graph_view* v, uint32_t nparts, uint32_t part, const fpr_b200_options* opts,
+                         uint64_t* bounds_out, uint64_t* slice_out, fpr_b200_graph** out) {
+  if (!v || !out) return fail(FPR_B200_EINVAL, "fpr_b200_part_create: null argument");
+  *out = nullptr;
+  if (nparts == 0 || nparts > 64 || part >= nparts)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_create: need 1 <= nparts <= 64, part < nparts");
+  if (v->n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  if (v->n >= (1ULL << 31))
+    return fail(FPR_B200_ERANGE, "fpr_b200: n = " + std::to_string(v->n) +
+                                     " exceeds the int32 vertex-id range (n < 2^31)");
+  if (!v->in_start || !v->out_degree || (v->m > 0 && !v->in_src))
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_create: null array");
+  if (v->in_start[0] != 0 || v->in_start[v->n] != v->m)
+    return fail(FPR_B200_EINVAL, "fpr_b200: in_start is not a valid CSR offset array "
+                                 "(in_start[0]==0, non-decreasing, in_start[n]==m)");
+  const std::vector<int64_t> b = host_part_bounds(v->in_start, (int64_t)v->n, (int64_t)v->m, nparts);
+  int64_t slice = 0;
+  for (uint32_t r = 0; r < nparts; ++r) slice = std::max<int64_t>(slice, b[r + 1] - b[r]);
+  if ((int64_t)nparts * slice >= INT32_MAX)
+    return fail(FPR_B200_ERANGE, "fpr_b200: padded exchange space exceeds int32 ids");
+  const int64_t b0 = b[part], b1 = b[part + 1];
+  const int64_t e0 = (int64_t)v->in_start[b0], e1 = (int64_t)v->in_start[b1];
+  if (e1 < e0) return fail(FPR_B200_EINVAL, "fpr_b200: in_start is not a valid CSR offset array "
+                                            "(in_start[0]==0, non-decreasing, in_start[n]==m)");
+  fpr_b200_graph* h = nullptr;
+  int rc = open_handle(opts, &h);
+  if (rc) {
+    destroy_handle(h);
+    return rc;
+  }
+  auto bail = [&](int code) {
+    destroy_handle(h);
+    return code;
+  };
+  DevGraph& g = h->g;
+  g.n = (int32_t)(b1 - b0);
+  g.m = e1 - e0;
+  unsigned int* bad = nullptr;
+  int64_t* d_bounds = nullptr;
+  if ((rc = dalloc_n(h, &g.row, (int64_t)g.n + 1)) || (rc = dalloc_n(h, &g.src, g.m + 8)) ||
+      (rc = dalloc_n(h, &g.outdeg, std::max<int64_t>(g.n, 1))) || (rc = dalloc_n(h, &bad, 1)) ||
+      (rc = dalloc_n(h, &d_bounds, nparts + 1)))
+    return bail(rc);
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_bounds, b.data(), (nparts + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // b is a host vector
+  // Only this part's rows cross the link: in_start[b0..b1], in_src[e0..e1),
+  // out_degree[b0..b1) -- ids range-checked against the global n.
+  const bool pinned = is_pinned(v->in_start) && (g.m == 0 || is_pinned(v->in_src)) && is_pinned(v->out_degree);
+  if (e == cudaSuccess && pinned) {
+    const std::vector<IdUpload> arrays = {{v->in_src + e0, g.src, g.m, true}, {v->out_degree + b0, g.outdeg, g.n, false}};
+    if ((rc = upload_ids_pinned(h, arrays, v->n, bad, v->in_start + b0, g.row, ((size_t)g.n + 1) * sizeof(int64_t),
+                                &e)))
+      return bail(rc);
+  } else if (e == cudaSuccess) {
+    UploadRing* ring = get_ring(h->device);
+    if (!ring) return bail(fail(FPR_B200_ENOMEM, "fpr_b200: pinned upload ring allocation failed"));
+    std::lock_guard<std::mutex> lk(ring->mu);
+    int k = 0;
+    bool ok = ring_upload<int64_t>(ring, v->in_start + b0, g.row, (int64_t)g.n + 1, 0, h->stream, k, &e);
+    ok = ring_upload<int32_t>(ring, v->in_src + e0, g.src, g.m, v->n, h->stream, k, &e) && ok;
+    ok = ring_upload<int32_t>(ring, v->out_degree + b0, g.outdeg, g.n, v->n, h->stream, k, &e) && ok;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess && !ok) e = cudaMemsetAsync(bad, 1, 1, h->stream);
+  }
+  if (e == cudaSuccess) e = launch_offset_shift(g.row, (int64_t)g.n + 1, e0, h->stream);
+  if (e == cudaSuccess && g.n > 0) e = launch_check_offsets(g.row, g.n, g.m, bad, h->stream);
+  if (e == cudaSuccess) e = launch_part_remap(g.src, g.m, d_bounds, nparts, slice, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->h_iters, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess)
+    return bail(fail(FPR_B200_ECUDA, std::string("fpr_b200_part_create: ") + cudaGetErrorString(e)));
+  if (*h->h_iters & 1u)
+    return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_src/out_degree value outside [0," + std::to_string(v->n) + ")"));
+  if (*h->h_iters & 6u)
+    return bail(fail(FPR_B200_EINVAL, "fpr_b200: in_start is not a valid CSR offset array "
+                                      "(in_start[0]==0, non-decreasing, in_start[n]==m)"));
+  h->nparts = nparts;
+  h->part_id = part;
+  h->n_global = v->n;
+  h->row_begin = (uint64_t)b0;
+  h->slice = (uint64_t)slice;
+  if ((rc = finish_graph(h))) return bail(rc);
+  if (bounds_out)
+    for (uint32_t r = 0; r <= nparts; ++r) bounds_out[r] = (uint64_t)b[r];
+  if (slice_out) *slice_out = (uint64_t)slice;
+  *out = h;
+  return FPR_B200_OK;
+}
+
 int fpr_b200_part_init(fpr_b200_graph* h, double* exchange) {
   if (!h || !exchange) return fail(FPR_B200_EINVAL, "fpr_b200_part_init: null argument");
   CK(cudaSetDevice(h->device));

@@ -39,7 +39,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import (B200Error, DeviceGraph, PageRankConfig, _check, _Config, _options, lib, ENGINE_EC,
+from . import (B200Error, DeviceGraph, PageRankConfig, _check, _Config, _Options, _options, lib, ENGINE_EC,
                ENGINE_FUSED, NORM_L1, NORM_LINF)
 
 
@@ -114,6 +114,21 @@ class EmulatedExchange:
                     bufs[q][r * slice_:(r + 1) * slice_].copy_(src)
 
 
+_PINNED = {}
+
+
+def _pinned_f64(count: int):
+    """A reusable pinned host buffer of at least `count` doubles (pinned
+    allocation costs milliseconds; a per-call one would dominate a D2H)."""
+    import torch
+
+    buf = _PINNED.get("f64")
+    if buf is None or buf.numel() < count:
+        buf = torch.empty(count, dtype=torch.float64, pin_memory=True)
+        _PINNED["f64"] = buf
+    return buf[:count]
+
+
 # ------------------------------------------------------------------ local sweep
 class B200Part:
     """This rank's part on its GPU, driven through the C ABI."""
@@ -130,12 +145,6 @@ class B200Part:
         sl = C.c_uint64()
         h = C.c_void_p()
         L = lib()
-        L.fpr_b200_graph_partition.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
-                                               C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]
-        L.fpr_b200_part_init.argtypes = [C.c_void_p, C.c_void_p]
-        L.fpr_b200_part_sweep.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Config), C.c_void_p,
-                                          C.c_void_p, C.c_void_p]
-        L.fpr_b200_part_ranks.argtypes = [C.c_void_p, C.c_void_p]
         opts = _options(device=device, stream=stream)
         _check(L.fpr_b200_graph_partition(full._h, nparts, part, C.byref(opts), bounds.ctypes.data,
                                           C.byref(sl), C.byref(h)))
@@ -144,6 +153,33 @@ class B200Part:
         self.slice = int(sl.value)
         self.n_global = full.n
         self.n_local = int(self.bounds[part + 1] - self.bounds[part])
+
+    @classmethod
+    def from_view(cls, g, nparts: int, part: int, device: int = 0, stream=None) -> "B200Part":
+        """This rank's part straight from a host fpr::Graph (pinned or pageable
+        u64 arrays): only ~1/nparts of the graph is uploaded
+        (fpr_b200_part_create); same bounds and slice as from a full DeviceGraph."""
+        from . import _GraphView, _u64, torch_stream_handle
+
+        if stream is None:
+            stream = torch_stream_handle()
+        ins, src, od = (a if isinstance(a, np.ndarray) and a.dtype == np.uint64 and a.flags.c_contiguous
+                        else _u64(a) for a in (g.in_start, g.in_src, g.out_degree))
+        v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
+        bounds = np.empty(nparts + 1, np.uint64)
+        sl = C.c_uint64()
+        h = C.c_void_p()
+        L = lib()
+        _check(L.fpr_b200_part_create(C.byref(v), nparts, part, C.byref(_options(device=device, stream=stream)),
+                                      bounds.ctypes.data, C.byref(sl), C.byref(h)))
+        self = cls.__new__(cls)
+        self.nparts, self.part = nparts, part
+        self.graph = DeviceGraph(h.value)
+        self.bounds = bounds.astype(np.int64)
+        self.slice = int(sl.value)
+        self.n_global = g.n
+        self.n_local = int(self.bounds[part + 1] - self.bounds[part])
+        return self
 
     def init(self, exch) -> None:
         _check(lib().fpr_b200_part_init(self.graph._h, exch.data_ptr()))
@@ -160,19 +196,24 @@ class B200Part:
         c = cfg._c()
         arr = (C.c_void_p * len(peer_ptrs))(*peer_ptrs)
         L = lib()
-        L.fpr_b200_part_sweep_peers.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Config), C.c_void_p,
-                                                C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]
         _check(L.fpr_b200_part_sweep_peers(self.graph._h, engine, C.byref(c), read.data_ptr(),
                                            write.data_ptr(), arr, len(peer_ptrs), pair.data_ptr()))
 
-    def ranks(self, back: int = 0) -> np.ndarray:
-        """This part's ranks after the latest sweep, or (back=1) one sweep earlier."""
-        out = np.empty(max(self.n_local, 1), np.float64)
+    def ranks(self, back: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+        """This part's ranks after the latest sweep, or (back=1) one sweep
+        earlier.  `out` (n_local float64, ideally pinned) receives them
+        directly; otherwise they go through a reusable pinned buffer (a
+        pageable D2H of a large part runs at a fraction of the link rate)."""
         L = lib()
         fn = L.fpr_b200_part_ranks_prev if back else L.fpr_b200_part_ranks
-        fn.argtypes = [C.c_void_p, C.c_void_p]
-        _check(fn(self.graph._h, out.ctypes.data))
-        return out[: self.n_local]
+        if out is not None:
+            if out.dtype != np.float64 or not out.flags.c_contiguous or len(out) < self.n_local:
+                raise ValueError("ranks: out must be a contiguous float64 array of n_local entries")
+            _check(fn(self.graph._h, out.ctypes.data))
+            return out[: self.n_local]
+        pinned = _pinned_f64(max(self.n_local, 1))
+        _check(fn(self.graph._h, pinned.data_ptr()))
+        return pinned.numpy()[: self.n_local].copy()
 
     def close(self):
         self.graph.close()
@@ -185,7 +226,6 @@ IPC_HANDLE_BYTES = 72  # FPR_B200_IPC_HANDLE_BYTES
 def ipc_export(ptr: int) -> bytes:
     h = (C.c_char * IPC_HANDLE_BYTES)()
     L = lib()
-    L.fpr_b200_ipc_export.argtypes = [C.c_void_p, C.c_void_p]
     _check(L.fpr_b200_ipc_export(ptr, h))
     return bytes(h.raw)
 
@@ -193,14 +233,12 @@ def ipc_export(ptr: int) -> bytes:
 def ipc_import(handle: bytes, device: int) -> int:
     out = C.c_void_p()
     L = lib()
-    L.fpr_b200_ipc_import.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
     _check(L.fpr_b200_ipc_import(handle, device, C.byref(out)))
     return out.value
 
 
 def ipc_close(ptr: int) -> None:
     L = lib()
-    L.fpr_b200_ipc_close.argtypes = [C.c_void_p]
     _check(L.fpr_b200_ipc_close(ptr))
 
 
@@ -330,7 +368,7 @@ class PartitionedSolver:
         return host.numpy()
 
     def solve(self, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF,
-              want_ranks: bool = True) -> PartResult:
+              want_ranks: bool = True, ranks_out: np.ndarray | None = None) -> PartResult:
         if engine not in (ENGINE_EC, ENGINE_FUSED):
             raise ValueError("multi-GPU engines: EC or FUSED")
         spec = self.speculate and engine == ENGINE_EC
@@ -362,7 +400,7 @@ class PartitionedSolver:
         crit = res.l1_errors[-1] if norm == NORM_L1 else res.errors[-1]
         res.converged = crit <= cfg.threshold
         if want_ranks:
-            res.ranks = local.ranks(back=1) if ahead is not None else local.ranks()
+            res.ranks = local.ranks(back=1 if ahead is not None else 0, out=ranks_out)
         return res
 
     def close(self):

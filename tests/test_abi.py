@@ -85,3 +85,15 @@ def test_metrics_mirror():
     assert fb.linf_norm([1.0, 2.0], [1.5, 1.0]) == 1.0
     with pytest.raises(ValueError, match="length mismatch"):
         fb.l1_norm(np.zeros(2), np.zeros(3))
+
+
+def test_every_pointer_entry_point_has_argtypes():
+    """ctypes passes an un-declared Python int as a 32-bit C int, silently
+    truncating device pointers; lib() must declare every entry point that
+    takes arguments (a part created without the partition path once hit it)."""
+    L = fb.lib()
+    no_args = {"fpr_b200_last_error", "fpr_b200_version"}
+    for name in fb.EXPORTS:
+        if name in no_args:
+            continue
+        assert getattr(L, name).argtypes is not None, name

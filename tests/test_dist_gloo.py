@@ -51,8 +51,12 @@ class NumpyPart:
         p = pair.numpy()
         p[0], p[1] = (d.max() if d.size else 0.0), d.sum()
 
-    def ranks(self, back=0):
-        return self.prev if back else self.pr
+    def ranks(self, back=0, out=None):
+        r = self.prev if back else self.pr
+        if out is not None:
+            out[: len(r)] = r
+            return out[: len(r)]
+        return r
 
 
 def _worker(rank, world, port, engine, threshold, out_dir, speculate=False):

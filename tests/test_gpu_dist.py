@@ -132,3 +132,32 @@ def test_fused_exchange_two_processes_cuda_ipc():
     it, ref_it, rel, fconv, fl1, bound = q.get(timeout=5)
     assert it == ref_it and rel <= 1e-12
     assert fconv and fl1 <= bound
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_part_create_matches_partition(oracle, P):
+    """fpr_b200_part_create (each rank uploads only its rows) gives the same
+    bounds, slice, local CSR in exchange ids and EC result as partitioning a
+    full resident graph."""
+    n, s, d = oracle.generate_rmat(16, 16, seed=1)
+    g = oracle.build_csr(n, s, d)
+    hg = fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+    stream = fb.torch_stream_handle()
+    with fb.DeviceGraph.from_graph(hg) as full:
+        ref_parts = [B200Part(full, P, r, stream=stream) for r in range(P)]
+    parts = [B200Part.from_view(hg, P, r, stream=stream) for r in range(P)]
+    for a, b in zip(parts, ref_parts):
+        np.testing.assert_array_equal(a.bounds, b.bounds)
+        assert a.slice == b.slice and a.n_local == b.n_local
+        ga, gb = a.graph.download(), b.graph.download()
+        np.testing.assert_array_equal(ga.in_start, gb.in_start)
+        np.testing.assert_array_equal(ga.in_src, gb.in_src)
+        np.testing.assert_array_equal(ga.out_degree, gb.out_degree)
+    cfg = fb.PageRankConfig(threshold=1e-10)
+    r1 = solve_emulated(parts, fb.ENGINE_EC, cfg)
+    r2 = solve_emulated(ref_parts, fb.ENGINE_EC, cfg)
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(r1.ranks, r2.ranks)
+    for q in parts + ref_parts:
+        q.close()
+
