@@ -158,7 +158,7 @@ def run_reference(args) -> None:
     gteps = g.m * args.steps / t / 1e9
     line = {"metric": METRIC, "value": gteps, "unit": "GTEPS",
             "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_sparse seed 2)",
             "config": {"workload": WORKLOAD, "n": g.n, "m": g.m, "step": "1 EC iteration",
                        "engine": engine},
@@ -477,11 +477,12 @@ def main() -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "GTEPS",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            # config 2 at every N: total work fixed (N > 1 partitions it, run_multi)
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
             "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
                        "norm": "linf", "step": "1 full EC solve (time-to-converge)",
-                       "parallelism": "replicas" if ws > 1 else "single-gpu",
+                       "parallelism": "single-gpu",
                        "l2": "inputs larger than L2 (in_src 268 MB + contrib 33.5 MB + row_ptr 33.5 MB); no flush"},
             "time_to_converge_ms": ms_step,
             "iteration_us": it_us,
