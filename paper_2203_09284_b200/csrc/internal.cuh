@@ -77,6 +77,7 @@ struct SolveParams {
   const int32_t* wave_task;  // nwaves+1
   const int32_t* wave_row;   // nwaves+1
   int32_t nwaves;
+  int64_t nsrc;   // contributions addressable by a gather (n, or nparts*slice for a part)
   double* pr;      // ranks read (old value of each row)
   double* pr_out;  // ranks written: == pr except in multi-GPU part sweeps (ping-pong)
   double* contrib0;

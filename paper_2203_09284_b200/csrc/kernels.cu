@@ -460,6 +460,31 @@ __device__ __forceinline__ unsigned load_bits8(const SolveParams& p, int t, int 
   return (__ldg(p.task_bits + 8 * (int64_t)t + (lane >> 2)) >> ((lane & 3) * 8)) & 0xffu;
 }
 
+#ifdef FPR_CHECKS
+// Debug build (make variant V=checks EXTRA=-DFPR_CHECKS): every task's
+// metadata and source ids are bounds-checked before use; a violation traps.
+__device__ __noinline__ void check_task(const SolveParams& p, int t, const TaskMeta& m, const Src8& sx, int lane) {
+  const bool meta_ok = t >= 0 && t < p.ntasks && m.i0 >= 0 && m.i0 <= m.i1 && m.i1 <= p.n && m.j0 >= 0 &&
+                       m.j0 <= m.j1 && m.j1 - m.j0 <= kTaskItems && __ldg(p.head_first + t) <= t;
+  const int off = (int)(m.j0 & (kPosAlign - 1));
+  const int valid_hi = off + (int)(m.j1 - m.j0);
+  const int sids[8] = {sx.a.x, sx.a.y, sx.a.z, sx.a.w, sx.b.x, sx.b.y, sx.b.z, sx.b.w};
+  bool ids_ok = true;
+  for (int i = 0; i < 8; ++i) {
+    const int q = 8 * lane + i;
+    if (q >= off && q < valid_hi) ids_ok = ids_ok && sids[i] >= 0 && (int64_t)sids[i] < p.nsrc;
+  }
+  if (!meta_ok || !ids_ok) {
+    printf("FPR_CHECKS: task %d lane %d meta_ok %d ids_ok %d i0 %d i1 %d j0 %lld j1 %lld\n", t, lane, (int)meta_ok,
+           (int)ids_ok, m.i0, m.i1, (long long)m.j0, (long long)m.j1);
+    __trap();
+  }
+}
+#define FPR_CHECK_TASK(p, t, m, sx, lane) check_task(p, t, m, sx, lane)
+#else
+#define FPR_CHECK_TASK(p, t, m, sx, lane) ((void)0)
+#endif
+
 template <bool ASYNC, int MODE>
 __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, int gwarp,
                                           int nwarps, int fresh_below, const double* prev,
@@ -471,6 +496,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   double v[8];
   {
     const Src8 sx = load_src8(p, m, lane, pol);
+    FPR_CHECK_TASK(p, t, m, sx, lane);
     issue_gathers8<ASYNC>(m, sx, lane, fresh_below, prev, cur, v);
   }
   RowPre rp = load_rowpre<MODE>(p, m, lane);
@@ -490,6 +516,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
     Src8 snn{{0, 0, 0, 0}, {0, 0, 0, 0}};
     TaskMeta mnnn{0, 0, 0, 0};
     if (tn < te) {
+      FPR_CHECK_TASK(p, tn, mn, sn, lane);
       issue_gathers8<ASYNC>(mn, sn, lane, fresh_below, prev, cur, v);
       rpn = load_rowpre<MODE>(p, mn, lane);
       bitsn = load_bits8(p, tn, lane);

@@ -936,6 +936,7 @@ int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, dou
   CK(cudaEventRecord(h->ev[1], h->stream));
   const int wpb = solve_block_threads(kEC) / 32;
   SolveParams p{};
+  p.nsrc = g.n;
   p.pr = h->pr;
   p.pr_out = h->pr;
   p.damping = cfg->damping;
@@ -1075,6 +1076,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   p.wave_task = wv->d_task;
   p.wave_row = wv->d_row;
   p.nwaves = wv->nwaves;
+  p.nsrc = g.n;
   p.pr = h->pr;
   p.pr_out = h->pr;
   p.contrib0 = h->contrib[0];
@@ -1414,6 +1416,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   p.nwaves = wv->nwaves;
   // ranks ping-pong between two buffers, so the state before the latest
   // sweep stays readable (fpr_b200_part_ranks_prev: speculative drivers)
+  p.nsrc = (int64_t)h->nparts * (int64_t)(h->nparts > 1 ? h->slice : (uint64_t)h->g.n);
   p.pr = h->part_pr[h->part_pr_cur];
   p.pr_out = h->part_pr[h->part_pr_cur ^ 1];
   p.contrib0 = const_cast<double*>(exch_read);
