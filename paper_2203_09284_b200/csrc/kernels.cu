@@ -569,6 +569,12 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
       }
       par ^= 1;
     }
+#ifdef FPR_TRACE_WARPS
+    // diagnostic build (scripts/warp_tail.py): when each warp finished sweep 2,
+    // stored past the tail partials (the runtime over-allocates that array)
+    if (it == 2 && lane == 0)
+      reinterpret_cast<unsigned long long*>(p.tail_partial)[p.ntasks + 1 + gwarp] = globaltimer();
+#endif
     block_reduce(lmax, lsum, sred);
     double tmax, tsum;
     grid_sync_reduce(p, lmax, lsum, tmax, tsum, sred);

@@ -346,6 +346,12 @@ int open_handle(const fpr_b200_options* opts, fpr_b200_graph** out) {
 
 // Partition + solver state, common to create/generate (after the optional
 // locality reorder, which swaps in the renumbered CSR).
+#ifdef FPR_TRACE_WARPS
+constexpr int64_t kTraceWarps = 8192;  // per-warp timestamps after the tail partials
+#else
+constexpr int64_t kTraceWarps = 0;
+#endif
+
 int finish_graph(fpr_b200_graph* h) {
   if ((h->flags & FPR_B200_OPT_REORDER) && h->g.n > 1) {
     DevGraph re;
@@ -375,7 +381,7 @@ int finish_graph(fpr_b200_graph* h) {
     return rc;
   if (g.n > 0) CK(launch_partition(g, p, h->stream));
   if ((rc = dalloc_n(h, &h->pr, g.n)) || (rc = dalloc_n(h, &h->contrib[0], g.n)) ||
-      (rc = dalloc_n(h, &h->contrib[1], g.n)) || (rc = dalloc_n(h, &h->tail_partial, nt + 1)))
+      (rc = dalloc_n(h, &h->contrib[1], g.n)) || (rc = dalloc_n(h, &h->tail_partial, nt + 1 + kTraceWarps)))
     return rc;
   // tail partials start "not ready" (NaN); each consumer re-arms what it reads.
   CK(cudaMemsetAsync(h->tail_partial, 0xFF, (nt + 1) * sizeof(double), h->stream));
@@ -1728,4 +1734,14 @@ int fpr_b200_ipc_close(void* dev_ptr) {
 }
 
 }  // extern "C"
+
+#ifdef FPR_TRACE_WARPS
+// Diagnostic build only: per-warp finish times of sweep 2 and the sweep stamps.
+extern "C" int fpr_b200_debug_warp_times(fpr_b200_graph* h, uint64_t* out, uint64_t nwarps) {
+  cudaMemcpy(out, reinterpret_cast<unsigned long long*>(h->tail_partial) + h->part.ntasks + 1, nwarps * 8,
+             cudaMemcpyDeviceToHost);
+  cudaMemcpy(out + nwarps, h->d_ns, 5 * 8, cudaMemcpyDeviceToHost);
+  return 0;
+}
+#endif
 

@@ -1,4 +1,6 @@
-"""Per-warp finish times within EC sweep 3 (variant lib built with -DFPR_TRACE_WARPS)."""
+"""Per-warp finish times within EC sweep 3.  Needs the diagnostic build:
+make -C paper_2203_09284_b200/csrc variant V=trace EXTRA=-DFPR_TRACE_WARPS, then
+FPR_B200_LIB=paper_2203_09284_b200/csrc/build/libfpr_b200_trace.so python scripts/warp_tail.py"""
 import ctypes as C, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
