@@ -41,6 +41,7 @@ NORM_LINF, NORM_L1 = 0, 1
 GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
 OPT_REORDER = 1  # FPR_B200_OPT_REORDER
 OPT_BLOCKED = 2  # FPR_B200_OPT_BLOCKED
+OPT_PB = 4  # FPR_B200_OPT_PB
 
 
 class B200Error(RuntimeError):
@@ -278,13 +279,13 @@ def torch_stream_handle() -> int:
     return h if h else CUDA_STREAM_LEGACY
 
 
-def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False) -> _Options:
+def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False, pb=False) -> _Options:
     o = _Options()
     lib().fpr_b200_options_init(C.byref(o))
     o.device = device
     o.norm = norm
     o.wave_count = wave_count
-    o.flags = (OPT_REORDER if reorder else 0) | (OPT_BLOCKED if blocked else 0)
+    o.flags = (OPT_REORDER if reorder else 0) | (OPT_BLOCKED if blocked else 0) | (OPT_PB if pb else 0)
     o.stream = stream
     return o
 
@@ -306,49 +307,49 @@ class DeviceGraph:
     # -- construction ---------------------------------------------------
     @classmethod
     def from_graph(cls, g: Graph, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
-                   blocked=False):
+                   blocked=False, pb=False):
         ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
         v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
         h = C.c_void_p()
         _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream, reorder,
-                                                                        blocked)),
+                                                                        blocked, pb)),
                                            C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
-    def _generate(cls, gp, device, norm, wave_count, stream, reorder=False, blocked=False):
+    def _generate(cls, gp, device, norm, wave_count, stream, reorder=False, blocked=False, pb=False):
         h = C.c_void_p()
         _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream, reorder,
-                                                                          blocked)),
+                                                                          blocked, pb)),
                                              C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
     def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None,
-                      relabel_bfs=False, bfs_root=0, reorder=False, blocked=False):
+                      relabel_bfs=False, bfs_root=0, reorder=False, blocked=False, pb=False):
         """build_csr(generate_rmat(p)) on the device; relabel_bfs=True gives
         BASELINE config 3's crawl order (BFS from bfs_root over out-edges)."""
         gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed,
                         0, 0.0, 0, int(relabel_bfs), 0, bfs_root)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
 
     @classmethod
     def generate_uniform(cls, n: int, avg_degree: int, seed: int, device=-1, norm=NORM_LINF,
-                         wave_count=0, stream=None, reorder=False, blocked=False):
+                         wave_count=0, stream=None, reorder=False, blocked=False, pb=False):
         """build_csr(testutil::random_sparse(n, avg_degree, SplitMix64(seed)))."""
         gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, n, avg_degree, seed)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
 
     @classmethod
     def generate_chunglu(cls, n: int, draws: int, seed: int, alpha: float = 2.1, kmax: int = 1_000_000,
-                         device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False):
+                         device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False, pb=False):
         """BASELINE config 4 (definition: DESIGN.md §4.1; oracle fo_generate_chunglu)."""
         gp = _GenParams(GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, n, 0, seed, draws, alpha, kmax)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
 
     @classmethod
     def from_edges(cls, n: int, src, dst, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
-                   blocked=False):
+                   blocked=False, pb=False):
         """fpr::build_csr(EdgeSet{n, (src, dst)}) on the device (graph.hpp:35-70):
         duplicates and self-loops dropped, in-segments ascending; ValueError
         names the first out-of-range edge as build_csr does."""
@@ -359,7 +360,7 @@ class DeviceGraph:
         L = lib()
         _check(L.fpr_b200_graph_from_edges(n, len(s_), s_.ctypes.data if len(s_) else None,
                                            d_.ctypes.data if len(d_) else None,
-                                           C.byref(_options(device, norm, wave_count, stream, reorder, blocked)),
+                                           C.byref(_options(device, norm, wave_count, stream, reorder, blocked, pb)),
                                            C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 

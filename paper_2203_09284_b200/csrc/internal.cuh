@@ -220,4 +220,37 @@ void free_blocks(BlockSet& bs, cudaStream_t st);
 cudaError_t launch_apply(const BlockSet& bs, int32_t n, const int32_t* outdeg, double* pr, double* cur,
                          double base, double damping, double* err, double* l1, cudaStream_t st);
 
+// pb.cu: propagation-blocked EC (FPR_B200_OPT_PB).
+struct PbSet {
+  int shift = 0;         // destination bin = row >> shift (at most 2^16 rows: uint16 offsets)
+  int chunk_shift = 0;   // source chunk = src >> chunk_shift
+  int64_t nbins = 0, nchunks = 0, m = 0;
+  int32_t* src_bm = nullptr;     // m: source of each entry; bin b's entries are the in-CSR's edges of its rows,
+                                 //    regrouped by source chunk: (bin, chunk, k) order
+  uint16_t* dstl_bm = nullptr;   // m: the entry's row minus the bin's first row
+  double* val = nullptr;         // m: per-sweep scratch, contributions in (bin, chunk, k) order
+  uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
+  int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
+  int64_t nitems = 0;            // phase-1 work items: segment pieces in chunk-major order
+  int64_t* item_start = nullptr;
+  uint32_t* item_len = nullptr;
+  unsigned long long* next_item = nullptr;  // [0] phase-1 piece counter, [1] phase-2 unit counter (reset per sweep)
+  int64_t nunits = 0;            // phase-2 work units: whole bins, heavy bins cut into pieces
+  int32_t* unit_bin = nullptr;
+  int64_t* unit_e = nullptr;     // nunits + 1: first entry of each unit
+  int32_t* unit_k = nullptr;     // units of the unit's bin (1 = the bin is whole)
+  double* psum = nullptr;        // n: partial row sums of split bins (zero between sweeps)
+  unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep
+  double* cta_pairs = nullptr;   // per phase-2 CTA (max, sum)
+  int p2_grid = 0;
+  std::vector<void*> allocs;
+};
+// Builds the layout from the resident in-CSR (duplicates and self loops kept
+// exactly as the CSR holds them).  *msg set (no error) on bad geometry.
+cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg);
+void free_pb(PbSet& pb, cudaStream_t st);
+// One propagation-blocked EC sweep: prev -> (pr, cur), residual into err/l1.
+cudaError_t launch_pb_sweep(const PbSet& pb, const DevGraph& g, const double* prev, double* pr, double* cur,
+                            double base, double damping, double* err, double* l1, cudaStream_t st);
+
 }  // namespace fprb

@@ -243,6 +243,7 @@ struct fpr_b200_graph {
   uint32_t flags = 0;
   int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
   BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
+  PbSet* pb = nullptr;            // FPR_B200_OPT_PB: built at the first EC run
   uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
   double* part_pr[2] = {nullptr, nullptr};  // part ranks ping-pong ([0] = pr)
   int part_pr_cur = 0;                       // buffer holding the latest sweep
@@ -275,6 +276,11 @@ void destroy_handle(fpr_b200_graph* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
+  if (h->pb) {
+    free_pb(*h->pb, h->stream);
+    delete h->pb;
+    h->pb = nullptr;
+  }
   if (h->blk) {
     free_blocks(*h->blk, h->stream);
     delete h->blk;
@@ -1032,6 +1038,86 @@ int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, dou
   }
   return FPR_B200_OK;
 }
+
+// Propagation-blocked EC (FPR_B200_OPT_PB, pb.cu): per iteration one gather
+// pass and one bin-accumulate pass; the host checks the stop rule after each
+// sweep, exactly like the blocked engine above.
+int run_pb(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* errors_out, double* l1_out,
+           uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
+  const DevGraph& g = h->g;
+  float setup_ms = 0.f, solve_ms = 0.f;
+  uint64_t launches = 0;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  if (!h->pb) {
+    // 2^13-row bins (64 KB of shared accumulators, 2 CTAs per SM) and 2^20-
+    // source chunks (an 8 MB contribution window) measured best on configs
+    // 4/5; the environment overrides are for tests/probes.
+    int shift = 13, chunk_shift = 20;
+    if (const char* s = std::getenv("FPR_B200_PB_SHIFT")) shift = std::atoi(s);
+    if (const char* s = std::getenv("FPR_B200_PB_CHUNK_SHIFT")) chunk_shift = std::atoi(s);
+    auto* pb = new PbSet;
+    const char* msg = nullptr;
+    cudaError_t e = build_pb(g, shift, chunk_shift, h->stream, *pb, &msg);
+    if (e != cudaSuccess || msg) {
+      delete pb;
+      if (msg) return fail(FPR_B200_EINVAL, std::string("fpr_b200 propagation-blocked layout: ") + msg);
+      return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                  std::string("fpr_b200 propagation-blocked layout: ") + cudaGetErrorString(e));
+    }
+    h->pb = pb;
+  }
+  CK(launch_init(g, h->pr, h->contrib[0], h->stream));
+  ++launches;
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  const double base = (1.0 - cfg->damping) / (double)g.n;  // pagerank.hpp:81
+  uint64_t total = 0;
+  int par = 0;
+  double last_err = 1.0, last_l1 = 1.0;
+  while (total < cfg->max_iterations) {
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(launch_pb_sweep(*h->pb, g, h->contrib[par], h->pr, h->contrib[par ^ 1], base, cfg->damping, h->d_errors,
+                       h->d_l1, h->stream));
+    launches += h->pb->m > 0 ? 3 : 2;
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    CK(cudaMemcpyAsync(h->h_errors, h->d_errors, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->h_l1, h->d_l1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (total == 0) cudaEventElapsedTime(&setup_ms, h->ev[0], h->ev[1]);
+    float it_ms = 0.f;
+    cudaEventElapsedTime(&it_ms, h->ev[1], h->ev[2]);
+    solve_ms += it_ms;
+    if (errors_out && errors_cap < total + 1)
+      return fail(FPR_B200_EINVAL, "fpr_b200_run: errors buffer holds " + std::to_string(errors_cap) +
+                                       " entries, need " + std::to_string(total + 1));
+    last_err = h->h_errors[0];
+    last_l1 = h->h_l1[0];
+    if (errors_out) errors_out[total] = last_err;
+    if (l1_out) l1_out[total] = last_l1;
+    if (iter_ns_out) iter_ns_out[total] = (uint64_t)(it_ms * 1e6);
+    ++total;
+    par ^= 1;
+    if ((h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err) <= cfg->threshold) break;
+  }
+  if (ranks_out) {
+    const double* src = h->pr;
+    if (h->new_of_old) {
+      CK(launch_gather_ranks(h->pr, h->new_of_old, g.n, h->ranks_tmp, h->stream));
+      src = h->ranks_tmp;
+    }
+    CK(cudaMemcpyAsync(ranks_out, src, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  if (result) {
+    result->iterations = total;
+    const double crit = h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err;
+    result->converged = (total > 0 && crit <= cfg->threshold) ? 1 : 0;
+    result->final_error = total > 0 ? last_err : 1.0;
+    result->setup_ms = setup_ms;
+    result->solve_ms = solve_ms;
+    result->kernel_launches = launches;
+  }
+  return FPR_B200_OK;
+}
 }  // namespace
 
 int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* ranks_out,
@@ -1044,6 +1130,8 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   if (engine != kEC && engine != kFused && engine != kLockstep)
     return fail(FPR_B200_EINVAL, "fpr_b200: unknown engine " + std::to_string(engine));
   CK(cudaSetDevice(h->device));
+  if (engine == kEC && (h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
+    return run_pb(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
   if (engine == kEC && (h->flags & FPR_B200_OPT_BLOCKED) && h->nparts <= 1)
     return run_blocked(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
 

@@ -265,3 +265,54 @@ def test_blocked_ec_matches_oracle(config1, oracle, shift, reorder, monkeypatch)
     assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
     assert np.max(np.abs(r.trace.errors - ref.errors)) <= EC_RTOL * float(ref.ranks.max())
     assert fu.trace.converged
+
+
+@pytest.mark.parametrize("shift,chunk_shift,reorder,piece", [(13, 20, False, 0), (5, 4, False, 0),
+                                                             (9, 12, False, 0), (14, 10, True, 0), (7, 6, False, 0),
+                                                             (13, 20, False, 1000), (9, 12, True, 77)])
+def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piece, monkeypatch):
+    """FPR_B200_OPT_PB: propagation-blocked EC sweeps (gather pass into the
+    bin-major value stream + shared-memory bin accumulation) give the
+    reference's per-iteration ranks within 1e-12 relative and its iteration
+    count, from one bin/chunk to thousands of each, with whole bins and with
+    bins split into units finished by their last-arriving CTA."""
+    rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_PB_SHIFT", str(shift))
+    monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", str(chunk_shift))
+    if piece:  # heavy bins split into phase-2 units of about `piece` entries
+        monkeypatch.setenv("FPR_B200_PB_PIECE", str(piece))
+    ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
+    with fb.DeviceGraph.from_graph(to_fb(g), pb=True, reorder=reorder) as d2:
+        r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=1))
+        assert rel(r1.ranks.values, ref.history[0]) <= EC_RTOL
+        r3 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
+        assert rel(r3.ranks.values, ref.history[2]) <= EC_RTOL
+        r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))  # unblocked engines still work
+    assert r.trace.iterations == ref.iterations and r.trace.converged
+    assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
+    assert np.max(np.abs(r.trace.errors - ref.errors)) <= EC_RTOL * float(ref.ranks.max())
+    assert fu.trace.converged
+
+
+def test_pb_l1_rule_matches_pull(config1):
+    """The L1 stop rule stops the propagation-blocked engine at the pull
+    engine's iteration with the same trace (within the 1e-12 tolerance)."""
+    rec, g, dg = config1
+    cfg = fb.PageRankConfig(threshold=1e-9)
+    with fb.DeviceGraph.from_graph(to_fb(g), norm=fb.NORM_L1) as a, \
+            fb.DeviceGraph.from_graph(to_fb(g), norm=fb.NORM_L1, pb=True) as b:
+        ra, rb = a.run(fb.ENGINE_EC, cfg), b.run(fb.ENGINE_EC, cfg)
+    assert ra.trace.iterations == rb.trace.iterations
+    assert rel(rb.ranks.values, ra.ranks.values) <= EC_RTOL
+    assert np.max(np.abs(ra.trace.l1_errors - rb.trace.l1_errors)) <= 1e-12
+
+
+def test_pb_rejects_bad_geometry(config1, monkeypatch):
+    """Bins wider than the uint16 row offset (or too narrow) are an argument
+    error at the first EC run, not a silent fallback."""
+    rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_PB_SHIFT", "17")
+    with fb.DeviceGraph.from_graph(to_fb(g), pb=True) as d2:
+        with pytest.raises(ValueError, match="propagation-blocked"):
+            d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
