@@ -262,7 +262,8 @@ def ingest_leg(fb, g, device) -> dict:
 def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
     """BASELINE configs 3-5 on one GPU, generated on the device (untimed):
     EC and FusEd time-to-converge at L-inf 1e-10, ms per sweep, GTEPS and
-    the HBM-roofline fraction (12 m + 36 n bytes per sweep).  Not the
+    the HBM-roofline fraction (12 m + 36 n bytes per sweep); on configs 4/5
+    also the propagation-blocked EC engine (FPR_B200_OPT_PB).  Not the
     headline metric; reported beside it.  Solve times are CUDA-event times
     of the persistent solve launches (resident graph)."""
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
@@ -289,6 +290,23 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
                             "gteps": dg.m / ms_it / 1e6,
                             "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
             out["config" + c] = rec
+        if c != "3":
+            # FPR_B200_OPT_PB (propagation-blocked EC) on a
+            # second handle; its one-time layout build is outside solve_ms
+            if c == "4":
+                dg = fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, device=device, pb=True)
+            else:
+                dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device,
+                                                  reorder=c.endswith("r"), pb=True)
+            with dg:
+                dg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1),
+                       copy_ranks=False, copy_trace=False)  # builds the layout
+                r = dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
+                ms_it = r.solve_ms / r.trace.iterations
+                rec["ec_pb"] = {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
+                                "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it,
+                                "gteps": dg.m / ms_it / 1e6,
+                                "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
     return out
 
 

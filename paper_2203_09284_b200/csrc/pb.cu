@@ -44,7 +44,13 @@ constexpr int kPbThreads = 1024;
 constexpr int kGatherThreads = 256;
 
 constexpr int kPieceEntries = 1024;  // phase-1 work item: up to this many entries of one segment
-constexpr int kLaneRun = 8;          // phase 2: warp steps (32 entries each) with loads in flight
+#ifndef FPR_PB_STEPS
+#define FPR_PB_STEPS 4
+#endif
+#ifndef FPR_PB_MINB
+#define FPR_PB_MINB 2
+#endif
+constexpr int kLaneRun = FPR_PB_STEPS;  // phase 2: warp steps (32 entries each) with loads in flight
 
 // One CTA per bin: histogram its edges by source chunk, scan, then a stable
 // scatter (tiles of the bin's CSR edges, block radix-sorted by chunk) so each
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
 // run and only its last lane adds into shared memory (a heavy row costs one
 // shared atomic per 32 entries, not one per edge).  Then the rows' update,
 // contribution and residual.
-__global__ void __launch_bounds__(kPbThreads) pb_accum_kernel(const double* val, const uint16_t* dstl,
+__global__ void __launch_bounds__(kPbThreads, FPR_PB_MINB) pb_accum_kernel(const double* val, const uint16_t* dstl,
                                                               const int32_t* unit_bin, const int64_t* unit_e,
                                                               const int32_t* unit_k, int64_t nunits, int shift,
                                                               int32_t n, const int32_t* outdeg, double* pr,

@@ -1049,10 +1049,11 @@ int run_pb(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* 
   uint64_t launches = 0;
   CK(cudaEventRecord(h->ev[0], h->stream));
   if (!h->pb) {
-    // 2^13-row bins (64 KB of shared accumulators, 2 CTAs per SM) and 2^20-
-    // source chunks (an 8 MB contribution window) measured best on configs
-    // 4/5; the environment overrides are for tests/probes.
-    int shift = 13, chunk_shift = 20;
+    // 2^13-row bins (64 KB of shared accumulators, 2 CTAs per SM) and 2^23-
+    // source chunks (a 64 MB contribution window, half of L2) measured best
+    // on configs 4/5; the environment overrides are for
+    // tests and probes.
+    int shift = 13, chunk_shift = 23;
     if (const char* s = std::getenv("FPR_B200_PB_SHIFT")) shift = std::atoi(s);
     if (const char* s = std::getenv("FPR_B200_PB_CHUNK_SHIFT")) chunk_shift = std::atoi(s);
     auto* pb = new PbSet;
