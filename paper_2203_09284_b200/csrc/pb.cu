@@ -15,8 +15,8 @@
 //   * entry = (source id, row offset inside the bin as uint16).
 // Per sweep:
 //   * phase 1 (pb_gather_kernel): warps walk the segments chunk by chunk, so
-//     the sources read at any moment span one chunk's contributions (an
-//     L2-resident 8 MB window at the default chunk of 2^20 sources), and write
+//     the sources read at any moment span one chunk's contributions (a 64 MB
+//     window at the default chunk of 2^23 sources, half of L2), and write
 //     val[pos] = prev[src_bm[pos]] contiguously;
 //   * phase 2 (pb_accum_kernel): one CTA per bin accumulates val into the
 //     bin's rows in shared memory and finishes the rows exactly like the
@@ -26,7 +26,8 @@
 // all sequential, where a missed pull gather moved ~64 B of DRAM.
 // A row's sum is accumulated in shared-memory atomic order, a regrouping of
 // the reference's left-to-right sum: bit patterns may differ from run to run,
-// well inside the 1e-12 per-iteration tolerance (tests/test_gpu_pb.py).
+// well inside the 1e-12 per-iteration tolerance (tests/test_gpu_engines.py
+// test_pb_*).  Measurements and rejected variants: DESIGN.md §3.4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
