@@ -45,18 +45,27 @@ constexpr int kPbThreads = 1024;
 constexpr int kGatherThreads = 256;
 
 constexpr int kPieceEntries = 1024;  // phase-1 work item: up to this many entries of one segment
-#ifndef FPR_PB_STEPS
-#define FPR_PB_STEPS 4
+// phase 2 shape: entries per lane, threads per CTA, CTAs per SM (shared
+// memory permitting); EPL 4 x 1024 x 2 measured best
+#ifndef FPR_PB_EPL
+#define FPR_PB_EPL 4
 #endif
-#ifndef FPR_PB_MINB
-#define FPR_PB_MINB 2
+#ifndef FPR_PB_ACC_THREADS
+#define FPR_PB_ACC_THREADS 1024
 #endif
-constexpr int kLaneRun = FPR_PB_STEPS;  // phase 2: warp steps (32 entries each) with loads in flight
+#ifndef FPR_PB_ACC_CTAS
+#define FPR_PB_ACC_CTAS 2
+#endif
+// phase 1 gathers: L1-allocating (default: hub sources recur across the bins a
+// CTA walks in one chunk, 4-6% faster on configs 4/5) or L2-only (0)
+#ifndef FPR_PB_GATHER_L1
+#define FPR_PB_GATHER_L1 1
+#endif
 
 // One CTA per bin: histogram its edges by source chunk, scan, then a stable
 // scatter (tiles of the bin's CSR edges, block radix-sorted by chunk) so each
 // (bin, chunk) segment lists its entries in ascending row order -- phase 2
-// merges runs of one row before touching shared memory.  counts/start are
+// folds runs of one row before touching shared memory.  counts/start are
 // chunk-major.
 __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* row, const int32_t* src, int32_t n,
                                                                 int shift, int chunk_shift, int key_bits,
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
       }
       double v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = s[u] >= 0 ? __ldcg(prev + s[u]) : 0.0;
+      for (int u = 0; u < U; ++u) v[u] = s[u] >= 0 ? (FPR_PB_GATHER_L1 ? __ldca(prev + s[u]) : __ldcg(prev + s[u])) : 0.0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t k = k0 + u * 32 + lane;
@@ -189,24 +198,46 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
 // Phase 2: CTAs take work units from a counter: a unit is a whole bin, or a
 // piece of a heavy bin (skewed graphs put a large share of the edges in the
 // bins of the hub rows; one CTA per bin left one SM working 7x longer than
-// the average on config 3).  Warps read the unit's entries
-// coalesced, 32 consecutive entries per step; inside a segment rows ascend,
-// so equal rows sit in consecutive lanes: a warp segmented scan folds each
-// run and only its last lane adds into shared memory (a heavy row costs one
-// shared atomic per 32 entries, not one per edge).  Then the rows' update,
-// contribution and residual.
-__global__ void __launch_bounds__(kPbThreads, FPR_PB_MINB) pb_accum_kernel(const double* val, const uint16_t* dstl,
-                                                              const int32_t* unit_bin, const int64_t* unit_e,
-                                                              const int32_t* unit_k, int64_t nunits, int shift,
-                                                              int32_t n, const int32_t* outdeg, double* pr,
-                                                              double* cur, double base, double damping,
-                                                              double* psum, unsigned int* bin_done,
-                                                              unsigned long long* next_unit, double* cta_pairs) {
-  constexpr int U = kLaneRun;
+// the average on config 3).  Lane L of a warp step owns EPL consecutive
+// entries, read as 32-B value vectors and one key vector.  It
+// folds runs of equal rows in registers; runs strictly inside the lane go to
+// shared memory at once.  The run that ends the lane (its "tail") may
+// continue in the next lanes: one segmented warp scan of the tails per
+// 32*EPL entries carries it, and each run is added exactly once, by the lane
+// where it ends (its first part, if it began in earlier lanes, arrives in
+// the carry).  Shared fp64 adds are CAS loops on sm_100.  The first form of
+// this pass scanned every 32 entries across the warp; its shuffles were ~60%
+// of the L1TEX data-pipe wavefronts, the pass's limiter.
+// Then each finished row: base + d*sum without FMA, contribution, residual.
+template <int EPL>
+__device__ __forceinline__ void pb_ld_vals(const double* p, double (&v)[EPL]) {
+#pragma unroll
+  for (int j = 0; j < EPL; j += 4)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[j]), "=d"(v[j + 1]), "=d"(v[j + 2]), "=d"(v[j + 3])
+                 : "l"(p + j));
+}
+template <int EPL>
+__device__ __forceinline__ void pb_ld_keys(const uint16_t* p, uint32_t (&k)[EPL / 2]) {
+  if constexpr (EPL == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(k[0]), "=r"(k[1]) : "l"(p));
+  } else {
+    static_assert(EPL == 8, "EPL is 4 or 8");
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3])
+                 : "l"(p));
+  }
+}
+
+template <int EPL, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) pb_accum_kernel(
+    const double* val, const uint16_t* dstl, const int32_t* unit_bin, const int64_t* unit_e, const int32_t* unit_k,
+    int64_t nunits, int shift, int32_t n, const int32_t* outdeg, double* pr, double* cur, double base,
+    double damping, double* psum, unsigned int* bin_done, unsigned long long* next_unit, double* cta_pairs) {
   extern __shared__ double acc[];
+  constexpr int W = 32 * EPL;  // entries per warp step
   const int R = 1 << shift;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const unsigned below = (2u << lane) - 1u;  // lanes 0..lane
   double lmax = 0.0, lsum = 0.0;
   __shared__ long long s_unit;
   __shared__ int s_last;
@@ -217,48 +248,80 @@ __global__ void __launch_bounds__(kPbThreads, FPR_PB_MINB) pb_accum_kernel(const
     if (u >= nunits) break;
     const int64_t b = __ldg(unit_bin + u);
     const int k = __ldg(unit_k + u);
-    const int64_t e1 = __ldg(unit_e + u + 1);
+    const int64_t e0 = __ldg(unit_e + u), e1 = __ldg(unit_e + u + 1);
     for (int i = threadIdx.x; i < R; i += blockDim.x) acc[i] = 0.0;
     __syncthreads();
     const int64_t r0 = b << shift;
     const int64_t r1 = min((int64_t)n, r0 + R);
-    for (int64_t w = __ldg(unit_e + u) + (int64_t)warp * 32 * U; w < e1; w += (int64_t)nwarps * 32 * U) {
-      double v[U];
-      int d[U];
+    for (int64_t w = (e0 & ~int64_t(EPL - 1)) + (int64_t)warp * W; w < e1; w += (int64_t)nwarps * W) {
+      const int64_t e = w + lane * EPL;
+      double v[EPL];
+      uint32_t kw[EPL / 2];
+      if (e < e1) {
+        pb_ld_vals<EPL>(val + e, v);
+        pb_ld_keys<EPL>(dstl + e, kw);
+      } else {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t e = w + u * 32 + lane;
-        const bool ok = e < e1;
-        v[u] = ok ? __ldcs(val + e) : 0.0;
-        d[u] = ok ? (int)__ldcs(dstl + e) : -1;
+        for (int j = 0; j < EPL / 2; ++j) kw[j] = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) v[j] = 0.0;
       }
+      // fold: first run (fk, fs), current run (ck, cs); interior runs go out
+      int fk = -2, ck = -2;
+      double fs = 0.0, cs = 0.0;
+      bool multi = false;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int key = d[u];
-        double run = v[u];
-        const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
-        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || kprev != key);
-        bool last = true;
-        if (heads != 0xffffffffu) {
-          const int seg0 = 31 - __clz(heads & below);
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(0xffffffffu, run, o);
-            if (lane - o >= seg0) run += t;
+      for (int i = 0; i < EPL; ++i) {
+        const uint32_t raw = (kw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+        const int ki = (e + i >= e0 && e + i < e1) ? (int)raw : -1;
+        if (i == 0) {
+          ck = ki;
+          cs = v[0];
+        } else if (ki == ck) {
+          cs += v[i];
+        } else {
+          if (!multi) {
+            fk = ck;
+            fs = cs;
+            multi = true;
+          } else if (ck >= 0) {
+            atomicAdd(&acc[ck], cs);  // a run strictly inside this lane
           }
-          last = lane == 31 || ((heads >> (lane + 1)) & 1u);
+          ck = ki;
+          cs = v[i];
         }
-        if (key >= 0 && last) atomicAdd(&acc[key], run);
       }
+      if (!multi) {
+        fk = ck;
+        fs = cs;
+      }
+      // carry the tails: lane L continues lane L-1's tail if its first key
+      // equals that tail's key; a single-run continuing lane passes it on
+      const int pk = __shfl_up_sync(0xffffffffu, ck, 1);
+      const bool cont = lane > 0 && fk >= 0 && fk == pk;
+      const bool through = cont && !multi;
+      const unsigned starts = __ballot_sync(0xffffffffu, !through);
+      double S = cs;
+      if (starts != 0xffffffffu) {
+        const unsigned below = (2u << lane) - 1u;
+        const int seg0 = 31 - __clz(starts & below);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, S, o);
+          if (lane - o >= seg0) S += t;
+        }
+      }
+      const double Sp = __shfl_up_sync(0xffffffffu, S, 1);
+      const bool next_cont = __shfl_down_sync(0xffffffffu, cont, 1) && lane < 31;
+      if (multi && fk >= 0) atomicAdd(&acc[fk], cont ? fs + Sp : fs);  // the first run ends in this lane
+      if (!next_cont && ck >= 0) atomicAdd(&acc[ck], S);                // the tail run ends here
     }
     __syncthreads();
     bool fin = true, from_psum = false;
     if (k > 1) {
-      // a heavy bin split into k units: fold this unit's sums into psum; the
-      // last unit to arrive finishes the bin's rows
       for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        const double v = acc[r - r0];
-        if (v != 0.0) atomicAdd(psum + r, v);
+        const double x = acc[r - r0];
+        if (x != 0.0) atomicAdd(psum + r, x);
       }
       __threadfence();
       __syncthreads();
@@ -384,8 +447,10 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   PK(alloc((void**)&pb.counts, nbins * nchunks * sizeof(uint32_t)));
   PK(alloc((void**)&pb.start, nbins * nchunks * sizeof(int64_t)));
   PK(alloc((void**)&pb.src_bm, m * sizeof(int32_t)));
-  PK(alloc((void**)&pb.dstl_bm, m * sizeof(uint16_t)));
-  PK(alloc((void**)&pb.val, m * sizeof(double)));
+  // 8 pad entries: the lane-sequential phase 2 loads 8-entry vectors that may
+  // run past the end
+  PK(alloc((void**)&pb.dstl_bm, (m + 8) * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.val, (m + 8) * sizeof(double)));
   {
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
@@ -429,10 +494,10 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     if (e != cudaSuccess) goto out;
   }
   {
-    // phase-2 residency: the bin's accumulators in shared memory, 1024
-    // threads per CTA (at most 2 CTAs per SM)
+    // phase-2 residency: the bin's accumulators in shared memory,
+    // FPR_PB_ACC_CTAS CTAs per SM when they fit
     const int by_smem = (int)std::max<size_t>(1, (size_t)(227 * 1024) / (acc_smem + 1024));
-    pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * std::min(2, by_smem));
+    pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * std::min(FPR_PB_ACC_CTAS, by_smem));
   }
   {
     // phase-2 units: bins, heavy ones cut into pieces of about `piece` entries
@@ -477,7 +542,8 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   }
   PK(alloc((void**)&pb.next_item, 2 * sizeof(unsigned long long)));
   PK(alloc((void**)&pb.cta_pairs, 2 * (size_t)pb.p2_grid * sizeof(double)));
-  PK(cudaFuncSetAttribute(pb_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
+  PK(cudaFuncSetAttribute(pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
   PK(cudaStreamSynchronize(st));
 out:
   if (e != cudaSuccess) {
@@ -497,7 +563,8 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const DevGraph& g, const double* pr
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  pb_accum_kernel<<<pb.p2_grid, kPbThreads, (size_t)sizeof(double) << pb.shift, st>>>(
+  pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>
+      <<<pb.p2_grid, FPR_PB_ACC_THREADS, (size_t)sizeof(double) << pb.shift, st>>>(
       pb.val, pb.dstl_bm, pb.unit_bin, pb.unit_e, pb.unit_k, pb.nunits, pb.shift, g.n, g.outdeg, pr, cur, base,
       damping, pb.psum, pb.bin_done, pb.next_item + 1, pb.cta_pairs);
   e = cudaGetLastError();
