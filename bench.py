@@ -263,12 +263,20 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
     """BASELINE configs 3-5 on one GPU, generated on the device (untimed):
     EC and FusEd time-to-converge at L-inf 1e-10, ms per sweep, GTEPS and
     the HBM-roofline fraction (12 m + 36 n bytes per sweep); on configs 4/5
-    also the propagation-blocked EC engine (FPR_B200_OPT_PB).  Not the
+    also the propagation-blocked engines (FPR_B200_OPT_PB): EC, and the
+    lockstep FusEd schedule on PB sweeps (auto wave count).  Not the
     headline metric; reported beside it.  Solve times are CUDA-event times
-    of the persistent solve launches (resident graph)."""
+    of the solve launches (resident graph)."""
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     peak, _ = peaks()
     out = {}
+
+    def record(dg, r):
+        ms_it = r.solve_ms / r.trace.iterations
+        return {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
+                "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it, "gteps": dg.m / ms_it / 1e6,
+                "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
+
     for c in which:
         if c == "3":
             dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(24, 16, seed=3), relabel_bfs=True, device=device)
@@ -283,12 +291,7 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
         with dg:
             rec = {"workload": name, "n": dg.n, "m": dg.m}
             for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED, "fused")):
-                r = dg.run(eng, cfg, copy_ranks=False, copy_trace=False)
-                ms_it = r.solve_ms / r.trace.iterations
-                rec[tag] = {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
-                            "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it,
-                            "gteps": dg.m / ms_it / 1e6,
-                            "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
+                rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
             out["config" + c] = rec
         if c != "3":
             # FPR_B200_OPT_PB (propagation-blocked EC) on a
@@ -299,14 +302,11 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
                 dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device,
                                                   reorder=c.endswith("r"), pb=True)
             with dg:
-                dg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1),
-                       copy_ranks=False, copy_trace=False)  # builds the layout
-                r = dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
-                ms_it = r.solve_ms / r.trace.iterations
-                rec["ec_pb"] = {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
-                                "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it,
-                                "gteps": dg.m / ms_it / 1e6,
-                                "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
+                one = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1)
+                for eng, tag in ((fb.ENGINE_EC, "ec_pb"), (fb.ENGINE_FUSED_LOCKSTEP, "lockstep_pb")):
+                    dg.run(eng, one, copy_ranks=False, copy_trace=False)  # builds the layout and the wave plan
+                    rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
+                rec["lockstep_pb"]["waves"] = len(dg.wave_starts()) - 1
     return out
 
 

@@ -90,12 +90,14 @@ typedef struct fpr_config {
                                   gathers of a block pass stay near L2; only for graphs
                                   whose contribution vector far exceeds L2 (configs 4/5
                                   in natural order) */
-#define FPR_B200_OPT_PB 4u      /* EC engine: propagation-blocked sweeps (bins of 2^13
-                                  rows, source chunks of 2^23; FPR_B200_PB_SHIFT /
-                                  FPR_B200_PB_CHUNK_SHIFT override): two streaming
-                                  passes instead of the random pull gather, for graphs
-                                  whose contribution vector far exceeds L2 (DESIGN.md
-                                  §3.4); takes precedence over OPT_BLOCKED */
+#define FPR_B200_OPT_PB 4u      /* EC and lockstep engines: propagation-blocked sweeps
+                                  (bins of 2^13 rows, source chunks of 2^23;
+                                  FPR_B200_PB_SHIFT / FPR_B200_PB_CHUNK_SHIFT override):
+                                  two streaming passes instead of the random pull
+                                  gather, for graphs whose contribution vector far
+                                  exceeds L2.  Lockstep waves are then
+                                  runs of whole bins (fpr_b200_graph_wave_starts reports
+                                  them).  Takes precedence over OPT_BLOCKED */
 
 typedef struct fpr_b200_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <string>
+#include <map>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -221,36 +222,53 @@ cudaError_t launch_apply(const BlockSet& bs, int32_t n, const int32_t* outdeg, d
                          double base, double damping, double* err, double* l1, cudaStream_t st);
 
 // pb.cu: propagation-blocked EC (FPR_B200_OPT_PB).
+// A sweep plan: the bins cut into waves of consecutive bins (1 wave = EC,
+// S waves = the lockstep Gauss-Seidel schedule), phase-1 pieces ordered
+// (wave, chunk, bin) so each wave walks the chunks in order.
+struct PbPlan {
+  int nwaves = 0;
+  std::vector<int64_t> wave_bin;  // nwaves + 1: first bin of each wave
+  std::vector<int64_t> item0;     // nwaves + 1: first phase-1 piece of each wave
+  std::vector<int64_t> unit0;     // nwaves + 1: first phase-2 unit of each wave
+  int64_t* item_start = nullptr;  // pieces: first entry and length
+  uint32_t* item_len = nullptr;
+  unsigned long long* ctr = nullptr;  // 2 x nwaves work counters (reset per sweep)
+  double* cta_pairs = nullptr;        // nwaves x phase-2 CTAs (max, sum)
+  std::vector<void*> allocs;
+};
 struct PbSet {
   int shift = 0;         // destination bin = row >> shift (at most 2^16 rows: uint16 offsets)
   int chunk_shift = 0;   // source chunk = src >> chunk_shift
   int64_t nbins = 0, nchunks = 0, m = 0;
   int32_t* src_bm = nullptr;     // m: source of each entry; bin b's entries are the in-CSR's edges of its rows,
                                  //    regrouped by source chunk: (bin, chunk, k) order
-  uint16_t* dstl_bm = nullptr;   // m: the entry's row minus the bin's first row
-  double* val = nullptr;         // m: per-sweep scratch, contributions in (bin, chunk, k) order
+  uint16_t* dstl_bm = nullptr;   // m + 8: the entry's row minus the bin's first row
+  double* val = nullptr;         // m + 8: per-sweep scratch, contributions in (bin, chunk, k) order
   uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
   int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
-  int64_t nitems = 0;            // phase-1 work items: segment pieces in chunk-major order
-  int64_t* item_start = nullptr;
-  uint32_t* item_len = nullptr;
-  unsigned long long* next_item = nullptr;  // [0] phase-1 piece counter, [1] phase-2 unit counter (reset per sweep)
   int64_t nunits = 0;            // phase-2 work units: whole bins, heavy bins cut into pieces
   int32_t* unit_bin = nullptr;
   int64_t* unit_e = nullptr;     // nunits + 1: first entry of each unit
   int32_t* unit_k = nullptr;     // units of the unit's bin (1 = the bin is whole)
+  std::vector<int32_t> unit_bin_host;
   double* psum = nullptr;        // n: partial row sums of split bins (zero between sweeps)
   unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep
-  double* cta_pairs = nullptr;   // per phase-2 CTA (max, sum)
-  int p2_grid = 0;
+  int p1_grid = 0, p2_grid = 0;
+  std::map<uint32_t, PbPlan> plans;  // by wave count
   std::vector<void*> allocs;
 };
 // Builds the layout from the resident in-CSR (duplicates and self loops kept
 // exactly as the CSR holds them).  *msg set (no error) on bad geometry.
 cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg);
 void free_pb(PbSet& pb, cudaStream_t st);
-// One propagation-blocked EC sweep: prev -> (pr, cur), residual into err/l1.
-cudaError_t launch_pb_sweep(const PbSet& pb, const DevGraph& g, const double* prev, double* pr, double* cur,
-                            double base, double damping, double* err, double* l1, cudaStream_t st);
+// First bin of each of (at most) S waves of equal bin counts: S' + 1 values.
+std::vector<int64_t> pb_wave_bins(int64_t nbins, uint32_t S);
+// The plan for S waves, built on first use and cached in pb.plans.
+cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** out);
+// One propagation-blocked sweep: for each wave, gather from prev then
+// finish the wave's rows into (pr, cur); residual into err/l1.  EC passes
+// prev != cur with one wave; lockstep passes prev == cur (in place).
+cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev, double* pr,
+                            double* cur, double base, double damping, double* err, double* l1, cudaStream_t st);
 
 }  // namespace fprb

@@ -140,19 +140,39 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
   }
 }
 
-__global__ void pb_piece_count_kernel(const uint32_t* counts, int64_t nseg, uint32_t* npieces) {
+// Plan order: position p walks the waves (runs of consecutive bins), chunk-
+// major inside a wave, so each wave's pieces are contiguous and in chunk
+// order.  Returns the chunk-major segment index c * nbins + b of position p.
+__device__ __forceinline__ int64_t pb_seg_of(int64_t p, const int64_t* wave_bin, int nwaves, int64_t nbins,
+                                             int64_t nchunks) {
+  int lo = 0, hi = nwaves - 1;  // last wave w with wave_bin[w] * nchunks <= p
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (wave_bin[mid] * nchunks <= p) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t b0 = wave_bin[lo], nb = wave_bin[lo + 1] - b0;
+  const int64_t q = p - b0 * nchunks;
+  const int64_t c = q / nb;
+  return c * nbins + b0 + (q - c * nb);
+}
+
+__global__ void pb_piece_count_kernel(const uint32_t* counts, int64_t nseg, const int64_t* wave_bin, int nwaves,
+                                      int64_t nbins, int64_t nchunks, uint32_t* npieces) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride)
-    npieces[s] = (counts[s] + kPieceEntries - 1) / kPieceEntries;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nseg; p += stride)
+    npieces[p] = (counts[pb_seg_of(p, wave_bin, nwaves, nbins, nchunks)] + kPieceEntries - 1) / kPieceEntries;
 }
 
 __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* start, const uint32_t* piece_off,
-                                     int64_t nseg, int64_t* item_start, uint32_t* item_len) {
+                                     int64_t nseg, const int64_t* wave_bin, int nwaves, int64_t nbins,
+                                     int64_t nchunks, int64_t* item_start, uint32_t* item_len) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nseg; p += stride) {
+    const int64_t s = pb_seg_of(p, wave_bin, nwaves, nbins, nchunks);
     const uint32_t cnt = counts[s];
     const int64_t p0 = start[s];
-    uint32_t o = piece_off[s];
+    uint32_t o = piece_off[p];
     for (uint32_t k = 0; k < cnt; k += kPieceEntries, ++o) {
       item_start[o] = p0 + k;
       item_len[o] = min((uint32_t)kPieceEntries, cnt - k);
@@ -414,9 +434,93 @@ int sm_count() {
 }  // namespace
 
 void free_pb(PbSet& pb, cudaStream_t st) {
+  for (auto& kv : pb.plans)
+    for (void* p : kv.second.allocs)
+      if (p) cudaFreeAsync(p, st);
   for (void* p : pb.allocs)
     if (p) cudaFreeAsync(p, st);
   pb = PbSet{};
+}
+
+std::vector<int64_t> pb_wave_bins(int64_t nbins, uint32_t S) {
+  const int64_t w = std::max<int64_t>(1, std::min<int64_t>(S, nbins));
+  std::vector<int64_t> wb(w + 1);
+  for (int64_t i = 0; i <= w; ++i) wb[i] = nbins * i / w;
+  return wb;
+}
+
+cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** out) {
+  auto it = pb.plans.find(S);
+  if (it != pb.plans.end()) {
+    *out = &it->second;
+    return cudaSuccess;
+  }
+  const int sms = sm_count();
+  PbPlan plan;
+  plan.wave_bin = pb_wave_bins(pb.nbins, S);
+  plan.nwaves = (int)plan.wave_bin.size() - 1;
+  const int W = plan.nwaves;
+  const int64_t nbins = pb.nbins, nchunks = pb.nchunks, nseg = nbins * nchunks;
+  auto alloc = [&](void** p, size_t bytes) {
+    cudaError_t r = cudaMallocAsync(p, std::max<size_t>(bytes, 16), st);
+    if (r == cudaSuccess) plan.allocs.push_back(*p);
+    return r;
+  };
+  uint32_t* npieces = nullptr;
+  uint32_t* piece_off = nullptr;
+  int64_t* d_wb = nullptr;
+  void* temp = nullptr;
+  size_t tb = 0;
+  std::vector<uint32_t> off(W + 1, 0);
+  uint32_t last = 0;
+  cudaError_t e = cudaMallocAsync(&npieces, nseg * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&piece_off, nseg * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_wb, (W + 1) * sizeof(int64_t), st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_wb, plan.wave_bin.data(), (W + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    pb_piece_count_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, nseg, d_wb, W, nbins, nchunks, npieces);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, npieces, piece_off, nseg, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, tb, npieces, piece_off, nseg, st);
+  for (int w = 1; w < W && e == cudaSuccess; ++w)
+    e = cudaMemcpyAsync(&off[w], piece_off + plan.wave_bin[w] * nchunks, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&off[W], piece_off + nseg - 1, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last, npieces + nseg - 1, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) {
+    off[W] += last;
+    plan.item0.assign(off.begin(), off.end());
+    e = alloc((void**)&plan.item_start, off[W] * sizeof(int64_t));
+  }
+  if (e == cudaSuccess) e = alloc((void**)&plan.item_len, off[W] * sizeof(uint32_t));
+  if (e == cudaSuccess) {
+    pb_piece_fill_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, pb.start, piece_off, nseg, d_wb, W, nbins, nchunks,
+                                                   plan.item_start, plan.item_len);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = alloc((void**)&plan.ctr, 2 * (size_t)W * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = alloc((void**)&plan.cta_pairs, 2 * (size_t)W * pb.p2_grid * sizeof(double));
+  for (void* q : {(void*)npieces, (void*)piece_off, (void*)d_wb, temp})
+    if (q) cudaFreeAsync(q, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    for (void* q : plan.allocs) cudaFreeAsync(q, st);
+    cudaStreamSynchronize(st);
+    return e;
+  }
+  // phase-2 units are bin-ordered: wave w's units are a contiguous range
+  plan.unit0.assign(W + 1, pb.nunits);
+  for (int64_t u = pb.nunits - 1; u >= 0; --u) {
+    const int64_t b = pb.unit_bin_host[u];
+    const int w = (int)(std::upper_bound(plan.wave_bin.begin(), plan.wave_bin.end(), b) - plan.wave_bin.begin()) - 1;
+    plan.unit0[w] = u;
+  }
+  for (int w = W - 1; w >= 0; --w) plan.unit0[w] = std::min(plan.unit0[w], plan.unit0[w + 1]);
+  *out = &pb.plans.emplace(S, std::move(plan)).first->second;
+  return cudaSuccess;
 }
 
 cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg) {
@@ -461,43 +565,11 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     PK(cudaGetLastError());
   }
   {
-    const int64_t nseg = nbins * nchunks;
-    uint32_t* npieces = nullptr;
-    uint32_t* piece_off = nullptr;
-    void* temp = nullptr;
-    size_t tb = 0;
-    uint32_t last[2] = {0, 0};
-    e = cudaMallocAsync(&npieces, nseg * sizeof(uint32_t), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&piece_off, nseg * sizeof(uint32_t), st);
-    if (e == cudaSuccess) {
-      pb_piece_count_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, nseg, npieces);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, npieces, piece_off, nseg, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st);
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, tb, npieces, piece_off, nseg, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&last[0], piece_off + nseg - 1, 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&last[1], npieces + nseg - 1, 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e == cudaSuccess) {
-      pb.nitems = (int64_t)last[0] + last[1];
-      e = alloc((void**)&pb.item_start, pb.nitems * sizeof(int64_t));
-    }
-    if (e == cudaSuccess) e = alloc((void**)&pb.item_len, pb.nitems * sizeof(uint32_t));
-    if (e == cudaSuccess) {
-      pb_piece_fill_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, pb.start, piece_off, nseg, pb.item_start,
-                                                     pb.item_len);
-      e = cudaGetLastError();
-    }
-    for (void* q : {(void*)npieces, (void*)piece_off, temp})
-      if (q) cudaFreeAsync(q, st);
-    if (e != cudaSuccess) goto out;
-  }
-  {
     // phase-2 residency: the bin's accumulators in shared memory,
     // FPR_PB_ACC_CTAS CTAs per SM when they fit
     const int by_smem = (int)std::max<size_t>(1, (size_t)(227 * 1024) / (acc_smem + 1024));
     pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * std::min(FPR_PB_ACC_CTAS, by_smem));
+    pb.p1_grid = sms * 8;
   }
   {
     // phase-2 units: bins, heavy ones cut into pieces of about `piece` entries
@@ -528,6 +600,7 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     }
     ue.push_back(m);
     pb.nunits = (int64_t)ubin.size();
+    pb.unit_bin_host = ubin;
     PK(alloc((void**)&pb.unit_bin, ubin.size() * sizeof(int32_t)));
     PK(alloc((void**)&pb.unit_k, uk.size() * sizeof(int32_t)));
     PK(alloc((void**)&pb.unit_e, ue.size() * sizeof(int64_t)));
@@ -540,8 +613,6 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
     PK(cudaStreamSynchronize(st));  // the host vectors die at the end of this block
   }
-  PK(alloc((void**)&pb.next_item, 2 * sizeof(unsigned long long)));
-  PK(alloc((void**)&pb.cta_pairs, 2 * (size_t)pb.p2_grid * sizeof(double)));
   PK(cudaFuncSetAttribute(pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
   PK(cudaStreamSynchronize(st));
@@ -553,23 +624,27 @@ out:
   return e;
 }
 
-cudaError_t launch_pb_sweep(const PbSet& pb, const DevGraph& g, const double* prev, double* pr, double* cur,
-                            double base, double damping, double* err, double* l1, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(pb.next_item, 0, 2 * sizeof(unsigned long long), st);  // both work counters
+cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev, double* pr,
+                            double* cur, double base, double damping, double* err, double* l1, cudaStream_t st) {
+  const int W = plan.nwaves;
+  // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
+  cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  if (pb.m > 0) {
-    pb_gather_kernel<<<sm_count() * 8, kGatherThreads, 0, st>>>(pb.src_bm, pb.item_start, pb.item_len,
-                                                                 pb.nitems, prev, pb.val, pb.next_item);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+  for (int w = 0; w < W; ++w) {
+    const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
+    if (plan.item0[w + 1] > i0) {
+      pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.src_bm, plan.item_start + i0, plan.item_len + i0,
+                                                              plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>
+        <<<pb.p2_grid, FPR_PB_ACC_THREADS, (size_t)sizeof(double) << pb.shift, st>>>(
+            pb.val, pb.dstl_bm, pb.unit_bin + u0, pb.unit_e + u0, pb.unit_k + u0, plan.unit0[w + 1] - u0, pb.shift,
+            g.n, g.outdeg, pr, cur, base, damping, pb.psum, pb.bin_done, plan.ctr + W + w,
+            plan.cta_pairs + 2 * (size_t)w * pb.p2_grid);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>
-      <<<pb.p2_grid, FPR_PB_ACC_THREADS, (size_t)sizeof(double) << pb.shift, st>>>(
-      pb.val, pb.dstl_bm, pb.unit_bin, pb.unit_e, pb.unit_k, pb.nunits, pb.shift, g.n, g.outdeg, pr, cur, base,
-      damping, pb.psum, pb.bin_done, pb.next_item + 1, pb.cta_pairs);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  pb_reduce_kernel<<<1, 32, 0, st>>>(pb.p2_grid, pb.cta_pairs, err, l1);
+  pb_reduce_kernel<<<1, 32, 0, st>>>(W * pb.p2_grid, plan.cta_pairs, err, l1);
   return cudaGetLastError();
 }
 

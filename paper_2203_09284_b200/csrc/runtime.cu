@@ -486,6 +486,30 @@ int validate_config(const fpr_config* cfg) {
   return FPR_B200_OK;
 }
 
+// Propagation-blocked geometry: 2^13-row bins (64 KB of shared accumulators,
+// 2 CTAs per SM) and 2^23-source chunks (a 64 MB contribution window, half of
+// L2) measured best on configs 4/5; the environment
+// overrides are for tests and probes.
+void pb_geometry(int* shift, int* chunk_shift) {
+  *shift = 13;
+  *chunk_shift = 23;
+  if (const char* s = std::getenv("FPR_B200_PB_SHIFT")) *shift = std::atoi(s);
+  if (const char* s = std::getenv("FPR_B200_PB_CHUNK_SHIFT")) *chunk_shift = std::atoi(s);
+}
+
+// Lockstep wave count: the requested one, or an auto rule.  Plain sweeps:
+// the rule of get_waves.  Propagation-blocked sweeps: every wave re-walks
+// all chunk windows and drains two launches, so fewer waves pay: one per
+// 128 M merge items, 2-8 (measured optima: config 4 4-8 waves, config 5 8;
+// DESIGN.md §3.4).
+uint32_t lockstep_waves(const fpr_b200_graph* h) {
+  if (h->wave_count) return h->wave_count;
+  const int64_t items = (int64_t)h->g.n + h->g.m;
+  if ((h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
+    return (uint32_t)std::min<int64_t>(8, std::max<int64_t>(2, items >> 27));
+  return (uint32_t)std::min<int64_t>(32, std::max<int64_t>(2, items >> 25));
+}
+
 }  // namespace
 
 extern "C" {
@@ -899,14 +923,25 @@ int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t*
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_wave_starts: null graph");
   if (h->g.n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
   CK(cudaSetDevice(h->device));
-  const Waves* wv = nullptr;
-  int rc = get_waves(h, wave_count ? wave_count : h->wave_count, &wv);
-  if (rc) return rc;
-  if (nwaves) *nwaves = (uint64_t)wv->nwaves;
+  std::vector<uint64_t> vs;
+  if ((h->flags & FPR_B200_OPT_PB) && h->nparts <= 1) {
+    // propagation-blocked lockstep: waves of consecutive bins (run_pb)
+    int shift = 0, chunk_shift = 0;
+    pb_geometry(&shift, &chunk_shift);
+    if (shift < 5 || shift > 14) return fail(FPR_B200_EINVAL, "fpr_b200 propagation-blocked layout: bin/chunk geometry out of range");
+    const int64_t nbins = ((int64_t)h->g.n + (1ll << shift) - 1) >> shift;
+    for (int64_t b : pb_wave_bins(nbins, wave_count ? wave_count : lockstep_waves(h)))
+      vs.push_back((uint64_t)std::min<int64_t>(h->g.n, b << shift));
+  } else {
+    const Waves* wv = nullptr;
+    int rc = get_waves(h, wave_count ? wave_count : h->wave_count, &wv);
+    if (rc) return rc;
+    vs = wv->vertex_start;
+  }
+  if (nwaves) *nwaves = (uint64_t)vs.size() - 1;
   if (wave_start) {
-    if (cap < wv->vertex_start.size())
-      return fail(FPR_B200_EINVAL, "fpr_b200_graph_wave_starts: buffer too small");
-    std::copy(wv->vertex_start.begin(), wv->vertex_start.end(), wave_start);
+    if (cap < vs.size()) return fail(FPR_B200_EINVAL, "fpr_b200_graph_wave_starts: buffer too small");
+    std::copy(vs.begin(), vs.end(), wave_start);
   }
   return FPR_B200_OK;
 }
@@ -1039,23 +1074,21 @@ int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, dou
   return FPR_B200_OK;
 }
 
-// Propagation-blocked EC (FPR_B200_OPT_PB, pb.cu): per iteration one gather
-// pass and one bin-accumulate pass; the host checks the stop rule after each
-// sweep, exactly like the blocked engine above.
-int run_pb(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* errors_out, double* l1_out,
-           uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
+// Propagation-blocked sweeps (FPR_B200_OPT_PB, pb.cu).  EC: one wave, the
+// gather reads contrib[par] and the rows write contrib[par ^ 1].  Lockstep
+// (the deterministic FusEd schedule): S waves of consecutive bins, gathered
+// from and written to contrib[0] in place, so wave w reads this sweep's
+// contributions of waves < w (fo_pagerank_lockstep).  The host checks the
+// stop rule after each sweep, exactly like the blocked engine above.
+int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* ranks_out, double* errors_out,
+           double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
   const DevGraph& g = h->g;
   float setup_ms = 0.f, solve_ms = 0.f;
   uint64_t launches = 0;
   CK(cudaEventRecord(h->ev[0], h->stream));
   if (!h->pb) {
-    // 2^13-row bins (64 KB of shared accumulators, 2 CTAs per SM) and 2^23-
-    // source chunks (a 64 MB contribution window, half of L2) measured best
-    // on configs 4/5; the environment overrides are for
-    // tests and probes.
-    int shift = 13, chunk_shift = 23;
-    if (const char* s = std::getenv("FPR_B200_PB_SHIFT")) shift = std::atoi(s);
-    if (const char* s = std::getenv("FPR_B200_PB_CHUNK_SHIFT")) chunk_shift = std::atoi(s);
+    int shift = 0, chunk_shift = 0;
+    pb_geometry(&shift, &chunk_shift);
     auto* pb = new PbSet;
     const char* msg = nullptr;
     cudaError_t e = build_pb(g, shift, chunk_shift, h->stream, *pb, &msg);
@@ -1067,6 +1100,13 @@ int run_pb(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* 
     }
     h->pb = pb;
   }
+  const PbPlan* plan = nullptr;
+  {
+    cudaError_t e = get_pb_plan(*h->pb, lockstep ? lockstep_waves(h) : 1u, h->stream, &plan);
+    if (e != cudaSuccess)
+      return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                  std::string("fpr_b200 propagation-blocked plan: ") + cudaGetErrorString(e));
+  }
   CK(launch_init(g, h->pr, h->contrib[0], h->stream));
   ++launches;
   CK(cudaEventRecord(h->ev[1], h->stream));
@@ -1076,9 +1116,11 @@ int run_pb(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* 
   double last_err = 1.0, last_l1 = 1.0;
   while (total < cfg->max_iterations) {
     CK(cudaEventRecord(h->ev[1], h->stream));
-    CK(launch_pb_sweep(*h->pb, g, h->contrib[par], h->pr, h->contrib[par ^ 1], base, cfg->damping, h->d_errors,
+    double* prev = h->contrib[lockstep ? 0 : par];
+    double* next = h->contrib[lockstep ? 0 : par ^ 1];
+    CK(launch_pb_sweep(*h->pb, *plan, g, prev, h->pr, next, base, cfg->damping, h->d_errors,
                        h->d_l1, h->stream));
-    launches += h->pb->m > 0 ? 3 : 2;
+    launches += (uint64_t)plan->nwaves + (uint64_t)(plan->item0.back() > 0 ? plan->nwaves : 0) + 1;
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(cudaMemcpyAsync(h->h_errors, h->d_errors, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->h_l1, h->d_l1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1131,8 +1173,8 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   if (engine != kEC && engine != kFused && engine != kLockstep)
     return fail(FPR_B200_EINVAL, "fpr_b200: unknown engine " + std::to_string(engine));
   CK(cudaSetDevice(h->device));
-  if (engine == kEC && (h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
-    return run_pb(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
+  if ((engine == kEC || engine == kLockstep) && (h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
+    return run_pb(h, engine == kLockstep, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
   if (engine == kEC && (h->flags & FPR_B200_OPT_BLOCKED) && h->nparts <= 1)
     return run_blocked(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
 

@@ -295,6 +295,36 @@ def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piec
     assert fu.trace.converged
 
 
+@pytest.mark.parametrize("shift,chunk_shift,waves,piece", [(13, 20, 0, 0), (9, 12, 4, 0), (7, 10, 16, 300),
+                                                         (5, 6, 64, 0), (9, 12, 3, 77), (13, 20, 100, 0)])
+def test_pb_lockstep_vs_restated_schedule(config1, oracle, shift, chunk_shift, waves, piece, monkeypatch):
+    """FPR_B200_OPT_PB + the lockstep engine: S waves of consecutive bins,
+    each gathered from and written back to the one contribution vector, is
+    the deterministic FusEd schedule of fo_pagerank_lockstep at bin-aligned
+    wave starts: per-sweep 1e-12 relative and the same sweep count (more
+    waves than bins included: the waves shrink to one bin each)."""
+    rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_PB_SHIFT", str(shift))
+    monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", str(chunk_shift))
+    if piece:
+        monkeypatch.setenv("FPR_B200_PB_PIECE", str(piece))
+    with fb.DeviceGraph.from_graph(to_fb(g), pb=True, wave_count=waves) as d2:
+        ws = d2.wave_starts(waves)
+        assert ws[0] == 0 and ws[-1] == g.n and np.all(np.diff(ws.astype(np.int64)) > 0)
+        assert np.all(ws[:-1] % (1 << shift) == 0)
+        ref = oracle.pagerank_lockstep(g, ws, threshold=1e-10, history_cap=200)
+        for k in (1, 2, 5, ref.iterations):
+            r = d2.run(fb.ENGINE_FUSED_LOCKSTEP, fb.PageRankConfig(threshold=1e-10, max_iterations=k))
+            assert rel(r.ranks.values, ref.history[k - 1]) <= EC_RTOL
+        r = d2.run(fb.ENGINE_FUSED_LOCKSTEP, fb.PageRankConfig(threshold=1e-10))
+        ec = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))  # both plans cached side by side
+    assert r.trace.iterations == ref.iterations and r.trace.converged
+    assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
+    assert ec.trace.iterations == rec["runs"]["ec_seq@1e-10"]["iterations"]
+    if len(ws) - 1 >= 8:
+        assert r.trace.iterations < ec.trace.iterations  # Gauss-Seidel gain
+
+
 def test_pb_l1_rule_matches_pull(config1):
     """The L1 stop rule stops the propagation-blocked engine at the pull
     engine's iteration with the same trace (within the 1e-12 tolerance)."""
