@@ -230,6 +230,11 @@ struct PbPlan {
   std::vector<int64_t> wave_bin;  // nwaves + 1: first bin of each wave
   std::vector<int64_t> item0;     // nwaves + 1: first phase-1 piece of each wave
   std::vector<int64_t> unit0;     // nwaves + 1: first phase-2 unit of each wave
+  // phase-2 units: whole bins, heavy bins cut into pieces (smaller pieces for
+  // more waves, so that every wave has a few units per CTA)
+  int32_t* unit_bin = nullptr;
+  int64_t* unit_e = nullptr;      // units + 1: first entry of each unit
+  int32_t* unit_k = nullptr;      // units of the unit's bin (1 = the bin is whole)
   int64_t* item_start = nullptr;  // pieces: first entry and length
   uint32_t* item_len = nullptr;
   unsigned long long* ctr = nullptr;  // 2 x nwaves work counters (reset per sweep)
@@ -246,11 +251,7 @@ struct PbSet {
   double* val = nullptr;         // m + 8: per-sweep scratch, contributions in (bin, chunk, k) order
   uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
   int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
-  int64_t nunits = 0;            // phase-2 work units: whole bins, heavy bins cut into pieces
-  int32_t* unit_bin = nullptr;
-  int64_t* unit_e = nullptr;     // nunits + 1: first entry of each unit
-  int32_t* unit_k = nullptr;     // units of the unit's bin (1 = the bin is whole)
-  std::vector<int32_t> unit_bin_host;
+  std::vector<int64_t> bin_edge;  // nbins + 1: first entry of each bin
   double* psum = nullptr;        // n: partial row sums of split bins (zero between sweeps)
   unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep
   int p1_grid = 0, p2_grid = 0;

@@ -511,14 +511,47 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     cudaStreamSynchronize(st);
     return e;
   }
-  // phase-2 units are bin-ordered: wave w's units are a contiguous range
-  plan.unit0.assign(W + 1, pb.nunits);
-  for (int64_t u = pb.nunits - 1; u >= 0; --u) {
-    const int64_t b = pb.unit_bin_host[u];
-    const int w = (int)(std::upper_bound(plan.wave_bin.begin(), plan.wave_bin.end(), b) - plan.wave_bin.begin()) - 1;
-    plan.unit0[w] = u;
+  {
+    // phase-2 units: bins, heavy ones cut into pieces of about `piece`
+    // entries: small enough that each wave has several units per CTA, never
+    // below twice the average bin (a split bin pays psum atomics per row;
+    // splitting config 4's even bins cost 5-10%)
+    const int64_t avg_bin = pb.m / std::max<int64_t>(1, pb.nbins);
+    int64_t piece = std::max<int64_t>({int64_t(1) << 16, 2 * avg_bin, pb.m / ((int64_t)pb.p2_grid * 8 * W)});
+    if (const char* v = std::getenv("FPR_B200_PB_PIECE")) piece = std::max<int64_t>(32, std::atoll(v));  // tests
+    std::vector<int32_t> ubin, uk;
+    std::vector<int64_t> ue;
+    plan.unit0.assign(W + 1, 0);
+    for (int w = 0; w < W; ++w) {
+      plan.unit0[w] = (int64_t)ubin.size();
+      for (int64_t b = plan.wave_bin[w]; b < plan.wave_bin[w + 1]; ++b) {
+        const int64_t E = pb.bin_edge[b + 1] - pb.bin_edge[b];
+        const int64_t k = std::max<int64_t>(1, (E + piece - 1) / piece);
+        for (int64_t j = 0; j < k; ++j) {
+          ubin.push_back((int32_t)b);
+          uk.push_back((int32_t)k);
+          ue.push_back(pb.bin_edge[b] + E * j / k);
+        }
+      }
+    }
+    plan.unit0[W] = (int64_t)ubin.size();
+    ue.push_back(pb.m);
+    e = alloc((void**)&plan.unit_bin, ubin.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_k, uk.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_e, ue.size() * sizeof(int64_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(plan.unit_bin, ubin.data(), ubin.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(plan.unit_k, uk.data(), uk.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(plan.unit_e, ue.data(), ue.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host vectors die at the end of this block
+    if (e != cudaSuccess) {
+      for (void* q : plan.allocs) cudaFreeAsync(q, st);
+      cudaStreamSynchronize(st);
+      return e;
+    }
   }
-  for (int w = W - 1; w >= 0; --w) plan.unit0[w] = std::min(plan.unit0[w], plan.unit0[w + 1]);
   *out = &pb.plans.emplace(S, std::move(plan)).first->second;
   return cudaSuccess;
 }
@@ -572,7 +605,7 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     pb.p1_grid = sms * 8;
   }
   {
-    // phase-2 units: bins, heavy ones cut into pieces of about `piece` entries
+    // bin edge offsets (host copy: each wave plan cuts its phase-2 units)
     std::vector<int64_t> be(nbins + 1);
     int64_t* d_be = nullptr;
     e = cudaMallocAsync(&d_be, (nbins + 1) * sizeof(int64_t), st);
@@ -585,28 +618,7 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (d_be) cudaFreeAsync(d_be, st);
     if (e != cudaSuccess) goto out;
-    int64_t piece = std::max<int64_t>(1 << 16, m / ((int64_t)pb.p2_grid * 8));
-    if (const char* v = std::getenv("FPR_B200_PB_PIECE")) piece = std::max<int64_t>(32, std::atoll(v));  // tests
-    std::vector<int32_t> ubin, uk;
-    std::vector<int64_t> ue;
-    for (int64_t b = 0; b < nbins; ++b) {
-      const int64_t E = be[b + 1] - be[b];
-      const int64_t k = std::max<int64_t>(1, (E + piece - 1) / piece);
-      for (int64_t j = 0; j < k; ++j) {
-        ubin.push_back((int32_t)b);
-        uk.push_back((int32_t)k);
-        ue.push_back(be[b] + E * j / k);
-      }
-    }
-    ue.push_back(m);
-    pb.nunits = (int64_t)ubin.size();
-    pb.unit_bin_host = ubin;
-    PK(alloc((void**)&pb.unit_bin, ubin.size() * sizeof(int32_t)));
-    PK(alloc((void**)&pb.unit_k, uk.size() * sizeof(int32_t)));
-    PK(alloc((void**)&pb.unit_e, ue.size() * sizeof(int64_t)));
-    PK(cudaMemcpyAsync(pb.unit_bin, ubin.data(), ubin.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    PK(cudaMemcpyAsync(pb.unit_k, uk.data(), uk.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    PK(cudaMemcpyAsync(pb.unit_e, ue.data(), ue.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    pb.bin_edge = be;
     PK(alloc((void**)&pb.psum, n * sizeof(double)));
     PK(cudaMemsetAsync(pb.psum, 0, n * sizeof(double), st));
     PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
@@ -639,7 +651,8 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
     }
     pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>
         <<<pb.p2_grid, FPR_PB_ACC_THREADS, (size_t)sizeof(double) << pb.shift, st>>>(
-            pb.val, pb.dstl_bm, pb.unit_bin + u0, pb.unit_e + u0, pb.unit_k + u0, plan.unit0[w + 1] - u0, pb.shift,
+            pb.val, pb.dstl_bm, plan.unit_bin + u0, plan.unit_e + u0, plan.unit_k + u0, plan.unit0[w + 1] - u0,
+            pb.shift,
             g.n, g.outdeg, pr, cur, base, damping, pb.psum, pb.bin_done, plan.ctr + W + w,
             plan.cta_pairs + 2 * (size_t)w * pb.p2_grid);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
