@@ -1,5 +1,6 @@
-// pb.cu -- propagation-blocked EC sweep (FPR_B200_OPT_PB) for graphs whose
-// contribution vector far exceeds L2 (configs 4/5).
+// pb.cu -- propagation-blocked sweeps (FPR_B200_OPT_PB) for graphs whose
+// contribution vector far exceeds L2 (configs 4/5): EC (Jacobi) and the
+// lockstep FusEd schedule (waves of whole bins, in place).
 //
 // The pull gather contrib[in_src[e]] misses L2 on such graphs, and each miss
 // pulls ~64 B from HBM for 8 useful bytes (profiles/r1_large_configs_ncu.md).
@@ -11,17 +12,17 @@
 //   * rows are cut into bins of 2^shift consecutive rows; a bin's entries are
 //     exactly its rows' in-edges (duplicates and self loops included);
 //   * inside a bin, entries are regrouped by source chunk (src >> chunk_shift):
-//     segment (bin b, chunk c) is contiguous;
+//     segment (bin b, chunk c) is contiguous and keeps ascending rows;
 //   * entry = (source id, row offset inside the bin as uint16).
-// Per sweep:
-//   * phase 1 (pb_gather_kernel): warps walk the segments chunk by chunk, so
-//     the sources read at any moment span one chunk's contributions (a 64 MB
-//     window at the default chunk of 2^23 sources, half of L2), and write
-//     val[pos] = prev[src_bm[pos]] contiguously;
-//   * phase 2 (pb_accum_kernel): one CTA per bin accumulates val into the
-//     bin's rows in shared memory and finishes the rows exactly like the
-//     blocked engine's apply (blocked.cu): base + d*sum without FMA,
-//     contribution, residual.
+// A sweep plan (get_pb_plan, cached per wave count) cuts the bins into waves
+// of consecutive bins: 1 wave for EC, S for lockstep.  Per wave:
+//   * phase 1 (pb_gather_kernel): warps walk the wave's segments chunk by
+//     chunk, so the sources read at any moment span one chunk's
+//     contributions (a 64 MB window at the default chunk of 2^23 sources,
+//     half of L2), and write val[pos] = prev[src_bm[pos]] contiguously;
+//   * phase 2 (pb_accum_kernel): CTAs accumulate val into a bin's rows in
+//     shared memory and finish the rows exactly like the blocked engine's
+//     apply (blocked.cu): base + d*sum without FMA, contribution, residual.
 // Per edge and sweep: 4 B source + 8 B value written + 8 B read + 2 B offset,
 // all sequential, where a missed pull gather moved ~64 B of DRAM.
 // A row's sum is accumulated in shared-memory atomic order, a regrouping of
