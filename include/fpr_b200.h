@@ -85,6 +85,14 @@ typedef struct fpr_config {
 #define FPR_B200_OPT_REORDER 1u /* renumber vertices by descending out-degree inside
                                   the library (locality for contrib gathers); ranks
                                   and traces are reported in the caller's ids */
+#define FPR_B200_OPT_REORDER_SOURCES 8u /* renumber inside the library so that the
+                                  vertices with out-degree > 0 (the only ones whose
+                                  contributions are ever read) come first, the
+                                  caller's order otherwise kept: the gathered vector
+                                  shrinks to the sources without losing a crawl
+                                  order's locality; ranks and
+                                  traces in the caller's ids.  OPT_REORDER wins if
+                                  both are set */
 #define FPR_B200_OPT_BLOCKED 2u /* EC engine: source-blocked sweeps (column blocks of
                                   2^24 vertices, FPR_B200_BLOCK_SHIFT overrides) so the
                                   gathers of a block pass stay near L2; only for graphs

@@ -42,6 +42,7 @@ GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
 OPT_REORDER = 1  # FPR_B200_OPT_REORDER
 OPT_BLOCKED = 2  # FPR_B200_OPT_BLOCKED
 OPT_PB = 4  # FPR_B200_OPT_PB
+OPT_REORDER_SOURCES = 8  # FPR_B200_OPT_REORDER_SOURCES
 
 
 class B200Error(RuntimeError):
@@ -285,7 +286,12 @@ def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False
     o.device = device
     o.norm = norm
     o.wave_count = wave_count
-    o.flags = (OPT_REORDER if reorder else 0) | (OPT_BLOCKED if blocked else 0) | (OPT_PB if pb else 0)
+    # reorder: False, True / "degree" (FPR_B200_OPT_REORDER) or "sources"
+    # (FPR_B200_OPT_REORDER_SOURCES)
+    if reorder not in (False, True, "degree", "sources"):
+        raise ValueError(f"reorder must be False, True, 'degree' or 'sources', not {reorder!r}")
+    ro = OPT_REORDER_SOURCES if reorder == "sources" else (OPT_REORDER if reorder else 0)
+    o.flags = ro | (OPT_BLOCKED if blocked else 0) | (OPT_PB if pb else 0)
     o.stream = stream
     return o
 

@@ -651,19 +651,25 @@ cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_o
   return e;
 }
 
-// Locality reorder (opt-in, FPR_B200_OPT_REORDER): vertices renumbered by
+// Locality reorders (opt-in).  FPR_B200_OPT_REORDER: vertices renumbered by
 // descending out-degree (ties by id) -- the gather frequency of contrib[s] is
 // out_degree(s), so hot contributions share sectors and stay L2-resident.
-// Returns the new CSR in `out` and new_of_old (device, n int32) in *perm.
-__global__ void degree_key_kernel(const int32_t* outdeg, int32_t n, uint64_t* keys, int32_t* ids) {
+// FPR_B200_OPT_REORDER_SOURCES (sources_only): a stable partition, vertices
+// with out-degree > 0 first -- only they are ever gathered, so the gathered
+// vector shrinks to them while the caller's (crawl) order is kept inside
+// each class.  Returns the new CSR in `out` and new_of_old (device, n int32)
+// in *perm.
+__global__ void degree_key_kernel(const int32_t* outdeg, int32_t n, bool sources_only, uint64_t* keys,
+                                  int32_t* ids) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    keys[i] = ((uint64_t)(uint32_t)(INT32_MAX - outdeg[i]) << 32) | (uint32_t)i;
+    const uint32_t major = sources_only ? (outdeg[i] == 0 ? 1u : 0u) : (uint32_t)(INT32_MAX - outdeg[i]);
+    keys[i] = ((uint64_t)major << 32) | (uint32_t)i;
     ids[i] = (int32_t)i;
   }
 }
 
-cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, cudaStream_t st,
+cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, DevGraph& out, int32_t** perm, cudaStream_t st,
                               const char** msg) {
   *msg = nullptr;
   *perm = nullptr;
@@ -682,7 +688,7 @@ cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, 
   GK(cudaMallocAsync(&i1, n * sizeof(int32_t), st));
   GK(cudaMallocAsync(&i2, n * sizeof(int32_t), st));
   GK(cudaMallocAsync(&p, n * sizeof(int32_t), st));
-  degree_key_kernel<<<blocks_for(n), 256, 0, st>>>(g.outdeg, n, k1, i1);
+  degree_key_kernel<<<blocks_for(n), 256, 0, st>>>(g.outdeg, n, sources_only, k1, i1);
   GK(cudaGetLastError());
   GK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, i1, i2, (int64_t)n, 0, 64, st));
   GK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));

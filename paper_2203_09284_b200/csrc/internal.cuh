@@ -161,9 +161,10 @@ struct GenRequest {
 // Builds row/src/outdeg on the device (allocates them into g).  Returns a
 // cudaError_t; *msg receives a static description on non-CUDA failures.
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t s, const char** msg);
-// Locality reorder by descending out-degree: new CSR in `out` (allocated on
-// stream s), *perm = device new_of_old (n int32, caller frees).
-cudaError_t reorder_by_degree(const DevGraph& g, DevGraph& out, int32_t** perm, cudaStream_t s,
+// Locality reorder by descending out-degree, or (sources_only) the stable
+// partition with the out-degree > 0 vertices first: new CSR in `out`
+// (allocated on stream s), *perm = device new_of_old (n int32, caller frees).
+cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, DevGraph& out, int32_t** perm, cudaStream_t s,
                               const char** msg);
 // BFS discovery order of g (config-3 relabel) into a host buffer of n int32.
 cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_out,

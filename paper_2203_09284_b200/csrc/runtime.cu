@@ -241,7 +241,7 @@ struct fpr_b200_graph {
   // multi-GPU part (fpr_b200_graph_partition); nparts == 1 for a whole graph
   uint32_t nparts = 1, part_id = 0;
   uint32_t flags = 0;
-  int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER: caller id -> internal id
+  int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER(_SOURCES): caller id -> internal id
   BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
   PbSet* pb = nullptr;            // FPR_B200_OPT_PB: built at the first EC run
   uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
@@ -359,11 +359,12 @@ constexpr int64_t kTraceWarps = 0;
 #endif
 
 int finish_graph(fpr_b200_graph* h) {
-  if ((h->flags & FPR_B200_OPT_REORDER) && h->g.n > 1) {
+  if ((h->flags & (FPR_B200_OPT_REORDER | FPR_B200_OPT_REORDER_SOURCES)) && h->g.n > 1) {
     DevGraph re;
     int32_t* perm = nullptr;
     const char* msg = nullptr;
-    CK(reorder_by_degree(h->g, re, &perm, h->stream, &msg));
+    const bool sources_only = !(h->flags & FPR_B200_OPT_REORDER);
+    CK(reorder_by_degree(h->g, sources_only, re, &perm, h->stream, &msg));
     if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200 reorder: ") + msg);
     h->allocs.push_back(re.row);
     h->allocs.push_back(re.src);
@@ -852,7 +853,7 @@ int fpr_b200_graph_download_csr(const fpr_b200_graph* hc, uint64_t* in_start, ui
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: null graph");
   if (h->new_of_old)
     return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: graph was created with "
-                                 "FPR_B200_OPT_REORDER (resident CSR uses internal ids)");
+                                 "FPR_B200_OPT_REORDER or OPT_REORDER_SOURCES (resident CSR uses internal ids)");
   CK(cudaSetDevice(h->device));
   const DevGraph& g = h->g;
   const int64_t chunk = 1 << 24;

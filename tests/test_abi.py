@@ -97,3 +97,19 @@ def test_every_pointer_entry_point_has_argtypes():
         if name in no_args:
             continue
         assert getattr(L, name).argtypes is not None, name
+
+
+def test_option_flags_match_header():
+    """The Python flag constants are the header's, and `reorder` maps to the
+    two reorder flags (anything else is rejected before any device work)."""
+    text = open(HEADER).read()
+    for name, val in (("REORDER", fb.OPT_REORDER), ("BLOCKED", fb.OPT_BLOCKED), ("PB", fb.OPT_PB),
+                      ("REORDER_SOURCES", fb.OPT_REORDER_SOURCES)):
+        m = re.search(rf"#define FPR_B200_OPT_{name} (\d+)u", text)
+        assert m and int(m.group(1)) == val, name
+    assert fb._options(reorder=True).flags == fb.OPT_REORDER
+    assert fb._options(reorder="degree").flags == fb.OPT_REORDER
+    assert fb._options(reorder="sources", pb=True).flags == fb.OPT_REORDER_SOURCES | fb.OPT_PB
+    assert fb._options().flags == 0
+    with pytest.raises(ValueError, match="reorder"):
+        fb._options(reorder="bfs")
