@@ -371,14 +371,15 @@ class DeviceGraph:
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
-    def from_edge_list(cls, text, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False):
+    def from_edge_list(cls, text, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
+                       blocked=False, pb=False):
         """build_csr(parse_edge_list(text)) -- parsing, id compaction and the
         CSR build all on the device (edge_list.hpp:39-80, graph.hpp:35-70)."""
         ptr, nbytes, keep = _text_arg(text)
         h = C.c_void_p()
         perr = _ParseErr()
         _check(lib().fpr_b200_graph_from_edge_list(ptr, nbytes, C.byref(_options(device, norm, wave_count,
-                                                                                stream, reorder)),
+                                                                                stream, reorder, blocked, pb)),
                                                    C.byref(h), C.byref(perr)), perr)
         del keep
         return cls(h.value, device, norm, wave_count)

@@ -56,19 +56,24 @@ def open_graph(args, norm=NORM_LINF) -> tuple[DeviceGraph, str]:
                          "(--graph/--rmat/--rmat-bfs/--uniform/--chunglu/--edges)")
     k = given[0]
     v = getattr(args, k)
+    # library options: internal renumbering,
+    # propagation-blocked sweeps, lockstep waves per sweep
+    ro = getattr(args, "reorder", "none")
+    kw = {"norm": norm, "reorder": False if ro == "none" else ro, "pb": bool(getattr(args, "pb", False)),
+          "wave_count": int(getattr(args, "waves", 0))}
     if k == "graph":
         g = load_cache(v)  # CacheError -> I/O exit code
-        return DeviceGraph.from_graph(g, norm=norm), v
+        return DeviceGraph.from_graph(g, **kw), v
     if k == "edges":
         text = np.fromfile(v, dtype=np.uint8)  # OSError -> I/O exit code
-        return DeviceGraph.from_edge_list(text, norm=norm), v
+        return DeviceGraph.from_edge_list(text, **kw), v
     a, b, c = _triple(v, k.replace("_", "-"))
     if k in ("rmat", "rmat_bfs"):
-        return DeviceGraph.generate_rmat(RmatParams(scale=a, edge_factor=b, seed=c), norm=norm,
-                                         relabel_bfs=(k == "rmat_bfs")), f"{k}:{v}"
+        return DeviceGraph.generate_rmat(RmatParams(scale=a, edge_factor=b, seed=c),
+                                         relabel_bfs=(k == "rmat_bfs"), **kw), f"{k}:{v}"
     if k == "uniform":
-        return DeviceGraph.generate_uniform(a, b, c, norm=norm), f"uniform:{v}"
-    return DeviceGraph.generate_chunglu(a, b, c, norm=norm), f"chunglu:{v}"
+        return DeviceGraph.generate_uniform(a, b, c, **kw), f"uniform:{v}"
+    return DeviceGraph.generate_chunglu(a, b, c, **kw), f"chunglu:{v}"
 
 
 def _engine(tag: str) -> int:
@@ -133,6 +138,8 @@ def cmd_bench(args, out) -> int:
 
 
 def cmd_gen(args, out) -> int:
+    if args.reorder != "none":
+        raise UsageError("gen writes the graph in the caller's ids; --reorder applies to run/bench")
     dg, label = open_graph(args)
     with dg:
         g = dg.download()
@@ -183,6 +190,11 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--threshold", type=float, default=1e-15)
         p.add_argument("--threads", type=int, default=1)
         p.add_argument("--max-iters", dest="max_iters", type=int, default=10000)
+        p.add_argument("--reorder", choices=["none", "degree", "sources"], default="none",
+                       help="internal renumbering (FPR_B200_OPT_REORDER / _REORDER_SOURCES)")
+        p.add_argument("--pb", action="store_true",
+                       help="propagation-blocked sweeps for ec_b200 / fused_lockstep_b200 (FPR_B200_OPT_PB)")
+        p.add_argument("--waves", type=int, default=0, help="lockstep waves per sweep (0 = auto)")
 
     p = sub.add_parser("run")
     common(p)

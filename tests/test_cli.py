@@ -23,6 +23,11 @@ def test_usage_errors():
     assert _run(["run", "--rmat", "4:2:1", "--engine", "ec_seq"])[0] == EXIT_USAGE
 
 
+def test_option_usage_errors():
+    assert _run(["gen", "--rmat", "4:2:1", "--out", "/dev/null", "--reorder", "degree"])[0] == EXIT_USAGE
+    assert _run(["run", "--rmat", "4:2:1", "--reorder", "bfs"])[0] == EXIT_USAGE
+
+
 def test_missing_file_is_io_error(tmp_path):
     assert _run(["run", "--graph", str(tmp_path / "missing.fprg")])[0] == EXIT_IO
 
@@ -51,6 +56,23 @@ def test_bench_csv_schema(tmp_path):
         if r["engine"] == "ec_b200":
             assert float(r["l1_vs_seq_ec"]) == 0.0
         assert r["converged"] == "true"
+
+
+@pytest.mark.gpu
+def test_bench_library_options(tmp_path):
+    """--pb / --reorder / --waves reach the library: the propagation-blocked
+    EC and lockstep engines on a sources-first renumbered graph converge, and
+    PB EC matches the plain EC row's iteration count."""
+    out = tmp_path / "o.csv"
+    rc, _ = _run(["bench", "--rmat", "10:16:1", "--engines", "ec_b200,fused_lockstep_b200", "--thresholds", "1e-10",
+                  "--pb", "--reorder", "sources", "--waves", "4", "--out", str(out)])
+    assert rc == EXIT_OK
+    rows = {r["engine"]: r for r in csv.DictReader(open(out))}
+    assert all(r["converged"] == "true" for r in rows.values())
+    plain = tmp_path / "p.csv"
+    assert _run(["bench", "--rmat", "10:16:1", "--engines", "ec_b200", "--thresholds", "1e-10",
+                 "--out", str(plain)])[0] == EXIT_OK
+    assert next(csv.DictReader(open(plain)))["iterations"] == rows["ec_b200"]["iterations"]
 
 
 @pytest.mark.gpu
