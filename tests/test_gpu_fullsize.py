@@ -55,3 +55,31 @@ def test_config5_rmat28():
         assert dg.validate() == 0
         assert 4_000_000_000 < dg.m < 4_294_967_296
         _properties(dg, "config5")
+
+
+@pytest.mark.parametrize("config", ["4", "5"])
+def test_pb_engines_full_size(config):
+    """FPR_B200_OPT_PB at full size: the propagation-blocked EC gives the pull
+    EC's iteration count and ranks within 1e-12 relative (the oracle's
+    per-iteration bar, here against the oracle-checked pull engine); the
+    FusEd schedule on PB sweeps converges in fewer sweeps to within the
+    geometric-tail bound of the EC fixed point."""
+    def make(**kw):
+        if config == "4":
+            return fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, **kw)
+        return fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), **kw)
+
+    cfg = fb.PageRankConfig(threshold=T)
+    with make() as dg:
+        ec = dg.run(fb.ENGINE_EC, cfg)
+    with make(pb=True) as dg:
+        pb = dg.run(fb.ENGINE_EC, cfg)
+        ls = dg.run(fb.ENGINE_FUSED_LOCKSTEP, cfg)
+        waves = len(dg.wave_starts()) - 1
+        n = dg.n
+    assert pb.trace.iterations == ec.trace.iterations and pb.trace.converged
+    assert float(np.max(np.abs(pb.ranks.values - ec.ranks.values) / ec.ranks.values)) <= 1e-12
+    assert ls.trace.converged and ls.trace.iterations < ec.trace.iterations
+    assert fb.l1_norm(ls.ranks.values, ec.ranks.values) <= 2 * n * T * D / (1 - D)
+    print(f"\nconfig{config} PB: ec {pb.trace.iterations} it {pb.solve_ms:.1f} ms, "
+          f"lockstep ({waves} waves) {ls.trace.iterations} it {ls.solve_ms:.1f} ms")
