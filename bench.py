@@ -306,6 +306,10 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
                 for eng, tag in ((fb.ENGINE_EC, "ec_pb"), (fb.ENGINE_FUSED_LOCKSTEP, "lockstep_pb")):
                     dg.run(eng, one, copy_ranks=False, copy_trace=False)  # builds the layout and the wave plan
                     rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
+                    # the PB sweep's own streamed bytes: 22 B per edge
+                    # (source, value written and read back, row offset) + 36 B per vertex
+                    ms_it = rec[tag]["ms_per_sweep"]
+                    rec[tag]["pb_stream_bytes_frac"] = (22 * dg.m + 36 * dg.n) / (ms_it * 1e-3) / 1e9 / peak
                 rec["lockstep_pb"]["waves"] = len(dg.wave_starts()) - 1
     return out
 
