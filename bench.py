@@ -511,7 +511,10 @@ def main() -> None:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("config2_ec", 1), "peak_kind": peak_kind,
                          "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+                         # the random-fetch ceiling measured by bench_micro/gather_bench.cu (an
+                         # L2-side request limit): the kernel's real bound on config 2
                          "gather_ceiling_gteps": 270.0,
+                         "gather_ceiling_frac": m * iters / (kms * 1e-3) / 1e9 / 270.0,
                          "kernel": "solve_kernel<false> (persistent EC, all iterations)",
                          "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": algorithmic_bytes(n, m) * iters},
