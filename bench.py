@@ -304,8 +304,10 @@ def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
             with dg:
                 one = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1)
                 for eng, tag in ((fb.ENGINE_EC, "ec_pb"), (fb.ENGINE_FUSED_LOCKSTEP, "lockstep_pb")):
-                    dg.run(eng, one, copy_ranks=False, copy_trace=False)  # builds the layout and the wave plan
+                    first = dg.run(eng, one, copy_ranks=False, copy_trace=False)  # builds the layout / wave plan
                     rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
+                    # one-time device setup on this handle (EC: the PB layout; lockstep: its wave plan)
+                    rec[tag]["setup_ms_first_run"] = first.setup_ms
                     # the PB sweep's own streamed bytes: 22 B per edge
                     # (source, value written and read back, row offset) + 36 B per vertex
                     ms_it = rec[tag]["ms_per_sweep"]

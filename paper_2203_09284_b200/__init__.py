@@ -208,6 +208,7 @@ class PageRankResult:
     trace: ConvergenceTrace
     solve_ms: float = 0.0
     kernel_launches: int = 0
+    setup_ms: float = 0.0  # device time before the first sweep (init; one-time layouts on first use)
 
 
 @dataclass
@@ -453,7 +454,7 @@ class DeviceGraph:
         trace = ConvergenceTrace(errors[:k].copy() if copy_trace else np.empty(0), k, bool(res.converged),
                                  l1[:k].copy() if copy_trace else None, ns[:k].copy() if copy_trace else None)
         rv = RankVector(ranks[: self.n] if copy_ranks else np.empty(0), res.final_error)
-        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches)
+        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches, res.setup_ms)
 
 
 def run_engine(kind: EngineKind | str, g, cfg: PageRankConfig, **kw) -> PageRankResult:

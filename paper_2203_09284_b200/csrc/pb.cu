@@ -81,15 +81,17 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
     typename ScanI::TempStorage scani;
   } tmp;
   __shared__ uint32_t skey[kPbThreads];
-  extern __shared__ uint32_t h[];
+  extern __shared__ uint32_t h[];           // nchunks chunk counters, then
+  uint32_t* srow = h + ((nchunks + 3) & ~3ll);  // the bin's row offsets relative to its first edge
   const int tid = threadIdx.x;
   const uint32_t sentinel = (uint32_t)nchunks;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
     for (int64_t c = tid; c < nchunks; c += blockDim.x) h[c] = 0;
-    __syncthreads();
     const int64_t r0 = b << shift;
     const int64_t r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
     const int64_t e0 = row[r0], e1 = row[r1];
+    for (int64_t r = r0 + tid; r <= r1; r += blockDim.x) srow[r - r0] = (uint32_t)(__ldg(row + r) - e0);
+    __syncthreads();
     for (int64_t e = e0 + tid; e < e1; e += blockDim.x) atomicAdd(&h[(uint32_t)__ldg(src + e) >> chunk_shift], 1u);
     __syncthreads();
     uint32_t running = 0;
@@ -111,16 +113,17 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       uint32_t key[1] = {sentinel};
       uint64_t val[1] = {0};
       if (e < e1) {
-        // row of edge e: last r in [r0, r1) with row[r] <= e
-        int64_t lo = r0, hi = r1 - 1;
+        // row of edge e: last r in [0, r1 - r0) with srow[r] <= e - e0
+        const uint32_t el = (uint32_t)(e - e0);
+        int lo = 0, hi = (int)(r1 - r0) - 1;
         while (lo < hi) {
-          const int64_t mid = (lo + hi + 1) >> 1;
-          if (__ldg(row + mid) <= e) lo = mid;
+          const int mid = (lo + hi + 1) >> 1;
+          if (srow[mid] <= el) lo = mid;
           else hi = mid - 1;
         }
         const uint32_t s = (uint32_t)__ldg(src + e);
         key[0] = s >> chunk_shift;
-        val[0] = ((uint64_t)s << 16) | (uint64_t)(lo - r0);
+        val[0] = ((uint64_t)s << 16) | (uint64_t)lo;
       }
       Sort(tmp.sort).Sort(key, val, 0, key_bits);
       __syncthreads();
@@ -565,9 +568,11 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   const int64_t n = g.n, m = g.m;
   const int64_t nbins = n > 0 ? (n + (1ll << shift) - 1) >> shift : 0;
   const int64_t nchunks = std::max<int64_t>(1, (n + (1ll << chunk_shift) - 1) >> chunk_shift);
-  const size_t hist_smem = (size_t)nchunks * sizeof(uint32_t);
+  // layout kernel: chunk counters + the bin's (2^shift + 1) relative row offsets
+  const size_t hist_smem = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t) +
+                           (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t);
   const size_t acc_smem = (size_t)sizeof(double) << shift;
-  if (n == 0 || shift < 5 || shift > 14 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 160 * 1024 ||
+  if (n == 0 || shift < 5 || shift > 14 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 192 * 1024 ||
       nbins * nchunks > (1ll << 31)) {
     *msg = "bin/chunk geometry out of range";
     return cudaSuccess;
@@ -590,6 +595,28 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   PK(alloc((void**)&pb.dstl_bm, (m + 8) * sizeof(uint16_t)));
   PK(alloc((void**)&pb.val, (m + 8) * sizeof(double)));
   {
+    // bin edge offsets (host copy: each wave plan cuts its phase-2 units)
+    std::vector<int64_t> be(nbins + 1);
+    int64_t* d_be = nullptr;
+    e = cudaMallocAsync(&d_be, (nbins + 1) * sizeof(int64_t), st);
+    if (e == cudaSuccess) {
+      pb_bin_edges_kernel<<<(unsigned)((nbins + 256) / 256), 256, 0, st>>>(g.row, g.n, shift, nbins, d_be);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(be.data(), d_be, (nbins + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (d_be) cudaFreeAsync(d_be, st);
+    if (e != cudaSuccess) goto out;
+    pb.bin_edge = be;
+    for (int64_t b = 0; b < nbins; ++b)
+      if (be[b + 1] - be[b] >= (1ll << 32)) {  // the layout kernel's uint32 in-bin offsets
+        *msg = "a bin holds 2^32 or more edges (use a smaller FPR_B200_PB_SHIFT)";
+        break;
+      }
+    if (*msg) goto out;
+  }
+  {
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
     PK(cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem));
@@ -606,31 +633,16 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
     pb.p1_grid = sms * 8;
   }
   {
-    // bin edge offsets (host copy: each wave plan cuts its phase-2 units)
-    std::vector<int64_t> be(nbins + 1);
-    int64_t* d_be = nullptr;
-    e = cudaMallocAsync(&d_be, (nbins + 1) * sizeof(int64_t), st);
-    if (e == cudaSuccess) {
-      pb_bin_edges_kernel<<<(unsigned)((nbins + 256) / 256), 256, 0, st>>>(g.row, g.n, shift, nbins, d_be);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(be.data(), d_be, (nbins + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (d_be) cudaFreeAsync(d_be, st);
-    if (e != cudaSuccess) goto out;
-    pb.bin_edge = be;
     PK(alloc((void**)&pb.psum, n * sizeof(double)));
     PK(cudaMemsetAsync(pb.psum, 0, n * sizeof(double), st));
     PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
     PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
-    PK(cudaStreamSynchronize(st));  // the host vectors die at the end of this block
   }
   PK(cudaFuncSetAttribute(pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
   PK(cudaStreamSynchronize(st));
 out:
-  if (e != cudaSuccess) {
+  if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
     cudaStreamSynchronize(st);
   }
