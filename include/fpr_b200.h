@@ -99,7 +99,7 @@ typedef struct fpr_config {
                                   whose contribution vector far exceeds L2 (configs 4/5
                                   in natural order) */
 #define FPR_B200_OPT_PB 4u      /* EC and lockstep engines: propagation-blocked sweeps
-                                  (bins of 2^13 rows, source chunks of 2^23;
+                                  (bins of 2^13 rows, source chunks of 2^21;
                                   FPR_B200_PB_SHIFT / FPR_B200_PB_CHUNK_SHIFT override):
                                   two streaming passes instead of the random pull
                                   gather, for graphs whose contribution vector far

@@ -18,8 +18,8 @@
 // of consecutive bins: 1 wave for EC, S for lockstep.  Per wave:
 //   * phase 1 (pb_gather_kernel): warps walk the wave's segments chunk by
 //     chunk, so the sources read at any moment span one chunk's
-//     contributions (a 64 MB window at the default chunk of 2^23 sources,
-//     half of L2), and write val[pos] = prev[src_bm[pos]] contiguously;
+//     contributions (a 16 MB window at the default chunk of 2^21 sources),
+//     and write val[pos] = prev[src_bm[pos]] contiguously;
 //   * phase 2 (pb_accum_kernel): CTAs accumulate val into a bin's rows in
 //     shared memory and finish the rows exactly like the blocked engine's
 //     apply (blocked.cu): base + d*sum without FMA, contribution, residual.
