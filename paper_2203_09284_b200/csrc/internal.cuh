@@ -263,8 +263,11 @@ struct PbSet {
 // exactly as the CSR holds them).  *msg set (no error) on bad geometry.
 cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg);
 void free_pb(PbSet& pb, cudaStream_t st);
-// First bin of each of (at most) S waves of equal bin counts: S' + 1 values.
-std::vector<int64_t> pb_wave_bins(int64_t nbins, uint32_t S);
+// First bin of each of (at most) S edge-balanced waves, from the bins' edge
+// offsets (nbins + 1 values): S' + 1 values.
+std::vector<int64_t> pb_wave_bins(const std::vector<int64_t>& bin_edge, uint32_t S);
+// Edge offset of every 2^shift-row bin boundary of g (nbins + 1 values).
+cudaError_t pb_bin_edges(const DevGraph& g, int shift, cudaStream_t st, std::vector<int64_t>* out);
 // The plan for S waves, built on first use and cached in pb.plans.
 cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** out);
 // One propagation-blocked sweep: for each wave, gather from prev then

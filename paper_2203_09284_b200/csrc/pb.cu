@@ -446,11 +446,37 @@ void free_pb(PbSet& pb, cudaStream_t st) {
   pb = PbSet{};
 }
 
-std::vector<int64_t> pb_wave_bins(int64_t nbins, uint32_t S) {
-  const int64_t w = std::max<int64_t>(1, std::min<int64_t>(S, nbins));
-  std::vector<int64_t> wb(w + 1);
-  for (int64_t i = 0; i <= w; ++i) wb[i] = nbins * i / w;
+// Edge-balanced waves: wave w starts at the first bin whose edges begin at or
+// after w/S of all edges (skewed and crawl-ordered graphs put most edges in
+// their first bins; vertex-balanced waves gave config 3's BFS order almost
+// no Gauss-Seidel gain).  Empty waves are dropped.
+std::vector<int64_t> pb_wave_bins(const std::vector<int64_t>& bin_edge, uint32_t S) {
+  const int64_t nbins = (int64_t)bin_edge.size() - 1;
+  const int64_t m = bin_edge.back();
+  std::vector<int64_t> wb{0};
+  for (uint32_t w = 1; w < S; ++w) {
+    const int64_t target = (int64_t)((double)m * w / S);
+    const int64_t b = std::lower_bound(bin_edge.begin(), bin_edge.end() - 1, target) - bin_edge.begin();
+    if (b > wb.back() && b < nbins) wb.push_back(b);
+  }
+  wb.push_back(nbins);
   return wb;
+}
+
+cudaError_t pb_bin_edges(const DevGraph& g, int shift, cudaStream_t st, std::vector<int64_t>* out) {
+  const int64_t nbins = ((int64_t)g.n + (1ll << shift) - 1) >> shift;
+  std::vector<int64_t> be(nbins + 1);
+  int64_t* d_be = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_be, (nbins + 1) * sizeof(int64_t), st);
+  if (e == cudaSuccess) {
+    pb_bin_edges_kernel<<<(unsigned)((nbins + 256) / 256), 256, 0, st>>>(g.row, g.n, shift, nbins, d_be);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(be.data(), d_be, (nbins + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d_be) cudaFreeAsync(d_be, st);
+  if (e == cudaSuccess) *out = std::move(be);
+  return e;
 }
 
 cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** out) {
@@ -461,7 +487,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
   }
   const int sms = sm_count();
   PbPlan plan;
-  plan.wave_bin = pb_wave_bins(pb.nbins, S);
+  plan.wave_bin = pb_wave_bins(pb.bin_edge, S);
   plan.nwaves = (int)plan.wave_bin.size() - 1;
   const int W = plan.nwaves;
   const int64_t nbins = pb.nbins, nchunks = pb.nchunks, nseg = nbins * nchunks;
@@ -595,18 +621,9 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   PK(alloc((void**)&pb.dstl_bm, (m + 8) * sizeof(uint16_t)));
   PK(alloc((void**)&pb.val, (m + 8) * sizeof(double)));
   {
-    // bin edge offsets (host copy: each wave plan cuts its phase-2 units)
-    std::vector<int64_t> be(nbins + 1);
-    int64_t* d_be = nullptr;
-    e = cudaMallocAsync(&d_be, (nbins + 1) * sizeof(int64_t), st);
-    if (e == cudaSuccess) {
-      pb_bin_edges_kernel<<<(unsigned)((nbins + 256) / 256), 256, 0, st>>>(g.row, g.n, shift, nbins, d_be);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(be.data(), d_be, (nbins + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (d_be) cudaFreeAsync(d_be, st);
+    // bin edge offsets (host copy: wave plans cut waves and phase-2 units)
+    std::vector<int64_t> be;
+    e = pb_bin_edges(g, shift, st, &be);
     if (e != cudaSuccess) goto out;
     pb.bin_edge = be;
     for (int64_t b = 0; b < nbins; ++b)

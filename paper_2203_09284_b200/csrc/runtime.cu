@@ -930,8 +930,13 @@ int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t*
     int shift = 0, chunk_shift = 0;
     pb_geometry(&shift, &chunk_shift);
     if (shift < 5 || shift > 14) return fail(FPR_B200_EINVAL, "fpr_b200 propagation-blocked layout: bin/chunk geometry out of range");
-    const int64_t nbins = ((int64_t)h->g.n + (1ll << shift) - 1) >> shift;
-    for (int64_t b : pb_wave_bins(nbins, wave_count ? wave_count : lockstep_waves(h)))
+    std::vector<int64_t> be;
+    if (h->pb && h->pb->shift == shift) {
+      be = h->pb->bin_edge;
+    } else {
+      CK(pb_bin_edges(h->g, shift, h->stream, &be));
+    }
+    for (int64_t b : pb_wave_bins(be, wave_count ? wave_count : lockstep_waves(h)))
       vs.push_back((uint64_t)std::min<int64_t>(h->g.n, b << shift));
   } else {
     const Waves* wv = nullptr;
