@@ -6,6 +6,6 @@ for c in $cfgs; do
   for v in "$@"; do
     if [ "$v" = main ]; then lib=""; else lib=paper_2203_09284_b200/csrc/build/libfpr_b200_$v.so; fi
     echo "== $v cfg$c"
-    FPR_B200_LIB=$lib GEOMS=${GEOMS:-13:23} PB_ONLY=1 timeout -s KILL 300 python scripts/pb_probe.py $c 2>&1 | grep -v "^$" | sed 's/; per-iter.*//' | tail -2
+    FPR_B200_LIB=$lib GEOMS=${GEOMS:-13:21} PB_ONLY=1 timeout -s KILL 300 python scripts/pb_probe.py $c 2>&1 | grep -v "^$" | sed 's/; per-iter.*//' | tail -2
   done
 done

@@ -4,6 +4,6 @@ cfgs="$1"; shift
 for c in $cfgs; do
   for envs in "$@"; do
     echo "== [$envs] cfg$c"
-    env $envs GEOMS=${GEOMS:-13:23} PB_ONLY=1 timeout -s KILL 300 python scripts/pb_probe.py $c 2>&1 | grep -v "^$" | sed 's/; per-iter.*//' | tail -1
+    env $envs GEOMS=${GEOMS:-13:21} PB_ONLY=1 timeout -s KILL 300 python scripts/pb_probe.py $c 2>&1 | grep -v "^$" | sed 's/; per-iter.*//' | tail -1
   done
 done

@@ -20,7 +20,7 @@ def make(c, **kw):
 
 
 def main():
-    geoms = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("GEOMS", "13:23").split(",")]
+    geoms = [tuple(int(v) for v in x.split(":")) for x in os.environ.get("GEOMS", "13:21").split(",")]
     for c in (sys.argv[1:] or ["2", "4", "5"]):
         reorder = c.endswith("r")
         plain = None
