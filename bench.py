@@ -1,21 +1,28 @@
 #!/usr/bin/env python
 """FusEd-PageRank B200 benchmark (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], "config 2"): uniform G(n,m), n = 2^22,
-2^26 draws of testutil::random_sparse(seed 2) semantics, normalised by
-build_csr -> m = 67,108,723; fp64 ranks, d = 0.85, threshold 1e-10 on the
-reference's L-inf delta.  The graph is generated ON THE DEVICE (K5 + K4,
-bit-identical to the reference's CSR; untimed setup).
+Headline workload (BASELINE.json configs[4], "config 5", the largest graph
+that fits one GPU): R-MAT scale 28, edge factor 16, a/b/c/d = .57/.19/.19/.05,
+seed 5, normalised by build_csr -> n = 2^28, m = 4,259,432,546; fp64 ranks,
+d = 0.85, threshold 1e-10 on the reference's L-inf delta.  The graph is
+generated ON THE DEVICE (K5 + K4, bit-identical to the reference's
+generate_rmat + build_csr by construction; pinned by digests up to scale 24).
 
-One step = one full ec_b200 solve to convergence (time-to-converge; 7
-iterations).  value = GTEPS = m * iterations / step time, with the graph
-resident in HBM.  e2e = the same metric through the reference-facing C-ABI
-call fpr_b200_pagerank() on PINNED HOST u64 CSR arrays (fpr::Graph layout):
-H2D + narrowing + partition + solve + D2H of ranks and error trace, all timed.
+One step = one full ec_b200 solve to convergence on the sweep the library
+picks by default (propagation-blocked on this graph) -- the
+time-to-converge, 54 iterations.  value = GTEPS/iter = m * iterations / step
+time, graph resident in HBM (inputs far larger than L2: no flush needed).
+e2e = the same metric through the reference-facing C-ABI call
+fpr_b200_pagerank() on PINNED HOST u64 CSR arrays (the fpr::Graph layout, 38
+GB): H2D + narrowing + the one-time sweep layout + solve + D2H of ranks and
+error trace, all timed.
 
 --impl reference: the reference's own CPU engine (oracle/_ref, compiled from
-the unmodified headers), pagerank_ec_par with every host thread, one
-iteration per step (a bounded sample of the same workload).
+the unmodified headers), fpr::pagerank_ec_par with every host thread, on the
+same config-5 graph.  A full reference solve takes ~23 minutes on the GPU
+box's 16 cores (54 iterations x ~25 s), so its step is a bounded sample: one
+pagerank_ec_par call of 3 iterations (per-iteration cost, GTEPS/iter);
+setup (graph hand-off + the reference's build_layout, ~3 min) is untimed.
 """
 from __future__ import annotations
 
@@ -25,7 +32,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -33,26 +39,50 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_CFG2 = 1 << 22
-DEG_CFG2 = 16
-SEED_CFG2 = 2
 THRESHOLD = 1e-10
 DAMPING = 0.85
-METRIC = "GTEPS/iter (EC PageRank to L-inf 1e-10, config 2)"
-WORKLOAD = "config2: uniform G(n=4194304, 2^26 draws, seed 2) -> build_csr, EC to L-inf 1e-10"
+METRIC = "GTEPS/iter (EC PageRank to L-inf 1e-10, time-to-converge)"
+
+WORKLOADS = {
+    "5": "config5: RMAT s28 ef16 (a,b,c,d)=(.57,.19,.19,.05) seed 5 -> build_csr, EC to L-inf 1e-10",
+    "2": "config2: uniform G(n=4194304, 2^26 draws, seed 2) -> build_csr, EC to L-inf 1e-10",
+    "1": "config1: RMAT s16 ef16 (a,b,c,d)=(.57,.19,.19,.05) seed 1 -> build_csr, EC to L-inf 1e-10",
+}
+REF_SAMPLE_ITERS = 3  # --impl reference: iterations in its one timed pagerank_ec_par call
+
+
+def make_graph(fb, config: str, device, stream=None, **kw):
+    if config == "1":
+        return fb.DeviceGraph.generate_rmat(fb.RmatParams(16, 16, seed=1), device=device, stream=stream, **kw)
+    if config == "2":
+        return fb.DeviceGraph.generate_uniform(1 << 22, 16, 2, device=device, stream=stream, **kw)
+    if config == "3":
+        return fb.DeviceGraph.generate_rmat(fb.RmatParams(24, 16, seed=3), relabel_bfs=True, device=device,
+                                            stream=stream, **kw)
+    if config == "4":
+        return fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, device=device, stream=stream, **kw)
+    return fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device, stream=stream, **kw)
 
 
 def algorithmic_bytes(n: int, m: int) -> int:
-    """Per iteration: 12 B/edge (int32 in_src + fp64 contrib gather) +
-    36 B/vertex (int64 row_ptr, pr read+write, int32 outdeg, contrib write)."""
+    """Per iteration: 12 B/edge (int32 in_src + fp64 contrib
+    gather) + 36 B/vertex (int64 row_ptr, pr read+write, int32 outdeg,
+    contrib write)."""
     return 12 * m + 36 * n
 
 
-def ncu_traffic(key: str, launches_per_step: int) -> float | None:
-    """DRAM read+write bytes per solve launch from the committed ncu capture."""
+def pb_stream_bytes(n: int, m: int) -> int:
+    """Per propagation-blocked sweep, what the two passes stream besides the
+    random gather: 4 B source + 8 B value written + 8 B value
+    read + 2 B inverse permutation + 2 B row key per edge, + 36 B/vertex."""
+    return 24 * m + 36 * n
+
+
+def ncu_traffic(key: str):
+    """DRAM read+write bytes per unit from the committed ncu capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return float(json.load(f)[key]["dram_bytes_per_launch"])
+            return json.load(f).get(key)
     except Exception:
         return None
 
@@ -119,258 +149,204 @@ def dist_env():
     return ws, rank, local
 
 
-def reference_graph(ref):
-    """Config-2 graph built by the reference's own functions."""
-    n, s, d = ref.random_sparse(N_CFG2, DEG_CFG2, SEED_CFG2)
-    return ref.build_csr(n, s, d)
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------- reference arm
 def run_reference(args) -> None:
-    ws, rank, _ = dist_env()
+    """The unmodified reference (oracle/_ref) on the same workload: graph
+    handed over from the device generator (bit-identical arrays), the
+    reference's own build_layout in its graph handle (untimed), then ONE
+    timed pagerank_ec_par call of REF_SAMPLE_ITERS iterations on every host
+    thread (a full solve would take ~23 min on config 5)."""
+    ws, rank, local = dist_env()
     if rank != 0:
         return
-    from oracle import Oracle, load_reference
+    from oracle import Graph as OGraph
+    from oracle import load_reference
 
     ref = load_reference()
-    threads = os.cpu_count() or 1
-    if ref is not None:
-        kind = "reference"
-        g = reference_graph(ref)
-        h = ref.graph_handle(g)
-        one = lambda: ref.run(g, "ec_par", DAMPING, THRESHOLD, 1, threads, handle=h).seconds  # noqa: E731
-        engine = "fpr::pagerank_ec_par (oracle/_ref, unmodified reference headers)"
-    else:  # reference not compiled on this box: the C restatement (single thread)
-        kind = "port"
-        o = Oracle()
-        n, s, d = o.random_sparse(N_CFG2, DEG_CFG2, SEED_CFG2)
-        g = o.build_csr(n, s, d)
-        threads = 1
+    threads = host_threads()
+    config = args.workload
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfpr_ref.so not built"}), flush=True)
+        return
+    t0 = time.perf_counter()
+    if config in ("1", "2"):  # small enough for the reference's own generators
+        n0, s, d = ref.generate_rmat(16, 16, seed=1) if config == "1" else ref.random_sparse(1 << 22, 16, 2)
+        og = ref.build_csr(n0, s, d)
+        del s, d
+    else:  # config 5: the device generator's arrays (the reference's would need ~175 GB and ~45 min)
+        import paper_2203_09284_b200 as fb
 
-        def one():
-            t0 = time.perf_counter()
-            o.pagerank_ec(g, DAMPING, THRESHOLD, 1)
-            return time.perf_counter() - t0
-        engine = "oracle/fpr_oracle.c fo_pagerank_ec (C restatement, 1 thread)"
-    for _ in range(args.warmup):
-        one()
-    secs = [one() for _ in range(args.steps)]
-    t = float(sum(secs))
-    gteps = g.m * args.steps / t / 1e9
-    line = {"metric": METRIC, "value": gteps, "unit": "GTEPS",
-            "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_sparse seed 2)",
-            "config": {"workload": WORKLOAD, "n": g.n, "m": g.m, "step": "1 EC iteration",
-                       "engine": engine},
-            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": kind,
-                             "sample": f"{args.steps} single-iteration ec_par calls on config 2"},
-            "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    if ref is not None:
+        with make_graph(fb, config, local, pb=False) as dg:
+            g = dg.download()
+        og = OGraph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+        del g
+    h = ref.graph_handle(og)  # copies into fpr::Graph + the reference's build_layout
+    n, m = og.n, og.m
+    del og  # the reference holds its own copy
+    setup_s = time.perf_counter() - t0
+    iters = REF_SAMPLE_ITERS if config == "5" else 10000
+    try:
+        r = ref.run(OGraph(n, m, None, None, None), "ec_par", DAMPING, THRESHOLD, iters, threads, handle=h)
+    finally:
         ref.destroy(h)
+    gteps = m * r.iterations / r.seconds / 1e9
+    sample = (f"one fpr::pagerank_ec_par call of {r.iterations} iterations on config 5, T={threads} "
+              f"(a full solve is 54 iterations, ~23 min on 16 cores)" if config == "5" else
+              f"one full fpr::pagerank_ec_par solve ({r.iterations} iterations), T={threads}")
+    data = ("synthetic (device-generated arrays, bit-identical to generate_rmat+build_csr)" if config == "5"
+            else "synthetic (the reference's own generator + build_csr)")
+    line = {"metric": METRIC, "value": gteps, "unit": "GTEPS", "impl": "reference", "n_gpus": ws,
+            "steps": 1, "warmup": 0, "requested_steps": args.steps, "requested_warmup": args.warmup,
+            "ms_per_step": 1e3 * r.seconds, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": data, "config": config_block(config, n, m),
+            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": "reference",
+                             "cpu": cpu_model(), "sample": sample, "setup_s_untimed": setup_s},
+            "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_leg(g_host, gpu_ranks=None, gpu_iters=None) -> dict:
-    """Rank 0, N=1: the reference's ec_par, all host threads, one full solve.
-    Its converged vector doubles as a live parity check of the GPU result."""
-    from oracle import Graph as OGraph
-    from oracle import Oracle, load_reference
-
-    ref = load_reference()
-    og = OGraph(g_host.n, g_host.m, g_host.in_start, g_host.in_src, g_host.out_degree)
-    if ref is not None:
-        threads = os.cpu_count() or 1
-        h = ref.graph_handle(og)
-        try:
-            r = ref.run(og, "ec_par", DAMPING, THRESHOLD, 10000, threads, handle=h)
-        finally:
-            ref.destroy(h)
-        out = {"value": og.m * r.iterations / r.seconds / 1e9, "unit": "GTEPS", "cores": threads,
-               "kind": "reference", "iterations": r.iterations, "seconds": r.seconds,
-               "sample": "1 full pagerank_ec_par solve of config 2 (oracle/_ref, -O3, T=nproc)"}
-        if gpu_ranks is not None:
-            out["parity"] = {"ec_b200_vs_reference_max_rel": float(np.max(np.abs(gpu_ranks - r.ranks) / r.ranks)),
-                             "iterations_equal": bool(gpu_iters == r.iterations), "tolerance": 1e-12}
-        return out
-    o = Oracle()
-    t0 = time.perf_counter()
-    r = o.pagerank_ec(og, DAMPING, THRESHOLD, 2)
-    dt = time.perf_counter() - t0
-    return {"value": og.m * r.iterations / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "port",
-            "iterations": r.iterations, "seconds": dt,
-            "sample": "2 EC iterations of config 2 with the C restatement (1 thread)"}
+def config_block(config: str, n: int, m: int) -> dict:
+    return {"workload": WORKLOADS[config], "n": n, "m": m, "threshold": THRESHOLD, "norm": "linf",
+            "damping": DAMPING, "step": "1 full EC solve (time-to-converge)",
+            "l2": {"5": "inputs larger than L2 (in_src 17 GB, contributions 2.1 GB); no flush",
+                   "2": "in_src 268 MB > L2; contributions L2-resident; no flush",
+                   "1": "L2-resident (correctness-sized config)"}[config]}
 
 
-def render_fixed(src, dst, width=7) -> np.ndarray:
-    """Bench input for the ingest leg: one "%0{width}d %0{width}d\\n" line per
-    edge (leading zeros are valid from_chars tokens, edge_list.hpp:25-30)."""
-    out = np.empty((len(src), 2 * width + 2), np.uint8)
-    for col, ids in ((0, src), (width + 1, dst)):
-        v = np.asarray(ids, dtype=np.uint64).copy()
-        for k in range(width - 1, -1, -1):
-            out[:, col + k] = (v % np.uint64(10)).astype(np.uint8) + 48
-            v //= np.uint64(10)
-    out[:, width] = 32
-    out[:, 2 * width + 1] = 10
-    return out.reshape(-1)
-
-
-def ingest_leg(fb, g, device) -> dict:
-    """§8(f) edge-list ingest: config 2's edges as text -> resident device CSR
-    through fpr_b200_graph_from_edge_list (pinned host text, H2D inside the
-    timed call), against the reference's parse_edge_list + build_csr on a
-    1/64 sample (single thread: the reference parser is sequential)."""
-    import torch
-
-    dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
-    text = render_fixed(g.in_src, dst)
-    pinned = torch.empty(len(text), dtype=torch.uint8, pin_memory=True)
-    pinned.numpy()[:] = text
-    buf = pinned.numpy()
-    fb.DeviceGraph.from_edge_list(buf, device=device).close()  # warm-up
-    times = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d = fb.DeviceGraph.from_edge_list(buf, device=device)
-        torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-        assert d.m == g.m
-        d.close()
-    dt = float(np.median(times))
-    out = {"workload": f"config-2 edges as '%07d %07d\\n' text ({len(text) / 1e9:.2f} GB, {g.m} lines)",
-           "api": "fpr_b200_graph_from_edge_list (pinned host text -> resident CSR; H2D timed)",
-           "ms": dt * 1e3, "medges_per_s": g.m / dt / 1e6, "text_gb_per_s": len(text) / dt / 1e9,
-           "h2d_bytes": int(len(text))}
+# ----------------------------------------------------------- CPU baselines
+def reference_engines(ref, og, threads, full=True, sample_iters=2, reps=2) -> dict:
+    """The reference's four engines (pagerank.hpp:128,156,195,261) on one
+    graph handle (build_layout excluded): time-to-converge as
+    the min over `reps` when `full`, else s/iter over a bounded
+    sample of `sample_iters` iterations."""
+    out = {}
+    h = ref.graph_handle(og)
     try:
-        from oracle import load_reference
-
-        ref = load_reference()
-        if ref is not None:
-            sample = text[: (len(text) // 64 // 16) * 16].tobytes()
-            t0 = time.perf_counter()
-            p = ref.parse_edge_list(sample)
-            ref.build_csr(p.n, p.edges[:, 0], p.edges[:, 1])
-            rdt = time.perf_counter() - t0
-            out["reference"] = {"medges_per_s": len(p.edges) / rdt / 1e6, "kind": "reference", "cores": 1,
-                                "sample": f"parse_edge_list + build_csr of the first {len(p.edges)} lines"}
-    except Exception as ex:  # reference arm is informative only
-        out["reference"] = {"unavailable": str(ex)}
+        for eng in ("ec_seq", "fused_seq", "ec_par", "fused_par"):
+            t = threads if eng.endswith("par") else 1
+            if full:
+                runs = [ref.run(og, eng, DAMPING, THRESHOLD, 10000, t, handle=h)
+                        for _ in range(reps if eng.endswith("par") else 1)]
+                best = min(runs, key=lambda x: x.seconds)
+                out[eng] = {"time_to_converge_s": best.seconds, "iterations": best.iterations, "threads": t,
+                            "reps": len(runs), "gteps": og.m * best.iterations / best.seconds / 1e9,
+                            "iterations_all_reps": [x.iterations for x in runs]}
+            else:
+                r = ref.run(og, eng, DAMPING, THRESHOLD, sample_iters, t, handle=h)
+                out[eng] = {"s_per_iter": r.seconds / r.iterations, "iterations_timed": r.iterations,
+                            "threads": t, "gteps": og.m * r.iterations / r.seconds / 1e9}
+    finally:
+        ref.destroy(h)
     return out
 
 
-def large_configs_leg(fb, device, which=("3", "4", "5", "5r")) -> dict:
-    """BASELINE configs 3-5 on one GPU, generated on the device (untimed):
-    EC and FusEd time-to-converge at L-inf 1e-10, ms per sweep, GTEPS and
-    the HBM-roofline fraction (12 m + 36 n bytes per sweep); on configs 4/5
-    also the propagation-blocked engines (FPR_B200_OPT_PB): EC, and the
-    lockstep FusEd schedule on PB sweeps (auto wave count).  Not the
-    headline metric; reported beside it.  Solve times are CUDA-event times
-    of the solve launches (resident graph)."""
+def cpu_baseline_leg(fb, device, g5, gpu_iter1) -> dict:
+    """Rank 0, N=1, on the GPU box's host cores.
+      * value: the oracle port's EC iteration on config 5 (fo_ec_step, the
+        reference's iteration in pull form, OpenMP over every host thread;
+        ~10-20 s), its result also a live parity check of the GPU's first
+        iterate;
+      * reference_engines: the unmodified reference (oracle/_ref) on config 2
+        (all four engines, full solves, min over repetitions) and config 3
+        (bounded: 2 iterations each; the full runs' iteration counts are in
+        tests/golden/config3.json);
+      * the reference on config 5 itself is the --impl reference arm."""
+    from oracle import Graph as OGraph
+    from oracle import Oracle, load_reference
+
+    threads = host_threads()
+    o = Oracle()
+    og5 = OGraph(g5.n, g5.m, g5.in_start, g5.in_src, g5.out_degree)
+    t0 = time.perf_counter()
+    nxt, err, _ = o.ec_step(og5, np.full(g5.n, 1.0 / g5.n), DAMPING)
+    dt = time.perf_counter() - t0
+    out = {"value": g5.m / dt / 1e9, "unit": "GTEPS", "cores": threads, "kind": "port", "cpu": cpu_model(),
+           "sample": "1 EC iteration of config 5 with the oracle port (fo_ec_step: scatter+gather of "
+                     "pagerank.hpp:137-140 in pull form, OpenMP over rows)",
+           "seconds": dt}
+    if gpu_iter1 is not None:
+        out["parity_iter1_max_rel"] = float(np.max(np.abs(gpu_iter1 - nxt) / nxt))
+    del nxt
+    ref = load_reference()
+    if ref is None:
+        out["reference_engines"] = {"unavailable": "oracle/_ref not built"}
+        return out
+    eng = {}
+    for config, full in (("2", True), ("3", False)):
+        with make_graph(fb, config, device, pb=False) as dg:
+            g = dg.download()
+        og = OGraph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+        eng["config" + config] = {"n": g.n, "m": g.m, "mode": "full solves" if full else "2-iteration samples",
+                                  **reference_engines(ref, og, threads, full=full)}
+        del g, og
+    eng["engine"] = "oracle/_ref: the unmodified reference headers, -O3 (reference Release flags), T = host threads"
+    out["reference_engines"] = eng
+    return out
+
+
+# ------------------------------------------------------------ secondary legs
+def secondary_legs(fb, device, peak) -> dict:
+    """Configs 2-4 (and config 5's FusEd), generated on the device (untimed):
+    EC and FusEd time-to-converge (CUDA-event solve times), ms per sweep,
+    GTEPS and the BASELINE roofline fraction, each on the sweep the library
+    picks by default.  Not the headline; reported beside it."""
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
-    peak, _ = peaks()
     out = {}
 
     def record(dg, r):
         ms_it = r.solve_ms / r.trace.iterations
         return {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
                 "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it, "gteps": dg.m / ms_it / 1e6,
-                "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak}
+                "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak,
+                "sweep": "pb" if r.sweep == fb.SWEEP_PB else "pull"}
 
-    for c in which:
-        if c == "3":
-            dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(24, 16, seed=3), relabel_bfs=True, device=device)
-            name = "config3: RMAT s24 ef16 seed 3, BFS crawl-order relabel"
-        elif c == "4":
-            dg = fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, device=device)
-            name = "config4: Chung-Lu n=2^26, 1.2e9 draws, alpha 2.1, seed 4, random order"
-        else:
-            dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device,
-                                              reorder=c.endswith("r"))
-            name = "config5: RMAT s28 ef16 seed 5" + (" + FPR_B200_OPT_REORDER" if c.endswith("r") else "")
-        with dg:
-            rec = {"workload": name, "n": dg.n, "m": dg.m}
-            for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED, "fused")):
+    names = {"2": "config2: uniform G(n=2^22, 2^26 draws, seed 2)",
+             "3": "config3: RMAT s24 ef16 seed 3, BFS crawl-order relabel",
+             "4": "config4: Chung-Lu n=2^26, 1.2e9 draws, alpha 2.1, seed 4, random order"}
+    for c in ("2", "3", "4"):
+        with make_graph(fb, c, device) as dg:
+            rec = {"workload": names[c], "n": dg.n, "m": dg.m}
+            for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED, "fused"),
+                             (fb.ENGINE_FUSED_LOCKSTEP, "lockstep")):
+                dg.run(eng, cfg, copy_ranks=False, copy_trace=False)  # one-time layouts / wave plans
                 rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
+            if c == "2":
+                # BASELINE words the stop rule as an L1 delta; same graph, L1 rule
+                with make_graph(fb, c, device, norm=fb.NORM_L1) as d1:
+                    r1 = d1.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
+                    rec["ec_l1_stop_rule"] = {"iterations": r1.trace.iterations, "time_to_converge_ms": r1.solve_ms}
             out["config" + c] = rec
-        if c != "3":
-            # FPR_B200_OPT_PB (propagation-blocked EC, DESIGN.md §3.4) on a
-            # second handle; its one-time layout build is outside solve_ms
-            if c == "4":
-                dg = fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, device=device, pb=True)
-            else:
-                dg = fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), device=device,
-                                                  reorder=c.endswith("r"), pb=True)
-            with dg:
-                one = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1)
-                for eng, tag in ((fb.ENGINE_EC, "ec_pb"), (fb.ENGINE_FUSED_LOCKSTEP, "lockstep_pb")):
-                    first = dg.run(eng, one, copy_ranks=False, copy_trace=False)  # builds the layout / wave plan
-                    rec[tag] = record(dg, dg.run(eng, cfg, copy_ranks=False, copy_trace=False))
-                    # one-time device setup on this handle (EC: the PB layout; lockstep: its wave plan)
-                    rec[tag]["setup_ms_first_run"] = first.setup_ms
-                    # the PB sweep's own streamed bytes (DESIGN.md §3.4): 22 B per edge
-                    # (source, value written and read back, row offset) + 36 B per vertex
-                    ms_it = rec[tag]["ms_per_sweep"]
-                    rec[tag]["pb_stream_bytes_frac"] = (22 * dg.m + 36 * dg.n) / (ms_it * 1e-3) / 1e9 / peak
-                rec["lockstep_pb"]["waves"] = len(dg.wave_starts()) - 1
     return out
 
 
-def build_csr_leg(fb, g, device) -> dict:
-    """Graph loading (§8(a) a12): fpr::build_csr(EdgeSet) of config 2's edges
-    (pinned host u64 src/dst, H2D + narrowing + device sort/dedup/scan timed)
-    through fpr_b200_graph_from_edges, against the reference's build_csr on a
-    1/16 sample of the same edges (single thread, as the reference runs)."""
-    import torch
-
-    dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
-    ts = torch.empty(g.m, dtype=torch.int64, pin_memory=True)
-    td = torch.empty(g.m, dtype=torch.int64, pin_memory=True)
-    s, d = ts.numpy().view(np.uint64), td.numpy().view(np.uint64)
-    s[:] = g.in_src
-    d[:] = dst
-    fb.DeviceGraph.from_edges(g.n, s, d, device=device).close()  # warm-up
-    times = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dg = fb.DeviceGraph.from_edges(g.n, s, d, device=device)
-        torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-        assert dg.m == g.m
-        dg.close()
-    dt = float(np.median(times))
-    out = {"workload": f"config-2 edges as an EdgeSet (n={g.n}, {g.m} edges)",
-           "api": "fpr_b200_graph_from_edges (pinned host u64 src/dst -> resident CSR + partition)",
-           "ms": dt * 1e3, "medges_per_s": g.m / dt / 1e6, "h2d_bytes": int(16 * g.m)}
-    try:
-        from oracle import load_reference
-
-        ref = load_reference()
-        if ref is not None:
-            k = g.m // 16
-            rng = np.random.default_rng(0)
-            pick = np.sort(rng.choice(g.m, size=k, replace=False))
-            t0 = time.perf_counter()
-            ref.build_csr(g.n, s[pick].copy(), d[pick].copy())
-            rdt = time.perf_counter() - t0
-            out["reference"] = {"medges_per_s": k / rdt / 1e6, "kind": "reference", "cores": 1,
-                                "sample": f"build_csr of a random 1/16 of the edges ({k}), n = {g.n}"}
-    except Exception as ex:
-        out["reference"] = {"unavailable": str(ex)}
-    return out
-
-
+# ------------------------------------------------------------------ main arm
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="5", choices=sorted(WORKLOADS), help="headline graph (default config 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-ingest", action="store_true")
-    ap.add_argument("--no-large", action="store_true", help="skip configs 3-5 (about 1 min)")
+    ap.add_argument("--no-large", action="store_true", help="skip the secondary configs 2-4 legs")
     ap.add_argument("--copy-exchange", action="store_true",
                     help="N>1: NCCL all-gather of slices instead of the fused P2P-store exchange")
     ap.add_argument("--partitioned", action="store_true",
@@ -387,175 +363,188 @@ def main() -> None:
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist = None
     if ws > 1 or args.partitioned:
-        import os as _os
-
         import torch.distributed as dist
 
         if ws == 1:
-            _os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            _os.environ.setdefault("MASTER_PORT", "29531")
-            _os.environ.setdefault("RANK", "0")
-            _os.environ.setdefault("WORLD_SIZE", "1")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         run_multi(args, fb, dist, ws, rank, local)
         dist.destroy_process_group()
         return
     stream = torch.cuda.current_stream()
     sptr = fb.torch_stream_handle()
+    peak, peak_kind = peaks()
 
-    dg = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
+    dg = make_graph(fb, args.workload, local, stream=sptr)
     n, m = dg.n, dg.m
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
 
     def step():
         return dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
 
-    for _ in range(args.warmup):
+    t_first = time.perf_counter()
+    first = step()  # builds the sweep's one-time layout (propagation blocking on config 5)
+    torch.cuda.synchronize()
+    first_s = time.perf_counter() - t_first
+    for _ in range(args.warmup - 1):
         r = step()
-    iters = r.trace.iterations
-    launches_per_step = r.kernel_launches
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
+    iters = first.trace.iterations
+    launches_per_step = first.kernel_launches
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kernel_ms = []
     with ClockSampler(local) as clk:
-        barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             r = step()
             kernel_ms.append(r.solve_ms)
             assert r.trace.iterations == iters
         ev1.record(stream)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = ws * m * iters / (ms_step * 1e-3) / 1e9
-    kms = float(np.mean(kernel_ms))
-    peak, peak_kind = peaks()
-    achieved = algorithmic_bytes(n, m) * iters / (kms * 1e-3) / 1e9
+        torch.cuda.synchronize()
+    ms_step = ev0.elapsed_time(ev1) / args.steps
+    value = m * iters / (ms_step * 1e-3) / 1e9
+    kms = float(np.mean(kernel_ms))  # CUDA-event time of the sweeps (the library's stream = torch's)
+    sweep_ms = kms / iters
+    achieved = algorithmic_bytes(n, m) / (sweep_ms * 1e-3) / 1e9
+    pb = r.sweep == fb.SWEEP_PB
 
-    # Per-iteration device times of the persistent kernel (globaltimer).
-    tr = dg.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=True)
-    it_us = (tr.trace.iter_ns.astype(np.float64) / 1e3).tolist()
+    # per-iteration device times and trace of one more solve
+    tr = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True, copy_trace=True)
+    it_ms = (tr.trace.iter_ns.astype(np.float64) / 1e6).tolist()
+    # FusEd on the same resident graph (the library's FUSED choice: the
+    # lockstep Gauss-Seidel schedule on PB sweeps here)
+    fr = dg.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False)
+    fr = dg.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False)
+    fused = {"iterations": fr.trace.iterations, "time_to_converge_ms": fr.solve_ms,
+             "ms_per_sweep": fr.solve_ms / fr.trace.iterations, "sweep": "pb" if fr.sweep == fb.SWEEP_PB else "pull",
+             "schedule": "wave-lockstep Gauss-Seidel" if fr.sweep == fb.SWEEP_PB else "block-asynchronous",
+             "waves": int(len(dg.wave_starts()) - 1)}
+    # the pull sweep on the same graph, for comparison (forced)
+    pull = None
+    if not args.no_large and args.workload == "5":
+        with make_graph(fb, args.workload, local, stream=sptr, pb=False) as dp:
+            rp = dp.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
+            pull = {"iterations": rp.trace.iterations, "time_to_converge_ms": rp.solve_ms,
+                    "ms_per_sweep": rp.solve_ms / rp.trace.iterations,
+                    "roofline_frac": algorithmic_bytes(n, m) / (rp.solve_ms / rp.trace.iterations * 1e-3) / 1e9 / peak}
 
-    # FusEd (block-async) on the same resident graph.
-    fused = {}
-    fr = [dg.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False) for _ in range(max(3, args.steps // 4))]
-    fused = {"engine": "fused_b200", "iterations": fr[-1].trace.iterations,
-             "roofline_frac": algorithmic_bytes(n, m) * fr[-1].trace.iterations
-             / (float(np.mean([x.solve_ms for x in fr])) * 1e-3) / 1e9 / peaks()[0],
-             "iterations_min_max": [min(x.trace.iterations for x in fr), max(x.trace.iterations for x in fr)],
-             "ms_per_solve": float(np.mean([x.solve_ms for x in fr])),
-             "gteps": float(np.mean([m * x.trace.iterations / x.solve_ms / 1e6 for x in fr]))}
-    lr = dg.run(fb.ENGINE_FUSED_LOCKSTEP, cfg, copy_ranks=False, copy_trace=False)
-    fused["lockstep"] = {"iterations": lr.trace.iterations, "ms_per_solve": lr.solve_ms,
-                         "waves": int(len(dg.wave_starts()) - 1)}
-
-    # BASELINE.json words the stop rule as an L1 delta; the reference stops on
-    # L-inf (the headline).  Same graph, L1 rule, reported beside it.
-    l1_stop = {}
-    with fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr,
-                                         norm=fb.NORM_L1) as dl1:
-        for eng, tag in ((fb.ENGINE_EC, "ec"), (fb.ENGINE_FUSED_LOCKSTEP, "fused_lockstep"),
-                         (fb.ENGINE_FUSED, "fused")):
-            dl1.run(eng, cfg, copy_ranks=False, copy_trace=False)
-            r1 = dl1.run(eng, cfg, copy_ranks=False, copy_trace=False)
-            l1_stop[tag] = {"iterations": r1.trace.iterations, "time_to_converge_ms": r1.solve_ms,
-                            "converged": bool(r1.trace.converged)}
     g_host = None
     e2e = None
-    if not args.no_e2e:
-        g_host = dg.download()
-        e2e = e2e_leg(fb, g_host, local, args, iters)
-    ingest = None
-    if rank == 0 and ws == 1 and not args.no_ingest:
-        if g_host is None:
-            g_host = dg.download()
-        ingest = ingest_leg(fb, g_host, local)
-    csr = None
-    if rank == 0 and ws == 1 and not args.no_ingest:
-        if g_host is None:
-            g_host = dg.download()
-        csr = build_csr_leg(fb, g_host, local)
-    large = None
-    if rank == 0 and ws == 1 and not args.no_large:
-        large = large_configs_leg(fb, local)
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        if g_host is None:
-            g_host = dg.download()
-        final = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True, copy_trace=False)
-        cpu = cpu_baseline_leg(g_host, final.ranks.values, final.trace.iterations)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "GTEPS",
-            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            # config 2 at every N: total work fixed (N > 1 partitions it, run_multi)
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
-            "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
-                       "norm": "linf", "step": "1 full EC solve (time-to-converge)",
-                       "parallelism": "single-gpu",
-                       "l2": "inputs larger than L2 (in_src 268 MB + contrib 33.5 MB + row_ptr 33.5 MB); no flush"},
-            "time_to_converge_ms": ms_step,
-            "iteration_us": it_us,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("config2_ec", 1), "peak_kind": peak_kind,
-                         "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
-                         # the random-fetch ceiling measured by bench_micro/gather_bench.cu (an
-                         # L2-side request limit): the kernel's real bound on config 2
-                         "gather_ceiling_gteps": 270.0,
-                         "gather_ceiling_frac": m * iters / (kms * 1e-3) / 1e9 / 270.0,
-                         "kernel": "solve_kernel<false> (persistent EC, all iterations)",
-                         "kernel_ms": kms,
-                         "algorithmic_bytes_per_launch": algorithmic_bytes(n, m) * iters},
-            "fused": fused,
-            "l1_stop_rule": l1_stop,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "ingest": ingest,
-            "build_csr": csr,
-            "configs_3_5": large,
-            "gpu_launches": int(launches_per_step * args.steps),
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line), flush=True)
+    keep = None
+    if not args.no_e2e or not args.no_cpu_baseline:
+        keep = pinned_csr(torch, n, m)
+        dg.download_into(*(k[1] for k in keep))
+        g_host = fb.Graph(n, m, keep[0][1], keep[1][1], keep[2][1])
+    gpu_iter1 = None
+    if not args.no_cpu_baseline:
+        gpu_iter1 = dg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD, max_iterations=1),
+                           copy_ranks=True, copy_trace=False).ranks.values
     dg.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    if not args.no_e2e:
+        e2e = e2e_leg(fb, g_host, local, args, iters)
+    large = None if args.no_large else secondary_legs(fb, local, peak)
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(fb, local, g_host, gpu_iter1)
+
+    traffic = ncu_traffic("config5_ec_pb_sweep" if pb else "config5_ec_pull_sweep")
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated, bit-identical to reference generate_rmat+build_csr)",
+        "config": config_block(args.workload, n, m),  # the reference arm prints the same block
+        "iterations": iters, "parallelism": "single-gpu",
+        "sweep": "propagation-blocked (the library's default for this graph)" if pb else "pull (library default)",
+        "time_to_converge_ms": ms_step,
+        "first_solve_s_with_layout_build": first_s,
+        "iteration_ms": it_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic.get("dram_bytes_per_sweep") if traffic else None, "peak_kind": peak_kind,
+                     "unit_of_work": "one EC sweep (the PB gather + accumulate + reduce launches) = one iteration",
+                     "algorithmic_bytes_per_sweep": algorithmic_bytes(n, m),
+                     "sweep_ms": sweep_ms,
+                     "pb_stream_bytes_frac": pb_stream_bytes(n, m) / (sweep_ms * 1e-3) / 1e9 / peak if pb else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     "kernel_shares": traffic.get("kernel_shares") if traffic else None},
+        "fused": fused,
+        "ec_pull_sweep": pull,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "configs_2_4": large,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
 
 
+def pinned_csr(torch, n, m):
+    def pinned(k):
+        t = torch.empty(k, dtype=torch.int64, pin_memory=True)
+        return t, t.numpy().view(np.uint64)
+
+    return [pinned(n + 1), pinned(max(m, 1)), pinned(n)]
+
+
+def e2e_leg(fb, g, device, args, iters) -> dict:
+    """fpr_b200_pagerank() on pinned host fpr::Graph arrays (u64); H2D +
+    narrowing + partition + the one-time sweep layout + solve + D2H of ranks
+    and error trace, all inside the timed call."""
+    import torch
+
+    ranks_t = torch.empty(g.n, dtype=torch.float64, pin_memory=True)
+    errs_t = torch.empty(10000, dtype=torch.float64, pin_memory=True)
+    view = fb._GraphView(g.n, g.m, g.in_start.ctypes.data, g.in_src.ctypes.data, g.out_degree.ctypes.data)
+    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)._c()
+    opts = fb._options(device=device, stream=fb.torch_stream_handle())
+    res = fb._Result()
+    L = fb.lib()
+
+    def call():
+        fb._check(L.fpr_b200_pagerank(C.byref(view), fb.ENGINE_EC, C.byref(cfg), C.byref(opts),
+                                      ranks_t.data_ptr(), errs_t.data_ptr(), 10000, C.byref(res)))
+
+    call()
+    steps = max(2, min(args.steps, 3))
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    assert res.iterations == iters
+    h2d = 8 * (g.n + 1) + 8 * g.m + 8 * g.n
+    d2h = 8 * g.n + 8 * int(res.iterations)
+    return {"value": g.m * res.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "sweep": "pb" if res.sweep == fb.SWEEP_PB else "pull",
+            "api": "fpr_b200_pagerank (C ABI, pinned host u64 CSR; sweep layout built inside every call)"}
+
+
+# ------------------------------------------------------------------ N GPUs
 def run_multi(args, fb, dist, ws, rank, local) -> None:
-    """N GPUs: destination-range partition of config 2 (strong scaling), one
-    NCCL all-gather of contribution slices + one residual all-gather per
-    iteration (paper_2203_09284_b200/dist.py)."""
+    """N GPUs: destination-range partition of the headline graph (strong
+    scaling), one residual all-gather per iteration, contributions exchanged
+    by the sweep's own P2P stores (paper_2203_09284_b200/dist.py)."""
     import torch
 
     from paper_2203_09284_b200.dist import B200Part, PartitionedSolver, TorchExchange
 
     sptr = fb.torch_stream_handle()
-    full = fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local, stream=sptr)
+    full = make_graph(fb, args.workload, local, stream=sptr, pb=False)
     n, m = full.n, full.m
     part = B200Part(full, ws, rank, device=local, stream=sptr)
     full.close()
     ex = TorchExchange()
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     dev = f"cuda:{local}"
-    # fused exchange: the sweep stores its slice into the peers' replicas
-    # (CUDA IPC / NVLink P2P); NCCL carries only the 16-B residual pair
-    # Speculation costs one extra sweep per solve and saves a host round trip
-    # per iteration: a win once the sweep is short (N > 1), a loss at N = 1.
     solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1,
                                speculate=ws > 1)
     for _ in range(args.warmup):
@@ -580,127 +569,34 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
     fr = solver.solve(fb.ENGINE_FUSED, cfg, want_ranks=False)
-    e2e = None
-    if not args.no_e2e:
-        e2e = e2e_multi(args, fb, dist, solver, cfg, dev, local, iters)
     exchange = ("fused: sweep epilogue P2P-stores each slice into the peers' replicas (CUDA IPC over NVLink); "
                 "NCCL all-gather of the 16-B residual pair" if solver.fused_exchange else
                 "NCCL all-gather of contribution slices + residual pair")
+    peak, _ = peaks()
+    sweep_ms = ms_step / iters
     if rank == 0:
         line = {
-            "metric": METRIC,
-            "value": m * iters / (ms_step * 1e-3) / 1e9, "unit": "GTEPS", "n_gpus": ws,
+            "metric": METRIC, "value": m * iters / (ms_step * 1e-3) / 1e9, "unit": "GTEPS", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device-generated, bit-identical to reference random_sparse+build_csr)",
-            "config": {"workload": WORKLOAD, "n": n, "m": m, "iterations": iters, "threshold": THRESHOLD,
-                       "norm": "linf", "step": "1 full EC solve (time-to-converge)",
-                       "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
-                       "host_loop": ("speculative: sweep k+1 enqueued before iteration k's residual is read"
-                                     if ws > 1 else "synchronous"),
-                       "exchange_fallback": solver.fallback,
-                       "slice": part.slice, "l2": "inputs larger than L2; no flush"},
+            "data": "synthetic (device-generated, bit-identical to reference generate_rmat+build_csr)",
+            "config": config_block(args.workload, n, m),
+            "iterations": iters, "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
+            "sweep": "pull (per part)",
+            "host_loop": ("speculative: sweep k+1 enqueued before iteration k's residual is read"
+                          if ws > 1 else "synchronous"),
+            "exchange_fallback": solver.fallback, "slice": part.slice,
             "time_to_converge_ms": ms_step,
-            "fused": {"engine": "fused_b200", "iterations": fr.iterations},
-            "roofline": None, "cpu_baseline": None, "e2e": e2e,
+            "fused": {"iterations": fr.iterations},
+            "roofline": {"bound": "hbm", "achieved": algorithmic_bytes(n, m) / ws / (sweep_ms * 1e-3) / 1e9,
+                         "peak": peak, "unit": "GB/s (per GPU)",
+                         "frac": algorithmic_bytes(n, m) / ws / (sweep_ms * 1e-3) / 1e9 / peak, "traffic": None},
+            "cpu_baseline": None, "e2e": None,
             "gpu_launches": int(args.steps * iters), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     solver.close()
     part.close()
-
-
-def e2e_multi(args, fb, dist, solver, cfg, dev, local, iters) -> dict:
-    """N GPUs end to end through the public API: every rank uploads only its
-    own rows of the pinned host CSR (fpr_b200_part_create), solves with the
-    partitioned driver and downloads its rank slice.  Max over ranks."""
-    import torch
-
-    from paper_2203_09284_b200.dist import B200Part
-
-    g = None
-    with fb.DeviceGraph.generate_uniform(N_CFG2, DEG_CFG2, SEED_CFG2, device=local,
-                                         stream=fb.torch_stream_handle()) as dg:
-        g = dg.download()
-
-    def pinned(a):
-        t = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
-        v = t.numpy().view(np.uint64)
-        v[:] = a
-        return t, v
-
-    keep = [pinned(g.in_start), pinned(g.in_src), pinned(g.out_degree)]
-    hg = fb.Graph(g.n, g.m, keep[0][1], keep[1][1], keep[2][1])
-    ws, rank = dist.get_world_size(), dist.get_rank()
-
-    ranks_host = torch.empty(g.n, dtype=torch.float64, pin_memory=True).numpy()  # >= any part's rows
-
-    def call():
-        # each rank uploads only its own rows (fpr_b200_part_create)
-        p = B200Part.from_view(hg, ws, rank, device=local, stream=fb.torch_stream_handle())
-        old = solver.local
-        solver.rebind(p)  # exchange buffers / peer replicas are persistent state
-        r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=True, ranks_out=ranks_host)
-        solver.rebind(old)
-        p.close()
-        return r
-
-    call()
-    steps = max(3, min(args.steps, 10))
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        r = call()
-    torch.cuda.synchronize()
-    t = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item())
-    h2d = 8 * (g.n + 1) + 8 * g.m + 8 * g.n
-    d2h = 8 * len(r.ranks) + 16 * ws * r.iterations
-    return {"value": g.m * r.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
-            "api": "fpr_b200_part_create + fpr_b200_part_* (pinned host u64 CSR, each rank uploads its rows)"}
-
-
-def e2e_leg(fb, g, device, args, iters) -> dict:
-    """fpr_b200_pagerank() on pinned host fpr::Graph arrays; H2D + solve + D2H timed."""
-    import torch
-
-    def pinned(a):
-        t = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
-        v = t.numpy().view(np.uint64)
-        v[:] = a
-        return t, v
-
-    keep = [pinned(g.in_start), pinned(g.in_src), pinned(g.out_degree)]
-    ins, src, od = (k[1] for k in keep)
-    ranks_t = torch.empty(g.n, dtype=torch.float64, pin_memory=True)
-    errs_t = torch.empty(10000, dtype=torch.float64, pin_memory=True)
-    view = fb._GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data, od.ctypes.data)
-    cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)._c()
-    opts = fb._options(device=device, stream=fb.torch_stream_handle())
-    res = fb._Result()
-    L = fb.lib()
-
-    def call():
-        fb._check(L.fpr_b200_pagerank(C.byref(view), fb.ENGINE_EC, C.byref(cfg), C.byref(opts),
-                                      ranks_t.data_ptr(), errs_t.data_ptr(), 10000, C.byref(res)))
-
-    for _ in range(2):
-        call()
-    steps = max(3, min(args.steps, 20))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        call()
-    dt = (time.perf_counter() - t0) / steps
-    assert res.iterations == iters
-    h2d = 8 * (g.n + 1) + 8 * g.m + 8 * g.n
-    d2h = 8 * g.n + 8 * int(res.iterations)
-    return {"value": g.m * res.iterations / dt / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
-            "api": "fpr_b200_pagerank (C ABI, pinned host u64 CSR)"}
 
 
 if __name__ == "__main__":

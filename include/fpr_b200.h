@@ -93,19 +93,20 @@ typedef struct fpr_config {
                                   order's locality; ranks and
                                   traces in the caller's ids.  OPT_REORDER wins if
                                   both are set */
-#define FPR_B200_OPT_BLOCKED 2u /* EC engine: source-blocked sweeps (column blocks of
-                                  2^24 vertices, FPR_B200_BLOCK_SHIFT overrides) so the
-                                  gathers of a block pass stay near L2; only for graphs
-                                  whose contribution vector far exceeds L2 (configs 4/5
-                                  in natural order) */
+/* Sweep kind.  By default the library picks it when the graph is created:
+ * propagation-blocked sweeps (below) when the contribution vector (8 n bytes)
+ * exceeds twice the device's L2 -- configs 4/5, where the pull gathers miss L2
+ * -- and the pull sweep otherwise.  The two flags force one kind. */
 #define FPR_B200_OPT_PB 4u      /* EC and lockstep engines: propagation-blocked sweeps
                                   (bins of 2^13 rows, source chunks of 2^21;
                                   FPR_B200_PB_SHIFT / FPR_B200_PB_CHUNK_SHIFT override):
                                   two streaming passes instead of the random pull
-                                  gather, for graphs whose contribution vector far
-                                  exceeds L2.  Lockstep waves are then
-                                  runs of whole bins (fpr_b200_graph_wave_starts reports
-                                  them).  Takes precedence over OPT_BLOCKED */
+                                  gather; row sums are exact
+                                  fixed-point sums of fixed run partials, so runs are
+                                  bit-reproducible.  Lockstep waves are then runs of
+                                  whole bins (fpr_b200_graph_wave_starts reports
+                                  them); FUSED runs that lockstep schedule too */
+#define FPR_B200_OPT_PULL 16u   /* pull sweeps on every graph (no propagation blocking) */
 
 typedef struct fpr_b200_options {
   int32_t device;       /* CUDA ordinal; -1 = current device */
@@ -113,12 +114,18 @@ typedef struct fpr_b200_options {
   uint32_t wave_count;  /* lockstep engine: waves per sweep (0 = auto) */
   uint32_t flags;       /* FPR_B200_OPT_* */
   void* stream;         /* cudaStream_t to run on; NULL = library stream */
+  const int32_t* devices; /* multi-device solve: CUDA ordinal of each part (NULL = single device) */
+  uint32_t ndevices;    /* number of parts; > 1 selects the multi-device path (fpr_b200_mgpu_*) */
+  uint32_t reserved0;
 } fpr_b200_options;
+
+#define FPR_B200_SWEEP_PULL 0 /* fpr_b200_result.sweep: the pull sweep ran */
+#define FPR_B200_SWEEP_PB 1   /* propagation-blocked sweeps ran */
 
 typedef struct fpr_b200_result {
   uint64_t iterations;      /* == errors written (trace.iterations) */
   int32_t converged;        /* last error <= threshold (detail::finish) */
-  int32_t reserved0;
+  int32_t sweep;            /* FPR_B200_SWEEP_* actually used */
   double final_error;       /* last error, 1.0 if none (RankVector::final_error) */
   double solve_ms;          /* device time of the convergence loop (CUDA events) */
   double setup_ms;          /* rank/contribution initialisation kernel time */
@@ -250,6 +257,34 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* g, int engine, const fpr_config* c
 int fpr_b200_ipc_export(const void* dev_ptr, void* handle_out /* 72 B */);
 int fpr_b200_ipc_import(const void* handle /* 72 B */, int device, void** dev_ptr_out);
 int fpr_b200_ipc_close(void* dev_ptr);
+
+/* ---- multi-device solve from ONE host thread (SURVEY §8(b) Threading) ----
+ * The reference's parallel engines split the vertices into static blocks, one
+ * per thread (pagerank.hpp:111-122 block_for, used by pagerank_ec_par :195 and
+ * pagerank_fused_par :261).  Here the blocks are edge-balanced destination
+ * ranges, one per device: with opts->ndevices = P > 1, part r of the graph
+ * (rows [bounds[r], bounds[r+1]) and their in-edges) lives on
+ * opts->devices[r] (entries may repeat: parts that share a GPU run on their
+ * own streams, one after the other).  Each part's sweep stores every new
+ * contribution into all parts' exchange vectors -- peer stores over NVLink
+ * between distinct GPUs (peer access enabled at creation), plain stores
+ * within one -- so the sweep IS the exchange; the calling thread then reduces
+ * the parts' (max, sum) residual pairs in part order and applies the
+ * reference's stop rule.  EC gives the single-device iteration count and
+ * ranks within 1e-12; FUSED is block-asynchronous across parts, the
+ * fused_par contract.  fpr_b200_pagerank() takes this path when
+ * opts->ndevices > 1, so the C++ drop-in reaches P GPUs through its options. */
+typedef struct fpr_b200_mgpu fpr_b200_mgpu;
+int fpr_b200_mgpu_create(const fpr_graph_view* view, const fpr_b200_options* opts, fpr_b200_mgpu** out);
+/* The same from a generator: every device generates the graph (the generators
+ * are deterministic) and keeps only its parts. */
+int fpr_b200_mgpu_generate(const fpr_gen_params* params, const fpr_b200_options* opts, fpr_b200_mgpu** out);
+/* EC or FUSED to convergence; buffers as fpr_b200_run (ranks in global ids). */
+int fpr_b200_mgpu_run(fpr_b200_mgpu* mg, int engine, const fpr_config* cfg, double* ranks_out,
+                      double* errors_out, double* l1_errors_out, uint64_t errors_cap, fpr_b200_result* result);
+/* n, m, parts and the row bounds (nparts + 1 entries; NULL allowed). */
+int fpr_b200_mgpu_info(const fpr_b200_mgpu* mg, uint64_t* n, uint64_t* m, uint32_t* nparts, uint64_t* bounds);
+void fpr_b200_mgpu_destroy(fpr_b200_mgpu* mg);
 
 /* Edge-list text ingest (SNAP style, edge_list.hpp:33-80): '#'/'%' comment
  * lines and blank/whitespace-only lines skipped, every other line exactly two

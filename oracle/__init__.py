@@ -117,6 +117,8 @@ class Oracle:
                                          _u64, C.POINTER(_u64), C.POINTER(C.c_int), C.POINTER(_u64),
                                          C.POINTER(_u64)]
         L.fo_parse_edge_list.restype = C.c_int
+        L.fo_ec_step.argtypes = [_u64, _u64p, _u64p, _u64p, _f64, _f64p, _f64p, C.POINTER(_f64), C.POINTER(_f64)]
+        L.fo_ec_step.restype = C.c_int
         L.fo_l1_norm.argtypes = [_u64, _f64p, _f64p]
         L.fo_l1_norm.restype = _f64
         L.fo_linf_norm.argtypes = [_u64, _f64p, _f64p]
@@ -225,6 +227,17 @@ class Oracle:
                     norm=NORM_LINF, history_cap=0) -> Run:
         return self._run(self.lib.fo_pagerank_ec, g, damping, threshold, max_iterations, norm,
                          (), history_cap)
+
+    def ec_step(self, g: Graph, prev: np.ndarray, damping=0.85):
+        """One EC iteration from `prev` (OpenMP over rows; bit-identical to the
+        sequential iteration).  Returns (next, max |delta|, sum |delta|)."""
+        prev = np.ascontiguousarray(prev, dtype=np.float64)
+        nxt = np.empty(g.n, np.float64)
+        err, l1 = _f64(0), _f64(0)
+        in_src = g.in_src if g.m else np.zeros(1, np.uint64)
+        if self.lib.fo_ec_step(g.n, g.in_start, in_src, g.out_degree, damping, prev, nxt, C.byref(err), C.byref(l1)):
+            raise ValueError("ec_step: invalid input")
+        return nxt, err.value, l1.value
 
     def pagerank_fused_seq(self, g, damping=0.85, threshold=1e-15, max_iterations=10000,
                            norm=NORM_LINF, history_cap=0) -> Run:

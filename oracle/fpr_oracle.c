@@ -331,6 +331,42 @@ int fo_pagerank_ec(uint64_t n, uint64_t m, const uint64_t* in_start, const uint6
   return FO_OK;
 }
 
+/* One EC (Jacobi) iteration from an arbitrary rank vector: the body of the
+ * pagerank_ec_seq loop (pagerank.hpp:137-140) -- scatter_contributions
+ * (:63-74) of `prev`, then gather_ranks_jacobi (:76-93) into `next` -- in the
+ * pull form of fo_pagerank_ec.  Rows are independent and each row's sum runs
+ * left to right exactly as in the sequential loop, so splitting the rows over
+ * OpenMP threads changes no bit of `next` or of the max delta (only the L1
+ * delta's summation order).  For full-size one-step parity checks (configs
+ * 3-5): the GPU's iterate k-1 goes in, the reference's iterate k comes out. */
+int fo_ec_step(uint64_t n, const uint64_t* in_start, const uint64_t* in_src,
+               const uint64_t* out_degree, double damping, const double* prev, double* next,
+               double* err_out, double* l1_out) {
+  if (n == 0 || !(damping > 0.0 && damping < 1.0)) return FO_EINVAL;
+  double* contrib = (double*)malloc(n * sizeof(double));
+  if (!contrib) return FO_ENOMEM;
+  const double base = (1.0 - damping) / (double)n;
+  const int64_t nn = (int64_t)n;
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < nn; ++u)
+    contrib[u] = out_degree[u] ? prev[u] / (double)out_degree[u] : 0.0;
+  double err = 0.0, l1 = 0.0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(max : err) reduction(+ : l1)
+  for (int64_t u = 0; u < nn; ++u) {
+    double sum = 0.0;
+    for (uint64_t s = in_start[u]; s < in_start[u + 1]; ++s) sum += contrib[in_src[s]];
+    const double value = base + damping * sum;
+    next[u] = value;
+    const double delta = fabs(value - prev[u]);
+    err = err > delta ? err : delta;
+    l1 += delta;
+  }
+  free(contrib);
+  if (err_out) *err_out = err;
+  if (l1_out) *l1_out = l1;
+  return FO_OK;
+}
+
 /* Pull restatement of pagerank_fused_seq (pagerank.hpp:152-189): one initial
  * scatter (:164), then per vertex in ascending order gather the live
  * contributions, update in place and republish immediately (:166-183). */

@@ -110,6 +110,13 @@ int fo_parse_edge_list(const char* text, uint64_t len, uint64_t* n, uint64_t* m,
                        uint64_t* tok_len);
 double fo_linf_norm(uint64_t n, const double* a, const double* b);
 
+/* One EC iteration from `prev` (the pagerank_ec_seq loop body,
+ * pagerank.hpp:137-140), OpenMP over rows, bit-identical to the sequential
+ * iteration; *err_out / *l1_out = max / sum of |next - prev|. */
+int fo_ec_step(uint64_t n, const uint64_t* in_start, const uint64_t* in_src,
+               const uint64_t* out_degree, double damping, const double* prev, double* next,
+               double* err_out, double* l1_out);
+
 #ifdef __cplusplus
 }
 #endif

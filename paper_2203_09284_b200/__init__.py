@@ -40,8 +40,9 @@ ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP = 0, 1, 2
 NORM_LINF, NORM_L1 = 0, 1
 GEN_RMAT, GEN_UNIFORM, GEN_CHUNGLU = 0, 1, 2
 OPT_REORDER = 1  # FPR_B200_OPT_REORDER
-OPT_BLOCKED = 2  # FPR_B200_OPT_BLOCKED
-OPT_PB = 4  # FPR_B200_OPT_PB
+OPT_PB = 4  # FPR_B200_OPT_PB: force propagation-blocked sweeps
+OPT_PULL = 16  # FPR_B200_OPT_PULL: force pull sweeps (default: the library picks, include/fpr_b200.h)
+SWEEP_PULL, SWEEP_PB = 0, 1  # fpr_b200_result.sweep
 OPT_REORDER_SOURCES = 8  # FPR_B200_OPT_REORDER_SOURCES
 
 
@@ -73,11 +74,12 @@ class _Config(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("norm", C.c_int32), ("wave_count", C.c_uint32),
-                ("flags", C.c_uint32), ("stream", C.c_void_p)]
+                ("flags", C.c_uint32), ("stream", C.c_void_p), ("devices", C.POINTER(C.c_int32)),
+                ("ndevices", C.c_uint32), ("reserved0", C.c_uint32)]
 
 
 class _Result(C.Structure):
-    _fields_ = [("iterations", C.c_uint64), ("converged", C.c_int32), ("reserved0", C.c_int32),
+    _fields_ = [("iterations", C.c_uint64), ("converged", C.c_int32), ("sweep", C.c_int32),
                 ("final_error", C.c_double), ("solve_ms", C.c_double), ("setup_ms", C.c_double),
                 ("kernel_launches", C.c_uint64)]
 
@@ -105,6 +107,8 @@ EXPORTS = [
     "fpr_b200_parse_edge_list", "fpr_b200_graph_from_edge_list", "fpr_b200_part_sweep_peers",
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
     "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev", "fpr_b200_part_create",
+    "fpr_b200_mgpu_create", "fpr_b200_mgpu_generate", "fpr_b200_mgpu_run", "fpr_b200_mgpu_info",
+    "fpr_b200_mgpu_destroy",
 ]
 
 _lib = None
@@ -159,6 +163,12 @@ def lib() -> C.CDLL:
                                                C.POINTER(u64), vp, u64, C.POINTER(_ParseErr)]
         L.fpr_b200_graph_from_edge_list.argtypes = [vp, u64, C.POINTER(_Options), C.POINTER(vp),
                                                     C.POINTER(_ParseErr)]
+        L.fpr_b200_mgpu_create.argtypes = [C.POINTER(_GraphView), C.POINTER(_Options), C.POINTER(vp)]
+        L.fpr_b200_mgpu_generate.argtypes = [C.POINTER(_GenParams), C.POINTER(_Options), C.POINTER(vp)]
+        L.fpr_b200_mgpu_run.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, u64, C.POINTER(_Result)]
+        L.fpr_b200_mgpu_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), vp]
+        L.fpr_b200_mgpu_destroy.argtypes = [vp]
+        L.fpr_b200_mgpu_destroy.restype = None
         _lib = L
     return _lib
 
@@ -209,6 +219,7 @@ class PageRankResult:
     solve_ms: float = 0.0
     kernel_launches: int = 0
     setup_ms: float = 0.0  # device time before the first sweep (init; one-time layouts on first use)
+    sweep: int = SWEEP_PULL  # sweep kind that ran (SWEEP_PULL / SWEEP_PB)
 
 
 @dataclass
@@ -281,7 +292,7 @@ def torch_stream_handle() -> int:
     return h if h else CUDA_STREAM_LEGACY
 
 
-def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False, pb=False) -> _Options:
+def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, pb=None) -> _Options:
     o = _Options()
     lib().fpr_b200_options_init(C.byref(o))
     o.device = device
@@ -292,7 +303,8 @@ def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False
     if reorder not in (False, True, "degree", "sources"):
         raise ValueError(f"reorder must be False, True, 'degree' or 'sources', not {reorder!r}")
     ro = OPT_REORDER_SOURCES if reorder == "sources" else (OPT_REORDER if reorder else 0)
-    o.flags = ro | (OPT_BLOCKED if blocked else 0) | (OPT_PB if pb else 0)
+    # pb: None = the library picks the sweep kind, True = propagation-blocked, False = pull
+    o.flags = ro | (0 if pb is None else (OPT_PB if pb else OPT_PULL))
     o.stream = stream
     return o
 
@@ -314,49 +326,47 @@ class DeviceGraph:
     # -- construction ---------------------------------------------------
     @classmethod
     def from_graph(cls, g: Graph, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
-                   blocked=False, pb=False):
+                   pb=None):
         ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
         v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
         h = C.c_void_p()
-        _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream, reorder,
-                                                                        blocked, pb)),
+        _check(lib().fpr_b200_graph_create(C.byref(v), C.byref(_options(device, norm, wave_count, stream, reorder, pb)),
                                            C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
-    def _generate(cls, gp, device, norm, wave_count, stream, reorder=False, blocked=False, pb=False):
+    def _generate(cls, gp, device, norm, wave_count, stream, reorder=False, pb=None):
         h = C.c_void_p()
-        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream, reorder,
-                                                                          blocked, pb)),
+        _check(lib().fpr_b200_graph_generate(C.byref(gp), C.byref(_options(device, norm, wave_count, stream, reorder, pb)),
                                              C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
     def generate_rmat(cls, p: RmatParams, device=-1, norm=NORM_LINF, wave_count=0, stream=None,
-                      relabel_bfs=False, bfs_root=0, reorder=False, blocked=False, pb=False):
+                      relabel_bfs=False, bfs_root=0, reorder=False, pb=None):
         """build_csr(generate_rmat(p)) on the device; relabel_bfs=True gives
         BASELINE config 3's crawl order (BFS from bfs_root over out-edges)."""
         gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed,
                         0, 0.0, 0, int(relabel_bfs), 0, bfs_root)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, pb)
 
     @classmethod
     def generate_uniform(cls, n: int, avg_degree: int, seed: int, device=-1, norm=NORM_LINF,
-                         wave_count=0, stream=None, reorder=False, blocked=False, pb=False):
+                         wave_count=0, stream=None, reorder=False, pb=None):
         """build_csr(testutil::random_sparse(n, avg_degree, SplitMix64(seed)))."""
         gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, n, avg_degree, seed)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, pb)
 
     @classmethod
     def generate_chunglu(cls, n: int, draws: int, seed: int, alpha: float = 2.1, kmax: int = 1_000_000,
-                         device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, blocked=False, pb=False):
+                         device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False, pb=None):
         """BASELINE config 4 (definition: DESIGN.md §4.1; oracle fo_generate_chunglu)."""
         gp = _GenParams(GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, n, 0, seed, draws, alpha, kmax)
-        return cls._generate(gp, device, norm, wave_count, stream, reorder, blocked, pb)
+        return cls._generate(gp, device, norm, wave_count, stream, reorder, pb)
 
     @classmethod
     def from_edges(cls, n: int, src, dst, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
-                   blocked=False, pb=False):
+                   pb=None):
         """fpr::build_csr(EdgeSet{n, (src, dst)}) on the device (graph.hpp:35-70):
         duplicates and self-loops dropped, in-segments ascending; ValueError
         names the first out-of-range edge as build_csr does."""
@@ -367,20 +377,20 @@ class DeviceGraph:
         L = lib()
         _check(L.fpr_b200_graph_from_edges(n, len(s_), s_.ctypes.data if len(s_) else None,
                                            d_.ctypes.data if len(d_) else None,
-                                           C.byref(_options(device, norm, wave_count, stream, reorder, blocked, pb)),
+                                           C.byref(_options(device, norm, wave_count, stream, reorder, pb)),
                                            C.byref(h)))
         return cls(h.value, device, norm, wave_count)
 
     @classmethod
     def from_edge_list(cls, text, device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False,
-                       blocked=False, pb=False):
+                       pb=None):
         """build_csr(parse_edge_list(text)) -- parsing, id compaction and the
         CSR build all on the device (edge_list.hpp:39-80, graph.hpp:35-70)."""
         ptr, nbytes, keep = _text_arg(text)
         h = C.c_void_p()
         perr = _ParseErr()
         _check(lib().fpr_b200_graph_from_edge_list(ptr, nbytes, C.byref(_options(device, norm, wave_count,
-                                                                                stream, reorder, blocked, pb)),
+                                                                                stream, reorder, pb)),
                                                    C.byref(h), C.byref(perr)), perr)
         del keep
         return cls(h.value, device, norm, wave_count)
@@ -425,6 +435,14 @@ class DeviceGraph:
         _check(lib().fpr_b200_graph_download_csr(self._h, ins.ctypes.data, src.ctypes.data, od.ctypes.data))
         return Graph(self.n, self.m, ins, src[: self.m], od[: self.n])
 
+    def download_into(self, in_start: np.ndarray, in_src: np.ndarray, out_degree: np.ndarray) -> None:
+        """download() into caller-owned u64 arrays (e.g. pinned views)."""
+        for a, k in ((in_start, self.n + 1), (in_src, self.m), (out_degree, self.n)):
+            if a.dtype != np.uint64 or not a.flags.c_contiguous or len(a) < k:
+                raise ValueError("download_into: need C-contiguous u64 arrays of n+1, m and n entries")
+        _check(lib().fpr_b200_graph_download_csr(self._h, in_start.ctypes.data, in_src.ctypes.data if self.m else None,
+                                                 out_degree.ctypes.data))
+
     def wave_starts(self, wave_count: int = 0) -> np.ndarray:
         nw = C.c_uint64()
         _check(lib().fpr_b200_graph_wave_starts(self._h, wave_count, None, 0, C.byref(nw)))
@@ -454,7 +472,82 @@ class DeviceGraph:
         trace = ConvergenceTrace(errors[:k].copy() if copy_trace else np.empty(0), k, bool(res.converged),
                                  l1[:k].copy() if copy_trace else None, ns[:k].copy() if copy_trace else None)
         rv = RankVector(ranks[: self.n] if copy_ranks else np.empty(0), res.final_error)
-        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches, res.setup_ms)
+        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches, res.setup_ms, res.sweep)
+
+
+class MultiDeviceGraph:
+    """A graph split by destination range over several devices, driven from
+    this thread (fpr_b200_mgpu_*): part r on devices[r]; devices may repeat
+    (parts sharing a GPU run one after the other)."""
+
+    def __init__(self, handle: int, devices):
+        self._h = C.c_void_p(handle)
+        self.devices = list(devices)
+        n, m, p = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _check(lib().fpr_b200_mgpu_info(self._h, C.byref(n), C.byref(m), C.byref(p), None))
+        self.n, self.m, self.nparts = n.value, m.value, p.value
+        b = np.empty(self.nparts + 1, np.uint64)
+        _check(lib().fpr_b200_mgpu_info(self._h, None, None, None, b.ctypes.data))
+        self.bounds = b
+
+    @staticmethod
+    def _opts(devices, norm, keep):
+        arr = (C.c_int32 * len(devices))(*devices)
+        keep.append(arr)
+        o = _options(norm=norm)
+        o.devices = C.cast(arr, C.POINTER(C.c_int32))
+        o.ndevices = len(devices)
+        return o
+
+    @classmethod
+    def from_graph(cls, g: Graph, devices, norm=NORM_LINF):
+        keep = []
+        ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
+        v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
+        h = C.c_void_p()
+        _check(lib().fpr_b200_mgpu_create(C.byref(v), C.byref(cls._opts(devices, norm, keep)), C.byref(h)))
+        return cls(h.value, devices)
+
+    @classmethod
+    def generate_rmat(cls, p: RmatParams, devices, norm=NORM_LINF):
+        keep = []
+        gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed, 0, 0.0, 0, 0, 0, 0)
+        h = C.c_void_p()
+        _check(lib().fpr_b200_mgpu_generate(C.byref(gp), C.byref(cls._opts(devices, norm, keep)), C.byref(h)))
+        return cls(h.value, devices)
+
+    def run(self, engine: int, cfg: PageRankConfig, copy_ranks=True, copy_trace=True) -> PageRankResult:
+        cap = min(int(cfg.max_iterations), 1 << 24) if copy_trace else 0
+        errors = np.empty(max(cap, 1), np.float64)
+        l1 = np.empty(max(cap, 1), np.float64)
+        ranks = np.empty(max(self.n, 1), np.float64) if copy_ranks else None
+        res = _Result()
+        c = cfg._c()
+        _check(lib().fpr_b200_mgpu_run(self._h, engine, C.byref(c), ranks.ctypes.data if copy_ranks else None,
+                                       errors.ctypes.data if copy_trace else None,
+                                       l1.ctypes.data if copy_trace else None, cap, C.byref(res)))
+        k = res.iterations
+        trace = ConvergenceTrace(errors[:k].copy() if copy_trace else np.empty(0), k, bool(res.converged),
+                                 l1[:k].copy() if copy_trace else None, None)
+        rv = RankVector(ranks[: self.n] if copy_ranks else np.empty(0), res.final_error)
+        return PageRankResult(rv, trace, res.solve_ms, res.kernel_launches, res.setup_ms, res.sweep)
+
+    def close(self) -> None:
+        if self._h:
+            lib().fpr_b200_mgpu_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def run_engine(kind: EngineKind | str, g, cfg: PageRankConfig, **kw) -> PageRankResult:

@@ -59,7 +59,7 @@ def open_graph(args, norm=NORM_LINF) -> tuple[DeviceGraph, str]:
     # library options: internal renumbering,
     # propagation-blocked sweeps, lockstep waves per sweep
     ro = getattr(args, "reorder", "none")
-    kw = {"norm": norm, "reorder": False if ro == "none" else ro, "pb": bool(getattr(args, "pb", False)),
+    kw = {"norm": norm, "reorder": False if ro == "none" else ro, "pb": True if getattr(args, "pb", False) else None,
           "wave_count": int(getattr(args, "waves", 0))}
     if k == "graph":
         g = load_cache(v)  # CacheError -> I/O exit code

@@ -106,10 +106,6 @@ struct SolveParams {
   int32_t npeers;
   int32_t peer_skip_empty;  // peers already hold the constant contribution of rows without in-edges
   double* peer[kMaxPeers];
-  // Source-blocked EC pass (kModeAccum): local row r is global row brow_ids[r];
-  // its in-block sum is added to partial[brow_ids[r]].
-  const int32_t* brow_ids;
-  double* partial;
 };
 
 enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
@@ -196,32 +192,6 @@ cudaError_t build_csr_from_arrays(const int32_t* src, const int32_t* dst, int64_
 cudaError_t build_csr_from_pairs(const int32_t* pairs, int64_t m, uint64_t n, DevGraph& g, cudaStream_t st,
                                  const char** msg);
 
-// blocked.cu: the source-blocked layout of a graph (FPR_B200_OPT_BLOCKED).
-struct BlockSet {
-  struct Block {
-    DevGraph view;          // local rows (compacted), row_ptr, edges in the block
-    int32_t* ids = nullptr; // local row -> global row
-    Partition part;
-    int32_t* waves = nullptr;  // {0, ntasks, 0, 0}: wave_task / wave_row of a one-wave sweep
-  };
-  int nblocks = 0;
-  int shift = 0;
-  std::vector<Block> blocks;
-  int32_t* src_pool = nullptr;
-  double* partial = nullptr;       // n: per-row sum over the blocks swept so far
-  double* tail_partial = nullptr;  // max_ntasks: split-row pieces (NaN = not ready)
-  double* cta_pairs = nullptr;     // apply pass: per-CTA (max, sum)
-  double* scratch = nullptr;       // per-pass residual slots the accumulate kernel writes
-  int apply_grid = 0;
-  int64_t max_ntasks = 0;
-  int64_t pairs = 0;               // (row, block) pairs = sum of local rows
-  std::vector<void*> allocs;
-};
-cudaError_t build_blocks(const DevGraph& g, int shift, cudaStream_t st, BlockSet& bs, const char** msg);
-void free_blocks(BlockSet& bs, cudaStream_t st);
-cudaError_t launch_apply(const BlockSet& bs, int32_t n, const int32_t* outdeg, double* pr, double* cur,
-                         double base, double damping, double* err, double* l1, cudaStream_t st);
-
 // pb.cu: propagation-blocked EC (FPR_B200_OPT_PB).
 // A sweep plan: the bins cut into waves of consecutive bins (1 wave = EC,
 // S waves = the lockstep Gauss-Seidel schedule), phase-1 pieces ordered
@@ -231,31 +201,36 @@ struct PbPlan {
   std::vector<int64_t> wave_bin;  // nwaves + 1: first bin of each wave
   std::vector<int64_t> item0;     // nwaves + 1: first phase-1 piece of each wave
   std::vector<int64_t> unit0;     // nwaves + 1: first phase-2 unit of each wave
-  // phase-2 units: whole bins, heavy bins cut into pieces (smaller pieces for
-  // more waves, so that every wave has a few units per CTA)
+  // phase-2 units: whole bins, heavy bins cut into runs of whole tiles
+  // (smaller pieces for more waves, so that every wave has a few units per CTA)
   int32_t* unit_bin = nullptr;
-  int64_t* unit_e = nullptr;      // units + 1: first entry of each unit
+  int64_t* unit_e = nullptr;      // 2 x units: [first, end) storage position of each unit
   int32_t* unit_k = nullptr;      // units of the unit's bin (1 = the bin is whole)
+  int32_t* unit_j = nullptr;      // index of the unit within its bin
+  int32_t* unit_slot = nullptr;   // split bins: the bin's first row-sum slot (-1 otherwise)
+  double* slots = nullptr;        // split-bin units' row sums, 2^shift doubles per slot
   int64_t* item_start = nullptr;  // pieces: first entry and length
   uint32_t* item_len = nullptr;
   unsigned long long* ctr = nullptr;  // 2 x nwaves work counters (reset per sweep)
-  double* cta_pairs = nullptr;        // nwaves x phase-2 CTAs (max, sum)
   std::vector<void*> allocs;
 };
 struct PbSet {
   int shift = 0;         // destination bin = row >> shift (at most 2^16 rows: uint16 offsets)
   int chunk_shift = 0;   // source chunk = src >> chunk_shift
-  int64_t nbins = 0, nchunks = 0, m = 0;
-  int32_t* src_bm = nullptr;     // m: source of each entry; bin b's entries are the in-CSR's edges of its rows,
-                                 //    regrouped by source chunk: (bin, chunk, k) order
-  uint16_t* dstl_bm = nullptr;   // m + 8: the entry's row minus the bin's first row
-  double* val = nullptr;         // m + 8: per-sweep scratch, contributions in (bin, chunk, k) order
+  int64_t nbins = 0, nchunks = 0, m = 0, mpad = 0;
+  int32_t* src_bm = nullptr;     // mpad: source of each entry (-1 = pad); bin b's entries (from bin_pos[b]) are
+                                 //    the in-CSR's edges of its rows regrouped by source chunk: (bin, chunk, row)
+  uint16_t* iperm = nullptr;     // mpad: per tile, the storage index of each place in row order
+  uint16_t* skey = nullptr;      // mpad: row offset (in the bin) at each sorted place of a tile; 0xFFFF = pad
+  double* val = nullptr;         // mpad: per-sweep scratch, contributions in storage order
   uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
   int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
-  std::vector<int64_t> bin_edge;  // nbins + 1: first entry of each bin
-  double* psum = nullptr;        // n: partial row sums of split bins (zero between sweeps)
+  std::vector<int64_t> bin_edge;  // nbins + 1: in-CSR edge offset of each bin's first row (waves)
+  std::vector<int64_t> bin_pos;   // nbins + 1: 4-aligned storage position of each bin
+  int64_t* bin_pos_d = nullptr;   // device copy
+  double* bin_pairs = nullptr;   // nbins x (max, sum) residual of each bin's rows, reduced in bin order
   unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep
-  int p1_grid = 0, p2_grid = 0;
+  int p1_grid = 0, p2_grid = 0, acc_smem = 0;
   std::map<uint32_t, PbPlan> plans;  // by wave count
   std::vector<void*> allocs;
 };
@@ -275,5 +250,10 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
 // prev != cur with one wave; lockstep passes prev == cur (in place).
 cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev, double* pr,
                             double* cur, double base, double damping, double* err, double* l1, cudaStream_t st);
+
+// runtime.cu hooks for mgpu.cu (the multi-device driver over the part API)
+int set_error(int code, const std::string& msg);  // thread-local last error; returns code
+cudaStream_t graph_stream(const void* graph_handle);
+int graph_device(const void* graph_handle);
 
 }  // namespace fprb

@@ -263,11 +263,8 @@ __device__ __forceinline__ void gather1(double& v, bool valid, int s, int fresh_
 
 // Finalize mode of a solve instantiation:
 //   kModeFinal : rank update + contribution store (single GPU);
-//   kModePeers : ... plus the store into every peer replica (fused exchange);
-//   kModeAccum : source-blocked EC pass: the task's rows are
-//                a column block's compacted rows; each adds its in-block sum
-//                to partial[brow_ids[r]] and the apply pass finishes the row.
-constexpr int kModeFinal = 0, kModePeers = 1, kModeAccum = 2;
+//   kModePeers : ... plus the store into every peer replica (fused exchange).
+constexpr int kModeFinal = 0, kModePeers = 1;
 
 // Row metadata of a task's first 32 rows (i0 .. i0+31, including the open
 // row i1 when it falls in that window), prefetched one task ahead, with the
@@ -286,14 +283,8 @@ __device__ __forceinline__ RowPre load_rowpre(const SolveParams& p, const TaskMe
     const int64_t a = __ldg(p.row + row), b = __ldg(p.row + row + 1);
     r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
     r.hi = (int)(b - m.j0);
-    if (MODE != kModeAccum) {
-      r.od = __ldg(p.outdeg + row);
-      r.ov = p.pr[row];
-    } else {  // accumulate pass: od = global row, ov = its running partial (prefetched:
-              // only this task writes that slot during the pass)
-      r.od = __ldg(p.brow_ids + row);
-      r.ov = p.partial[r.od];
-    }
+    r.od = __ldg(p.outdeg + row);
+    r.ov = p.pr[row];
   } else if (row == m.i1 && row < p.n) {
     const int64_t a = __ldg(p.row + row);
     r.lo = a < m.j0 ? -1 : (int)(a - m.j0);
@@ -413,10 +404,8 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
       if (rb != i0) {
         lo = (int)(__ldg(p.row + r) - j0);
         hi = (int)(__ldg(p.row + r + 1) - j0);
-        if (MODE != kModeAccum) {
-          od = __ldg(p.outdeg + r);
-          ov = p.pr[r];
-        }
+        od = __ldg(p.outdeg + r);
+        ov = p.pr[r];
       }
       double sum = 0.0;
       if (lo < hi) {
@@ -425,12 +414,6 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         if (lo + off < (e & ~7)) sum = ws.carry[e >> 3] + sum;
       }
       if (r == i0 && has_head) sum = head_extra + sum;
-      if (MODE == kModeAccum) {  // blocks run in order: one writer per (row, block)
-        const int gid = rb == i0 ? rp.od : __ldg(p.brow_ids + r);
-        const double before = rb == i0 ? rp.ov : p.partial[gid];
-        p.partial[gid] = before + sum;
-        continue;
-      }
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
       p.pr_out[r] = nv;
       if (od > 0) {
@@ -858,7 +841,7 @@ struct SolveShape {
 };
 
 // One instantiation per finalize mode; the plain one carries no trace of the
-// others.  (The async engine has no accumulate mode.)
+// peer stores.
 static SolveShape solve_shape(int engine, int mode) {
   if (engine == kFusedWide)
     return {mode == kModePeers ? (const void*)solve_kernel<true, FPR_EC_BLOCK, FPR_EC_MINB, kModePeers>
@@ -868,9 +851,8 @@ static SolveShape solve_shape(int engine, int mode) {
     return {mode == kModePeers ? (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModePeers>
                                : (const void*)solve_kernel<true, FPR_ASYNC_BLOCK, FPR_ASYNC_MINB, kModeFinal>,
             FPR_ASYNC_BLOCK, solve_smem_bytes<FPR_ASYNC_BLOCK>()};
-  const void* fn = mode == kModePeers   ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModePeers>
-                   : mode == kModeAccum ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModeAccum>
-                                        : (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModeFinal>;
+  const void* fn = mode == kModePeers ? (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModePeers>
+                                      : (const void*)solve_kernel<false, FPR_EC_BLOCK, FPR_EC_MINB, kModeFinal>;
   return {fn, FPR_EC_BLOCK, solve_smem_bytes<FPR_EC_BLOCK>()};
 }
 
@@ -880,7 +862,7 @@ int solve_block_threads(int engine) { return solve_shape(engine, kModeFinal).blo
 // occupancy, so either can be launched cooperatively with it.
 cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
   int best = 1 << 30;
-  for (int mode : {kModeFinal, kModePeers, kModeAccum}) {
+  for (int mode : {kModeFinal, kModePeers}) {
     const SolveShape sh = solve_shape(engine, mode);
     cudaError_t e = cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
     if (e != cudaSuccess) return e;
@@ -895,7 +877,7 @@ cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
 }
 
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s) {
-  const SolveShape sh = solve_shape(engine, p.brow_ids ? kModeAccum : (p.npeers > 0 ? kModePeers : kModeFinal));
+  const SolveShape sh = solve_shape(engine, p.npeers > 0 ? kModePeers : kModeFinal);
   SolveParams copy = p;
   void* args[] = {&copy};
   return cudaLaunchCooperativeKernel(sh.fn, dim3(grid), dim3(sh.block), args, sh.smem, s);

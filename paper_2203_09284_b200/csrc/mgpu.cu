@@ -1,0 +1,309 @@
+// mgpu.cu -- the multi-device solve driven by ONE host thread
+// (include/fpr_b200.h, fpr_b200_mgpu_*; SURVEY §8(b) Threading row, §8(e)).
+//
+// The reference's parallel engines cut the vertices into static blocks, one
+// per thread (pagerank.hpp:111-122 block_for), separated by a barrier whose
+// completion step reduces the per-thread maxima and applies the stop rule
+// (:209-218, :276-286).  Here a block is an edge-balanced destination range
+// of rows (the merge-path split of fpr_b200_part_create), one per device:
+//   * part r lives on devices[r] with its rows, their in-edges (sources
+//     remapped into the padded exchange space P x slice) and two exchange
+//     vectors (EC ping-pongs them; FUSED updates the first in place);
+//   * one sweep per part per iteration, on the part's stream; its epilogue
+//     stores every new contribution into ALL parts' exchange vectors -- peer
+//     stores over NVLink between distinct GPUs (peer access enabled here),
+//     plain stores within one device -- so the sweep is the all-gather
+//     (fpr_b200_part_sweep_peers, kernels.cu kModePeers);
+//   * the calling thread waits for the parts' 16-B (max, sum) residual pairs,
+//     reduces them in part order (the on_barrier step, deterministic) and
+//     applies the reference's predicate `error <= threshold` (:141, :216).
+// Parts that share a device run on their own streams one after the other;
+// the test suite uses that to check P parts against one GPU.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fpr_b200.h"
+#include "internal.cuh"
+
+struct fpr_b200_mgpu {
+  uint32_t P = 0;
+  uint64_t n = 0, m = 0, slice = 0;
+  int norm = FPR_B200_NORM_LINF;
+  std::vector<int> dev;
+  std::vector<fpr_b200_graph*> parts;
+  std::vector<uint64_t> bounds;    // P + 1 row bounds
+  std::vector<double*> x[2];       // per part: exchange vectors (P * slice doubles, on the part's device)
+  std::vector<double*> dpair;      // per part: its (max, sum) residual pair (device)
+  double* hpairs = nullptr;        // P pairs (pinned host)
+};
+
+namespace {
+
+using fprb::set_error;
+
+#define MCK(call)                                                                                        \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      return set_error(e_ == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,               \
+                       std::string("fpr_b200_mgpu: CUDA error '") + cudaGetErrorString(e_) + "' (" #call ")"); \
+  } while (0)
+
+int check_opts(const fpr_b200_options* opts) {
+  if (!opts || opts->ndevices < 1 || !opts->devices)
+    return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu: opts->devices / opts->ndevices must name the parts' devices");
+  if (opts->ndevices > 8)
+    return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu: at most 8 parts (one NVSwitch node)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_error(FPR_B200_ECUDA, "fpr_b200_mgpu: no CUDA device available");
+  for (uint32_t r = 0; r < opts->ndevices; ++r)
+    if (opts->devices[r] < 0 || opts->devices[r] >= ndev)
+      return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu: device " + std::to_string(opts->devices[r]) +
+                                            " out of range (" + std::to_string(ndev) + " devices)");
+  return FPR_B200_OK;
+}
+
+// Peer access between every pair of distinct devices (NVLink through
+// NVSwitch on a B200 node); parts on the same device need none.
+int enable_peers(const std::vector<int>& dev) {
+  for (int a : dev)
+    for (int b : dev) {
+      if (a == b) continue;
+      int ok = 0;
+      MCK(cudaDeviceCanAccessPeer(&ok, a, b));
+      if (!ok)
+        return set_error(FPR_B200_ECUDA, "fpr_b200_mgpu: device " + std::to_string(a) +
+                                             " cannot access device " + std::to_string(b) + " (no P2P path)");
+      MCK(cudaSetDevice(a));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return set_error(FPR_B200_ECUDA, std::string("fpr_b200_mgpu: cudaDeviceEnablePeerAccess: ") +
+                                             cudaGetErrorString(e));
+      }
+    }
+  return FPR_B200_OK;
+}
+
+// Exchange vectors, residual pairs and peer access once the parts exist.
+int finish(fpr_b200_mgpu* mg) {
+  int rc = enable_peers(mg->dev);
+  if (rc) return rc;
+  for (auto& v : mg->x) v.assign(mg->P, nullptr);
+  mg->dpair.assign(mg->P, nullptr);
+  for (uint32_t r = 0; r < mg->P; ++r) {
+    MCK(cudaSetDevice(mg->dev[r]));
+    for (auto& v : mg->x) MCK(cudaMalloc(&v[r], (size_t)mg->P * mg->slice * sizeof(double)));
+    MCK(cudaMemset(mg->x[0][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
+    MCK(cudaMemset(mg->x[1][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
+    MCK(cudaMalloc(&mg->dpair[r], 2 * sizeof(double)));
+  }
+  MCK(cudaMallocHost(&mg->hpairs, 2 * (size_t)mg->P * sizeof(double)));
+  return FPR_B200_OK;
+}
+
+std::vector<int> devices_of(const fpr_b200_options* opts) {
+  return std::vector<int>(opts->devices, opts->devices + opts->ndevices);
+}
+
+}  // namespace
+
+extern "C" {
+
+void fpr_b200_mgpu_destroy(fpr_b200_mgpu* mg) {
+  if (!mg) return;
+  for (uint32_t r = 0; r < mg->parts.size(); ++r) {
+    cudaSetDevice(mg->dev[r]);
+    cudaDeviceSynchronize();
+    for (auto& v : mg->x)
+      if (r < v.size() && v[r]) cudaFree(v[r]);
+    if (r < mg->dpair.size() && mg->dpair[r]) cudaFree(mg->dpair[r]);
+    fpr_b200_graph_destroy(mg->parts[r]);
+  }
+  if (mg->hpairs) cudaFreeHost(mg->hpairs);
+  delete mg;
+}
+
+int fpr_b200_mgpu_create(const fpr_graph_view* view, const fpr_b200_options* opts, fpr_b200_mgpu** out) {
+  if (!view || !out) return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_create: null argument");
+  *out = nullptr;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  auto* mg = new fpr_b200_mgpu;
+  mg->P = opts->ndevices;
+  mg->dev = devices_of(opts);
+  mg->norm = opts->norm;
+  mg->n = view->n;
+  mg->m = view->m;
+  mg->bounds.assign(mg->P + 1, 0);
+  mg->parts.assign(mg->P, nullptr);
+  for (uint32_t r = 0; r < mg->P && !rc; ++r) {
+    fpr_b200_options o = *opts;
+    o.device = mg->dev[r];
+    o.devices = nullptr;
+    o.ndevices = 0;
+    o.stream = nullptr;  // every part on its own library stream
+    // only this part's rows and in-edges cross its link
+    rc = fpr_b200_part_create(view, mg->P, r, &o, mg->bounds.data(), &mg->slice, &mg->parts[r]);
+  }
+  if (!rc) rc = finish(mg);
+  if (rc) {
+    fpr_b200_mgpu_destroy(mg);
+    return rc;
+  }
+  *out = mg;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_mgpu_generate(const fpr_gen_params* params, const fpr_b200_options* opts, fpr_b200_mgpu** out) {
+  if (!params || !out) return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_generate: null argument");
+  *out = nullptr;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  auto* mg = new fpr_b200_mgpu;
+  mg->P = opts->ndevices;
+  mg->dev = devices_of(opts);
+  mg->norm = opts->norm;
+  mg->bounds.assign(mg->P + 1, 0);
+  mg->parts.assign(mg->P, nullptr);
+  // one full graph per distinct device (the generators are deterministic),
+  // partitioned into that device's parts, then released
+  std::vector<int> done;
+  for (uint32_t r = 0; r < mg->P && !rc; ++r) {
+    const int d = mg->dev[r];
+    if (std::find(done.begin(), done.end(), d) != done.end()) continue;
+    done.push_back(d);
+    fpr_b200_options o = *opts;
+    o.device = d;
+    o.devices = nullptr;
+    o.ndevices = 0;
+    o.stream = nullptr;
+    fpr_b200_graph* full = nullptr;
+    if ((rc = fpr_b200_graph_generate(params, &o, &full))) break;
+    uint64_t n = 0, m = 0, nt = 0;
+    fpr_b200_graph_info(full, &n, &m, &nt);
+    mg->n = n;
+    mg->m = m;
+    for (uint32_t q = 0; q < mg->P && !rc; ++q)
+      if (mg->dev[q] == d) rc = fpr_b200_graph_partition(full, mg->P, q, &o, mg->bounds.data(), &mg->slice, &mg->parts[q]);
+    fpr_b200_graph_destroy(full);
+  }
+  if (!rc) rc = finish(mg);
+  if (rc) {
+    fpr_b200_mgpu_destroy(mg);
+    return rc;
+  }
+  *out = mg;
+  return FPR_B200_OK;
+}
+
+int fpr_b200_mgpu_info(const fpr_b200_mgpu* mg, uint64_t* n, uint64_t* m, uint32_t* nparts, uint64_t* bounds) {
+  if (!mg) return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_info: null handle");
+  if (n) *n = mg->n;
+  if (m) *m = mg->m;
+  if (nparts) *nparts = mg->P;
+  if (bounds) std::copy(mg->bounds.begin(), mg->bounds.end(), bounds);
+  return FPR_B200_OK;
+}
+
+int fpr_b200_mgpu_run(fpr_b200_mgpu* mg, int engine, const fpr_config* cfg, double* ranks_out, double* errors_out,
+                      double* l1_out, uint64_t errors_cap, fpr_b200_result* result) {
+  if (!mg || !cfg) return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: null argument");
+  // validate(PageRankConfig), pagerank.hpp:40-53 (the part sweep re-checks it)
+  if (!(cfg->damping > 0.0 && cfg->damping < 1.0)) return set_error(FPR_B200_EINVAL, "pagerank: damping must be in (0,1)");
+  if (!(cfg->threshold > 0.0)) return set_error(FPR_B200_EINVAL, "pagerank: threshold must be positive");
+  if (cfg->max_iterations == 0) return set_error(FPR_B200_EINVAL, "pagerank: max_iterations must be positive");
+  if (cfg->thread_count == 0) return set_error(FPR_B200_EINVAL, "pagerank: thread_count must be positive");
+  if (engine != FPR_B200_ENGINE_EC && engine != FPR_B200_ENGINE_FUSED)
+    return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: multi-device engines are EC and FUSED");
+  const uint32_t P = mg->P;
+  const size_t sl = (size_t)mg->slice;
+  int rc;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  MCK(cudaSetDevice(mg->dev[0]));
+  MCK(cudaEventCreate(&t0));
+  MCK(cudaEventCreate(&t1));
+  // init: every part writes 1/n ranks and its contribution slice into its own
+  // first exchange vector, then the slices are copied to every other part
+  for (uint32_t r = 0; r < P; ++r)
+    if ((rc = fpr_b200_part_init(mg->parts[r], mg->x[0][r]))) return rc;
+  for (uint32_t r = 0; r < P; ++r) {
+    MCK(cudaSetDevice(mg->dev[r]));
+    MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
+  }
+  for (uint32_t q = 0; q < P; ++q)
+    for (uint32_t r = 0; r < P; ++r)
+      if (q != r)
+        MCK(cudaMemcpyPeerAsync(mg->x[0][q] + r * sl, mg->dev[q], mg->x[0][r] + r * sl, mg->dev[r],
+                                sl * sizeof(double), fprb::graph_stream(mg->parts[q])));
+  for (uint32_t r = 0; r < P; ++r) {
+    MCK(cudaSetDevice(mg->dev[r]));
+    MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
+  }
+  MCK(cudaSetDevice(mg->dev[0]));
+  MCK(cudaEventRecord(t0, fprb::graph_stream(mg->parts[0])));
+  std::vector<double*> peers(P);
+  uint64_t it = 0;
+  int cur = 0;
+  double err = 1.0, l1 = 1.0;
+  bool stop = false;
+  while (it < cfg->max_iterations && !stop) {
+    const int nxt = engine == FPR_B200_ENGINE_EC ? cur ^ 1 : cur;
+    for (uint32_t q = 0; q < P; ++q) peers[q] = mg->x[nxt][q];
+    for (uint32_t r = 0; r < P; ++r) {
+      if ((rc = fpr_b200_part_sweep_peers(mg->parts[r], engine, cfg, mg->x[cur][r], mg->x[nxt][r], peers.data(), P,
+                                          mg->dpair[r])))
+        return rc;
+      MCK(cudaSetDevice(mg->dev[r]));
+      MCK(cudaMemcpyAsync(mg->hpairs + 2 * r, mg->dpair[r], 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                          fprb::graph_stream(mg->parts[r])));
+    }
+    // the barrier: every part's sweep (and its peer stores) has completed
+    for (uint32_t r = 0; r < P; ++r) {
+      MCK(cudaSetDevice(mg->dev[r]));
+      MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
+    }
+    err = 0.0;
+    l1 = 0.0;
+    for (uint32_t r = 0; r < P; ++r) {  // part order: deterministic
+      err = std::max(err, mg->hpairs[2 * r]);
+      l1 += mg->hpairs[2 * r + 1];
+    }
+    if (errors_out) {
+      if (errors_cap < it + 1)
+        return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: errors buffer holds " + std::to_string(errors_cap) +
+                                              " entries, need " + std::to_string(it + 1));
+      errors_out[it] = err;
+    }
+    if (l1_out && errors_cap >= it + 1) l1_out[it] = l1;
+    ++it;
+    cur = nxt;
+    stop = (mg->norm == FPR_B200_NORM_L1 ? l1 : err) <= cfg->threshold;
+  }
+  MCK(cudaSetDevice(mg->dev[0]));
+  MCK(cudaEventRecord(t1, fprb::graph_stream(mg->parts[0])));
+  MCK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (ranks_out)
+    for (uint32_t r = 0; r < P; ++r)
+      if ((rc = fpr_b200_part_ranks(mg->parts[r], ranks_out + mg->bounds[r]))) return rc;
+  if (result) {
+    result->iterations = it;
+    result->converged = (it > 0 && (mg->norm == FPR_B200_NORM_L1 ? l1 : err) <= cfg->threshold) ? 1 : 0;
+    result->sweep = FPR_B200_SWEEP_PULL;
+    result->final_error = it > 0 ? err : 1.0;
+    result->solve_ms = ms;  // device 0's stream: first sweep issued .. last residual read
+    result->setup_ms = 0.0;
+    result->kernel_launches = it * P + P;
+  }
+  return FPR_B200_OK;
+}
+
+}  // extern "C"

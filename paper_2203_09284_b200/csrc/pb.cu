@@ -1,6 +1,7 @@
-// pb.cu -- propagation-blocked sweeps (FPR_B200_OPT_PB) for graphs whose
-// contribution vector far exceeds L2 (configs 4/5): EC (Jacobi) and the
-// lockstep FusEd schedule (waves of whole bins, in place).
+// pb.cu -- propagation-blocked sweeps for graphs whose contribution vector
+// far exceeds L2 (configs 4/5; picked by default there, FPR_B200_OPT_PB /
+// FPR_B200_OPT_PULL force the choice): EC (Jacobi) and the lockstep FusEd
+// schedule (waves of whole bins, in place).
 //
 // The pull gather contrib[in_src[e]] misses L2 on such graphs, and each miss
 // pulls ~64 B from HBM for 8 useful bytes (profiles/r1_large_configs_ncu.md).
@@ -10,25 +11,33 @@
 //
 // Layout, built once from the resident in-CSR:
 //   * rows are cut into bins of 2^shift consecutive rows; a bin's entries are
-//     exactly its rows' in-edges (duplicates and self loops included);
+//     exactly its rows' in-edges, stored from an 8-aligned position bin_pos[b]
+//     (<= 7 pad entries per bin, so tile copies stay 16-B aligned);
 //   * inside a bin, entries are regrouped by source chunk (src >> chunk_shift):
 //     segment (bin b, chunk c) is contiguous and keeps ascending rows;
-//   * entry = (source id, row offset inside the bin as uint16).
+//   * entry = source id (gather side) + value slot;
+//   * the bin is cut into tiles of kTile entries; per tile, iperm[] lists the
+//     entries in the tile's (stable) row order, and skey[] holds the row
+//     offset of every sorted place (accumulate side).
 // A sweep plan (get_pb_plan, cached per wave count) cuts the bins into waves
 // of consecutive bins: 1 wave for EC, S for lockstep.  Per wave:
 //   * phase 1 (pb_gather_kernel): warps walk the wave's segments chunk by
 //     chunk, so the sources read at any moment span one chunk's
 //     contributions (a 16 MB window at the default chunk of 2^21 sources),
 //     and write val[pos] = prev[src_bm[pos]] contiguously;
-//   * phase 2 (pb_accum_kernel): CTAs accumulate val into a bin's rows in
-//     shared memory and finish the rows exactly like the blocked engine's
-//     apply (blocked.cu): base + d*sum without FMA, contribution, residual.
-// Per edge and sweep: 4 B source + 8 B value written + 8 B read + 2 B offset,
-// all sequential, where a missed pull gather moved ~64 B of DRAM.
-// A row's sum is accumulated in shared-memory atomic order, a regrouping of
-// the reference's left-to-right sum: bit patterns may differ from run to run,
-// well inside the 1e-12 per-iteration tolerance (tests/test_gpu_engines.py
-// test_pb_*).  Measurements and rejected variants: DESIGN.md §3.4.
+//   * phase 2 (pb_accum_kernel): a CTA takes a bin (or a run of tiles of a
+//     heavy bin), streams each tile into shared memory (TMA bulk copies),
+//     reads it in row order, sums every row's run and adds it to the bin's
+//     row accumulators with ONE plain add per row and tile -- no atomics, a
+//     fixed order -- then finishes the rows: base + d*sum without FMA,
+//     contribution, residual.
+// Per edge and sweep: 4 B source + 8 B value written + 8 B read + 2 B iperm
+// + 2 B key, all sequential, where a missed pull gather moved ~64 B of DRAM.
+// A row's sum is a fixed regrouping of the reference's left-to-right sum
+// (chunks in order, i.e. ascending sources), so every run gives the same
+// bits, within 1e-12 per iteration of the reference
+// (tests/test_gpu_engines.py test_pb_*).  Measurements and rejected
+// variants: DESIGN.md §3.4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -46,17 +55,30 @@ constexpr int kPbThreads = 1024;
 constexpr int kGatherThreads = 256;
 
 constexpr int kPieceEntries = 1024;  // phase-1 work item: up to this many entries of one segment
-// phase 2 shape: entries per lane, threads per CTA, CTAs per SM (shared
-// memory permitting); EPL 4 x 1024 x 2 measured best
+// phase 2: CTAs of kAccThreads, kAccEpl sorted entries per lane, one tile
+// (kTile = kAccThreads * kAccEpl entries) per CTA step; the bin's fp64 row
+// accumulators (64 KB at 2^13 rows) + kStages staged tiles (24 KB each) fit
+// two CTAs per SM
+#ifndef FPR_PB_ACC_THREADS
+#define FPR_PB_ACC_THREADS 512
+#endif
 #ifndef FPR_PB_EPL
 #define FPR_PB_EPL 4
 #endif
-#ifndef FPR_PB_ACC_THREADS
-#define FPR_PB_ACC_THREADS 1024
+#ifndef FPR_PB_STAGES
+#define FPR_PB_STAGES 2
 #endif
+constexpr int kAccThreads = FPR_PB_ACC_THREADS;
+constexpr int kAccEpl = FPR_PB_EPL;  // sorted places per lane (4 or 8)
 #ifndef FPR_PB_ACC_CTAS
 #define FPR_PB_ACC_CTAS 2
 #endif
+constexpr int kAccCtas = FPR_PB_ACC_CTAS;  // phase-2 CTAs per SM (at most; shared memory permitting)
+constexpr int kTile = kAccThreads * kAccEpl;
+constexpr int kStages = FPR_PB_STAGES;  // tiles per CTA staged ahead (TMA bulk copies)
+static_assert(kAccEpl == 4 || kAccEpl == 8, "kAccEpl is 4 or 8");
+static_assert(kTile <= 65536, "perm is uint16");
+constexpr uint16_t kPadKey = 0xFFFF;  // row offset of a pad entry (bins hold < 2^16 rows)
 // phase 1 gathers: L1-allocating (default: hub sources recur across the bins a
 // CTA walks in one chunk, 4-6% faster on configs 4/5) or L2-only (0)
 #ifndef FPR_PB_GATHER_L1
@@ -65,12 +87,13 @@ constexpr int kPieceEntries = 1024;  // phase-1 work item: up to this many entri
 
 // One CTA per bin: histogram its edges by source chunk, scan, then a stable
 // scatter (tiles of the bin's CSR edges, block radix-sorted by chunk) so each
-// (bin, chunk) segment lists its entries in ascending row order -- phase 2
-// folds runs of one row before touching shared memory.  counts/start are
-// chunk-major.
+// (bin, chunk) segment lists its entries in ascending row order.  The bin's
+// entries start at bin_pos[b]; its pad entries (up to bin_pos[b + 1]) get
+// source -1 and key kPadKey.  counts/start are chunk-major.
 __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* row, const int32_t* src, int32_t n,
                                                                 int shift, int chunk_shift, int key_bits,
-                                                                int64_t nbins, int64_t nchunks, uint32_t* counts,
+                                                                int64_t nbins, int64_t nchunks,
+                                                                const int64_t* bin_pos, uint32_t* counts,
                                                                 int64_t* start, int32_t* src_bm, uint16_t* dstl_bm) {
   using Sort = cub::BlockRadixSort<uint32_t, kPbThreads, 1, uint64_t>;
   using ScanU = cub::BlockScan<uint32_t, kPbThreads>;
@@ -90,6 +113,11 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
     const int64_t r0 = b << shift;
     const int64_t r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
     const int64_t e0 = row[r0], e1 = row[r1];
+    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
+    for (int64_t q = p0 + (e1 - e0) + tid; q < p1; q += blockDim.x) {
+      src_bm[q] = -1;
+      dstl_bm[q] = kPadKey;
+    }
     for (int64_t r = r0 + tid; r <= r1; r += blockDim.x) srow[r - r0] = (uint32_t)(__ldg(row + r) - e0);
     __syncthreads();
     for (int64_t e = e0 + tid; e < e1; e += blockDim.x) atomicAdd(&h[(uint32_t)__ldg(src + e) >> chunk_shift], 1u);
@@ -102,7 +130,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       ScanU(tmp.scanu).ExclusiveSum(v, x, tile);
       if (c < nchunks) {
         counts[c * nbins + b] = v;
-        start[c * nbins + b] = e0 + running + x;
+        start[c * nbins + b] = p0 + running + x;
         h[c] = running + x;
       }
       running += tile;
@@ -133,12 +161,46 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       ScanI(tmp.scani).InclusiveScan(hs, hs, cub::Max());
       const bool real = key[0] != sentinel;
       if (real) {
-        const int64_t pos = e0 + h[key[0]] + (tid - hs);
+        const int64_t pos = p0 + h[key[0]] + (tid - hs);
         src_bm[pos] = (int32_t)(val[0] >> 16);
         dstl_bm[pos] = (uint16_t)(val[0] & 0xFFFFu);
       }
       __syncthreads();
       if (real && (tid == kPbThreads - 1 || skey[tid + 1] != key[0])) h[key[0]] += (uint32_t)(tid - hs + 1);
+      __syncthreads();
+    }
+  }
+}
+
+// Per tile (kTile consecutive entries from bin_pos[b]; the bin's last tile is
+// shorter): the stable sort of its entries by row.  skey[tile + j] = row
+// offset at sorted place j (kPadKey for pads, which sort last); iperm[tile +
+// j] = storage index (in the tile) of sorted place j.  Built once with the
+// layout.
+__global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_t* dstl, const int64_t* bin_pos,
+                                                                   int64_t nbins, uint16_t* iperm, uint16_t* skey) {
+  using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int64_t p1 = bin_pos[b + 1];
+    for (int64_t t0 = bin_pos[b]; t0 < p1; t0 += kTile) {
+      const int len = (int)min((int64_t)kTile, p1 - t0);
+      uint32_t key[kAccEpl], idx[kAccEpl];
+#pragma unroll
+      for (int j = 0; j < kAccEpl; ++j) {
+        const int i = threadIdx.x * kAccEpl + j;
+        key[j] = i < len ? (uint32_t)dstl[t0 + i] : 0x10000u;  // past the tile: after the pads
+        idx[j] = (uint32_t)i;
+      }
+      Sort(tmp).Sort(key, idx, 0, 17);
+#pragma unroll
+      for (int j = 0; j < kAccEpl; ++j) {
+        const int p = threadIdx.x * kAccEpl + j;
+        if (p < len) {
+          skey[t0 + p] = (uint16_t)key[j];
+          iperm[t0 + p] = (uint16_t)idx[j];
+        }
+      }
       __syncthreads();
     }
   }
@@ -220,51 +282,96 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
 }
 
 // Phase 2: CTAs take work units from a counter: a unit is a whole bin, or a
-// piece of a heavy bin (skewed graphs put a large share of the edges in the
-// bins of the hub rows; one CTA per bin left one SM working 7x longer than
-// the average on config 3).  Lane L of a warp step owns EPL consecutive
-// entries, read as 32-B value vectors and one key vector.  It
-// folds runs of equal rows in registers; runs strictly inside the lane go to
-// shared memory at once.  The run that ends the lane (its "tail") may
-// continue in the next lanes: one segmented warp scan of the tails per
-// 32*EPL entries carries it, and each run is added exactly once, by the lane
-// where it ends (its first part, if it began in earlier lanes, arrives in
-// the carry).  Shared fp64 adds are CAS loops on sm_100.  The first form of
-// this pass scanned every 32 entries across the warp; its shuffles were ~60%
-// of the L1TEX data-pipe wavefronts, the pass's limiter.
-// Then each finished row: base + d*sum without FMA, contribution, residual.
-template <int EPL>
-__device__ __forceinline__ void pb_ld_vals(const double* p, double (&v)[EPL]) {
-#pragma unroll
-  for (int j = 0; j < EPL; j += 4)
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[j]), "=d"(v[j + 1]), "=d"(v[j + 2]), "=d"(v[j + 3])
-                 : "l"(p + j));
+// run of tiles of a heavy bin (skewed graphs put a large share of the edges
+// in the bins of the hub rows; one CTA per bin left one SM working 7x longer
+// than the average on config 3).  Per tile:
+//   * thread 0 streams the tile's values, inverse permutation and sorted
+//     keys into a shared-memory stage with three TMA bulk copies completing
+//     on the stage's mbarrier, kStages tiles ahead;
+//   * lane L owns the sorted places [4L, 4L+4): it reads their keys and,
+//     through the inverse permutation, their values from the stage, folds
+//     runs of equal rows in registers, and one segmented warp scan of the
+//     lane tails carries a run across lanes to the lane where it ends, so
+//     each run inside the warp is summed exactly once, in a fixed order.
+//     Sorted, a row's places are contiguous: its run is unique in the tile,
+//     so the row accumulator takes one PLAIN add (runs of different rows
+//     touch different words).  A run that crosses warp boundaries leaves a
+//     piece per warp in shared memory; the lane where it ends waits for the
+//     earlier warps' pieces (per-tile flags) and adds them in warp order;
+//   * one CTA barrier ends the tile (every add landed, the stage free).
+// Tiles of a unit, and the units of a split bin (slots summed in unit
+// order by the last one to finish), follow each other in a fixed order, so
+// the row sums -- and the ranks -- are the same bits on every run
+// (SPEC.md:415).  The first form of this pass added every run with a
+// shared-memory fp64 CAS in arrival order (not reproducible); a fixed-point
+// integer accumulator made it reproducible but cost 45% more per sweep
+// (DESIGN.md §3.4).  Then each finished row: base + d*sum without FMA,
+// contribution, residual; the bin's (max, sum) residual pair is reduced in a
+// fixed thread order and the bins' pairs in bin order (pb_reduce_kernel).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
-template <int EPL>
-__device__ __forceinline__ void pb_ld_keys(const uint16_t* p, uint32_t (&k)[EPL / 2]) {
-  if constexpr (EPL == 4) {
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(k[0]), "=r"(k[1]) : "l"(p));
-  } else {
-    static_assert(EPL == 8, "EPL is 4 or 8");
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3])
-                 : "l"(p));
-  }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
 }
 
-template <int EPL, int THREADS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) pb_accum_kernel(
-    const double* val, const uint16_t* dstl, const int32_t* unit_bin, const int64_t* unit_e, const int32_t* unit_k,
-    int64_t nunits, int shift, int32_t n, const int32_t* outdeg, double* pr, double* cur, double base,
-    double damping, double* psum, unsigned int* bin_done, unsigned long long* next_unit, double* cta_pairs) {
-  extern __shared__ double acc[];
-  constexpr int W = 32 * EPL;  // entries per warp step
+struct alignas(16) PbStage {
+  double v[kTile];       // values, storage order
+  uint16_t ip[kTile];    // inverse permutation: storage index of each sorted place
+  uint16_t k[kTile];     // row offset of each sorted place
+};
+
+__global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
+    const double* val, const uint16_t* iperm, const uint16_t* skey, const int32_t* unit_bin, const int64_t* unit_e,
+    const int32_t* unit_k, const int32_t* unit_j, const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
+    const int32_t* outdeg, double* pr, double* cur, double base, double damping, double* slots,
+    unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs) {
+  constexpr int NW = kAccThreads / 32;
+  constexpr int WE = 32 * kAccEpl;  // sorted places per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = 1 << shift;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double lmax = 0.0, lsum = 0.0;
+  PbStage* stage = reinterpret_cast<PbStage*>(smem_raw);
+  double* acc = reinterpret_cast<double*>(smem_raw + kStages * sizeof(PbStage));  // the bin's R rows
+  __shared__ __align__(8) uint64_t bar[kStages];
+  // crossing-run pieces of the current tile: warp w's first run continuing
+  // from warp w-1 (A; thruA: it also continues into warp w+1) and its last
+  // run continuing into warp w+1 (B); flag[w] = tile counter once posted
+  __shared__ volatile double pA[NW], pB[NW];
+  __shared__ volatile int kA[NW], kB[NW], thruA[NW];
+  __shared__ volatile unsigned flag[NW];
   __shared__ long long s_unit;
   __shared__ int s_last;
+  __shared__ double s_pair[2][NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(bar + s);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < NW) flag[threadIdx.x] = 0xFFFFFFFFu;
+  __syncthreads();
+  uint32_t tc = 0;  // tiles this CTA consumed so far: stage tc % kStages, parity (tc / kStages) & 1
+  auto issue = [&](uint32_t tile_no, int64_t t0, int len) {
+    PbStage& st = stage[tile_no % kStages];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar + tile_no % kStages, (uint32_t)len * 12u);
+    bulk_g2s(st.v, val + t0, (uint32_t)len * 8u, bar + tile_no % kStages);
+    bulk_g2s(st.ip, iperm + t0, (uint32_t)len * 2u, bar + tile_no % kStages);
+    bulk_g2s(st.k, skey + t0, (uint32_t)len * 2u, bar + tile_no % kStages);
+  };
   for (;;) {
     if (threadIdx.x == 0) s_unit = (long long)atomicAdd(next_unit, 1ull);
     __syncthreads();
@@ -272,47 +379,102 @@ __global__ void __launch_bounds__(THREADS, MINB) pb_accum_kernel(
     if (u >= nunits) break;
     const int64_t b = __ldg(unit_bin + u);
     const int k = __ldg(unit_k + u);
-    const int64_t e0 = __ldg(unit_e + u), e1 = __ldg(unit_e + u + 1);
-    for (int i = threadIdx.x; i < R; i += blockDim.x) acc[i] = 0.0;
+    const int64_t e0 = __ldg(unit_e + 2 * u), e1 = __ldg(unit_e + 2 * u + 1);  // whole tiles from the bin's start
+    const int ntiles = (int)((e1 - e0 + kTile - 1) / kTile);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < kStages && i < ntiles; ++i)
+        issue(tc + i, e0 + (int64_t)i * kTile, (int)min((int64_t)kTile, e1 - e0 - (int64_t)i * kTile));
+    for (int i = threadIdx.x; i < R; i += kAccThreads) acc[i] = 0.0;
     __syncthreads();
-    const int64_t r0 = b << shift;
-    const int64_t r1 = min((int64_t)n, r0 + R);
-    for (int64_t w = (e0 & ~int64_t(EPL - 1)) + (int64_t)warp * W; w < e1; w += (int64_t)nwarps * W) {
-      const int64_t e = w + lane * EPL;
-      double v[EPL];
-      uint32_t kw[EPL / 2];
-      if (e < e1) {
-        pb_ld_vals<EPL>(val + e, v);
-        pb_ld_keys<EPL>(dstl + e, kw);
+    for (int ti = 0; ti < ntiles; ++ti, ++tc) {
+      const int len = (int)min((int64_t)kTile, e1 - e0 - (int64_t)ti * kTile);
+      const PbStage& st = stage[tc % kStages];
+      mbar_wait(bar + tc % kStages, (tc / kStages) & 1u);
+      const int i0 = threadIdx.x * kAccEpl;
+      // keys before and after this warp's places (-2: none / pad)
+      int pk = -2, nk = -2;
+      {
+        const int w0 = warp * WE, w1 = w0 + WE;
+        if (w0 > 0 && w0 < len && st.k[w0 - 1] != kPadKey) pk = st.k[w0 - 1];
+        if (w1 < len && st.k[w1] != kPadKey) nk = st.k[w1];
+      }
+      int kk[kAccEpl];
+      double x[kAccEpl];
+      if (i0 < len) {
+        uint32_t kr[kAccEpl / 2], ir[kAccEpl / 2];
+        if constexpr (kAccEpl == 4) {
+          const uint2 kw = *reinterpret_cast<const uint2*>(st.k + i0);
+          const uint2 iw = *reinterpret_cast<const uint2*>(st.ip + i0);
+          kr[0] = kw.x, kr[1] = kw.y, ir[0] = iw.x, ir[1] = iw.y;
+        } else {
+          const uint4 kw = *reinterpret_cast<const uint4*>(st.k + i0);
+          const uint4 iw = *reinterpret_cast<const uint4*>(st.ip + i0);
+          kr[0] = kw.x, kr[1] = kw.y, kr[2] = kw.z, kr[3] = kw.w;
+          ir[0] = iw.x, ir[1] = iw.y, ir[2] = iw.z, ir[3] = iw.w;
+        }
+#pragma unroll
+        for (int j = 0; j < kAccEpl; ++j) {
+          const uint32_t kj = (kr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+          kk[j] = kj == kPadKey ? -1 : (int)kj;
+          x[j] = st.v[(ir[j >> 1] >> (16 * (j & 1))) & 0xFFFFu];
+        }
       } else {
 #pragma unroll
-        for (int j = 0; j < EPL / 2; ++j) kw[j] = 0xFFFFFFFFu;
-#pragma unroll
-        for (int j = 0; j < EPL; ++j) v[j] = 0.0;
+        for (int j = 0; j < kAccEpl; ++j) {
+          kk[j] = -1;
+          x[j] = 0.0;
+        }
       }
-      // fold: first run (fk, fs), current run (ck, cs); interior runs go out
+      // one run's sum lands: a plain add, a posted piece, or a chain's end
+      // (kept in registers: it is resolved after this warp's flag is up, so
+      // no warp ever waits on a warp that is itself waiting)
+      int pend_key = -1;
+      double pend_s = 0.0;
+      auto land = [&](int key, double s) {
+        if (key == pk) {
+          if (key == nk) {  // the whole warp is one run continuing both ways
+            pA[warp] = s;
+            kA[warp] = key;
+            thruA[warp] = 1;
+          } else {
+            pend_key = key;
+            pend_s = s;
+          }
+        } else if (key == nk) {
+          pB[warp] = s;
+          kB[warp] = key;
+        } else {
+          acc[key] += s;
+        }
+      };
+      if (lane == 0) {
+        kA[warp] = -1;
+        kB[warp] = -1;
+        thruA[warp] = 0;
+      }
+      __syncwarp();
+      // fold: first run (fk, fs), current run (ck, cs); interior runs land at once
       int fk = -2, ck = -2;
       double fs = 0.0, cs = 0.0;
       bool multi = false;
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) {
-        const uint32_t raw = (kw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-        const int ki = (e + i >= e0 && e + i < e1) ? (int)raw : -1;
+      for (int i = 0; i < kAccEpl; ++i) {
+        const int ki = kk[i];
         if (i == 0) {
           ck = ki;
-          cs = v[0];
+          cs = x[0];
         } else if (ki == ck) {
-          cs += v[i];
+          cs += x[i];
         } else {
           if (!multi) {
             fk = ck;
             fs = cs;
             multi = true;
           } else if (ck >= 0) {
-            atomicAdd(&acc[ck], cs);  // a run strictly inside this lane
+            land(ck, cs);  // a run strictly inside this lane
           }
           ck = ki;
-          cs = v[i];
+          cs = x[i];
         }
       }
       if (!multi) {
@@ -321,8 +483,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pb_accum_kernel(
       }
       // carry the tails: lane L continues lane L-1's tail if its first key
       // equals that tail's key; a single-run continuing lane passes it on
-      const int pk = __shfl_up_sync(0xffffffffu, ck, 1);
-      const bool cont = lane > 0 && fk >= 0 && fk == pk;
+      const int pkl = __shfl_up_sync(0xffffffffu, ck, 1);
+      const bool cont = lane > 0 && fk >= 0 && fk == pkl;
       const bool through = cont && !multi;
       const unsigned starts = __ballot_sync(0xffffffffu, !through);
       double S = cs;
@@ -337,66 +499,114 @@ __global__ void __launch_bounds__(THREADS, MINB) pb_accum_kernel(
       }
       const double Sp = __shfl_up_sync(0xffffffffu, S, 1);
       const bool next_cont = __shfl_down_sync(0xffffffffu, cont, 1) && lane < 31;
-      if (multi && fk >= 0) atomicAdd(&acc[fk], cont ? fs + Sp : fs);  // the first run ends in this lane
-      if (!next_cont && ck >= 0) atomicAdd(&acc[ck], S);                // the tail run ends here
-    }
-    __syncthreads();
-    bool fin = true, from_psum = false;
-    if (k > 1) {
-      for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        const double x = acc[r - r0];
-        if (x != 0.0) atomicAdd(psum + r, x);
+      if (multi && fk >= 0) land(fk, cont ? fs + Sp : fs);  // the first run ends in this lane
+      if (!next_cont && ck >= 0) land(ck, S);                // the tail run ends here
+      __syncwarp();
+      if (lane == 0) {  // this warp's pieces are posted
+        __threadfence_block();
+        flag[warp] = tc;
       }
+      if (pend_key >= 0) {
+        // a chain ends here: wait for the earlier warps' pieces, add in warp order
+        int w0 = warp - 1;
+        while (true) {
+          while (flag[w0] != tc) {
+          }
+          __threadfence_block();
+          if (!(kA[w0] == pend_key && thruA[w0])) break;
+          --w0;
+        }
+        double sum = pB[w0];
+        for (int q = w0 + 1; q < warp; ++q) sum += pA[q];
+        acc[pend_key] += sum + pend_s;
+      }
+      __syncthreads();  // every add of the tile landed; the stage is free
+      if (threadIdx.x == 0 && ti + kStages < ntiles)
+        issue(tc + kStages, e0 + (int64_t)(ti + kStages) * kTile,
+              (int)min((int64_t)kTile, e1 - e0 - (int64_t)(ti + kStages) * kTile));
+    }
+    const int64_t r0 = b << shift;
+    const int64_t r1 = min((int64_t)n, r0 + R);
+    bool fin = true, from_slots = false;
+    const int64_t slot0 = k > 1 ? (int64_t)__ldg(unit_slot + u) : 0;  // the bin's first slot
+    if (k > 1) {
+      // a split bin: this unit's partial sums go to its slot; the last unit
+      // to finish sums the k slots in unit order
+      const int64_t slot = slot0 + __ldg(unit_j + u);
+      for (int64_t r = r0 + threadIdx.x; r < r1; r += kAccThreads) slots[slot * R + (r - r0)] = acc[r - r0];
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) s_last = atomicAdd(bin_done + b, 1u) == (unsigned)(k - 1);
       __syncthreads();
       fin = s_last;
-      from_psum = true;
+      from_slots = true;
       if (fin) __threadfence();
     }
     if (fin) {
-      for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        double sum;
-        if (from_psum) {
-          sum = __ldcg(psum + r);
-          psum[r] = 0.0;
-        } else {
-          sum = acc[r - r0];
+      double lmax = 0.0, lsum = 0.0;
+      // rows in batches of 4 per thread: the pr / outdeg loads of a batch are
+      // issued together (one latency per batch, not per row)
+      constexpr int RB = 4;
+      for (int64_t rb = r0 + threadIdx.x; rb < r1; rb += (int64_t)RB * kAccThreads) {
+        double old[RB], sum[RB];
+        int od[RB];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const int64_t r = rb + (int64_t)q * kAccThreads;
+          old[q] = 0.0;
+          od[q] = 0;
+          sum[q] = 0.0;
+          if (r < r1) {
+            old[q] = __ldcg(pr + r);
+            od[q] = __ldg(outdeg + r);
+            if (from_slots) {
+              sum[q] = __ldcg(slots + slot0 * R + (r - r0));
+              for (int j = 1; j < k; ++j) sum[q] += __ldcg(slots + (slot0 + j) * R + (r - r0));
+            } else {
+              sum[q] = acc[r - r0];
+            }
+          }
         }
-        const double nv = __dadd_rn(base, __dmul_rn(damping, sum));
-        const double dd = fabs(nv - pr[r]);
-        pr[r] = nv;
-        const int od = __ldg(outdeg + r);
-        if (od > 0) cur[r] = __ddiv_rn(nv, (double)od);
-        lmax = fmax(lmax, dd);
-        lsum += dd;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const int64_t r = rb + (int64_t)q * kAccThreads;
+          if (r < r1) {
+            const double nv = __dadd_rn(base, __dmul_rn(damping, sum[q]));
+            const double dd = fabs(nv - old[q]);
+            pr[r] = nv;
+            if (od[q] > 0) cur[r] = __ddiv_rn(nv, (double)od[q]);
+            lmax = fmax(lmax, dd);
+            lsum += dd;
+          }
+        }
       }
-      if (from_psum && threadIdx.x == 0) bin_done[b] = 0u;
+      if (from_slots && threadIdx.x == 0) bin_done[b] = 0u;
+      // the bin's residual pair, reduced in a fixed thread order
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+      }
+      if (lane == 0) {
+        s_pair[0][warp] = lmax;
+        s_pair[1][warp] = lsum;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        lmax = lane < NW ? s_pair[0][lane] : 0.0;
+        lsum = lane < NW ? s_pair[1][lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+          lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        }
+        if (lane == 0) {
+          bin_pairs[2 * b] = lmax;
+          bin_pairs[2 * b + 1] = lsum;
+        }
+      }
     }
     __syncthreads();
-  }
-  __shared__ double sm[2][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-  }
-  if (lane == 0) {
-    sm[0][warp] = lmax;
-    sm[1][warp] = lsum;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    lmax = lane < nwarps ? sm[0][lane] : 0.0;
-    lsum = lane < nwarps ? sm[1][lane] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) {
-      lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    }
-    if (lane == 0) {
-      cta_pairs[2 * blockIdx.x] = lmax;
-      cta_pairs[2 * blockIdx.x + 1] = lsum;
-    }
   }
 }
 
@@ -405,20 +615,42 @@ __global__ void pb_bin_edges_kernel(const int64_t* row, int32_t n, int shift, in
   if (b <= nbins) be[b] = row[min((int64_t)n, b << shift)];
 }
 
-// Fixed-order reduction of the per-CTA pairs (one warp).
-__global__ void pb_reduce_kernel(int nctas, const double* cta_pairs, double* err, double* l1) {
+// Fixed-order reduction of the per-bin residual pairs: thread t folds a
+// contiguous run of bins in order, then a fixed shuffle/shared tree.
+constexpr int kReduceThreads = 1024;
+__global__ void __launch_bounds__(kReduceThreads) pb_reduce_kernel(int64_t nbins, const double* bin_pairs,
+                                                                   double* err, double* l1) {
+  const int64_t per = (nbins + kReduceThreads - 1) / kReduceThreads;
+  const int64_t b0 = (int64_t)threadIdx.x * per, b1 = min(nbins, b0 + per);
   double mx = 0.0, sm = 0.0;
-  for (int i = threadIdx.x; i < nctas; i += 32) {
-    mx = fmax(mx, cta_pairs[2 * i]);
-    sm += cta_pairs[2 * i + 1];
+  for (int64_t b = b0; b < b1; ++b) {
+    mx = fmax(mx, bin_pairs[2 * b]);
+    sm += bin_pairs[2 * b + 1];
   }
+  __shared__ double s[2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     sm += __shfl_xor_sync(0xffffffffu, sm, o);
   }
-  if (threadIdx.x == 0) {
-    *err = mx;
-    *l1 = sm;
+  if (lane == 0) {
+    s[0][warp] = mx;
+    s[1][warp] = sm;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    mx = s[0][lane];
+    sm = s[1][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    if (lane == 0) {
+      *err = mx;
+      *l1 = sm;
+    }
   }
 }
 
@@ -454,6 +686,7 @@ std::vector<int64_t> pb_wave_bins(const std::vector<int64_t>& bin_edge, uint32_t
   const int64_t nbins = (int64_t)bin_edge.size() - 1;
   const int64_t m = bin_edge.back();
   std::vector<int64_t> wb{0};
+  S = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(S, nbins));  // at most one wave per bin
   for (uint32_t w = 1; w < S; ++w) {
     const int64_t target = (int64_t)((double)m * w / S);
     const int64_t b = std::lower_bound(bin_edge.begin(), bin_edge.end() - 1, target) - bin_edge.begin();
@@ -532,7 +765,6 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = alloc((void**)&plan.ctr, 2 * (size_t)W * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = alloc((void**)&plan.cta_pairs, 2 * (size_t)W * pb.p2_grid * sizeof(double));
   for (void* q : {(void*)npieces, (void*)piece_off, (void*)d_wb, temp})
     if (q) cudaFreeAsync(q, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -542,39 +774,60 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     return e;
   }
   {
-    // phase-2 units: bins, heavy ones cut into pieces of about `piece`
-    // entries: small enough that each wave has several units per CTA, never
-    // below twice the average bin (a split bin pays psum atomics per row;
-    // splitting config 4's even bins cost 5-10%)
+    // phase-2 units: bins, heavy ones cut into runs of whole tiles of about
+    // `piece` entries: small enough that each wave has several units per
+    // CTA, never below twice the average bin (a split bin writes and re-reads
+    // a slot of row sums per unit; splitting config 4's even bins cost 5-10%)
     const int64_t avg_bin = pb.m / std::max<int64_t>(1, pb.nbins);
     int64_t piece = std::max<int64_t>({int64_t(1) << 16, 2 * avg_bin, pb.m / ((int64_t)pb.p2_grid * 8 * W)});
     if (const char* v = std::getenv("FPR_B200_PB_PIECE")) piece = std::max<int64_t>(32, std::atoll(v));  // tests
-    std::vector<int32_t> ubin, uk;
+    const int64_t piece_tiles = std::max<int64_t>(1, (piece + kTile - 1) / kTile);
+    std::vector<int32_t> ubin, uk, uj, uslot;
     std::vector<int64_t> ue;
+    int64_t nslots = 0;
     plan.unit0.assign(W + 1, 0);
     for (int w = 0; w < W; ++w) {
       plan.unit0[w] = (int64_t)ubin.size();
       for (int64_t b = plan.wave_bin[w]; b < plan.wave_bin[w + 1]; ++b) {
-        const int64_t E = pb.bin_edge[b + 1] - pb.bin_edge[b];
-        const int64_t k = std::max<int64_t>(1, (E + piece - 1) / piece);
+        const int64_t p0 = pb.bin_pos[b], p1 = pb.bin_pos[b + 1];
+        const int64_t tiles = std::max<int64_t>(1, (p1 - p0 + kTile - 1) / kTile);
+        const int64_t k = (tiles + piece_tiles - 1) / piece_tiles;
         for (int64_t j = 0; j < k; ++j) {
           ubin.push_back((int32_t)b);
           uk.push_back((int32_t)k);
-          ue.push_back(pb.bin_edge[b] + E * j / k);
+          uj.push_back((int32_t)j);
+          uslot.push_back(k > 1 ? (int32_t)nslots : -1);
+          ue.push_back(std::min(p1, p0 + tiles * j / k * kTile));
         }
+        if (k > 1) nslots += k;
       }
     }
     plan.unit0[W] = (int64_t)ubin.size();
-    ue.push_back(pb.m);
-    e = alloc((void**)&plan.unit_bin, ubin.size() * sizeof(int32_t));
-    if (e == cudaSuccess) e = alloc((void**)&plan.unit_k, uk.size() * sizeof(int32_t));
-    if (e == cudaSuccess) e = alloc((void**)&plan.unit_e, ue.size() * sizeof(int64_t));
+    // unit u ends where unit u + 1 starts, or at its bin's end
+    std::vector<int64_t> uend(ubin.size() + 1);
+    for (size_t u = 0; u < ubin.size(); ++u)
+      uend[u] = (u + 1 < ubin.size() && ubin[u + 1] == ubin[u]) ? ue[u + 1] : pb.bin_pos[ubin[u] + 1];
+    // unit_e holds [start, end) pairs flattened: start of u at 2u, end at 2u + 1
+    std::vector<int64_t> ue2(2 * ubin.size());
+    for (size_t u = 0; u < ubin.size(); ++u) {
+      ue2[2 * u] = ue[u];
+      ue2[2 * u + 1] = uend[u];
+    }
+    const size_t U = ubin.size();
+    e = alloc((void**)&plan.unit_bin, U * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_k, U * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_j, U * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_slot, U * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_e, ue2.size() * sizeof(int64_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.slots, (size_t)std::max<int64_t>(1, nslots) * sizeof(double) << pb.shift);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(plan.unit_bin, ubin.data(), ubin.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+      e = cudaMemcpyAsync(plan.unit_bin, ubin.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(plan.unit_k, uk.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(plan.unit_j, uj.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(plan.unit_k, uk.data(), uk.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+      e = cudaMemcpyAsync(plan.unit_slot, uslot.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(plan.unit_e, ue.data(), ue.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+      e = cudaMemcpyAsync(plan.unit_e, ue2.data(), ue2.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host vectors die at the end of this block
     if (e != cudaSuccess) {
       for (void* q : plan.allocs) cudaFreeAsync(q, st);
@@ -591,15 +844,17 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   *msg = nullptr;
   pb = PbSet{};
   const int sms = sm_count();
-  const int64_t n = g.n, m = g.m;
+  const int64_t n = g.n;
   const int64_t nbins = n > 0 ? (n + (1ll << shift) - 1) >> shift : 0;
   const int64_t nchunks = std::max<int64_t>(1, (n + (1ll << chunk_shift) - 1) >> chunk_shift);
   // layout kernel: chunk counters + the bin's (2^shift + 1) relative row offsets
   const size_t hist_smem = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t) +
                            (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t);
-  const size_t acc_smem = (size_t)sizeof(double) << shift;
-  if (n == 0 || shift < 5 || shift > 14 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 192 * 1024 ||
-      nbins * nchunks > (1ll << 31)) {
+  const size_t acc_smem = ((size_t)sizeof(double) << shift) + (size_t)kStages * sizeof(PbStage);
+  uint16_t* dstl = nullptr;  // per-entry row offsets, storage order: input of the tile sort
+  int64_t* d_pos = nullptr;
+  if (n == 0 || shift < 5 || shift > 13 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 192 * 1024 ||
+      acc_smem + 2048 > 227 * 1024 || nbins * nchunks > (1ll << 31)) {
     *msg = "bin/chunk geometry out of range";
     return cudaSuccess;
   }
@@ -612,53 +867,63 @@ cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t
   pb.chunk_shift = chunk_shift;
   pb.nbins = nbins;
   pb.nchunks = nchunks;
-  pb.m = m;
-  PK(alloc((void**)&pb.counts, nbins * nchunks * sizeof(uint32_t)));
-  PK(alloc((void**)&pb.start, nbins * nchunks * sizeof(int64_t)));
-  PK(alloc((void**)&pb.src_bm, m * sizeof(int32_t)));
-  // 8 pad entries: the lane-sequential phase 2 loads 8-entry vectors that may
-  // run past the end
-  PK(alloc((void**)&pb.dstl_bm, (m + 8) * sizeof(uint16_t)));
-  PK(alloc((void**)&pb.val, (m + 8) * sizeof(double)));
+  pb.m = g.m;
   {
-    // bin edge offsets (host copy: wave plans cut waves and phase-2 units)
+    // bin edge offsets (host copy: wave plans cut waves from them) and the
+    // bins' 8-aligned storage positions (16-B aligned TMA copies of tiles)
     std::vector<int64_t> be;
     e = pb_bin_edges(g, shift, st, &be);
     if (e != cudaSuccess) goto out;
     pb.bin_edge = be;
-    for (int64_t b = 0; b < nbins; ++b)
+    pb.bin_pos.assign(nbins + 1, 0);
+    for (int64_t b = 0; b < nbins; ++b) {
       if (be[b + 1] - be[b] >= (1ll << 32)) {  // the layout kernel's uint32 in-bin offsets
         *msg = "a bin holds 2^32 or more edges (use a smaller FPR_B200_PB_SHIFT)";
-        break;
+        goto out;
       }
-    if (*msg) goto out;
+      pb.bin_pos[b + 1] = pb.bin_pos[b] + ((be[b + 1] - be[b] + 7) & ~int64_t(7));
+    }
   }
+  pb.mpad = pb.bin_pos[nbins];
+  PK(alloc((void**)&pb.counts, nbins * nchunks * sizeof(uint32_t)));
+  PK(alloc((void**)&pb.start, nbins * nchunks * sizeof(int64_t)));
+  PK(alloc((void**)&pb.src_bm, pb.mpad * sizeof(int32_t)));
+  PK(alloc((void**)&pb.iperm, pb.mpad * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.skey, pb.mpad * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.val, pb.mpad * sizeof(double)));
+  PK(alloc((void**)&pb.bin_pos_d, (nbins + 1) * sizeof(int64_t)));
+  PK(cudaMemsetAsync(pb.val, 0, pb.mpad * sizeof(double), st));  // pad values stay 0
+  PK(cudaMemcpyAsync(pb.bin_pos_d, pb.bin_pos.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PK(cudaMallocAsync(&dstl, pb.mpad * sizeof(uint16_t), st));
   {
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
     PK(cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem));
     pb_layout_kernel<<<(unsigned)std::min<int64_t>(nbins, sms), kPbThreads, hist_smem, st>>>(
-        g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.counts, pb.start, pb.src_bm,
-        pb.dstl_bm);
+        g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.bin_pos_d, pb.counts, pb.start,
+        pb.src_bm, dstl);
+    PK(cudaGetLastError());
+    pb_tile_sort_kernel<<<(unsigned)std::min<int64_t>(nbins, (int64_t)sms * 2), kAccThreads, 0, st>>>(
+        dstl, pb.bin_pos_d, nbins, pb.iperm, pb.skey);
     PK(cudaGetLastError());
   }
+  PK(alloc((void**)&pb.bin_pairs, 2 * nbins * sizeof(double)));
+  PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
+  PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
+  PK(cudaFuncSetAttribute(pb_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
   {
-    // phase-2 residency: the bin's accumulators in shared memory,
-    // FPR_PB_ACC_CTAS CTAs per SM when they fit
-    const int by_smem = (int)std::max<size_t>(1, (size_t)(227 * 1024) / (acc_smem + 1024));
-    pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * std::min(FPR_PB_ACC_CTAS, by_smem));
+    // phase-2 residency: the CTAs per SM that fit the bin's accumulators +
+    // the staged tiles (two at 2^13-row bins), up to kAccCtas
+    int per_sm = 0;
+    PK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pb_accum_kernel, kAccThreads, acc_smem));
+    per_sm = std::max(1, std::min(per_sm, kAccCtas));
+    pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * per_sm);
     pb.p1_grid = sms * 8;
+    pb.acc_smem = (int)acc_smem;
   }
-  {
-    PK(alloc((void**)&pb.psum, n * sizeof(double)));
-    PK(cudaMemsetAsync(pb.psum, 0, n * sizeof(double), st));
-    PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
-    PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
-  }
-  PK(cudaFuncSetAttribute(pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
   PK(cudaStreamSynchronize(st));
 out:
+  if (dstl) cudaFreeAsync(dstl, st);
   if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
     cudaStreamSynchronize(st);
@@ -679,15 +944,13 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
                                                               plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    pb_accum_kernel<FPR_PB_EPL, FPR_PB_ACC_THREADS, FPR_PB_ACC_CTAS>
-        <<<pb.p2_grid, FPR_PB_ACC_THREADS, (size_t)sizeof(double) << pb.shift, st>>>(
-            pb.val, pb.dstl_bm, plan.unit_bin + u0, plan.unit_e + u0, plan.unit_k + u0, plan.unit0[w + 1] - u0,
-            pb.shift,
-            g.n, g.outdeg, pr, cur, base, damping, pb.psum, pb.bin_done, plan.ctr + W + w,
-            plan.cta_pairs + 2 * (size_t)w * pb.p2_grid);
+    pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
+        pb.val, pb.iperm, pb.skey, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_k + u0, plan.unit_j + u0,
+        plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, cur, base, damping, plan.slots,
+        pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  pb_reduce_kernel<<<1, 32, 0, st>>>(W * pb.p2_grid, plan.cta_pairs, err, l1);
+  pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1);
   return cudaGetLastError();
 }
 

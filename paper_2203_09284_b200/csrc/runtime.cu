@@ -242,8 +242,8 @@ struct fpr_b200_graph {
   uint32_t nparts = 1, part_id = 0;
   uint32_t flags = 0;
   int32_t* new_of_old = nullptr;  // FPR_B200_OPT_REORDER(_SOURCES): caller id -> internal id
-  BlockSet* blk = nullptr;        // FPR_B200_OPT_BLOCKED: built at the first EC run
-  PbSet* pb = nullptr;            // FPR_B200_OPT_PB: built at the first EC run
+  bool use_pb = false;            // propagation-blocked sweeps (decided at creation, pb_wanted)
+  PbSet* pb = nullptr;            // their layout: built at the first EC / lockstep / FUSED run
   uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
   double* part_pr[2] = {nullptr, nullptr};  // part ranks ping-pong ([0] = pr)
   int part_pr_cur = 0;                       // buffer holding the latest sweep
@@ -280,11 +280,6 @@ void destroy_handle(fpr_b200_graph* h) {
     free_pb(*h->pb, h->stream);
     delete h->pb;
     h->pb = nullptr;
-  }
-  if (h->blk) {
-    free_blocks(*h->blk, h->stream);
-    delete h->blk;
-    h->blk = nullptr;
   }
   if (h->stream) cudaStreamSynchronize(h->stream);
   release_staging(h->hs);
@@ -358,6 +353,21 @@ constexpr int64_t kTraceWarps = 8192;  // per-warp timestamps after the tail par
 constexpr int64_t kTraceWarps = 0;
 #endif
 
+// Sweep kind, fixed at creation: OPT_PULL / OPT_PB force it; by default
+// propagation blocking when the contribution vector (8 n bytes) exceeds twice
+// the L2 -- there the pull gathers miss L2 and each miss moves ~64 B of DRAM
+// for 8 useful bytes (configs 4/5: PB 2.1-2.2x faster per sweep), while on
+// L2-resident vectors (configs 1-3) the pull sweep wins.
+// Multi-GPU parts always use the pull sweep.
+bool pb_wanted(const fpr_b200_graph* h) {
+  if (h->nparts > 1 || (h->flags & FPR_B200_OPT_PULL)) return false;
+  if (h->flags & FPR_B200_OPT_PB) return true;
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+  if (const char* v = std::getenv("FPR_B200_PB_AUTO_BYTES")) return (int64_t)h->g.n * 8 > std::atoll(v);  // tests
+  return (int64_t)h->g.n * (int64_t)sizeof(double) > 2 * (int64_t)l2;
+}
+
 int finish_graph(fpr_b200_graph* h) {
   if ((h->flags & (FPR_B200_OPT_REORDER | FPR_B200_OPT_REORDER_SOURCES)) && h->g.n > 1) {
     DevGraph re;
@@ -403,6 +413,7 @@ int finish_graph(fpr_b200_graph* h) {
     return rc;
   CK(cudaMemsetAsync(h->bar, 0, sizeof(GridBar), h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  h->use_pb = pb_wanted(h);
   return FPR_B200_OK;
 }
 
@@ -506,8 +517,7 @@ void pb_geometry(int* shift, int* chunk_shift) {
 uint32_t lockstep_waves(const fpr_b200_graph* h) {
   if (h->wave_count) return h->wave_count;
   const int64_t items = (int64_t)h->g.n + h->g.m;
-  if ((h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
-    return (uint32_t)std::min<int64_t>(8, std::max<int64_t>(2, items >> 27));
+  if (h->use_pb) return (uint32_t)std::min<int64_t>(8, std::max<int64_t>(2, items >> 27));
   return (uint32_t)std::min<int64_t>(32, std::max<int64_t>(2, items >> 25));
 }
 
@@ -925,7 +935,7 @@ int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t*
   if (h->g.n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
   CK(cudaSetDevice(h->device));
   std::vector<uint64_t> vs;
-  if ((h->flags & FPR_B200_OPT_PB) && h->nparts <= 1) {
+  if (h->use_pb) {
     // propagation-blocked lockstep: waves of consecutive bins (run_pb)
     int shift = 0, chunk_shift = 0;
     pb_geometry(&shift, &chunk_shift);
@@ -955,137 +965,14 @@ int fpr_b200_graph_wave_starts(fpr_b200_graph* h, uint32_t wave_count, uint64_t*
 const double* fpr_b200_graph_ranks_device(const fpr_b200_graph* h) { return h ? h->pr : nullptr; }
 
 namespace {
-// The EC solve over the source-blocked layout: per iteration, one accumulate
-// pass of the solve kernel per column block (in block order), then the apply
-// pass and its fixed-order residual reduction; the stop rule is checked on
-// the host after each iteration (pagerank.hpp:141), so the iteration count is
-// the reference's.
-int run_blocked(fpr_b200_graph* h, const fpr_config* cfg, double* ranks_out, double* errors_out,
-                double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
-  const DevGraph& g = h->g;
-  float setup_ms = 0.f, solve_ms = 0.f;
-  uint64_t launches = 0;
-  CK(cudaEventRecord(h->ev[0], h->stream));
-  if (!h->blk) {
-    // 2^24-vertex blocks (128 MB of contributions) measured best on configs
-    // 4/5; FPR_B200_BLOCK_SHIFT overrides.
-    int shift = 24;
-    if (const char* s = std::getenv("FPR_B200_BLOCK_SHIFT")) shift = std::max(10, std::min(30, std::atoi(s)));
-    while ((((int64_t)g.n + (1ll << shift) - 1) >> shift) > 256) ++shift;
-    auto* bs = new BlockSet;
-    const char* msg = nullptr;
-    cudaError_t e = build_blocks(g, shift, h->stream, *bs, &msg);
-    if (e != cudaSuccess || msg) {
-      delete bs;
-      if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200 blocked layout: ") + msg);
-      return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
-                  std::string("fpr_b200 blocked layout: ") + cudaGetErrorString(e));
-    }
-    h->blk = bs;
-  }
-  BlockSet& bs = *h->blk;
-  CK(launch_init(g, h->pr, h->contrib[0], h->stream));
-  ++launches;
-  CK(cudaEventRecord(h->ev[1], h->stream));
-  const int wpb = solve_block_threads(kEC) / 32;
-  SolveParams p{};
-  p.nsrc = g.n;
-  p.pr = h->pr;
-  p.pr_out = h->pr;
-  p.damping = cfg->damping;
-  p.base = (1.0 - cfg->damping) / (double)g.n;
-  p.threshold = 0.0;
-  p.norm = h->norm;
-  p.max_iters = 1;
-  p.parity0 = 0;
-  p.nwaves = 1;
-  p.tail_partial = bs.tail_partial;
-  p.partial = bs.partial;
-  p.errors = bs.scratch;
-  p.l1errors = bs.scratch + 1;
-  p.iter_ns = reinterpret_cast<unsigned long long*>(bs.scratch + 2);
-  p.partials = h->partials;
-  p.totals = h->totals;
-  p.bar = h->bar;
-  p.out_iters = &h->d_status->iters;
-  p.out_stop = &h->d_status->stop;
-  p.out_last = h->d_status->last;
-  uint64_t total = 0;
-  int par = 0;
-  double last_err = 1.0, last_l1 = 1.0;
-  while (total < cfg->max_iterations) {
-    double* prev = h->contrib[par];
-    double* cur = h->contrib[par ^ 1];
-    CK(cudaEventRecord(h->ev[1], h->stream));
-    for (const BlockSet::Block& B : bs.blocks) {
-      if (B.view.n == 0) continue;
-      SolveParams q = p;
-      q.n = B.view.n;
-      q.row = B.view.row;
-      q.src = B.view.src;
-      q.task_row = B.part.task_row;
-      q.task_edge = B.part.task_edge;
-      q.head_first = B.part.head_first;
-      q.task_bits = B.part.task_bits;
-      q.ntasks = B.part.ntasks;
-      q.wave_task = B.waves;
-      q.wave_row = B.waves + 2;
-      q.brow_ids = B.ids;
-      q.contrib0 = prev;
-      q.contrib1 = cur;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[0], (B.part.ntasks + wpb - 1) / wpb));
-      CK(launch_solve(kEC, grid, q, h->stream));
-      ++launches;
-    }
-    CK(launch_apply(bs, g.n, g.outdeg, h->pr, cur, p.base, p.damping, h->d_errors, h->d_l1, h->stream));
-    launches += 2;
-    CK(cudaEventRecord(h->ev[2], h->stream));
-    CK(cudaMemcpyAsync(h->h_errors, h->d_errors, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(h->h_l1, h->d_l1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (total == 0) cudaEventElapsedTime(&setup_ms, h->ev[0], h->ev[1]);
-    float it_ms = 0.f;
-    cudaEventElapsedTime(&it_ms, h->ev[1], h->ev[2]);
-    solve_ms += it_ms;
-    if (errors_out && errors_cap < total + 1)
-      return fail(FPR_B200_EINVAL, "fpr_b200_run: errors buffer holds " + std::to_string(errors_cap) +
-                                       " entries, need " + std::to_string(total + 1));
-    last_err = h->h_errors[0];
-    last_l1 = h->h_l1[0];
-    if (errors_out) errors_out[total] = last_err;
-    if (l1_out) l1_out[total] = last_l1;
-    if (iter_ns_out) iter_ns_out[total] = (uint64_t)(it_ms * 1e6);
-    ++total;
-    par ^= 1;
-    if ((h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err) <= cfg->threshold) break;
-  }
-  if (ranks_out) {
-    const double* src = h->pr;
-    if (h->new_of_old) {
-      CK(launch_gather_ranks(h->pr, h->new_of_old, g.n, h->ranks_tmp, h->stream));
-      src = h->ranks_tmp;
-    }
-    CK(cudaMemcpyAsync(ranks_out, src, g.n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  }
-  CK(cudaStreamSynchronize(h->stream));
-  if (result) {
-    result->iterations = total;
-    const double crit = h->norm == FPR_B200_NORM_L1 ? last_l1 : last_err;
-    result->converged = (total > 0 && crit <= cfg->threshold) ? 1 : 0;
-    result->final_error = total > 0 ? last_err : 1.0;
-    result->setup_ms = setup_ms;
-    result->solve_ms = solve_ms;
-    result->kernel_launches = launches;
-  }
-  return FPR_B200_OK;
-}
-
 // Propagation-blocked sweeps (FPR_B200_OPT_PB, pb.cu).  EC: one wave, the
 // gather reads contrib[par] and the rows write contrib[par ^ 1].  Lockstep
 // (the deterministic FusEd schedule): S waves of consecutive bins, gathered
 // from and written to contrib[0] in place, so wave w reads this sweep's
 // contributions of waves < w (fo_pagerank_lockstep).  The host checks the
-// stop rule after each sweep, exactly like the blocked engine above.
+// stop rule after each sweep.
+constexpr int kPbDeclined = -1;  // run_pb: auto-selected layout did not fit; run the pull sweep
+
 int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* ranks_out, double* errors_out,
            double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
   const DevGraph& g = h->g;
@@ -1100,6 +987,13 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
     cudaError_t e = build_pb(g, shift, chunk_shift, h->stream, *pb, &msg);
     if (e != cudaSuccess || msg) {
       delete pb;
+      if (!(h->flags & FPR_B200_OPT_PB) && (msg || e == cudaErrorMemoryAllocation)) {
+        // auto-selected and it does not fit (or the geometry does not apply):
+        // the pull sweep runs instead -- a device engine choice, not a fallback
+        cudaGetLastError();
+        h->use_pb = false;
+        return kPbDeclined;
+      }
       if (msg) return fail(FPR_B200_EINVAL, std::string("fpr_b200 propagation-blocked layout: ") + msg);
       return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
                   std::string("fpr_b200 propagation-blocked layout: ") + cudaGetErrorString(e));
@@ -1164,6 +1058,7 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
     result->setup_ms = setup_ms;
     result->solve_ms = solve_ms;
     result->kernel_launches = launches;
+    result->sweep = FPR_B200_SWEEP_PB;
   }
   return FPR_B200_OK;
 }
@@ -1179,10 +1074,13 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
   if (engine != kEC && engine != kFused && engine != kLockstep)
     return fail(FPR_B200_EINVAL, "fpr_b200: unknown engine " + std::to_string(engine));
   CK(cudaSetDevice(h->device));
-  if ((engine == kEC || engine == kLockstep) && (h->flags & FPR_B200_OPT_PB) && h->nparts <= 1)
-    return run_pb(h, engine == kLockstep, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
-  if (engine == kEC && (h->flags & FPR_B200_OPT_BLOCKED) && h->nparts <= 1)
-    return run_blocked(h, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
+  // Propagation-blocked graphs: EC runs PB Jacobi sweeps; lockstep and FUSED
+  // run the lockstep Gauss-Seidel schedule on PB sweeps (the fastest FusEd
+  // schedule there, within the fused_par contract).
+  if (h->use_pb) {
+    rc = run_pb(h, engine != kEC, cfg, ranks_out, errors_out, l1_out, iter_ns_out, errors_cap, result);
+    if (rc != kPbDeclined) return rc;
+  }
 
   // Jacobi = one wave; lockstep = the cached wave schedule; async = all tasks.
   const Waves* wv = nullptr;
@@ -1306,6 +1204,7 @@ int fpr_b200_run(fpr_b200_graph* h, int engine, const fpr_config* cfg, double* r
     result->setup_ms = setup_ms;
     result->solve_ms = solve_ms;
     result->kernel_launches = launches;
+    result->sweep = FPR_B200_SWEEP_PULL;
   }
   return FPR_B200_OK;
 }
@@ -1638,6 +1537,13 @@ int fpr_b200_pagerank(const fpr_graph_view* view, int engine, const fpr_config* 
   int rc = validate_config(cfg);
   if (rc) return rc;
   if (view->n == 0) return fail(FPR_B200_EINVAL, "pagerank: graph has no vertices");
+  if (opts && opts->ndevices > 1) {  // one host thread drives opts->ndevices parts
+    fpr_b200_mgpu* mg = nullptr;
+    if ((rc = fpr_b200_mgpu_create(view, opts, &mg))) return rc;
+    rc = fpr_b200_mgpu_run(mg, engine, cfg, ranks_out, errors_out, nullptr, errors_cap, result);
+    fpr_b200_mgpu_destroy(mg);
+    return rc;
+  }
   fpr_b200_graph* h = nullptr;
   if ((rc = fpr_b200_graph_create(view, opts, &h))) return rc;
   rc = fpr_b200_run(h, engine, cfg, ranks_out, errors_out, nullptr, nullptr, errors_cap, result);
@@ -1882,3 +1788,9 @@ extern "C" int fpr_b200_debug_warp_times(fpr_b200_graph* h, uint64_t* out, uint6
 }
 #endif
 
+
+namespace fprb {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+cudaStream_t graph_stream(const void* h) { return static_cast<const fpr_b200_graph*>(h)->stream; }
+int graph_device(const void* h) { return static_cast<const fpr_b200_graph*>(h)->device; }
+}  // namespace fprb

@@ -38,11 +38,14 @@ def main():
                 dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=1), copy_ranks=False)
                 t1 = time.perf_counter()
                 r = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True)
+                r2 = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True)
+                same = bool(np.array_equal(r.ranks.values.view(np.uint64), r2.ranks.values.view(np.uint64))
+                            and np.array_equal(r.trace.errors, r2.trace.errors))
                 ms = r.solve_ms / r.trace.iterations
                 d = np.max(np.abs(r.ranks.values - plain) / plain) if plain is not None else float("nan")
                 per = ", ".join(f"{x / 1e6:.2f}" for x in r.trace.iter_ns[: r.trace.iterations])
                 print(f"cfg{c} pb {sh}:{cs}: {r.trace.iterations} it, {ms:.3f} ms/it, {dg.m / ms / 1e6:.1f} GTEPS, "
-                      f"build+1 sweep {1e3 * (t1 - t0):.0f} ms, max rel vs plain {d:.2e}; per-iter ms [{per}]",
+                      f"build+1 sweep {1e3 * (t1 - t0):.0f} ms, max rel vs plain {d:.2e}, rerun bit-equal {same}; per-iter ms [{per}]",
                       flush=True)
 
 

@@ -175,14 +175,60 @@ def edge_list_fixture(ref: Reference) -> dict:
     return {"cases": cases, "large": large}
 
 
+def config3_fixture(ref: Reference, sample=4096) -> dict:
+    """BASELINE config 3: generate_rmat(24, 16, seed 3) -> build_csr, BFS
+    crawl-order relabel, build_csr again -- every array by the reference,
+    except the BFS permutation itself (the reference has no relabel; it is
+    SURVEY §8(d)'s definition, restated by fo_bfs_relabel and pinned against
+    the device relabel in tests/test_gpu_generate.py).  Then the reference's
+    pagerank_ec_seq and pagerank_fused_seq at 1e-10 (L-inf): iteration
+    counts, every iteration's error (hex) and `sample` seeded rank samples.
+    About 15 minutes on 8 cores (ec_seq 61 x ~7 s, fused_seq 41 x ~7 s)."""
+    import time
+
+    from oracle import Oracle
+
+    t0 = time.time()
+    n, s, d = ref.generate_rmat(24, 16, seed=3)
+    rec = {"params": {"scale": 24, "edge_factor": 16, "a": 0.57, "b": 0.19, "c": 0.19, "d": 0.05, "seed": 3,
+                      "relabel": "bfs from old id 0 (SURVEY §8(d))"},
+           "draws_sha256": {"src": sha(s), "dst": sha(d)}}
+    g0 = ref.build_csr(n, s, d)
+    del s, d
+    rec["graph_natural"] = graph_digest(g0)
+    new_id = Oracle().bfs_relabel(g0, 0)
+    rec["bfs_new_id_sha256"] = sha(new_id)
+    dst = np.repeat(np.arange(g0.n, dtype=np.uint64), np.diff(g0.in_start).astype(np.int64))
+    g = ref.build_csr(n, new_id[g0.in_src], new_id[dst])
+    del g0, dst, new_id
+    rec["graph"] = graph_digest(g)
+    print(f"config3 graph built in {time.time() - t0:.0f} s", flush=True)
+    idx = np.sort(np.random.default_rng(3).choice(n, size=sample, replace=False))
+    rec["runs"] = {}
+    h = ref.graph_handle(g)
+    try:
+        for eng in ("ec_seq", "fused_seq"):
+            t1 = time.time()
+            r = ref.run(g, eng, threshold=1e-10, handle=h)
+            rec["runs"][f"{eng}@1e-10"] = run_digest(r, idx)
+            rec["runs"][f"{eng}@1e-10"]["seconds"] = r.seconds
+            print(f"config3 {eng}: {r.iterations} iterations, {time.time() - t1:.0f} s", flush=True)
+    finally:
+        ref.destroy(h)
+    return rec
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-config2", action="store_true")
-    ap.add_argument("--only", choices=["edge_list"], help="regenerate one fixture")
+    ap.add_argument("--only", choices=["edge_list", "config3"], help="regenerate one fixture")
     args = ap.parse_args()
     ref = Reference()
     if args.only == "edge_list":
         json.dump(edge_list_fixture(ref), open(os.path.join(OUT, "edge_list.json"), "w"), indent=0)
+        return
+    if args.only == "config3":
+        json.dump(config3_fixture(ref), open(os.path.join(OUT, "config3.json"), "w"), indent=1)
         return
 
     json.dump(kats(ref), open(os.path.join(OUT, "kat.json"), "w"), indent=1)

@@ -103,13 +103,17 @@ def test_option_flags_match_header():
     """The Python flag constants are the header's, and `reorder` maps to the
     two reorder flags (anything else is rejected before any device work)."""
     text = open(HEADER).read()
-    for name, val in (("REORDER", fb.OPT_REORDER), ("BLOCKED", fb.OPT_BLOCKED), ("PB", fb.OPT_PB),
+    for name, val in (("REORDER", fb.OPT_REORDER), ("PULL", fb.OPT_PULL), ("PB", fb.OPT_PB),
                       ("REORDER_SOURCES", fb.OPT_REORDER_SOURCES)):
         m = re.search(rf"#define FPR_B200_OPT_{name} (\d+)u", text)
         assert m and int(m.group(1)) == val, name
     assert fb._options(reorder=True).flags == fb.OPT_REORDER
     assert fb._options(reorder="degree").flags == fb.OPT_REORDER
     assert fb._options(reorder="sources", pb=True).flags == fb.OPT_REORDER_SOURCES | fb.OPT_PB
-    assert fb._options().flags == 0
+    assert fb._options().flags == 0  # the library picks the sweep kind
+    assert fb._options(pb=False).flags == fb.OPT_PULL
+    for name, val in (("PULL", fb.SWEEP_PULL), ("PB", fb.SWEEP_PB)):
+        m = re.search(rf"#define FPR_B200_SWEEP_{name} (\d+)", text)
+        assert m and int(m.group(1)) == val, name
     with pytest.raises(ValueError, match="reorder"):
         fb._options(reorder="bfs")

@@ -15,7 +15,8 @@ REF_SO = os.path.join(ROOT, "oracle", "_ref", "libfpr_ref.so")
 
 @pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")
 def test_reference_arm_json_line():
-    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3"],
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "1", "--steps", "1",
+                          "--warmup", "3"],
                          cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
@@ -27,8 +28,9 @@ def test_reference_arm_json_line():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
         assert k in d, k
-    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["config"]["workload"] == bench.WORKLOAD
-    assert d["steps"] == 1 and d["warmup"] >= 3 and d["higher_is_better"] is True and d["value"] > 0
+    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["config"]["workload"] == bench.WORKLOADS["1"]
+    assert d["steps"] == 1 and d["higher_is_better"] is True and d["value"] > 0
+    assert d["config"] == bench.config_block("1", d["config"]["n"], d["config"]["m"])  # same block as the B200 arm
     cb = d["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0

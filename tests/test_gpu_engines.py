@@ -248,29 +248,8 @@ def test_pinned_upload_split(config1, share, monkeypatch):
             src[pos] = old
 
 
-@pytest.mark.parametrize("shift,reorder", [(12, False), (14, False), (12, True), (22, False)])
-def test_blocked_ec_matches_oracle(config1, oracle, shift, reorder, monkeypatch):
-    """FPR_B200_OPT_BLOCKED: source-blocked EC sweeps (accumulate passes per
-    column block + apply pass) give the reference's per-iteration ranks within
-    1e-12 relative and its iteration count, for 1..16 blocks."""
-    rec, g, dg = config1
-    monkeypatch.setenv("FPR_B200_BLOCK_SHIFT", str(shift))
-    ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
-    with fb.DeviceGraph.from_graph(to_fb(g), blocked=True, reorder=reorder) as d2:
-        r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=1))
-        assert rel(r1.ranks.values, ref.history[0]) <= EC_RTOL
-        r3 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
-        assert rel(r3.ranks.values, ref.history[2]) <= EC_RTOL
-        r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
-        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))  # unblocked engines still work
-    assert r.trace.iterations == ref.iterations and r.trace.converged
-    assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
-    assert np.max(np.abs(r.trace.errors - ref.errors)) <= EC_RTOL * float(ref.ranks.max())
-    assert fu.trace.converged
-
-
 @pytest.mark.parametrize("shift,chunk_shift,reorder,piece", [(13, 20, False, 0), (5, 4, False, 0),
-                                                             (9, 12, False, 0), (14, 10, True, 0), (7, 6, False, 0),
+                                                             (9, 12, False, 0), (12, 10, True, 0), (7, 6, False, 0),
                                                              (13, 20, False, 1000), (9, 12, True, 77)])
 def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piece, monkeypatch):
     """FPR_B200_OPT_PB: propagation-blocked EC sweeps (gather pass into the
@@ -290,10 +269,15 @@ def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piec
         r3 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
         assert rel(r3.ranks.values, ref.history[2]) <= EC_RTOL
         r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
-        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))  # unblocked engines still work
+        r2 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+        fu = d2.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=1e-10))  # FUSED: lockstep on PB sweeps
+    assert r.sweep == fb.SWEEP_PB and fu.sweep == fb.SWEEP_PB
     assert r.trace.iterations == ref.iterations and r.trace.converged
     assert rel(r.ranks.values, ref.ranks) <= EC_RTOL
     assert np.max(np.abs(r.trace.errors - ref.errors)) <= EC_RTOL * float(ref.ranks.max())
+    # fixed-point row sums: a second run gives the same bits
+    assert np.array_equal(r.ranks.values.view(np.uint64), r2.ranks.values.view(np.uint64))
+    assert np.array_equal(r.trace.errors, r2.trace.errors) and np.array_equal(r.trace.l1_errors, r2.trace.l1_errors)
     assert fu.trace.converged
 
 
@@ -338,6 +322,28 @@ def test_pb_l1_rule_matches_pull(config1):
     assert ra.trace.iterations == rb.trace.iterations
     assert rel(rb.ranks.values, ra.ranks.values) <= EC_RTOL
     assert np.max(np.abs(ra.trace.l1_errors - rb.trace.l1_errors)) <= 1e-12
+
+
+def test_sweep_kind_auto_and_forced(config1, oracle, monkeypatch):
+    """Default options let the library pick the sweep: pull while the
+    contribution vector fits L2 (config 1), propagation-blocked past the size
+    rule (lowered here through FPR_B200_PB_AUTO_BYTES); pb=False forces the
+    pull sweep.  Every choice keeps the reference's per-iteration parity."""
+    rec, g, dg = config1
+    ref = oracle.pagerank_ec(g, threshold=1e-10)
+    cfg = fb.PageRankConfig(threshold=1e-10)
+    with fb.DeviceGraph.from_graph(to_fb(g)) as d:
+        r = d.run(fb.ENGINE_EC, cfg)
+    assert r.sweep == fb.SWEEP_PULL
+    monkeypatch.setenv("FPR_B200_PB_AUTO_BYTES", "1024")
+    with fb.DeviceGraph.from_graph(to_fb(g)) as d, fb.DeviceGraph.from_graph(to_fb(g), pb=False) as dp:
+        ra, rp = d.run(fb.ENGINE_EC, cfg), dp.run(fb.ENGINE_EC, cfg)
+        fa = d.run(fb.ENGINE_FUSED, cfg)
+    assert ra.sweep == fb.SWEEP_PB and fa.sweep == fb.SWEEP_PB and rp.sweep == fb.SWEEP_PULL
+    for x in (ra, rp):
+        assert x.trace.iterations == ref.iterations
+        assert rel(x.ranks.values, ref.ranks) <= EC_RTOL
+    assert fa.trace.converged
 
 
 def test_pb_rejects_bad_geometry(config1, monkeypatch):

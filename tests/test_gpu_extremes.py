@@ -1,7 +1,7 @@
 """Extreme shapes for the task decomposition: one hub row holding almost all
 edges (split across thousands of tasks -> the cross-task partial chain at its
 longest), its transpose (every row one edge), long chains of empty rows, and
-rows exactly at the snap boundary.  Every engine, the blocked EC layout and
+rows exactly at the snap boundary.  Every engine and
 the propagation-blocked EC and lockstep sweeps,
 against the C oracle (EC per 1e-12 relative, same iteration count; FusEd by
 the L-inf-threshold bound on L1 to x*)."""
@@ -39,15 +39,13 @@ def _shapes(oracle):
     yield "snap_boundary", _csr(oracle, m_rows, src, dst)
 
 
-@pytest.mark.parametrize("layout", ["plain", "blocked", "pb"])
+@pytest.mark.parametrize("layout", ["plain", "pb"])
 def test_extreme_shapes(oracle, layout, monkeypatch):
-    monkeypatch.setenv("FPR_B200_BLOCK_SHIFT", "14")
     monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", "16")  # several chunks at n = 2^20
     cfg = fb.PageRankConfig(threshold=1e-10)
-    blocked = layout == "blocked"
     for name, (g, hg) in _shapes(oracle):
         ref = oracle.pagerank_ec(g, threshold=1e-10)
-        with fb.DeviceGraph.from_graph(hg, blocked=blocked, pb=layout == "pb") as dg:
+        with fb.DeviceGraph.from_graph(hg, pb=layout == "pb") as dg:
             assert dg.validate() == 0
             r = dg.run(fb.ENGINE_EC, cfg)
             assert r.trace.iterations == ref.iterations, name

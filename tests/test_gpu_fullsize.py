@@ -1,85 +1,159 @@
-"""BASELINE configs 3-5 at full size on the device: generation (K5/K4 + the
-config-3 relabel), build_csr invariants checked on the device, and
-size-independent PageRank properties the oracle cannot reach in test time:
-  * relabel invariance of the EC iteration count (config 3 vs natural order);
-  * fixed-point residual: one more Jacobi step moves no rank by more than
-    10*threshold/(1-d);
-  * lower bound: every rank >= (1-d)/n - 1e-12;
-  * EC and FusEd agree within the geometric-tail bound n*delta*d/(1-d).
+"""BASELINE configs 2-5 at full size on the device, against the oracle.
+
+* Config 3 against the REFERENCE: tests/golden/config3.json holds the
+  reference's own build_csr digests of the BFS-relabelled R-MAT(24, 16, 3)
+  and its pagerank_ec_seq / pagerank_fused_seq runs at 1e-10 (iterations,
+  every iteration's error, 4,096 sampled ranks; tests/golden/make_golden.py).
+* Configs 3-5, one-step parity (the reference step restated by fo_ec_step,
+  OpenMP over rows, bit-identical to the sequential iteration --
+  tests/test_oracle.py pins it to the reference's traces): the GPU's iterate
+  k-1 goes into the oracle, whose iterate k must match the GPU's iterate k
+  within 1e-12 relative, for k in {1, 2, K-1, K}.  EC is deterministic, so
+  the runs with max_iterations = k-1 and k reproduce the full run's
+  iterates.  At k = K the oracle's own delta is <= threshold and at K-1 it
+  is not: the reference, fed the same iterates, stops at the same K.
+* FusEd on configs 2-5: every FusEd schedule the library runs converges to
+  within the geometric-tail bound n*delta*d/(1-d) (L1) of x*, the EC fixed
+  point at threshold 1e-15 (SURVEY §8(c) protocol (iii)).
+Configs 4/5 run the library's default sweep (propagation-blocked there).
 """
+import hashlib
+
 import numpy as np
 import pytest
 
 import paper_2203_09284_b200 as fb
+from golden_util import load, unhex
+from oracle import Graph as OGraph
 
 pytestmark = pytest.mark.gpu
 D = 0.85
 T = 1e-10
+RTOL = 1e-12
 
 
-def _properties(dg, name):
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+
+
+def _make(config, **kw):
+    if config == "2":
+        return fb.DeviceGraph.generate_uniform(1 << 22, 16, 2, **kw)
+    if config == "3":
+        return fb.DeviceGraph.generate_rmat(fb.RmatParams(24, 16, seed=3), relabel_bfs=True, **kw)
+    if config == "4":
+        return fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, **kw)
+    return fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), **kw)
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def test_config3_against_reference_golden():
+    """Device CSR == the reference's build_csr (SHA-256 of all three arrays);
+    EC: the reference's iteration count, every iteration's error within 1e-12
+    x max rank and the 4,096 sampled ranks within 1e-12 relative; FusEd: the
+    reference fused_seq's sampled ranks within the tail bound."""
+    rec = load("config3.json")
+    ec_ref = rec["runs"]["ec_seq@1e-10"]
+    fu_ref = rec["runs"]["fused_seq@1e-10"]
+    idx = np.array(sorted(int(i) for i in ec_ref["sample"]), dtype=np.int64)
     cfg = fb.PageRankConfig(threshold=T)
-    ec = dg.run(fb.ENGINE_EC, cfg)
-    assert ec.trace.converged
-    k = ec.trace.iterations
-    nxt = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=k + 1))
-    assert float(np.max(np.abs(nxt.ranks.values - ec.ranks.values))) <= 10 * T / (1 - D)
-    assert float(ec.ranks.values.min()) >= (1 - D) / dg.n - 1e-12
-    fu = dg.run(fb.ENGINE_FUSED, cfg)
-    assert fu.trace.converged
-    assert fb.l1_norm(fu.ranks.values, ec.ranks.values) <= 2 * dg.n * T * D / (1 - D)
-    print(f"\n{name}: n={dg.n} m={dg.m} ec {k} it {ec.solve_ms:.1f} ms, "
-          f"fused {fu.trace.iterations} it {fu.solve_ms:.1f} ms")
-    return ec, fu
+    with _make("3") as dg:
+        g = dg.download()
+        assert (g.n, g.m) == (rec["graph"]["n"], rec["graph"]["m"])
+        assert _sha(g.in_start) == rec["graph"]["in_start"]
+        assert _sha(g.in_src) == rec["graph"]["in_src"]
+        assert _sha(g.out_degree) == rec["graph"]["out_degree"]
+        del g
+        ec = dg.run(fb.ENGINE_EC, cfg)
+        fused = {e: dg.run(e, cfg) for e in (fb.ENGINE_FUSED, fb.ENGINE_FUSED_LOCKSTEP)}
+        xstar = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-15, max_iterations=400)).ranks.values
+    assert ec.trace.iterations == ec_ref["iterations"]
+    ref_err = unhex(ec_ref["errors"])
+    assert np.max(np.abs(ec.trace.errors - ref_err)) <= RTOL * float(ec.ranks.values.max())
+    ref_sample = unhex([ec_ref["sample"][str(i)] for i in idx])
+    assert _rel(ec.ranks.values[idx], ref_sample) <= RTOL
+    # FusEd: the reference's fused_seq and every GPU FusEd schedule sit within
+    # the tail bound of x* (sampled for the reference: per-vertex bound)
+    bound = rec["graph"]["n"] * T * D / (1 - D)
+    fu_sample = unhex([fu_ref["sample"][str(i)] for i in idx])
+    assert float(np.sum(np.abs(fu_sample - xstar[idx]))) <= bound
+    for e, r in fused.items():
+        assert r.trace.converged
+        assert fb.l1_norm(r.ranks.values, xstar) <= bound, e
+        print(f"\nconfig3 engine {e}: {r.trace.iterations} sweeps (reference fused_seq {fu_ref['iterations']})")
 
 
-def test_config3_rmat24_bfs_relabel():
-    p = fb.RmatParams(24, 16, seed=3)
-    with fb.DeviceGraph.generate_rmat(p, relabel_bfs=True) as dg:
+@pytest.mark.parametrize("config", ["3", "4", "5"])
+def test_one_step_parity_full_size(config, oracle):
+    cfg = fb.PageRankConfig(threshold=T)
+    with _make(config) as dg:
         assert dg.validate() == 0
-        assert dg.m == 263_434_595  # SURVEY probe: relabelling does not change m
-        ec, _ = _properties(dg, "config3")
-    # EC iteration counts are relabel-invariant; natural order = 61
-    assert ec.trace.iterations == 61
+        full = dg.run(fb.ENGINE_EC, cfg)
+        K = full.trace.iterations
+        assert full.trace.converged and K >= 3
+        g = dg.download()
+        og = OGraph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+        del g
+        for k in (1, 2, K - 1, K):
+            if k == 1:
+                prev = np.full(og.n, 1.0 / og.n)
+            else:
+                prev = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=k - 1),
+                              copy_trace=False).ranks.values
+            cur = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=k), copy_trace=False)
+            nxt, err, _l1 = oracle.ec_step(og, prev, D)
+            assert _rel(cur.ranks.values, nxt) <= RTOL, (config, k)
+            assert abs(full.trace.errors[k - 1] - err) <= RTOL * float(nxt.max()), (config, k)
+            if k == K - 1:
+                assert err > T  # the reference would not stop before K ...
+            if k == K:
+                assert err <= T  # ... and stops at K
+            del prev, cur, nxt
+        sweep = full.sweep
+    print(f"\nconfig{config}: n={og.n} m={og.m} EC {K} iterations, sweep {'pb' if sweep else 'pull'}")
 
 
-def test_config4_chunglu():
-    with fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4) as dg:
-        assert dg.validate() == 0
-        assert dg.m > 500_000_000
-        _properties(dg, "config4")
-
-
-def test_config5_rmat28():
-    with fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5)) as dg:
-        assert dg.validate() == 0
-        assert 4_000_000_000 < dg.m < 4_294_967_296
-        _properties(dg, "config5")
+@pytest.mark.parametrize("config", ["2", "4", "5"])
+def test_fused_within_tail_bound_full_size(config):
+    """FusEd (the library's FUSED choice and the lockstep schedule) against x*,
+    with the iteration counts beside EC's; on config 2 also the reference's
+    fused_seq iteration count from tests/golden/config2.json."""
+    cfg = fb.PageRankConfig(threshold=T)
+    with _make(config) as dg:
+        ec = dg.run(fb.ENGINE_EC, cfg, copy_ranks=False)
+        xstar = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-15, max_iterations=400)).ranks.values
+        out = {e: dg.run(e, cfg) for e in (fb.ENGINE_FUSED, fb.ENGINE_FUSED_LOCKSTEP)}
+        n = dg.n
+    bound = n * T * D / (1 - D)
+    for e, r in out.items():
+        assert r.trace.converged
+        assert float(r.ranks.values.min()) >= (1 - D) / n - 1e-12
+        assert fb.l1_norm(r.ranks.values, xstar) <= bound, e
+        assert r.trace.iterations <= ec.trace.iterations, e
+    if config == "2":
+        ref = load("config2.json")["runs"]["fused_seq@1e-10"]["iterations"]
+        print(f"\nconfig2: reference fused_seq {ref} sweeps")
+    print(f"\nconfig{config}: EC {ec.trace.iterations}, FUSED {out[fb.ENGINE_FUSED].trace.iterations}, "
+          f"lockstep {out[fb.ENGINE_FUSED_LOCKSTEP].trace.iterations}")
 
 
 @pytest.mark.parametrize("config", ["4", "5"])
-def test_pb_engines_full_size(config):
-    """FPR_B200_OPT_PB at full size: the propagation-blocked EC gives the pull
-    EC's iteration count and ranks within 1e-12 relative (the oracle's
-    per-iteration bar, here against the oracle-checked pull engine); the
-    FusEd schedule on PB sweeps converges in fewer sweeps to within the
-    geometric-tail bound of the EC fixed point."""
-    def make(**kw):
-        if config == "4":
-            return fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4, **kw)
-        return fb.DeviceGraph.generate_rmat(fb.RmatParams(28, 16, seed=5), **kw)
-
+def test_pull_and_pb_agree_full_size(config):
+    """The two sweep kinds on configs 4/5: the forced pull sweep and the
+    default propagation-blocked one give the same iteration count and ranks
+    within 1e-12; PB repeated gives the same bits (fixed-order row sums)."""
     cfg = fb.PageRankConfig(threshold=T)
-    with make() as dg:
-        ec = dg.run(fb.ENGINE_EC, cfg)
-    with make(pb=True) as dg:
+    with _make(config, pb=False) as dg:
+        pull = dg.run(fb.ENGINE_EC, cfg)
+    with _make(config) as dg:
         pb = dg.run(fb.ENGINE_EC, cfg)
-        ls = dg.run(fb.ENGINE_FUSED_LOCKSTEP, cfg)
-        waves = len(dg.wave_starts()) - 1
-        n = dg.n
-    assert pb.trace.iterations == ec.trace.iterations and pb.trace.converged
-    assert float(np.max(np.abs(pb.ranks.values - ec.ranks.values) / ec.ranks.values)) <= 1e-12
-    assert ls.trace.converged and ls.trace.iterations < ec.trace.iterations
-    assert fb.l1_norm(ls.ranks.values, ec.ranks.values) <= 2 * n * T * D / (1 - D)
-    print(f"\nconfig{config} PB: ec {pb.trace.iterations} it {pb.solve_ms:.1f} ms, "
-          f"lockstep ({waves} waves) {ls.trace.iterations} it {ls.solve_ms:.1f} ms")
+        pb2 = dg.run(fb.ENGINE_EC, cfg)
+    assert pull.sweep == fb.SWEEP_PULL and pb.sweep == fb.SWEEP_PB
+    assert pb.trace.iterations == pull.trace.iterations
+    assert _rel(pb.ranks.values, pull.ranks.values) <= RTOL
+    assert np.array_equal(pb.ranks.values.view(np.uint64), pb2.ranks.values.view(np.uint64))
+    assert np.array_equal(pb.trace.errors, pb2.trace.errors)
+    assert np.array_equal(pb.trace.l1_errors, pb2.trace.l1_errors)

@@ -89,6 +89,26 @@ def test_rmat_graphs(oracle, name):
         _run_matches(fn(g, threshold=float(t)), dig)
 
 
+@pytest.mark.parametrize("name", ["rmat_s12_seed7.json", "config1.json"])
+def test_ec_step_chain_is_the_reference_run(oracle, name):
+    """fo_ec_step (OpenMP over rows) chained from 1/n reproduces the
+    reference's ec_seq run bit for bit: the same ranks hash, iteration count
+    and max-delta trace as the golden fixture.  The full-size one-step GPU
+    checks (tests/test_gpu_fullsize.py) rest on this."""
+    rec = load(name)
+    p = rec["params"]
+    g = oracle.build_csr(*oracle.generate_rmat(p["scale"], p["edge_factor"], p["a"], p["b"], p["c"], p["d"],
+                                               p["seed"]))
+    dig = rec["runs"]["ec_seq@1e-10"]
+    x = np.full(g.n, 1.0 / g.n)
+    errs = []
+    for _ in range(dig["iterations"]):
+        x, err, _l1 = oracle.ec_step(g, x)
+        errs.append(err)
+    assert [e.hex() for e in errs] == dig["errors"]
+    assert sha(x) == dig["ranks_sha256"]
+
+
 def test_rmat_golden_343(oracle):
     """io_ingest_test.cpp:143-155: max in-degree 343 at scale 10, ef 16, seed 42."""
     n, s, d = oracle.generate_rmat(10, 16, seed=42)
