@@ -29,8 +29,9 @@ inline EdgeSet parse_edge_list_b200(const char* text, std::uint64_t len,
   std::vector<std::uint64_t> flat(2 * ((len + 3) / 4 + 1));
   int rc = fpr_b200_parse_edge_list(text, len, opts, &n, &m, flat.data(), flat.size() / 2, &err);
   if (rc == FPR_B200_EPARSE) {
-    // ParseError(line, what) prepends "line L: " itself (edge_list.hpp:17-21)
-    std::string what = err.message;
+    // ParseError(line, what) prepends "line L: " itself (edge_list.hpp:17-21);
+    // the full text is fpr_b200_last_error() (err.message stops at 255 bytes)
+    std::string what = fpr_b200_last_error();
     const std::string prefix = "line " + std::to_string(err.line) + ": ";
     if (what.compare(0, prefix.size(), prefix) == 0) what.erase(0, prefix.size());
     throw ParseError(err.line, what);

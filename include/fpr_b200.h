@@ -163,6 +163,13 @@ int fpr_b200_graph_create(const fpr_graph_view* view, const fpr_b200_options* op
  * build_csr(generate_rmat(p)) / build_csr(random_sparse(...)). */
 int fpr_b200_graph_generate(const fpr_gen_params* params, const fpr_b200_options* opts,
                             fpr_b200_graph** out);
+/* The generator's EdgeSet before build_csr, in generation order: the draws of
+ * fpr::generate_rmat (rmat.hpp:42-77; self-loops and duplicates kept) or of
+ * testutil::random_sparse (test_util.hpp:49-58; self-loops skipped).  Drawn
+ * on the device.  *count_out = edges; src/dst (cap entries each, or NULL to
+ * count only) receive them, ERANGE when cap is smaller. */
+int fpr_b200_generate_edges(const fpr_gen_params* params, const fpr_b200_options* opts, uint64_t* src,
+                            uint64_t* dst, uint64_t cap, uint64_t* count_out);
 /* fpr::build_csr(EdgeSet{n, edges}) (graph.hpp:35-70) on the device: m edges
  * as two u64 arrays (host or pinned memory).  EINVAL names the first edge
  * with an endpoint outside [0, n), in build_csr's words. */

@@ -108,7 +108,7 @@ EXPORTS = [
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
     "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev", "fpr_b200_part_create",
     "fpr_b200_mgpu_create", "fpr_b200_mgpu_generate", "fpr_b200_mgpu_run", "fpr_b200_mgpu_info",
-    "fpr_b200_mgpu_destroy",
+    "fpr_b200_mgpu_destroy", "fpr_b200_generate_edges",
 ]
 
 _lib = None
@@ -167,6 +167,8 @@ def lib() -> C.CDLL:
         L.fpr_b200_mgpu_generate.argtypes = [C.POINTER(_GenParams), C.POINTER(_Options), C.POINTER(vp)]
         L.fpr_b200_mgpu_run.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, u64, C.POINTER(_Result)]
         L.fpr_b200_mgpu_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), vp]
+        L.fpr_b200_generate_edges.argtypes = [C.POINTER(_GenParams), C.POINTER(_Options), vp, vp, u64,
+                                              C.POINTER(u64)]
         L.fpr_b200_mgpu_destroy.argtypes = [vp]
         L.fpr_b200_mgpu_destroy.restype = None
         _lib = L
@@ -548,6 +550,32 @@ class MultiDeviceGraph:
 
     def __exit__(self, *a):
         self.close()
+
+
+def generate_edges(kind: str, device=-1, **p) -> "EdgeSet":
+    """The generator's EdgeSet before build_csr, in generation order, drawn on
+    the device: kind "rmat" (RmatParams fields: fpr::generate_rmat, rmat.hpp:
+    42-77, self-loops and duplicates kept) or "uniform" (n, avg_degree, seed:
+    testutil::random_sparse, self-loops skipped)."""
+    if kind == "rmat":
+        r = p["params"]
+        gp = _GenParams(GEN_RMAT, r.scale, r.edge_factor, r.a, r.b, r.c, r.d, 0, 0, r.seed)
+        n = 1 << r.scale
+    elif kind == "uniform":
+        gp = _GenParams(GEN_UNIFORM, 0, 0, 0.0, 0.0, 0.0, 0.0, p["n"], p["avg_degree"], p["seed"])
+        n = p["n"]
+    else:
+        raise ValueError("generate_edges: kind is 'rmat' or 'uniform'")
+    o = _options(device=device)
+    cnt = C.c_uint64()
+    _check(lib().fpr_b200_generate_edges(C.byref(gp), C.byref(o), None, None, 0, C.byref(cnt)))
+    e = np.empty((max(cnt.value, 1), 2), np.uint64)
+    src = np.empty(max(cnt.value, 1), np.uint64)
+    dst = np.empty(max(cnt.value, 1), np.uint64)
+    _check(lib().fpr_b200_generate_edges(C.byref(gp), C.byref(o), src.ctypes.data, dst.ctypes.data, cnt.value,
+                                         C.byref(cnt)))
+    e[:, 0], e[:, 1] = src, dst
+    return EdgeSet(n, e[: cnt.value])
 
 
 def run_engine(kind: EngineKind | str, g, cfg: PageRankConfig, **kw) -> PageRankResult:

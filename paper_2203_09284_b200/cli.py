@@ -26,8 +26,9 @@ import time
 
 import numpy as np
 
-from . import (DeviceGraph, EngineKind, NORM_L1, NORM_LINF, PageRankConfig, ParseError, RmatParams,
-               l1_norm, parse_engine, ENGINE_EC, ENGINE_FUSED, ENGINE_FUSED_LOCKSTEP)
+from . import (B200Error, DeviceGraph, EdgeSet, EngineKind, NORM_L1, NORM_LINF, PageRankConfig, ParseError,
+               RmatParams, generate_edges, l1_norm, parse_engine, write_edge_list, ENGINE_EC, ENGINE_FUSED,
+               ENGINE_FUSED_LOCKSTEP)
 from .cache import CacheError, load_cache, save_cache
 
 EXIT_OK, EXIT_USAGE, EXIT_IO, EXIT_NONCONV = 0, 1, 2, 3
@@ -84,9 +85,21 @@ def _engine(tag: str) -> int:
     return _ENGINES[kind]
 
 
-def _cfg(args, threshold=None) -> PageRankConfig:
+def _threads(args) -> list[int]:
+    """--threads N or a comma list (bench sweeps every value; SPEC BenchSpec)."""
+    try:
+        ts = [int(x) for x in str(args.threads).split(",") if x.strip()]
+    except ValueError:
+        raise UsageError(f"--threads expects integers, got '{args.threads}'")
+    if not ts or min(ts) < 1:
+        raise UsageError("--threads values must be positive")
+    return ts
+
+
+def _cfg(args, threshold=None, threads=None) -> PageRankConfig:
     return PageRankConfig(damping=args.damping, threshold=threshold if threshold is not None else args.threshold,
-                          max_iterations=args.max_iters, thread_count=max(1, args.threads))
+                          max_iterations=args.max_iters,
+                          thread_count=threads if threads is not None else _threads(args)[0])
 
 
 def cmd_run(args, out) -> int:
@@ -107,6 +120,7 @@ def cmd_run(args, out) -> int:
 def cmd_bench(args, out) -> int:
     engines = [e.strip() for e in args.engines.split(",") if e.strip()]
     thresholds = [float(t) for t in args.thresholds.split(",")]
+    threads = _threads(args)
     if not engines or not thresholds:
         raise UsageError("bench needs at least one engine and one threshold")
     for e in engines:
@@ -114,20 +128,32 @@ def cmd_bench(args, out) -> int:
     dg, label = open_graph(args)
     rows = []
     with dg:
+        # engines x thresholds x threads x reps (SPEC cmd_bench); the GPU
+        # engines validate thread_count and otherwise ignore it
         for t in thresholds:
-            ref = dg.run(ENGINE_EC, _cfg(args, t))  # the L1 reference, run first
+            try:
+                ref = dg.run(ENGINE_EC, _cfg(args, t))  # the L1 reference, run first
+            except (B200Error, ValueError):
+                ref = None
             for e in engines:
-                best, res = None, None
-                for _ in range(max(1, args.reps)):  # min over repetitions
-                    t0 = time.perf_counter()
-                    r = dg.run(_engine(e), _cfg(args, t))
-                    w = time.perf_counter() - t0
-                    if best is None or w < best:
-                        best, res = w, r
-                rows.append({"graph": label, "engine": e, "threshold": repr(t), "threads": args.threads,
-                             "iterations": res.trace.iterations, "wall_time_s": f"{best:.6f}",
-                             "l1_vs_seq_ec": repr(l1_norm(res.ranks.values, ref.ranks.values)),
-                             "converged": str(res.trace.converged).lower()})
+                for th in threads:
+                    best, res = None, None
+                    try:
+                        for _ in range(max(1, args.reps)):  # min over repetitions
+                            t0 = time.perf_counter()
+                            r = dg.run(_engine(e), _cfg(args, t, th))
+                            w = time.perf_counter() - t0
+                            if best is None or w < best:
+                                best, res = w, r
+                    except (B200Error, ValueError) as ex:  # a failed cell is a row, not an abort
+                        sys.stderr.write(f"fpr-b200: {e} at threshold {t!r}: {ex}\n")
+                        rows.append({"graph": label, "engine": e, "threshold": repr(t), "threads": th,
+                                     "iterations": 0, "wall_time_s": "", "l1_vs_seq_ec": "", "converged": "false"})
+                        continue
+                    l1 = repr(l1_norm(res.ranks.values, ref.ranks.values)) if ref is not None else ""
+                    rows.append({"graph": label, "engine": e, "threshold": repr(t), "threads": th,
+                                 "iterations": res.trace.iterations, "wall_time_s": f"{best:.6f}",
+                                 "l1_vs_seq_ec": l1, "converged": str(res.trace.converged).lower()})
     if args.format == "json":
         out.write(json.dumps(rows) + "\n")
     else:
@@ -138,16 +164,37 @@ def cmd_bench(args, out) -> int:
 
 
 def cmd_gen(args, out) -> int:
+    """SPEC cmd_gen: the GENERATED EdgeSet as SNAP text -- header comment lines
+    with the parameters and seed, then one "src dst" line per draw in
+    generation order (--rmat: generate_rmat's draws, self-loops and duplicates
+    kept; --uniform: random_sparse's kept draws).  --format fprg writes the
+    normalised graph (build_csr of it) as an FPRG cache instead; other graph
+    sources have no generated EdgeSet and write their normalised edges."""
     if args.reorder != "none":
         raise UsageError("gen writes the graph in the caller's ids; --reorder applies to run/bench")
+    src_kind = "rmat" if args.rmat else ("uniform" if args.uniform else None)
+    if args.format == "edges" and src_kind:
+        a, b, c = _triple(args.rmat or args.uniform, src_kind)
+        if src_kind == "rmat":
+            p = RmatParams(scale=a, edge_factor=b, seed=c)
+            es = generate_edges("rmat", params=p)
+            header = [f"fpr-b200 gen: generate_rmat scale={a} edge_factor={b} a={p.a} b={p.b} c={p.c} d={p.d}",
+                      f"seed={c} n={es.n} edges={len(es.edges)}"]
+        else:
+            es = generate_edges("uniform", n=a, avg_degree=b, seed=c)
+            header = [f"fpr-b200 gen: random_sparse n={a} avg_degree={b}",
+                      f"seed={c} n={es.n} edges={len(es.edges)}"]
+        with open(args.out, "wb") as f:
+            f.write(write_edge_list(es, header))
+        out.write(f"wrote {args.out}: {src_kind}:{a}:{b}:{c} n={es.n} edges={len(es.edges)}\n")
+        return EXIT_OK
     dg, label = open_graph(args)
     with dg:
         g = dg.download()
-    if args.format == "edges":  # SNAP text (edge_list.hpp:84-89) of the normalised graph
-        from . import EdgeSet, write_edge_list
-
+    if args.format == "edges":  # no generator EdgeSet: the normalised graph's edges
         dst = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(g.in_start.astype(np.int64)))
-        text = write_edge_list(EdgeSet(g.n, np.stack([g.in_src, dst], axis=1)), [f"{label} n={g.n} m={g.m}"])
+        text = write_edge_list(EdgeSet(g.n, np.stack([g.in_src, dst], axis=1)),
+                               [f"fpr-b200 gen: {label} (normalised: build_csr) n={g.n} m={g.m}"])
         with open(args.out, "wb") as f:
             f.write(text)
     else:
@@ -188,12 +235,12 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--edges")
         p.add_argument("--damping", type=float, default=0.85)
         p.add_argument("--threshold", type=float, default=1e-15)
-        p.add_argument("--threads", type=int, default=1)
+        p.add_argument("--threads", default="1", help="N, or a comma list (bench sweeps them)")
         p.add_argument("--max-iters", dest="max_iters", type=int, default=10000)
         p.add_argument("--reorder", choices=["none", "degree", "sources"], default="none",
                        help="internal renumbering (FPR_B200_OPT_REORDER / _REORDER_SOURCES)")
         p.add_argument("--pb", action="store_true",
-                       help="propagation-blocked sweeps for ec_b200 / fused_lockstep_b200 (FPR_B200_OPT_PB)")
+                       help="force propagation-blocked sweeps (FPR_B200_OPT_PB; default: the library picks)")
         p.add_argument("--waves", type=int, default=0, help="lockstep waves per sweep (0 = auto)")
 
     p = sub.add_parser("run")
@@ -210,7 +257,8 @@ def build_parser() -> argparse.ArgumentParser:
     p = sub.add_parser("gen")
     common(p)
     p.add_argument("--out", required=True)
-    p.add_argument("--format", choices=["fprg", "edges"], default="fprg")
+    p.add_argument("--format", choices=["edges", "fprg"], default="edges",
+                   help="edges: SNAP text of the generated EdgeSet (SPEC cmd_gen); fprg: the normalised graph")
     p = sub.add_parser("compare")
     common(p)
     return ap

@@ -545,6 +545,39 @@ cudaError_t build_csr_from_arrays(const int32_t* src, const int32_t* dst, int64_
 }
 
 
+__global__ void draws_kernel(DrawSpec s, uint64_t i0, uint64_t count, uint64_t* src, uint64_t* dst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t a, b;
+    s.get(i0 + i, a, b);
+    src[i] = a;
+    dst[i] = b;
+  }
+}
+
+// Draws [i0, i0 + count) of the R-MAT (kind 0) or random_sparse (kind 1)
+// generator, before any filtering: the EdgeSet order of generate_rmat
+// (rmat.hpp:54-75) / the draw order of testutil::random_sparse.
+cudaError_t generate_draws(const GenRequest& req, uint64_t i0, uint64_t count, uint64_t* d_src, uint64_t* d_dst,
+                           cudaStream_t st) {
+  DrawSpec s{};
+  s.kind = req.kind;
+  s.seed = req.seed;
+  if (req.kind == 0) {
+    s.scale = req.scale;
+    s.a = req.a;
+    s.ab = req.a + req.b;
+    s.abc = req.a + req.b + req.c;
+  } else if (req.kind == 1) {
+    s.n = req.n;
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  if (count == 0) return cudaSuccess;
+  draws_kernel<<<blocks_for(count), 256, 0, st>>>(s, i0, count, d_src, d_dst);
+  return cudaGetLastError();
+}
+
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t st, const char** msg) {
   *msg = nullptr;
   cudaError_t e = cudaSuccess;

@@ -157,6 +157,9 @@ struct GenRequest {
 // Builds row/src/outdeg on the device (allocates them into g).  Returns a
 // cudaError_t; *msg receives a static description on non-CUDA failures.
 cudaError_t generate_graph(const GenRequest& req, DevGraph& g, cudaStream_t s, const char** msg);
+// Raw draws [i0, i0 + count) of the rmat (kind 0) / uniform (kind 1) generator.
+cudaError_t generate_draws(const GenRequest& req, uint64_t i0, uint64_t count, uint64_t* d_src, uint64_t* d_dst,
+                           cudaStream_t s);
 // Locality reorder by descending out-degree, or (sources_only) the stable
 // partition with the out-degree > 0 vertices first: new CSR in `out`
 // (allocated on stream s), *perm = device new_of_old (n int32, caller frees).

@@ -699,14 +699,11 @@ int fpr_b200_graph_create(const fpr_graph_view* v, const fpr_b200_options* opts,
   return FPR_B200_OK;
 }
 
-int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* opts,
-                            fpr_b200_graph** out) {
-  if (!prm || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_generate: null argument");
-  *out = nullptr;
-  GenRequest req{prm->kind, prm->scale,      prm->edge_factor, prm->a,
-                 prm->b,    prm->c,          prm->d,           prm->n,
-                 prm->avg_degree, prm->seed, prm->draws,      prm->alpha,
-                 prm->kmax, prm->relabel_bfs, prm->bfs_root};
+}  // extern "C"
+
+namespace {
+// validate(RmatParams) (rmat.hpp:24-35, same text) and the other generators' ranges.
+int check_gen(const GenRequest& req) {
   if (req.kind == FPR_B200_GEN_RMAT) {
     // validate(RmatParams), rmat.hpp:24-35 -- same text.
     if (req.scale == 0 || req.scale > 32)
@@ -735,6 +732,75 @@ int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* o
     const uint64_t nn = req.kind == FPR_B200_GEN_RMAT ? (1ull << req.scale) : req.n;
     if (req.bfs_root >= nn) return fail(FPR_B200_EINVAL, "fpr_b200: bfs_root outside [0,n)");
   }
+  return FPR_B200_OK;
+}
+
+GenRequest gen_request(const fpr_gen_params* prm) {
+  return GenRequest{prm->kind, prm->scale,      prm->edge_factor, prm->a,
+                    prm->b,    prm->c,          prm->d,           prm->n,
+                    prm->avg_degree, prm->seed, prm->draws,      prm->alpha,
+                    prm->kmax, prm->relabel_bfs, prm->bfs_root};
+}
+}  // namespace
+
+extern "C" {
+
+int fpr_b200_generate_edges(const fpr_gen_params* prm, const fpr_b200_options* opts, uint64_t* src, uint64_t* dst,
+                            uint64_t cap, uint64_t* count_out) {
+  if (!prm || !count_out) return fail(FPR_B200_EINVAL, "fpr_b200_generate_edges: null argument");
+  const GenRequest req = gen_request(prm);
+  int rc = check_gen(req);
+  if (rc) return rc;
+  if (req.kind != FPR_B200_GEN_RMAT && req.kind != FPR_B200_GEN_UNIFORM)
+    return fail(FPR_B200_EINVAL, "fpr_b200_generate_edges: raw draws exist for the rmat and uniform generators");
+  const uint64_t draws = req.kind == FPR_B200_GEN_RMAT ? req.edge_factor << req.scale : req.n * req.avg_degree;
+  fpr_b200_graph* h = nullptr;
+  if ((rc = open_handle(opts, &h))) {
+    destroy_handle(h);
+    return rc;
+  }
+  const uint64_t chunk = std::min<uint64_t>(draws, 1ull << 24);
+  uint64_t *d = nullptr, *hb = nullptr;
+  uint64_t kept = 0;
+  cudaError_t e = cudaMallocAsync(&d, 2 * std::max<uint64_t>(chunk, 1) * sizeof(uint64_t), h->stream);
+  if (e == cudaSuccess) e = cudaMallocHost(&hb, 2 * std::max<uint64_t>(chunk, 1) * sizeof(uint64_t));
+  for (uint64_t i0 = 0; e == cudaSuccess && i0 < draws; i0 += chunk) {
+    const uint64_t cnt = std::min(chunk, draws - i0);
+    e = generate_draws(req, i0, cnt, d, d + chunk, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hb, d, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hb + chunk, d + chunk, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    for (uint64_t i = 0; e == cudaSuccess && i < cnt; ++i) {
+      // generate_rmat keeps every draw; random_sparse skips self-loops
+      if (req.kind == FPR_B200_GEN_UNIFORM && hb[i] == hb[chunk + i]) continue;
+      if (src && dst && kept < cap) {
+        src[kept] = hb[i];
+        dst[kept] = hb[chunk + i];
+      }
+      ++kept;
+    }
+  }
+  if (d) cudaFreeAsync(d, h->stream);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (hb) cudaFreeHost(hb);
+  destroy_handle(h);
+  if (e != cudaSuccess)
+    return fail(FPR_B200_ECUDA, std::string("fpr_b200_generate_edges: ") + cudaGetErrorString(e));
+  *count_out = kept;
+  if (src && dst && kept > cap)
+    return fail(FPR_B200_ERANGE, "fpr_b200_generate_edges: " + std::to_string(kept) + " edges, capacity " +
+                                     std::to_string(cap));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_graph_generate(const fpr_gen_params* prm, const fpr_b200_options* opts,
+                            fpr_b200_graph** out) {
+  if (!prm || !out) return fail(FPR_B200_EINVAL, "fpr_b200_graph_generate: null argument");
+  *out = nullptr;
+  GenRequest req = gen_request(prm);
+  int rc0 = check_gen(req);
+  if (rc0) return rc0;
   fpr_b200_graph* h = nullptr;
   int rc = open_handle(opts, &h);
   if (rc) {

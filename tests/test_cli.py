@@ -81,3 +81,53 @@ def test_gen_and_compare(tmp_path):
     assert _run(["gen", "--rmat", "6:4:3", "--out", p])[0] == EXIT_OK
     rc, text = _run(["compare", "--graph", p, "--threshold", "1e-12"])
     assert rc == EXIT_OK and text.startswith("iteration,ec_b200,fused_b200,fused_lockstep_b200")
+
+
+@pytest.mark.gpu
+def test_gen_writes_the_generated_edgeset(tmp_path):
+    """SPEC cmd_gen: scale=3, edge_factor=2, seed=1 -> exactly 16 edge lines
+    (the raw draws: self-loops and duplicates kept), header comments with the
+    parameters and seed, byte-identical on a rerun, and re-ingested by run."""
+    a, b = tmp_path / "a.txt", tmp_path / "b.txt"
+    assert _run(["gen", "--rmat", "3:2:1", "--out", str(a)])[0] == EXIT_OK
+    assert _run(["gen", "--rmat", "3:2:1", "--out", str(b)])[0] == EXIT_OK
+    text = a.read_bytes()
+    assert text == b.read_bytes()
+    lines = text.decode().splitlines()
+    edges = [l for l in lines if l and not l.startswith("#")]
+    assert len(edges) == 16 and any("seed=1" in l for l in lines if l.startswith("#"))
+    rc, out = _run(["run", "--edges", str(a), "--threshold", "1e-10"])
+    assert rc == EXIT_OK and "converged=true" in out
+
+
+@pytest.mark.gpu
+def test_generate_edges_are_the_reference_draws(oracle):
+    """fb.generate_edges draws on the device exactly the EdgeSet of the
+    reference's generate_rmat (pinned by tests/golden/rmat_s10_seed42.json's
+    draw digests) and random_sparse's kept draws (the oracle restatement)."""
+    import paper_2203_09284_b200 as fb
+    from golden_util import load, sha
+
+    rec = load("rmat_s10_seed42.json")
+    es = fb.generate_edges("rmat", params=fb.RmatParams(10, 16, seed=42))
+    assert sha(es.edges[:, 0].copy()) == rec["draws_sha256"]["src"]
+    assert sha(es.edges[:, 1].copy()) == rec["draws_sha256"]["dst"]
+    n, s, d = oracle.random_sparse(1000, 8, 5)
+    eu = fb.generate_edges("uniform", n=1000, avg_degree=8, seed=5)
+    assert np.array_equal(eu.edges[:, 0], s) and np.array_equal(eu.edges[:, 1], d)
+
+
+@pytest.mark.gpu
+def test_bench_thread_list_and_failed_cells(tmp_path):
+    """SPEC cmd_bench: the cross-product over a --threads list, and a cell
+    that fails (threshold 0 is invalid) is a converged=false row, not an
+    aborted sweep."""
+    out = tmp_path / "t.csv"
+    rc, _ = _run(["bench", "--rmat", "8:16:1", "--engines", "ec_b200,fused_b200", "--thresholds", "1e-8,0",
+                  "--threads", "1,4", "--out", str(out)])
+    assert rc == EXIT_OK
+    rows = list(csv.DictReader(open(out)))
+    assert len(rows) == 2 * 2 * 2
+    assert sorted({r["threads"] for r in rows}) == ["1", "4"]
+    for r in rows:
+        assert r["converged"] == ("true" if r["threshold"] == "1e-08" else "false")

@@ -8,7 +8,10 @@
   OpenMP over rows, bit-identical to the sequential iteration --
   tests/test_oracle.py pins it to the reference's traces): the GPU's iterate
   k-1 goes into the oracle, whose iterate k must match the GPU's iterate k
-  within 1e-12 relative, for k in {1, 2, K-1, K}.  EC is deterministic, so
+  within 1e-12 relative, for k in {1, 2, K-1, K} -- except on rows whose
+  in-degree makes the reference's own sequential sum less exact than 1e-12
+  (hubs of configs 4/5): there the bound is the reference's a-priori error
+  2du, and the exact sum shows the GPU is the accurate side (_step_parity).  EC is deterministic, so
   the runs with max_iterations = k-1 and k reproduce the full run's
   iterates.  At k = K the oracle's own delta is <= threshold and at K-1 it
   is not: the reference, fed the same iterates, stops at the same K.
@@ -86,6 +89,40 @@ def test_config3_against_reference_golden():
         print(f"\nconfig3 engine {e}: {r.trace.iterations} sweeps (reference fused_seq {fu_ref['iterations']})")
 
 
+U = 2.0 ** -53  # unit roundoff
+
+
+def _step_parity(og, prev, gpu, ref, worst=12):
+    """Per-row parity of one EC iteration.  Every row within 1e-12 relative
+    of the reference's iterate, except rows whose in-degree d makes the
+    reference's own left-to-right fp64 sum (pagerank.hpp:85-87) less exact
+    than that: its a-priori error bound is (d-1)u relative (u = 2^-53), so a
+    row may differ by up to 2du.  For the worst rows the EXACT value (the
+    correctly rounded sum of the same fp64 contributions, math.fsum) shows
+    which side is off: the GPU's blocked sums stay within 1e-13 of it."""
+    import math
+
+    rel = np.abs(gpu - ref) / ref
+    deg = np.diff(og.in_start.astype(np.int64))
+    bound = np.maximum(RTOL, 2.0 * deg * U)
+    assert bool(np.all(rel <= bound)), float(np.max(rel / bound))
+    bad = np.flatnonzero(rel > RTOL)
+    if len(bad) == 0:
+        return 0, float(rel.max()), None
+    n = og.n
+    base = (1 - D) / n
+    od = og.out_degree.astype(np.float64)
+    worst_rows = bad[np.argsort(-rel[bad])][:worst]
+    gpu_err, ref_err = [], []
+    for r in worst_rows:
+        srcs = og.in_src[og.in_start[r]:og.in_start[r + 1]].astype(np.int64)
+        exact = base + D * math.fsum((prev[srcs] / od[srcs]).tolist())
+        gpu_err.append(abs(gpu[r] - exact) / exact)
+        ref_err.append(abs(ref[r] - exact) / exact)
+    assert max(gpu_err) <= 1e-13, max(gpu_err)
+    return len(bad), float(rel.max()), (max(gpu_err), max(ref_err), int(deg[worst_rows].min()))
+
+
 @pytest.mark.parametrize("config", ["3", "4", "5"])
 def test_one_step_parity_full_size(config, oracle):
     cfg = fb.PageRankConfig(threshold=T)
@@ -105,8 +142,14 @@ def test_one_step_parity_full_size(config, oracle):
                               copy_trace=False).ranks.values
             cur = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=k), copy_trace=False)
             nxt, err, _l1 = oracle.ec_step(og, prev, D)
-            assert _rel(cur.ranks.values, nxt) <= RTOL, (config, k)
-            assert abs(full.trace.errors[k - 1] - err) <= RTOL * float(nxt.max()), (config, k)
+            nbad, mx, exact = _step_parity(og, prev, cur.ranks.values, nxt)
+            if nbad:
+                print(f"\nconfig{config} k={k}: {nbad} rows beyond 1e-12 (max {mx:.2e}), all within the "
+                      f"reference's own summation bound; worst rows (in-degree >= {exact[2]}) vs the exact sum: "
+                      f"GPU {exact[0]:.1e}, reference {exact[1]:.1e}")
+            deg = np.diff(og.in_start.astype(np.int64))
+            allowed = 2 * float(np.max(np.maximum(RTOL, 2.0 * deg * U) * nxt))
+            assert abs(full.trace.errors[k - 1] - err) <= allowed, (config, k)
             if k == K - 1:
                 assert err > T  # the reference would not stop before K ...
             if k == K:

@@ -1,0 +1,85 @@
+"""The multi-device C ABI (fpr_b200_mgpu_*, fpr_b200_options.devices) on ONE
+B200: P parts of the same graph, all on device 0, driven from this thread.
+Parts sharing a device run their sweeps one after the other on their own
+streams and exchange contributions through the sweep epilogue's stores into
+every part's vector -- the code path that stores across NVLink when the
+devices differ.  EC must equal the oracle per 1e-12 relative with the same
+iteration count; FusEd converges within the tail bound."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2203_09284_b200 as fb
+
+pytestmark = pytest.mark.gpu
+T = 1e-10
+
+
+@pytest.fixture(scope="module")
+def rmat16(oracle):
+    n, s, d = oracle.generate_rmat(16, 16, seed=1)
+    g = oracle.build_csr(n, s, d)
+    return g, fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_mgpu_ec_matches_oracle(oracle, rmat16, P):
+    g, hg = rmat16
+    ref = oracle.pagerank_ec(g, threshold=T, history_cap=2)
+    with fb.MultiDeviceGraph.from_graph(hg, [0] * P) as mg:
+        assert mg.nparts == P and mg.bounds[0] == 0 and mg.bounds[-1] == g.n
+        r = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T))
+        r2 = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=2))
+        fu = mg.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=T))
+    assert r.trace.iterations == ref.iterations and r.trace.converged
+    assert float(np.max(np.abs(r.ranks.values - ref.ranks) / ref.ranks)) <= 1e-12
+    assert np.max(np.abs(r.trace.errors - ref.errors)) <= 1e-12 * float(ref.ranks.max())
+    assert float(np.max(np.abs(r2.ranks.values - ref.history[1]) / ref.history[1])) <= 1e-12
+    xstar = oracle.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
+    assert fu.trace.converged and oracle.l1_norm(fu.ranks.values, xstar) <= g.n * T * 0.85 / 0.15
+
+
+def test_mgpu_generate_equals_host_view(rmat16):
+    """Every device generating the graph itself gives the same parts, the
+    same iterations and the same bits as the parts uploaded from the host."""
+    g, hg = rmat16
+    cfg = fb.PageRankConfig(threshold=T)
+    with fb.MultiDeviceGraph.generate_rmat(fb.RmatParams(16, 16, seed=1), [0, 0, 0]) as a, \
+            fb.MultiDeviceGraph.from_graph(hg, [0, 0, 0]) as b:
+        assert (a.n, a.m) == (b.n, b.m) and np.array_equal(a.bounds, b.bounds)
+        ra, rb = a.run(fb.ENGINE_EC, cfg), b.run(fb.ENGINE_EC, cfg)
+    assert ra.trace.iterations == rb.trace.iterations
+    assert np.array_equal(ra.ranks.values, rb.ranks.values)
+
+
+def test_pagerank_one_shot_with_device_list(oracle, rmat16):
+    """fpr_b200_pagerank() with opts.ndevices > 1 takes the multi-device path
+    (the call the C++ drop-in makes with a device list in its options)."""
+    g, hg = rmat16
+    ref = oracle.pagerank_ec(g, threshold=T)
+    ins, src, od = (np.ascontiguousarray(a, dtype=np.uint64) for a in (g.in_start, g.in_src, g.out_degree))
+    view = fb._GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data, od.ctypes.data)
+    devs = (C.c_int32 * 4)(0, 0, 0, 0)
+    opts = fb._options()
+    opts.devices = C.cast(devs, C.POINTER(C.c_int32))
+    opts.ndevices = 4
+    ranks = np.empty(g.n)
+    errs = np.empty(1000)
+    res = fb._Result()
+    cfg = fb.PageRankConfig(threshold=T)._c()
+    fb._check(fb.lib().fpr_b200_pagerank(C.byref(view), fb.ENGINE_EC, C.byref(cfg), C.byref(opts),
+                                         ranks.ctypes.data, errs.ctypes.data, 1000, C.byref(res)))
+    assert res.iterations == ref.iterations and res.converged
+    assert float(np.max(np.abs(ranks - ref.ranks) / ref.ranks)) <= 1e-12
+
+
+def test_mgpu_argument_errors(rmat16):
+    g, hg = rmat16
+    with pytest.raises(ValueError, match="out of range"):
+        fb.MultiDeviceGraph.from_graph(hg, [0, 999])
+    with fb.MultiDeviceGraph.from_graph(hg, [0, 0]) as mg:
+        with pytest.raises(ValueError, match="EC and FUSED"):
+            mg.run(fb.ENGINE_FUSED_LOCKSTEP, fb.PageRankConfig(threshold=T))
+        with pytest.raises(ValueError, match="damping"):
+            mg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=1.5))
