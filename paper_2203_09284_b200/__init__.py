@@ -493,29 +493,29 @@ class MultiDeviceGraph:
         self.bounds = b
 
     @staticmethod
-    def _opts(devices, norm, keep):
+    def _opts(devices, norm, keep, pb=None):
         arr = (C.c_int32 * len(devices))(*devices)
         keep.append(arr)
-        o = _options(norm=norm)
+        o = _options(norm=norm, pb=pb)
         o.devices = C.cast(arr, C.POINTER(C.c_int32))
         o.ndevices = len(devices)
         return o
 
     @classmethod
-    def from_graph(cls, g: Graph, devices, norm=NORM_LINF):
+    def from_graph(cls, g: Graph, devices, norm=NORM_LINF, pb=None):
         keep = []
         ins, src, od = _u64(g.in_start), _u64(g.in_src), _u64(g.out_degree)
         v = _GraphView(g.n, g.m, ins.ctypes.data, src.ctypes.data if g.m else None, od.ctypes.data)
         h = C.c_void_p()
-        _check(lib().fpr_b200_mgpu_create(C.byref(v), C.byref(cls._opts(devices, norm, keep)), C.byref(h)))
+        _check(lib().fpr_b200_mgpu_create(C.byref(v), C.byref(cls._opts(devices, norm, keep, pb)), C.byref(h)))
         return cls(h.value, devices)
 
     @classmethod
-    def generate_rmat(cls, p: RmatParams, devices, norm=NORM_LINF):
+    def generate_rmat(cls, p: RmatParams, devices, norm=NORM_LINF, pb=None):
         keep = []
         gp = _GenParams(GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed, 0, 0.0, 0, 0, 0, 0)
         h = C.c_void_p()
-        _check(lib().fpr_b200_mgpu_generate(C.byref(gp), C.byref(cls._opts(devices, norm, keep)), C.byref(h)))
+        _check(lib().fpr_b200_mgpu_generate(C.byref(gp), C.byref(cls._opts(devices, norm, keep, pb)), C.byref(h)))
         return cls(h.value, devices)
 
     def run(self, engine: int, cfg: PageRankConfig, copy_ranks=True, copy_trace=True) -> PageRankResult:

@@ -237,9 +237,17 @@ struct PbSet {
   std::map<uint32_t, PbPlan> plans;  // by wave count
   std::vector<void*> allocs;
 };
+// Peer replicas a multi-GPU part's finalize also stores into (this part's
+// slice in each peer's exchange vector; n = 0 on one GPU).
+struct PbPeers {
+  int n = 0;
+  double* p[kMaxPeers] = {};
+};
 // Builds the layout from the resident in-CSR (duplicates and self loops kept
 // exactly as the CSR holds them).  *msg set (no error) on bad geometry.
-cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg);
+// nsrc: the source id space (n; nparts * slice for a multi-GPU part).
+cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift, cudaStream_t st, PbSet& pb,
+                     const char** msg);
 void free_pb(PbSet& pb, cudaStream_t st);
 // First bin of each of (at most) S edge-balanced waves, from the bins' edge
 // offsets (nbins + 1 values): S' + 1 values.
@@ -251,12 +259,16 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
 // One propagation-blocked sweep: for each wave, gather from prev then
 // finish the wave's rows into (pr, cur); residual into err/l1.  EC passes
 // prev != cur with one wave; lockstep passes prev == cur (in place).
-cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev, double* pr,
-                            double* cur, double base, double damping, double* err, double* l1, cudaStream_t st);
+// Ranks are read from pr and written to pr_out (the same array except for a
+// multi-GPU part's ping-pong); contributions go to cur (+ peers).
+cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
+                            const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
+                            double damping, double* err, double* l1, cudaStream_t st);
 
 // runtime.cu hooks for mgpu.cu (the multi-device driver over the part API)
 int set_error(int code, const std::string& msg);  // thread-local last error; returns code
 cudaStream_t graph_stream(const void* graph_handle);
 int graph_device(const void* graph_handle);
+bool graph_uses_pb(const void* graph_handle);
 
 }  // namespace fprb

@@ -13,7 +13,9 @@
 //     stores every new contribution into ALL parts' exchange vectors -- peer
 //     stores over NVLink between distinct GPUs (peer access enabled here),
 //     plain stores within one device -- so the sweep is the all-gather
-//     (fpr_b200_part_sweep_peers, kernels.cu kModePeers);
+//     (fpr_b200_part_sweep_peers: kernels.cu kModePeers for the pull sweep,
+//     the accumulate's finalize in pb.cu for propagation-blocked parts, which
+//     the library picks when the exchange space far exceeds L2);
 //   * the calling thread waits for the parts' 16-B (max, sum) residual pairs,
 //     reduces them in part order (the on_barrier step, deterministic) and
 //     applies the reference's predicate `error <= threshold` (:141, :216).
@@ -297,7 +299,7 @@ int fpr_b200_mgpu_run(fpr_b200_mgpu* mg, int engine, const fpr_config* cfg, doub
   if (result) {
     result->iterations = it;
     result->converged = (it > 0 && (mg->norm == FPR_B200_NORM_L1 ? l1 : err) <= cfg->threshold) ? 1 : 0;
-    result->sweep = FPR_B200_SWEEP_PULL;
+    result->sweep = fprb::graph_uses_pb(mg->parts[0]) ? FPR_B200_SWEEP_PB : FPR_B200_SWEEP_PULL;
     result->final_error = it > 0 ? err : 1.0;
     result->solve_ms = ms;  // device 0's stream: first sweep issued .. last residual read
     result->setup_ms = 0.0;

@@ -76,6 +76,7 @@ constexpr int kAccEpl = FPR_PB_EPL;  // sorted places per lane (4 or 8)
 constexpr int kAccCtas = FPR_PB_ACC_CTAS;  // phase-2 CTAs per SM (at most; shared memory permitting)
 constexpr int kTile = kAccThreads * kAccEpl;
 constexpr int kStages = FPR_PB_STAGES;  // tiles per CTA staged ahead (TMA bulk copies)
+
 static_assert(kAccEpl == 4 || kAccEpl == 8, "kAccEpl is 4 or 8");
 static_assert(kTile <= 65536, "perm is uint16");
 constexpr uint16_t kPadKey = 0xFFFF;  // row offset of a pad entry (bins hold < 2^16 rows)
@@ -338,8 +339,8 @@ struct alignas(16) PbStage {
 __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
     const double* val, const uint16_t* iperm, const uint16_t* skey, const int32_t* unit_bin, const int64_t* unit_e,
     const int32_t* unit_k, const int32_t* unit_j, const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
-    const int32_t* outdeg, double* pr, double* cur, double base, double damping, double* slots,
-    unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs) {
+    const int32_t* outdeg, const double* pr, double* pr_out, double* cur, PbPeers peers, double base,
+    double damping, double* slots, unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs) {
   constexpr int NW = kAccThreads / 32;
   constexpr int WE = 32 * kAccEpl;  // sorted places per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -573,8 +574,14 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
           if (r < r1) {
             const double nv = __dadd_rn(base, __dmul_rn(damping, sum[q]));
             const double dd = fabs(nv - old[q]);
-            pr[r] = nv;
-            if (od[q] > 0) cur[r] = __ddiv_rn(nv, (double)od[q]);
+            pr_out[r] = nv;
+            if (od[q] > 0) {
+              const double c = __ddiv_rn(nv, (double)od[q]);
+              cur[r] = c;
+              // multi-GPU part: the same store into every peer's replica (the
+              // sweep is the exchange, as in kernels.cu kModePeers)
+              for (int pq = 0; pq < peers.n; ++pq) peers.p[pq][r] = c;
+            }
             lmax = fmax(lmax, dd);
             lsum += dd;
           }
@@ -839,14 +846,15 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
   return cudaSuccess;
 }
 
-cudaError_t build_pb(const DevGraph& g, int shift, int chunk_shift, cudaStream_t st, PbSet& pb, const char** msg) {
+cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift, cudaStream_t st, PbSet& pb,
+                     const char** msg) {
   cudaError_t e = cudaSuccess;
   *msg = nullptr;
   pb = PbSet{};
   const int sms = sm_count();
   const int64_t n = g.n;
   const int64_t nbins = n > 0 ? (n + (1ll << shift) - 1) >> shift : 0;
-  const int64_t nchunks = std::max<int64_t>(1, (n + (1ll << chunk_shift) - 1) >> chunk_shift);
+  const int64_t nchunks = std::max<int64_t>(1, (nsrc + (1ll << chunk_shift) - 1) >> chunk_shift);
   // layout kernel: chunk counters + the bin's (2^shift + 1) relative row offsets
   const size_t hist_smem = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t) +
                            (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t);
@@ -931,8 +939,9 @@ out:
   return e;
 }
 
-cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev, double* pr,
-                            double* cur, double base, double damping, double* err, double* l1, cudaStream_t st) {
+cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
+                            const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
+                            double damping, double* err, double* l1, cudaStream_t st) {
   const int W = plan.nwaves;
   // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
   cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
@@ -946,8 +955,8 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
         pb.val, pb.iperm, pb.skey, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_k + u0, plan.unit_j + u0,
-        plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, cur, base, damping, plan.slots,
-        pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
+        plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur,
+        peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1);

@@ -358,14 +358,20 @@ constexpr int64_t kTraceWarps = 0;
 // the L2 -- there the pull gathers miss L2 and each miss moves ~64 B of DRAM
 // for 8 useful bytes (configs 4/5: PB 2.1-2.2x faster per sweep), while on
 // L2-resident vectors (configs 1-3) the pull sweep wins.
-// Multi-GPU parts always use the pull sweep.
+// A multi-GPU part gathers from the whole exchange space (nparts x slice
+// contributions), so the rule uses that size.
+int64_t source_space(const fpr_b200_graph* h) {
+  return h->nparts > 1 ? (int64_t)h->nparts * (int64_t)h->slice : (int64_t)h->g.n;
+}
+
 bool pb_wanted(const fpr_b200_graph* h) {
-  if (h->nparts > 1 || (h->flags & FPR_B200_OPT_PULL)) return false;
+  if (h->flags & FPR_B200_OPT_PULL) return false;
   if (h->flags & FPR_B200_OPT_PB) return true;
   int l2 = 0;
   if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
-  if (const char* v = std::getenv("FPR_B200_PB_AUTO_BYTES")) return (int64_t)h->g.n * 8 > std::atoll(v);  // tests
-  return (int64_t)h->g.n * (int64_t)sizeof(double) > 2 * (int64_t)l2;
+  const int64_t bytes = source_space(h) * (int64_t)sizeof(double);
+  if (const char* v = std::getenv("FPR_B200_PB_AUTO_BYTES")) return bytes > std::atoll(v);  // tests
+  return bytes > 2 * (int64_t)l2;
 }
 
 int finish_graph(fpr_b200_graph* h) {
@@ -1037,20 +1043,16 @@ namespace {
 // from and written to contrib[0] in place, so wave w reads this sweep's
 // contributions of waves < w (fo_pagerank_lockstep).  The host checks the
 // stop rule after each sweep.
-constexpr int kPbDeclined = -1;  // run_pb: auto-selected layout did not fit; run the pull sweep
+constexpr int kPbDeclined = -1;  // the auto-selected layout did not fit; run the pull sweep
 
-int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* ranks_out, double* errors_out,
-           double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
-  const DevGraph& g = h->g;
-  float setup_ms = 0.f, solve_ms = 0.f;
-  uint64_t launches = 0;
-  CK(cudaEventRecord(h->ev[0], h->stream));
+// The propagation-blocked layout of h, built at its first use.
+int ensure_pb(fpr_b200_graph* h) {
   if (!h->pb) {
     int shift = 0, chunk_shift = 0;
     pb_geometry(&shift, &chunk_shift);
     auto* pb = new PbSet;
     const char* msg = nullptr;
-    cudaError_t e = build_pb(g, shift, chunk_shift, h->stream, *pb, &msg);
+    cudaError_t e = build_pb(h->g, source_space(h), shift, chunk_shift, h->stream, *pb, &msg);
     if (e != cudaSuccess || msg) {
       delete pb;
       if (!(h->flags & FPR_B200_OPT_PB) && (msg || e == cudaErrorMemoryAllocation)) {
@@ -1065,6 +1067,19 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
                   std::string("fpr_b200 propagation-blocked layout: ") + cudaGetErrorString(e));
     }
     h->pb = pb;
+  }
+  return FPR_B200_OK;
+}
+
+int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* ranks_out, double* errors_out,
+           double* l1_out, uint64_t* iter_ns_out, uint64_t errors_cap, fpr_b200_result* result) {
+  const DevGraph& g = h->g;
+  float setup_ms = 0.f, solve_ms = 0.f;
+  uint64_t launches = 0;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  {
+    const int rc = ensure_pb(h);
+    if (rc) return rc;  // kPbDeclined included
   }
   const PbPlan* plan = nullptr;
   {
@@ -1084,7 +1099,7 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
     CK(cudaEventRecord(h->ev[1], h->stream));
     double* prev = h->contrib[lockstep ? 0 : par];
     double* next = h->contrib[lockstep ? 0 : par ^ 1];
-    CK(launch_pb_sweep(*h->pb, *plan, g, prev, h->pr, next, base, cfg->damping, h->d_errors,
+    CK(launch_pb_sweep(*h->pb, *plan, g, prev, h->pr, h->pr, next, PbPeers{}, base, cfg->damping, h->d_errors,
                        h->d_l1, h->stream));
     launches += (uint64_t)plan->nwaves + (uint64_t)(plan->item0.back() > 0 ? plan->nwaves : 0) + 1;
     CK(cudaEventRecord(h->ev[2], h->stream));
@@ -1501,6 +1516,37 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   if (engine == kFused && exch_read != exch_write)
     return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep: FUSED updates the exchange vector in place");
   CK(cudaSetDevice(h->device));
+  const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
+  if (h->use_pb) {
+    // propagation-blocked part sweep: bins over the part's rows, chunks over
+    // the exchange space; the accumulate's finalize stores each contribution
+    // into the part's slice and into every peer's replica.  EC: one wave;
+    // FUSED: the lockstep waves, in place.
+    rc = ensure_pb(h);
+    if (rc && rc != kPbDeclined) return rc;
+    if (!rc) {
+      const PbPlan* plan = nullptr;
+      const cudaError_t e = get_pb_plan(*h->pb, engine == kFused ? lockstep_waves(h) : 1u, h->stream, &plan);
+      if (e != cudaSuccess)
+        return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
+                    std::string("fpr_b200 propagation-blocked plan: ") + cudaGetErrorString(e));
+      const int64_t off = (int64_t)h->part_id * (int64_t)h->slice;
+      PbPeers peers;
+      for (uint32_t q = 0; q < npeer_bufs; ++q) {
+        if (q == h->part_id) continue;
+        if (!peer_write[q]) return fail(FPR_B200_EINVAL, "fpr_b200_part_sweep_peers: null peer pointer");
+        peers.p[peers.n++] = peer_write[q] + off;
+      }
+      ++h->part_sweeps;
+      CK(launch_pb_sweep(*h->pb, *plan, h->g, exch_read, h->part_pr[h->part_pr_cur], h->part_pr[h->part_pr_cur ^ 1],
+                         exch_write + off, peers, (1.0 - cfg->damping) / (double)ng, cfg->damping, h->d_errors,
+                         h->d_l1, h->stream));
+      h->part_pr_cur ^= 1;
+      CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      return FPR_B200_OK;
+    }
+  }
   const Waves* wv = nullptr;
   if ((rc = get_waves(h, 1u, &wv))) return rc;
   const int variant = engine == kFused ? 1 : 0;
@@ -1508,7 +1554,6 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   const int wpb = solve_block_threads(shape) / 32;
   const int64_t want = (h->part.ntasks + wpb - 1) / wpb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid_full[variant], want));
-  const uint64_t ng = h->nparts > 1 ? h->n_global : (uint64_t)h->g.n;
   SolveParams p{};
   p.n = h->g.n;
   p.row = h->g.row;
@@ -1859,4 +1904,5 @@ namespace fprb {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 cudaStream_t graph_stream(const void* h) { return static_cast<const fpr_b200_graph*>(h)->stream; }
 int graph_device(const void* h) { return static_cast<const fpr_b200_graph*>(h)->device; }
+bool graph_uses_pb(const void* h) { return static_cast<const fpr_b200_graph*>(h)->use_pb; }
 }  // namespace fprb

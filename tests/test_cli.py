@@ -78,7 +78,7 @@ def test_bench_library_options(tmp_path):
 @pytest.mark.gpu
 def test_gen_and_compare(tmp_path):
     p = str(tmp_path / "g.fprg")
-    assert _run(["gen", "--rmat", "6:4:3", "--out", p])[0] == EXIT_OK
+    assert _run(["gen", "--rmat", "6:4:3", "--format", "fprg", "--out", p])[0] == EXIT_OK
     rc, text = _run(["compare", "--graph", p, "--threshold", "1e-12"])
     assert rc == EXIT_OK and text.startswith("iteration,ec_b200,fused_b200,fused_lockstep_b200")
 

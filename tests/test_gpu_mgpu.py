@@ -23,15 +23,21 @@ def rmat16(oracle):
     return g, fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
 
 
-@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
-def test_mgpu_ec_matches_oracle(oracle, rmat16, P):
+@pytest.mark.parametrize("P,pb", [(1, False), (2, False), (3, False), (5, False), (8, False), (2, True), (3, True),
+                                  (8, True)])
+def test_mgpu_ec_matches_oracle(oracle, rmat16, P, pb, monkeypatch):
+    """pb=True: propagation-blocked part sweeps (bins over the part's rows,
+    chunks over the exchange space, the finalize storing into the peers),
+    small chunks so that every part walks several."""
     g, hg = rmat16
+    monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", "12")
     ref = oracle.pagerank_ec(g, threshold=T, history_cap=2)
-    with fb.MultiDeviceGraph.from_graph(hg, [0] * P) as mg:
+    with fb.MultiDeviceGraph.from_graph(hg, [0] * P, pb=pb) as mg:
         assert mg.nparts == P and mg.bounds[0] == 0 and mg.bounds[-1] == g.n
         r = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T))
         r2 = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=2))
         fu = mg.run(fb.ENGINE_FUSED, fb.PageRankConfig(threshold=T))
+    assert r.sweep == (fb.SWEEP_PB if pb else fb.SWEEP_PULL)
     assert r.trace.iterations == ref.iterations and r.trace.converged
     assert float(np.max(np.abs(r.ranks.values - ref.ranks) / ref.ranks)) <= 1e-12
     assert np.max(np.abs(r.trace.errors - ref.errors)) <= 1e-12 * float(ref.ranks.max())
