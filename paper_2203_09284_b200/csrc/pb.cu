@@ -250,11 +250,16 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 // Phase 1: warps take pieces in chunk order from a global counter (static
 // striding lets fast warps drift chunks ahead and the concurrently read
 // contribution window outgrow L2); 8 gathers in flight per lane.
-__global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t* src_bm, const int64_t* item_start,
+#ifndef FPR_PB_GATHER_VEC
+#define FPR_PB_GATHER_VEC 1
+#endif
+#ifndef FPR_PB_GATHER_MINB
+#define FPR_PB_GATHER_MINB 1
+#endif
+__global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(const int32_t* src_bm, const int64_t* item_start,
                                                                     const uint32_t* item_len, int64_t nitems,
                                                                     const double* prev, double* val,
                                                                     unsigned long long* next_item) {
-  constexpr int U = 8;
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long it = 0;
@@ -263,6 +268,48 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
     if ((int64_t)it >= nitems) break;
     const int64_t p0 = __ldg(item_start + it);
     const uint32_t len = __ldg(item_len + it);
+#if FPR_PB_GATHER_VEC
+    // Lane L owns 4 consecutive entries per step (positions from the piece's
+    // 4-aligned base): one 16-B source load and one 32-B value store per 4
+    // entries instead of one instruction per entry each, so the LSU queue
+    // (lg_throttle, 27% of the scalar form's stall samples) carries mostly
+    // the gathers.  Partial vectors at the piece's ends store per entry.
+    constexpr int U = 2;  // steps in flight: 8 gathers per lane
+    const int64_t a0 = p0 & ~int64_t(3), p1 = p0 + len;
+    for (int64_t q0 = a0; q0 < p1; q0 += 128 * U) {
+      int4 sv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * 128 + 4 * lane;
+        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(src_bm + q)) : make_int4(-1, -1, -1, -1);
+      }
+      double v[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * 128 + 4 * lane;
+        const int s4[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool ok = q + j >= p0 && q + j < p1 && s4[j] >= 0;
+          v[u][j] = ok ? (FPR_PB_GATHER_L1 ? __ldca(prev + s4[j]) : __ldcg(prev + s4[j])) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * 128 + 4 * lane;
+        if (q >= p0 && q + 4 <= p1) {
+          asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(val + q), "d"(v[u][0]), "d"(v[u][1]),
+                       "d"(v[u][2]), "d"(v[u][3])
+                       : "memory");
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (q + j >= p0 && q + j < p1) __stcs(val + q + j, v[u][j]);
+        }
+      }
+    }
+#else
+    constexpr int U = 8;
     for (uint32_t k0 = 0; k0 < len; k0 += 32 * U) {
       int32_t s[U];
 #pragma unroll
@@ -279,6 +326,7 @@ __global__ void __launch_bounds__(kGatherThreads) pb_gather_kernel(const int32_t
         if (k < len) __stcs(val + p0 + k, v[u]);
       }
     }
+#endif
   }
 }
 
