@@ -78,6 +78,7 @@ constexpr int kTile = kAccThreads * kAccEpl;
 constexpr int kStages = FPR_PB_STAGES;  // tiles per CTA staged ahead (TMA bulk copies)
 
 static_assert(kAccEpl == 4 || kAccEpl == 8, "kAccEpl is 4 or 8");
+
 static_assert(kTile <= 65536, "perm is uint16");
 constexpr uint16_t kPadKey = 0xFFFF;  // row offset of a pad entry (bins hold < 2^16 rows)
 // phase 1 gathers: L1-allocating (default: hub sources recur across the bins a
