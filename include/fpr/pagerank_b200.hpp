@@ -83,6 +83,23 @@ inline PageRankResult pagerank_fused_b200(const Graph& g, const PageRankConfig& 
   return b200::run(g, FPR_B200_ENGINE_FUSED, cfg);
 }
 
+// With library options: a device list (opts.devices / ndevices > 1) runs the
+// multi-device solve from this thread (the reference's thread fan-out,
+// pagerank.hpp:111-122, moved to GPUs); flags force a sweep kind.
+inline PageRankResult pagerank_ec_b200(const Graph& g, EdgeCentricLayout& layout, const PageRankConfig& cfg,
+                                       const fpr_b200_options& opts) {
+  validate(cfg);
+  detail::require_layout(g, layout);
+  return b200::run(g, FPR_B200_ENGINE_EC, cfg, &opts);
+}
+
+inline PageRankResult pagerank_fused_b200(const Graph& g, EdgeCentricLayout& layout, const PageRankConfig& cfg,
+                                          const fpr_b200_options& opts) {
+  validate(cfg);
+  detail::require_layout(g, layout);
+  return b200::run(g, FPR_B200_ENGINE_FUSED, cfg, &opts);
+}
+
 inline PageRankResult pagerank_fused_lockstep_b200(const Graph& g, EdgeCentricLayout& layout,
                                                    const PageRankConfig& cfg) {
   validate(cfg);

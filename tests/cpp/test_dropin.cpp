@@ -50,6 +50,21 @@ int main() {
   CHECK(max_rel(gpu.ranks.values, ref.ranks.values) <= 1e-12, "ec rel err %.3e",
         max_rel(gpu.ranks.values, ref.ranks.values));
 
+  // the same call site with a device list: three parts driven from this
+  // thread (all on device 0 here; distinct GPUs in production)
+  {
+    int32_t devs[3] = {0, 0, 0};
+    fpr_b200_options o;
+    fpr_b200_options_init(&o);
+    o.devices = devs;
+    o.ndevices = 3;
+    const fpr::PageRankResult mg = fpr::pagerank_ec_b200(g, layout, cfg, o);
+    CHECK(mg.trace.iterations == ref.trace.iterations, "multi-device iterations %llu vs %llu",
+          (unsigned long long)mg.trace.iterations, (unsigned long long)ref.trace.iterations);
+    CHECK(max_rel(mg.ranks.values, ref.ranks.values) <= 1e-12, "multi-device rel err %.3e",
+          max_rel(mg.ranks.values, ref.ranks.values));
+  }
+
   fpr::PageRankConfig tight = cfg;
   tight.threshold = 1e-13;
   const fpr::PageRankResult fref = fpr::pagerank_fused_seq(g, layout, tight);
