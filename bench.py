@@ -216,6 +216,8 @@ def run_reference(args) -> None:
             "steps": 1, "warmup": 0, "requested_steps": args.steps, "requested_warmup": args.warmup,
             "ms_per_step": 1e3 * r.seconds, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": data, "config": config_block(config, n, m),
+            "step": (f"bounded sample: {r.iterations} EC iterations in one pagerank_ec_par call (GTEPS/iter)"
+                     if config == "5" else "1 full EC solve (time-to-converge)"), "iterations_timed": r.iterations,
             "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": threads, "kind": "reference",
                              "cpu": cpu_model(), "sample": sample, "setup_s_untimed": setup_s},
             "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -224,7 +226,7 @@ def run_reference(args) -> None:
 
 def config_block(config: str, n: int, m: int) -> dict:
     return {"workload": WORKLOADS[config], "n": n, "m": m, "threshold": THRESHOLD, "norm": "linf",
-            "damping": DAMPING, "step": "1 full EC solve (time-to-converge)",
+            "damping": DAMPING,
             "l2": {"5": "inputs larger than L2 (in_src 17 GB, contributions 2.1 GB); no flush",
                    "2": "in_src 268 MB > L2; contributions L2-resident; no flush",
                    "1": "L2-resident (correctness-sized config)"}[config]}
@@ -459,7 +461,7 @@ def main() -> None:
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device-generated, bit-identical to reference generate_rmat+build_csr)",
         "config": config_block(args.workload, n, m),  # the reference arm prints the same block
-        "iterations": iters, "parallelism": "single-gpu",
+        "step": "1 full EC solve (time-to-converge)", "iterations": iters, "parallelism": "single-gpu",
         "sweep": "propagation-blocked (the library's default for this graph)" if pb else "pull (library default)",
         "time_to_converge_ms": ms_step,
         "first_solve_s_with_layout_build": first_s,
@@ -470,6 +472,12 @@ def main() -> None:
                      "algorithmic_bytes_per_sweep": algorithmic_bytes(n, m),
                      "sweep_ms": sweep_ms,
                      "pb_stream_bytes_frac": pb_stream_bytes(n, m) / (sweep_ms * 1e-3) / 1e9 / peak if pb else None,
+                     # the design's own floor: the gather pass at the measured
+                     # random-fetch ceiling (~270 G L2 requests/s, bench_micro/gather_bench.cu)
+                     # plus the accumulate's stream (20 B/edge + 36 B/vertex) at the copy peak
+                     "pb_design_floor_ms": (m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3 if pb else None,
+                     "pb_design_floor_frac": ((m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3 / sweep_ms
+                                              if pb else None),
                      "traffic_source": traffic.get("source") if traffic else None,
                      "kernel_shares": traffic.get("kernel_shares") if traffic else None},
         "fused": fused,
@@ -581,6 +589,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated, bit-identical to reference generate_rmat+build_csr)",
             "config": config_block(args.workload, n, m),
+            "step": "1 full EC solve (time-to-converge)",
             "iterations": iters, "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
             "sweep": "pull (per part)",
             "host_loop": ("speculative: sweep k+1 enqueued before iteration k's residual is read"

@@ -138,22 +138,36 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       running += tile;
       __syncthreads();
     }
+    int rcur = -1;  // row holding the current CSR tile's first edge (carried across tiles)
+    const int nrows = (int)(r1 - r0);
     for (int64_t t = e0; t < e1; t += kPbThreads) {
       const int64_t e = t + tid;
+      // row of every edge of the tile: each row that starts inside the tile
+      // marks its first position (empty rows share the next row's start, so
+      // the max wins), then one block max-scan fills the positions between
+      const uint32_t ts = (uint32_t)(t - e0), te = ts + kPbThreads;
+      skey[tid] = 0;
+      __syncthreads();
+      for (int r = rcur + 1 + tid; r < nrows; r += kPbThreads) {
+        const uint32_t sr = srow[r];
+        if (sr >= te) break;
+        if (sr >= ts) atomicMax(&skey[sr - ts], (uint32_t)(r + 1));  // +1: 0 = no mark
+      }
+      __syncthreads();
+      int rowp = (int)skey[tid] - 1;
+      if (tid == 0 && rowp < rcur) rowp = rcur;
+      ScanI(tmp.scani).InclusiveScan(rowp, rowp, cub::Max());
+      __syncthreads();
+      if (tid == kPbThreads - 1) skey[0] = (uint32_t)rowp;
+      __syncthreads();
+      rcur = (int)skey[0];
+      __syncthreads();
       uint32_t key[1] = {sentinel};
       uint64_t val[1] = {0};
       if (e < e1) {
-        // row of edge e: last r in [0, r1 - r0) with srow[r] <= e - e0
-        const uint32_t el = (uint32_t)(e - e0);
-        int lo = 0, hi = (int)(r1 - r0) - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (srow[mid] <= el) lo = mid;
-          else hi = mid - 1;
-        }
         const uint32_t s = (uint32_t)__ldg(src + e);
         key[0] = s >> chunk_shift;
-        val[0] = ((uint64_t)s << 16) | (uint64_t)lo;
+        val[0] = ((uint64_t)s << 16) | (uint64_t)rowp;
       }
       Sort(tmp.sort).Sort(key, val, 0, key_bits);
       __syncthreads();
@@ -180,9 +194,11 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
 // j] = storage index (in the tile) of sorted place j.  Built once with the
 // layout.
 __global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_t* dstl, const int64_t* bin_pos,
-                                                                   int64_t nbins, uint16_t* iperm, uint16_t* skey) {
+                                                                   int64_t nbins, int shift, uint16_t* iperm,
+                                                                   uint16_t* skey) {
   using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t>;
   __shared__ typename Sort::TempStorage tmp;
+  const uint32_t pad_key = 1u << shift;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
     const int64_t p1 = bin_pos[b + 1];
     for (int64_t t0 = bin_pos[b]; t0 < p1; t0 += kTile) {
@@ -191,15 +207,18 @@ __global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
         const int i = threadIdx.x * kAccEpl + j;
-        key[j] = i < len ? (uint32_t)dstl[t0 + i] : 0x10000u;  // past the tile: after the pads
+        // rows < 2^shift; pads sort after them, places past the tile last:
+        // shift + 1 key bits (radix passes) instead of 17
+        const uint32_t d = i < len ? (uint32_t)dstl[t0 + i] : 0x10000u;
+        key[j] = d == 0x10000u ? (pad_key + 1) : (d == kPadKey ? pad_key : d);
         idx[j] = (uint32_t)i;
       }
-      Sort(tmp).Sort(key, idx, 0, 17);
+      Sort(tmp).Sort(key, idx, 0, shift + 1);
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
         const int p = threadIdx.x * kAccEpl + j;
         if (p < len) {
-          skey[t0 + p] = (uint16_t)key[j];
+          skey[t0 + p] = key[j] == pad_key ? kPadKey : (uint16_t)key[j];
           iperm[t0 + p] = (uint16_t)idx[j];
         }
       }
@@ -961,7 +980,7 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
         pb.src_bm, dstl);
     PK(cudaGetLastError());
     pb_tile_sort_kernel<<<(unsigned)std::min<int64_t>(nbins, (int64_t)sms * 2), kAccThreads, 0, st>>>(
-        dstl, pb.bin_pos_d, nbins, pb.iperm, pb.skey);
+        dstl, pb.bin_pos_d, nbins, shift, pb.iperm, pb.skey);
     PK(cudaGetLastError());
   }
   PK(alloc((void**)&pb.bin_pairs, 2 * nbins * sizeof(double)));
