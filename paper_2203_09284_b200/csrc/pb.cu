@@ -386,10 +386,13 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// Tile streams are read once: evict-first in L2, so that a gather pass
+// running beside this accumulate keeps its contribution window resident.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -433,13 +436,15 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
   if (threadIdx.x < NW) flag[threadIdx.x] = 0xFFFFFFFFu;
   __syncthreads();
   uint32_t tc = 0;  // tiles this CTA consumed so far: stage tc % kStages, parity (tc / kStages) & 1
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   auto issue = [&](uint32_t tile_no, int64_t t0, int len) {
     PbStage& st = stage[tile_no % kStages];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(bar + tile_no % kStages, (uint32_t)len * 12u);
-    bulk_g2s(st.v, val + t0, (uint32_t)len * 8u, bar + tile_no % kStages);
-    bulk_g2s(st.ip, iperm + t0, (uint32_t)len * 2u, bar + tile_no % kStages);
-    bulk_g2s(st.k, skey + t0, (uint32_t)len * 2u, bar + tile_no % kStages);
+    bulk_g2s(st.v, val + t0, (uint32_t)len * 8u, bar + tile_no % kStages, pol);
+    bulk_g2s(st.ip, iperm + t0, (uint32_t)len * 2u, bar + tile_no % kStages, pol);
+    bulk_g2s(st.k, skey + t0, (uint32_t)len * 2u, bar + tile_no % kStages, pol);
   };
   for (;;) {
     if (threadIdx.x == 0) s_unit = (long long)atomicAdd(next_unit, 1ull);
@@ -745,6 +750,12 @@ int sm_count() {
 }  // namespace
 
 void free_pb(PbSet& pb, cudaStream_t st) {
+  if (pb.aux) {
+    cudaStreamSynchronize(pb.aux);
+    cudaStreamDestroy(pb.aux);
+  }
+  for (cudaEvent_t ev : pb.ev)
+    if (ev) cudaEventDestroy(ev);
   for (auto& kv : pb.plans)
     for (void* p : kv.second.allocs)
       if (p) cudaFreeAsync(p, st);
@@ -996,6 +1007,13 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * per_sm);
     pb.p1_grid = sms * 8;
     pb.acc_smem = (int)acc_smem;
+    // overlapped EC waves: one accumulate CTA + two gather CTAs per SM
+    // (registers: 512 x 64 + 2 x 256 x 48 < 64 K)
+    pb.p2_grid_overlap = (int)std::min<int64_t>(nbins, (int64_t)sms);
+    pb.p1_grid_overlap = sms * 2;
+    PK(cudaStreamCreateWithFlags(&pb.aux, cudaStreamNonBlocking));
+    pb.ev.assign(65, nullptr);
+    for (auto& ev : pb.ev) PK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   PK(cudaStreamSynchronize(st));
 out:
@@ -1014,6 +1032,30 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
   // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
   cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
+  if (prev != cur && W > 1 && pb.aux && (int)pb.ev.size() > W) {
+    // Jacobi waves are independent (all read prev, write cur), so wave w+1's
+    // gather pass (request-bound) runs on the side stream beside wave w's
+    // accumulate (stream-bound); grids sized so both fit on every SM
+    if ((e = cudaEventRecord(pb.ev[W], st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(pb.aux, pb.ev[W], 0)) != cudaSuccess) return e;
+    for (int w = 0; w < W; ++w) {
+      const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
+      if (plan.item0[w + 1] > i0) {
+        pb_gather_kernel<<<pb.p1_grid_overlap, kGatherThreads, 0, pb.aux>>>(
+            pb.src_bm, plan.item_start + i0, plan.item_len + i0, plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      }
+      if ((e = cudaEventRecord(pb.ev[w], pb.aux)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(st, pb.ev[w], 0)) != cudaSuccess) return e;
+      pb_accum_kernel<<<pb.p2_grid_overlap, kAccThreads, pb.acc_smem, st>>>(
+          pb.val, pb.iperm, pb.skey, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_k + u0, plan.unit_j + u0,
+          plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur, peers, base,
+          damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1);
+    return cudaGetLastError();
+  }
   for (int w = 0; w < W; ++w) {
     const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
     if (plan.item0[w + 1] > i0) {

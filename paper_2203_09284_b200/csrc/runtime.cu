@@ -520,6 +520,16 @@ void pb_geometry(int* shift, int* chunk_shift) {
 // all chunk windows and drains two launches, so fewer waves pay: one per
 // 128 M merge items, 2-8 (measured optima: config 4 4-8 waves, config 5 8;
 // DESIGN.md §3.4).
+// EC on propagation-blocked sweeps: waves overlapped on two streams (wave
+// w+1's gather beside wave w's accumulate, pb.cu launch_pb_sweep).
+// FPR_B200_PB_EC_WAVES overrides (1 = no overlap).
+uint32_t pb_ec_waves(const fpr_b200_graph* h) {
+  (void)h;
+  uint32_t w = 1;
+  if (const char* v = std::getenv("FPR_B200_PB_EC_WAVES")) w = (uint32_t)std::max(1, std::min(64, std::atoi(v)));
+  return w;
+}
+
 uint32_t lockstep_waves(const fpr_b200_graph* h) {
   if (h->wave_count) return h->wave_count;
   const int64_t items = (int64_t)h->g.n + h->g.m;
@@ -1083,7 +1093,7 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
   }
   const PbPlan* plan = nullptr;
   {
-    cudaError_t e = get_pb_plan(*h->pb, lockstep ? lockstep_waves(h) : 1u, h->stream, &plan);
+    cudaError_t e = get_pb_plan(*h->pb, lockstep ? lockstep_waves(h) : pb_ec_waves(h), h->stream, &plan);
     if (e != cudaSuccess)
       return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
                   std::string("fpr_b200 propagation-blocked plan: ") + cudaGetErrorString(e));
@@ -1526,7 +1536,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
     if (rc && rc != kPbDeclined) return rc;
     if (!rc) {
       const PbPlan* plan = nullptr;
-      const cudaError_t e = get_pb_plan(*h->pb, engine == kFused ? lockstep_waves(h) : 1u, h->stream, &plan);
+      const cudaError_t e = get_pb_plan(*h->pb, engine == kFused ? lockstep_waves(h) : pb_ec_waves(h), h->stream, &plan);
       if (e != cudaSuccess)
         return fail(e == cudaErrorMemoryAllocation ? FPR_B200_ENOMEM : FPR_B200_ECUDA,
                     std::string("fpr_b200 propagation-blocked plan: ") + cudaGetErrorString(e));
