@@ -52,6 +52,10 @@ namespace fprb {
 namespace {
 
 constexpr int kPbThreads = 1024;
+constexpr int64_t kSplitMaxChunks = 256;  // layout: multi-split fast path up to this many source chunks
+#ifndef FPR_PB_TSORT_BITS
+#define FPR_PB_TSORT_BITS 5  // tile sort radix digit: 14-bit keys in 3 passes
+#endif
 constexpr int kGatherThreads = 256;
 
 constexpr int kPieceEntries = 1024;  // phase-1 work item: up to this many entries of one segment
@@ -162,6 +166,44 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       __syncthreads();
       rcur = (int)skey[0];
       __syncthreads();
+      if (nchunks <= kSplitMaxChunks) {
+        // stable multi-split by chunk (the common geometry: <= 256 chunks):
+        // rank among equal chunks inside the warp from match.any, warps'
+        // counts scanned per chunk in warp order, positions from the
+        // chunk's running cursor h[] -- no radix passes
+        const int lane = tid & 31, warp = tid >> 5;
+        uint32_t* wcnt = srow + (((int64_t)1 << min(shift, 20)) + 1);  // (nchunks + 1) x 32 counts
+        const uint32_t ck = e < e1 ? ((uint32_t)__ldg(src + e) >> chunk_shift) : sentinel;
+        const uint32_t sv = e < e1 ? (uint32_t)__ldg(src + e) : 0u;
+        for (int64_t i = tid; i < (nchunks + 1) * 32; i += kPbThreads) wcnt[i] = 0;
+        __syncthreads();
+        const unsigned peers = __match_any_sync(0xffffffffu, ck);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (rank == 0) wcnt[ck * 32 + warp] = (uint32_t)__popc(peers);
+        __syncthreads();
+        // warp w scans chunks w, w + 32, ...: lane = warp index of the tile
+        for (int64_t c = warp; c <= nchunks; c += kPbThreads / 32) {
+          const uint32_t v = wcnt[c * 32 + lane];
+          uint32_t x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          wcnt[c * 32 + lane] = x - v;  // exclusive prefix over the warps
+          if (lane == 31 && c < nchunks) skey[c] = x;  // the tile's count of chunk c (skey is free here)
+        }
+        __syncthreads();
+        if (ck != sentinel) {
+          const int64_t pos = p0 + h[ck] + wcnt[ck * 32 + warp] + rank;
+          src_bm[pos] = (int32_t)sv;
+          dstl_bm[pos] = (uint16_t)rowp;
+        }
+        __syncthreads();
+        for (int64_t c = tid; c < nchunks; c += kPbThreads) h[c] += skey[c];
+        __syncthreads();
+        continue;
+      }
       uint32_t key[1] = {sentinel};
       uint64_t val[1] = {0};
       if (e < e1) {
@@ -196,7 +238,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
 __global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_t* dstl, const int64_t* bin_pos,
                                                                    int64_t nbins, int shift, uint16_t* iperm,
                                                                    uint16_t* skey) {
-  using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t>;
+  using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t, FPR_PB_TSORT_BITS>;
   __shared__ typename Sort::TempStorage tmp;
   const uint32_t pad_key = 1u << shift;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
@@ -936,7 +978,8 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   const int64_t nchunks = std::max<int64_t>(1, (nsrc + (1ll << chunk_shift) - 1) >> chunk_shift);
   // layout kernel: chunk counters + the bin's (2^shift + 1) relative row offsets
   const size_t hist_smem = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t) +
-                           (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t);
+                           (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t) +
+                           (nchunks <= kSplitMaxChunks ? (size_t)(nchunks + 1) * 32 * sizeof(uint32_t) : 0);
   const size_t acc_smem = ((size_t)sizeof(double) << shift) + (size_t)kStages * sizeof(PbStage);
   uint16_t* dstl = nullptr;  // per-entry row offsets, storage order: input of the tile sort
   int64_t* d_pos = nullptr;
