@@ -78,6 +78,22 @@ def pb_stream_bytes(n: int, m: int) -> int:
     return 24 * m + 36 * n
 
 
+# Random 8-B fetches per second against the contribution vector's size,
+# measured by bench_micro/gather_bench.cu (DESIGN.md §3 table).
+GATHER_CEILING = ((33.6e6, 270e9), (134e6, 113e9), (537e6, 56e9), (2.15e9, 46e9))
+
+
+def ceiling_ms(n: int, m: int, pb: bool, peak: float) -> float:
+    """The sweep's own floor: the pull sweep's gathers at the measured random-
+    fetch rate for 8 n bytes of contributions; a propagation-blocked sweep's
+    gather requests at ~270 G/s plus its 20 B/edge + 36 B/vertex stream."""
+    if pb:
+        return (m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3
+    size = 8 * n
+    rate = next((r for s, r in GATHER_CEILING if size <= s * 1.05), GATHER_CEILING[-1][1])
+    return m / rate * 1e3
+
+
 def ncu_traffic(key: str):
     """DRAM read+write bytes per unit from the committed ncu capture."""
     try:
@@ -314,10 +330,15 @@ def secondary_legs(fb, device, peak) -> dict:
 
     def record(dg, r):
         ms_it = r.solve_ms / r.trace.iterations
+        pb = r.sweep == fb.SWEEP_PB
         return {"iterations": r.trace.iterations, "converged": bool(r.trace.converged),
                 "time_to_converge_ms": r.solve_ms, "ms_per_sweep": ms_it, "gteps": dg.m / ms_it / 1e6,
                 "roofline_frac": algorithmic_bytes(dg.n, dg.m) / (ms_it * 1e-3) / 1e9 / peak,
-                "sweep": "pb" if r.sweep == fb.SWEEP_PB else "pull"}
+                "sweep": "pb" if pb else "pull",
+                # the sweep's own ceiling: pull = the measured random-fetch
+                # rate for a contribution vector of this size; PB = gather requests + stream
+                "ceiling_ms": ceiling_ms(dg.n, dg.m, pb, peak),
+                "ceiling_frac": ceiling_ms(dg.n, dg.m, pb, peak) / ms_it}
 
     names = {"2": "config2: uniform G(n=2^22, 2^26 draws, seed 2)",
              "3": "config3: RMAT s24 ef16 seed 3, BFS crawl-order relabel",

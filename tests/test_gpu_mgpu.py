@@ -89,3 +89,33 @@ def test_mgpu_argument_errors(rmat16):
             mg.run(fb.ENGINE_FUSED_LOCKSTEP, fb.PageRankConfig(threshold=T))
         with pytest.raises(ValueError, match="damping"):
             mg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=1.5))
+
+
+@pytest.mark.parametrize("config,P", [("4", 2), ("4", 3), ("5", 2)])
+def test_mgpu_full_size_equals_single_gpu(config, P):
+    """Configs 4/5 split into P destination-range parts on this one GPU, each
+    part generating the graph on its device and running propagation-blocked
+    part sweeps (the library's choice there), equal the single-GPU EC: the
+    same iteration count and ranks within 1e-12 (the per-part
+    sums are the same fixed regroupings as on one GPU, up to the part split)."""
+    cfg = fb.PageRankConfig(threshold=T)
+    if config == "4":
+        gp = fb._GenParams(fb.GEN_CHUNGLU, 0, 0, 0.0, 0.0, 0.0, 0.0, 1 << 26, 0, 4, 1_200_000_000, 2.1, 1_000_000)
+        one = fb.DeviceGraph.generate_chunglu(1 << 26, 1_200_000_000, seed=4)
+    else:
+        p = fb.RmatParams(28, 16, seed=5)
+        gp = fb._GenParams(fb.GEN_RMAT, p.scale, p.edge_factor, p.a, p.b, p.c, p.d, 0, 0, p.seed)
+        one = fb.DeviceGraph.generate_rmat(p)
+    with one:
+        ref = one.run(fb.ENGINE_EC, cfg)
+    keep = []
+    h = C.c_void_p()
+    fb._check(fb.lib().fpr_b200_mgpu_generate(C.byref(gp), C.byref(fb.MultiDeviceGraph._opts([0] * P, fb.NORM_LINF,
+                                                                                            keep)), C.byref(h)))
+    with fb.MultiDeviceGraph(h.value, [0] * P) as mg:
+        r = mg.run(fb.ENGINE_EC, cfg)
+    assert r.sweep == fb.SWEEP_PB
+    assert r.trace.iterations == ref.trace.iterations
+    assert float(np.max(np.abs(r.ranks.values - ref.ranks.values) / ref.ranks.values)) <= 1e-12
+    print(f"\nconfig{config} x{P} parts: {r.trace.iterations} iterations, {r.solve_ms:.0f} ms "
+          f"(one GPU, parts in turn; single-part {ref.solve_ms:.0f} ms)")
