@@ -315,6 +315,9 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 #ifndef FPR_PB_GATHER_VEC
 #define FPR_PB_GATHER_VEC 1
 #endif
+#ifndef FPR_PB_SRC_SORT
+#define FPR_PB_SRC_SORT 1
+#endif
 #ifndef FPR_PB_GATHER_MINB
 #define FPR_PB_GATHER_MINB 1
 #endif
@@ -776,6 +779,20 @@ __global__ void __launch_bounds__(kReduceThreads) pb_reduce_kernel(int64_t nbins
   }
 }
 
+// Segment offsets of bins [b0, b1) relative to base, bin-major (the sort's
+// segment order does not matter; bin-major keeps each group contiguous).
+__global__ void pb_group_offsets_kernel(const uint32_t* counts, const int64_t* start, int64_t nbins, int64_t nchunks,
+                                        int64_t b0, int64_t b1, int64_t base, int64_t* beg, int64_t* end) {
+  const int64_t nseg = (b1 - b0) * nchunks;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += stride) {
+    const int64_t b = b0 + i / nchunks, c = i % nchunks;
+    const int64_t st = start[c * nbins + b] - base;
+    beg[i] = st;
+    end[i] = st + counts[c * nbins + b];
+  }
+}
+
 int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1033,6 +1050,42 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
         g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.bin_pos_d, pb.counts, pb.start,
         pb.src_bm, dstl);
     PK(cudaGetLastError());
+    if (FPR_PB_SRC_SORT) {
+      // Sources ascending inside every (bin, chunk) segment: a hub source's
+      // repeats become neighbours, so the gather pass's lanes fetch the
+      // same or adjacent words in one instruction (one L2 request); the
+      // accumulate's tile sort restores row order.  CUB segmented sort, in
+      // groups of bins of < 2^31 entries (its item count is an int).
+      int64_t b0 = 0;
+      while (b0 < nbins) {
+        int64_t b1 = b0 + 1;
+        while (b1 < nbins && pb.bin_pos[b1 + 1] - pb.bin_pos[b0] < (int64_t(1) << 30)) ++b1;
+        const int64_t base = pb.bin_pos[b0], items = pb.bin_pos[b1] - base, nseg = (b1 - b0) * nchunks;
+        int64_t *beg = nullptr, *end = nullptr;
+        int32_t* ko = nullptr;
+        uint16_t* vo = nullptr;
+        void* temp = nullptr;
+        size_t tb = 0;
+        PK(cudaMallocAsync(&beg, nseg * sizeof(int64_t), st));
+        PK(cudaMallocAsync(&end, nseg * sizeof(int64_t), st));
+        PK(cudaMallocAsync(&ko, std::max<int64_t>(items, 1) * sizeof(int32_t), st));
+        PK(cudaMallocAsync(&vo, std::max<int64_t>(items, 1) * sizeof(uint16_t), st));
+        pb_group_offsets_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, sms * 32)), 256,
+                                  0, st>>>(pb.counts, pb.start, nbins, nchunks, b0, b1, base, beg, end);
+        PK(cudaGetLastError());
+        PK(cudaMemcpyAsync(ko, pb.src_bm + base, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));  // pads
+        PK(cudaMemcpyAsync(vo, dstl + base, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
+        PK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, pb.src_bm + base, ko, dstl + base, vo, (int)items,
+                                                     (int)nseg, beg, end, st));
+        PK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));
+        PK(cub::DeviceSegmentedSort::StableSortPairs(temp, tb, pb.src_bm + base, ko, dstl + base, vo, (int)items,
+                                                     (int)nseg, beg, end, st));
+        PK(cudaMemcpyAsync(pb.src_bm + base, ko, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        PK(cudaMemcpyAsync(dstl + base, vo, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
+        for (void* q : {(void*)beg, (void*)end, (void*)ko, (void*)vo, temp}) cudaFreeAsync(q, st);
+        b0 = b1;
+      }
+    }
     pb_tile_sort_kernel<<<(unsigned)std::min<int64_t>(nbins, (int64_t)sms * 2), kAccThreads, 0, st>>>(
         dstl, pb.bin_pos_d, nbins, shift, pb.iperm, pb.skey);
     PK(cudaGetLastError());
