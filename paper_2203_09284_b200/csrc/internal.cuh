@@ -208,6 +208,7 @@ struct PbPlan {
   // (smaller pieces for more waves, so that every wave has a few units per CTA)
   int32_t* unit_bin = nullptr;
   int64_t* unit_e = nullptr;      // 2 x units: [first, end) storage position of each unit
+  int64_t* unit_t = nullptr;      // units: the unit's first tile
   int32_t* unit_k = nullptr;      // units of the unit's bin (1 = the bin is whole)
   int32_t* unit_j = nullptr;      // index of the unit within its bin
   int32_t* unit_slot = nullptr;   // split bins: the bin's first row-sum slot (-1 otherwise)
@@ -221,13 +222,18 @@ struct PbSet {
   int shift = 0;         // destination bin = row >> shift (at most 2^16 rows: uint16 offsets)
   int chunk_shift = 0;   // source chunk = src >> chunk_shift
   int64_t nbins = 0, nchunks = 0, m = 0, mpad = 0;
-  int32_t* src_bm = nullptr;     // mpad: source of each entry (-1 = pad); bin b's entries (from bin_pos[b]) are
-                                 //    the in-CSR's edges of its rows regrouped by source chunk: (bin, chunk, row)
-  uint16_t* iperm = nullptr;     // mpad: per tile, the storage index of each place in row order
+  // Entries: bin b's (from bin_pos[b]) are the in-CSR's edges of its rows
+  // regrouped by source chunk, sources ascending inside each (bin, chunk)
+  // segment; each distinct (segment, source) is one value.
+  int64_t nvals = 0, ntiles = 0;
+  int32_t* usrc = nullptr;       // nvals: the source of each value (the gather list)
+  double* val = nullptr;         // nvals: per-sweep scratch, the values (contributions) in order
+  uint16_t* vidx = nullptr;      // mpad: per tile, the stage index of the value of each place in row order
   uint16_t* skey = nullptr;      // mpad: row offset (in the bin) at each sorted place of a tile; 0xFFFF = pad
-  double* val = nullptr;         // mpad: per-sweep scratch, contributions in storage order
-  uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
-  int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
+  uint64_t* tile_meta = nullptr;  // ntiles: first value << 16 | values of each tile
+  std::vector<int64_t> tile_off;  // nbins + 1: first tile of each bin
+  uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): values of segment (bin, chunk)
+  int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first value of segment (bin, chunk)
   std::vector<int64_t> bin_edge;  // nbins + 1: in-CSR edge offset of each bin's first row (waves)
   std::vector<int64_t> bin_pos;   // nbins + 1: 4-aligned storage position of each bin
   int64_t* bin_pos_d = nullptr;   // device copy

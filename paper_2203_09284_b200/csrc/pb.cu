@@ -230,21 +230,110 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
   }
 }
 
-// Per tile (kTile consecutive entries from bin_pos[b]; the bin's last tile is
-// shorter): the stable sort of its entries by row.  skey[tile + j] = row
-// offset at sorted place j (kPadKey for pads, which sort last); iperm[tile +
-// j] = storage index (in the tile) of sorted place j.  Built once with the
-// layout.
-__global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_t* dstl, const int64_t* bin_pos,
-                                                                   int64_t nbins, int shift, uint16_t* iperm,
-                                                                   uint16_t* skey) {
+// Distinct values.  Inside a segment the sources ascend, so the repeats of a
+// source (parallel edges into the bin's rows: hub sources on skewed graphs)
+// are neighbours; the gather pass fetches each (segment, source) once and
+// the tiles index the shared value.  An entry opens a new value when it is
+// real and its source differs from the previous entry's, or it starts its
+// bin (different chunks never share a source, so segment starts always
+// open one).  Pads open none.
+__device__ __forceinline__ bool pb_opens(const int32_t* src, int64_t q, int64_t p0, int32_t s) {
+  return s >= 0 && (q == p0 || __ldg(src + q - 1) != s);
+}
+
+// Pass A: the number of values each tile opens (tiles numbered bin by bin:
+// tile_off[b] is bin b's first).
+__global__ void __launch_bounds__(kAccThreads) pb_tile_count_kernel(const int32_t* src, const int64_t* bin_pos,
+                                                                    const int64_t* tile_off, int64_t nbins,
+                                                                    int64_t* tile_cnt) {
+  using Reduce = cub::BlockReduce<uint32_t, kAccThreads>;
+  __shared__ typename Reduce::TempStorage tmp;
+  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
+    int64_t g = tile_off[b];
+    for (int64_t t0 = p0; t0 < p1; t0 += kTile, ++g) {
+      const int len = (int)min((int64_t)kTile, p1 - t0);
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < kAccEpl; ++j) {
+        const int i = threadIdx.x * kAccEpl + j;
+        if (i < len) c += pb_opens(src, t0 + i, p0, __ldg(src + t0 + i)) ? 1u : 0u;
+      }
+      c = Reduce(tmp).Sum(c);
+      if (threadIdx.x == 0) tile_cnt[g] = (int64_t)c;
+      __syncthreads();
+    }
+  }
+}
+
+// Pass B, per tile (kTile consecutive entries from bin_pos[b]; the bin's last
+// tile is shorter), with tile_ex[g] = values opened before tile g:
+//   * value numbering: entry i's value is u(i) = tile_ex[g] + (values opened
+//     in [t0, i]) - 1; the opening entries write usrc[u] (the gather list);
+//     the tile's values are the contiguous run [u0, u0 + nu), staged from the
+//     even index u0 & ~1 (16-B aligned TMA copies): tile_meta[g] = u0 << 16 | nu;
+//   * segment bounds in value numbers: ustart (over the segment's first
+//     entry offset in `start`) and uend, for the gather plan;
+//   * the stable sort of the tile's entries by row: skey[t0 + j] = row offset
+//     at sorted place j (kPadKey for pads, which sort last); vidx[t0 + j] =
+//     the stage index of sorted place j's value.
+// Built once with the layout.
+__global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(
+    const uint16_t* dstl, const int32_t* src, const int64_t* bin_pos, const int64_t* tile_off, const int64_t* tile_ex,
+    int64_t nbins, int shift, int chunk_shift, uint16_t* vidx, uint16_t* skey, int32_t* usrc, uint64_t* tile_meta,
+    int64_t* ustart, int64_t* uend) {
   using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t, FPR_PB_TSORT_BITS>;
-  __shared__ typename Sort::TempStorage tmp;
+  using Scan = cub::BlockScan<uint32_t, kAccThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint16_t loc[kTile];  // stage index of each storage entry's value
+  __shared__ uint32_t s_f0;
   const uint32_t pad_key = 1u << shift;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
-    const int64_t p1 = bin_pos[b + 1];
-    for (int64_t t0 = bin_pos[b]; t0 < p1; t0 += kTile) {
+    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
+    int64_t g = tile_off[b];
+    for (int64_t t0 = p0; t0 < p1; t0 += kTile, ++g) {
       const int len = (int)min((int64_t)kTile, p1 - t0);
+      int32_t s[kAccEpl];
+      uint32_t f[kAccEpl], cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kAccEpl; ++j) {
+        const int i = threadIdx.x * kAccEpl + j;
+        s[j] = i < len ? __ldg(src + t0 + i) : -1;
+        f[j] = i < len && pb_opens(src, t0 + i, p0, s[j]) ? 1u : 0u;
+        cnt += f[j];
+      }
+      uint32_t before, total;
+      Scan(tmp.scan).ExclusiveSum(cnt, before, total);
+      if (threadIdx.x == 0) s_f0 = f[0];
+      __syncthreads();
+      const uint32_t f0 = s_f0;
+      const int64_t ex = tile_ex[g];
+      const int64_t u0 = ex + f0 - 1;  // the value of the tile's first entry
+      const uint32_t a = (uint32_t)(u0 & 1);
+      if (threadIdx.x == 0) tile_meta[g] = ((uint64_t)u0 << 16) | (uint64_t)(total - f0 + 1);
+      uint32_t L = before;  // values opened in [t0, i]
+#pragma unroll
+      for (int j = 0; j < kAccEpl; ++j) {
+        const int i = threadIdx.x * kAccEpl + j;
+        L += f[j];
+        if (i < len) {
+          const int64_t u = ex + (int64_t)L - 1;
+          loc[i] = (uint16_t)(L - f0 + a);
+          if (f[j]) usrc[u] = s[j];
+          if (s[j] >= 0) {
+            const int64_t q = t0 + i;
+            const uint32_t c = (uint32_t)s[j] >> chunk_shift;
+            const int64_t seg = (int64_t)c * nbins + b;
+            if (q == p0 || ((uint32_t)__ldg(src + q - 1) >> chunk_shift) != c) ustart[seg] = u;
+            const int32_t nx = q + 1 < p1 ? __ldg(src + q + 1) : -1;
+            if (nx < 0 || ((uint32_t)nx >> chunk_shift) != c) uend[seg] = u + 1;
+          }
+        }
+      }
+      __syncthreads();  // loc complete; the scan's storage free for the sort
       uint32_t key[kAccEpl], idx[kAccEpl];
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
@@ -255,18 +344,26 @@ __global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_
         key[j] = d == 0x10000u ? (pad_key + 1) : (d == kPadKey ? pad_key : d);
         idx[j] = (uint32_t)i;
       }
-      Sort(tmp).Sort(key, idx, 0, shift + 1);
+      Sort(tmp.sort).Sort(key, idx, 0, shift + 1);
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
         const int p = threadIdx.x * kAccEpl + j;
         if (p < len) {
           skey[t0 + p] = key[j] == pad_key ? kPadKey : (uint16_t)key[j];
-          iperm[t0 + p] = (uint16_t)idx[j];
+          vidx[t0 + p] = loc[idx[j]];
         }
       }
       __syncthreads();
     }
   }
+}
+
+// Segment (bin, chunk) in value numbers: start[s] = its first value (written
+// over the entry offset by pass B), counts[s] = its values.
+__global__ void pb_seg_values_kernel(int64_t nseg, const int64_t* uend, int64_t* start, uint32_t* counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride)
+    counts[s] = counts[s] ? (uint32_t)(uend[s] - start[s]) : 0u;
 }
 
 // Plan order: position p walks the waves (runs of consecutive bins), chunk-
@@ -321,7 +418,7 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 #ifndef FPR_PB_GATHER_MINB
 #define FPR_PB_GATHER_MINB 1
 #endif
-__global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(const int32_t* src_bm, const int64_t* item_start,
+__global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(const int32_t* usrc, const int64_t* item_start,
                                                                     const uint32_t* item_len, int64_t nitems,
                                                                     const double* prev, double* val,
                                                                     unsigned long long* next_item) {
@@ -346,7 +443,7 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t q = q0 + u * 128 + 4 * lane;
-        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(src_bm + q)) : make_int4(-1, -1, -1, -1);
+        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(usrc + q)) : make_int4(-1, -1, -1, -1);
       }
       double v[U][4];
 #pragma unroll
@@ -380,7 +477,7 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t k = k0 + u * 32 + lane;
-        s[u] = k < len ? __ldcs(src_bm + p0 + k) : -1;
+        s[u] = k < len ? __ldcs(usrc + p0 + k) : -1;
       }
       double v[U];
 #pragma unroll
@@ -447,14 +544,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 struct alignas(16) PbStage {
-  double v[kTile];       // values, storage order
-  uint16_t ip[kTile];    // inverse permutation: storage index of each sorted place
+  double v[kTile + 2];   // the tile's distinct values (from an even value index)
+  uint16_t ip[kTile];    // stage index of each sorted place's value
   uint16_t k[kTile];     // row offset of each sorted place
 };
 
 __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
-    const double* val, const uint16_t* iperm, const uint16_t* skey, const int32_t* unit_bin, const int64_t* unit_e,
-    const int32_t* unit_k, const int32_t* unit_j, const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
+    const double* val, const uint16_t* vidx, const uint16_t* skey, const uint64_t* tile_meta, const int32_t* unit_bin,
+    const int64_t* unit_e, const int64_t* unit_t, const int32_t* unit_k, const int32_t* unit_j,
+    const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
     const int32_t* outdeg, const double* pr, double* pr_out, double* cur, PbPeers peers, double base,
     double damping, double* slots, unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs) {
   constexpr int NW = kAccThreads / 32;
@@ -483,12 +581,16 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
   uint32_t tc = 0;  // tiles this CTA consumed so far: stage tc % kStages, parity (tc / kStages) & 1
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  auto issue = [&](uint32_t tile_no, int64_t t0, int len) {
+  // tile meta = first value << 16 | values: the values are staged from the
+  // even index below the first (16-B aligned copy), rounded up to pairs
+  auto issue = [&](uint32_t tile_no, uint64_t meta, int64_t t0, int len) {
     PbStage& st = stage[tile_no % kStages];
+    const int64_t u0 = (int64_t)(meta >> 16);
+    const uint32_t a = (uint32_t)(u0 & 1), vb = ((uint32_t)(meta & 0xFFFFu) + a + 1u) / 2u * 16u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar + tile_no % kStages, (uint32_t)len * 12u);
-    bulk_g2s(st.v, val + t0, (uint32_t)len * 8u, bar + tile_no % kStages, pol);
-    bulk_g2s(st.ip, iperm + t0, (uint32_t)len * 2u, bar + tile_no % kStages, pol);
+    mbar_expect_tx(bar + tile_no % kStages, vb + (uint32_t)len * 4u);
+    bulk_g2s(st.v, val + (u0 - a), vb, bar + tile_no % kStages, pol);
+    bulk_g2s(st.ip, vidx + t0, (uint32_t)len * 2u, bar + tile_no % kStages, pol);
     bulk_g2s(st.k, skey + t0, (uint32_t)len * 2u, bar + tile_no % kStages, pol);
   };
   for (;;) {
@@ -500,9 +602,13 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
     const int k = __ldg(unit_k + u);
     const int64_t e0 = __ldg(unit_e + 2 * u), e1 = __ldg(unit_e + 2 * u + 1);  // whole tiles from the bin's start
     const int ntiles = (int)((e1 - e0 + kTile - 1) / kTile);
-    if (threadIdx.x == 0)
+    const uint64_t* meta = tile_meta + __ldg(unit_t + u);  // this unit's tiles
+    uint64_t mnext = 0;  // thread 0: meta of the next tile to issue, loaded a tile ahead
+    if (threadIdx.x == 0) {
       for (int i = 0; i < kStages && i < ntiles; ++i)
-        issue(tc + i, e0 + (int64_t)i * kTile, (int)min((int64_t)kTile, e1 - e0 - (int64_t)i * kTile));
+        issue(tc + i, __ldg(meta + i), e0 + (int64_t)i * kTile, (int)min((int64_t)kTile, e1 - e0 - (int64_t)i * kTile));
+      if (kStages < ntiles) mnext = __ldg(meta + kStages);
+    }
     for (int i = threadIdx.x; i < R; i += kAccThreads) acc[i] = 0.0;
     __syncthreads();
     for (int ti = 0; ti < ntiles; ++ti, ++tc) {
@@ -640,9 +746,11 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
         acc[pend_key] += sum + pend_s;
       }
       __syncthreads();  // every add of the tile landed; the stage is free
-      if (threadIdx.x == 0 && ti + kStages < ntiles)
-        issue(tc + kStages, e0 + (int64_t)(ti + kStages) * kTile,
+      if (threadIdx.x == 0 && ti + kStages < ntiles) {
+        issue(tc + kStages, mnext, e0 + (int64_t)(ti + kStages) * kTile,
               (int)min((int64_t)kTile, e1 - e0 - (int64_t)(ti + kStages) * kTile));
+        if (ti + kStages + 1 < ntiles) mnext = __ldg(meta + ti + kStages + 1);
+      }
     }
     const int64_t r0 = b << shift;
     const int64_t r1 = min((int64_t)n, r0 + R);
@@ -928,7 +1036,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     if (const char* v = std::getenv("FPR_B200_PB_PIECE")) piece = std::max<int64_t>(32, std::atoll(v));  // tests
     const int64_t piece_tiles = std::max<int64_t>(1, (piece + kTile - 1) / kTile);
     std::vector<int32_t> ubin, uk, uj, uslot;
-    std::vector<int64_t> ue;
+    std::vector<int64_t> ue, ut;
     int64_t nslots = 0;
     plan.unit0.assign(W + 1, 0);
     for (int w = 0; w < W; ++w) {
@@ -943,6 +1051,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
           uj.push_back((int32_t)j);
           uslot.push_back(k > 1 ? (int32_t)nslots : -1);
           ue.push_back(std::min(p1, p0 + tiles * j / k * kTile));
+          ut.push_back(pb.tile_off[b] + tiles * j / k);
         }
         if (k > 1) nslots += k;
       }
@@ -964,6 +1073,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     if (e == cudaSuccess) e = alloc((void**)&plan.unit_j, U * sizeof(int32_t));
     if (e == cudaSuccess) e = alloc((void**)&plan.unit_slot, U * sizeof(int32_t));
     if (e == cudaSuccess) e = alloc((void**)&plan.unit_e, ue2.size() * sizeof(int64_t));
+    if (e == cudaSuccess) e = alloc((void**)&plan.unit_t, U * sizeof(int64_t));
     if (e == cudaSuccess) e = alloc((void**)&plan.slots, (size_t)std::max<int64_t>(1, nslots) * sizeof(double) << pb.shift);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(plan.unit_bin, ubin.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
@@ -973,6 +1083,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
       e = cudaMemcpyAsync(plan.unit_slot, uslot.data(), U * sizeof(int32_t), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(plan.unit_e, ue2.data(), ue2.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(plan.unit_t, ut.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host vectors die at the end of this block
     if (e != cudaSuccess) {
       for (void* q : plan.allocs) cudaFreeAsync(q, st);
@@ -998,8 +1109,12 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
                            (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t) +
                            (nchunks <= kSplitMaxChunks ? (size_t)(nchunks + 1) * 32 * sizeof(uint32_t) : 0);
   const size_t acc_smem = ((size_t)sizeof(double) << shift) + (size_t)kStages * sizeof(PbStage);
-  uint16_t* dstl = nullptr;  // per-entry row offsets, storage order: input of the tile sort
-  int64_t* d_pos = nullptr;
+  // layout temporaries: per-entry row offsets and sources (storage order),
+  // tile offsets, per-tile value counts and their exclusive scan, segment ends
+  uint16_t* dstl = nullptr;
+  int32_t* src_bm = nullptr;
+  int64_t *tile_off_d = nullptr, *tile_cnt = nullptr, *tile_ex = nullptr, *uend = nullptr;
+  void* scan_tmp = nullptr;
   if (n == 0 || shift < 5 || shift > 13 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 192 * 1024 ||
       acc_smem + 2048 > 227 * 1024 || nbins * nchunks > (1ll << 31)) {
     *msg = "bin/chunk geometry out of range";
@@ -1032,30 +1147,35 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     }
   }
   pb.mpad = pb.bin_pos[nbins];
+  pb.tile_off.assign(nbins + 1, 0);
+  for (int64_t b = 0; b < nbins; ++b)
+    pb.tile_off[b + 1] = pb.tile_off[b] + (pb.bin_pos[b + 1] - pb.bin_pos[b] + kTile - 1) / kTile;
+  pb.ntiles = pb.tile_off[nbins];
   PK(alloc((void**)&pb.counts, nbins * nchunks * sizeof(uint32_t)));
   PK(alloc((void**)&pb.start, nbins * nchunks * sizeof(int64_t)));
-  PK(alloc((void**)&pb.src_bm, pb.mpad * sizeof(int32_t)));
-  PK(alloc((void**)&pb.iperm, pb.mpad * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.vidx, pb.mpad * sizeof(uint16_t)));
   PK(alloc((void**)&pb.skey, pb.mpad * sizeof(uint16_t)));
-  PK(alloc((void**)&pb.val, pb.mpad * sizeof(double)));
+  PK(alloc((void**)&pb.tile_meta, pb.ntiles * sizeof(uint64_t)));
   PK(alloc((void**)&pb.bin_pos_d, (nbins + 1) * sizeof(int64_t)));
-  PK(cudaMemsetAsync(pb.val, 0, pb.mpad * sizeof(double), st));  // pad values stay 0
   PK(cudaMemcpyAsync(pb.bin_pos_d, pb.bin_pos.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PK(cudaMallocAsync(&dstl, pb.mpad * sizeof(uint16_t), st));
+  PK(cudaMallocAsync(&tile_off_d, (nbins + 1) * sizeof(int64_t), st));
+  PK(cudaMemcpyAsync(tile_off_d, pb.tile_off.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PK(cudaMallocAsync(&src_bm, std::max<int64_t>(pb.mpad, 1) * sizeof(int32_t), st));
+  PK(cudaMallocAsync(&dstl, std::max<int64_t>(pb.mpad, 1) * sizeof(uint16_t), st));
   {
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
     PK(cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem));
     pb_layout_kernel<<<(unsigned)std::min<int64_t>(nbins, sms), kPbThreads, hist_smem, st>>>(
         g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.bin_pos_d, pb.counts, pb.start,
-        pb.src_bm, dstl);
+        src_bm, dstl);
     PK(cudaGetLastError());
     if (FPR_PB_SRC_SORT) {
       // Sources ascending inside every (bin, chunk) segment: a hub source's
-      // repeats become neighbours, so the gather pass's lanes fetch the
-      // same or adjacent words in one instruction (one L2 request); the
-      // accumulate's tile sort restores row order.  CUB segmented sort, in
-      // groups of bins of < 2^31 entries (its item count is an int).
+      // repeats become neighbours and share one value; neighbouring sources
+      // share L2 lines in one gather instruction.  The accumulate's tile sort
+      // restores row order.  CUB segmented sort, in groups of bins of < 2^31
+      // entries (its item count is an int).
       int64_t b0 = 0;
       while (b0 < nbins) {
         int64_t b1 = b0 + 1;
@@ -1073,21 +1193,53 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
         pb_group_offsets_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, sms * 32)), 256,
                                   0, st>>>(pb.counts, pb.start, nbins, nchunks, b0, b1, base, beg, end);
         PK(cudaGetLastError());
-        PK(cudaMemcpyAsync(ko, pb.src_bm + base, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));  // pads
+        PK(cudaMemcpyAsync(ko, src_bm + base, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));  // pads
         PK(cudaMemcpyAsync(vo, dstl + base, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
-        PK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, pb.src_bm + base, ko, dstl + base, vo, (int)items,
+        PK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, src_bm + base, ko, dstl + base, vo, (int)items,
                                                      (int)nseg, beg, end, st));
         PK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));
-        PK(cub::DeviceSegmentedSort::StableSortPairs(temp, tb, pb.src_bm + base, ko, dstl + base, vo, (int)items,
+        PK(cub::DeviceSegmentedSort::StableSortPairs(temp, tb, src_bm + base, ko, dstl + base, vo, (int)items,
                                                      (int)nseg, beg, end, st));
-        PK(cudaMemcpyAsync(pb.src_bm + base, ko, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        PK(cudaMemcpyAsync(src_bm + base, ko, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         PK(cudaMemcpyAsync(dstl + base, vo, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
         for (void* q : {(void*)beg, (void*)end, (void*)ko, (void*)vo, temp}) cudaFreeAsync(q, st);
         b0 = b1;
       }
     }
-    pb_tile_sort_kernel<<<(unsigned)std::min<int64_t>(nbins, (int64_t)sms * 2), kAccThreads, 0, st>>>(
-        dstl, pb.bin_pos_d, nbins, shift, pb.iperm, pb.skey);
+    // value numbering: values opened per tile, scanned, then the tile pass
+    const int64_t nt = std::max<int64_t>(pb.ntiles, 1), nseg = nbins * nchunks;
+    const unsigned tgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 2));
+    PK(cudaMallocAsync(&tile_cnt, nt * sizeof(int64_t), st));
+    PK(cudaMallocAsync(&tile_ex, nt * sizeof(int64_t), st));
+    PK(cudaMallocAsync(&uend, nseg * sizeof(int64_t), st));
+    PK(cudaMemsetAsync(tile_cnt, 0, nt * sizeof(int64_t), st));
+    pb_tile_count_kernel<<<tgrid, kAccThreads, 0, st>>>(src_bm, pb.bin_pos_d, tile_off_d, nbins, tile_cnt);
+    PK(cudaGetLastError());
+    {
+      size_t tb = 0;
+      PK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tile_cnt, tile_ex, nt, st));
+      PK(cudaMallocAsync(&scan_tmp, std::max<size_t>(tb, 16), st));
+      PK(cub::DeviceScan::ExclusiveSum(scan_tmp, tb, tile_cnt, tile_ex, nt, st));
+    }
+    {
+      int64_t last_ex = 0, last_cnt = 0;
+      PK(cudaMemcpyAsync(&last_ex, tile_ex + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      PK(cudaMemcpyAsync(&last_cnt, tile_cnt + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      PK(cudaStreamSynchronize(st));
+      pb.nvals = last_ex + last_cnt;
+    }
+    // the gather's 16-B source loads and the stage's pair-rounded value
+    // copies read a few words past the end
+    PK(alloc((void**)&pb.usrc, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(int32_t) + 64));
+    PK(alloc((void**)&pb.val, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(double) + 64));
+    PK(cudaMemsetAsync(pb.val, 0, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(double) + 64, st));
+    PK(cudaMemsetAsync(pb.usrc, 0xFF, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(int32_t) + 64, st));
+    pb_tile_sort_kernel<<<tgrid, kAccThreads, 0, st>>>(dstl, src_bm, pb.bin_pos_d, tile_off_d, tile_ex, nbins, shift,
+                                                       chunk_shift, pb.vidx, pb.skey, pb.usrc, pb.tile_meta,
+                                                       pb.start, uend);
+    PK(cudaGetLastError());
+    pb_seg_values_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, sms * 32)), 256, 0,
+                           st>>>(nseg, uend, pb.start, pb.counts);
     PK(cudaGetLastError());
   }
   PK(alloc((void**)&pb.bin_pairs, 2 * nbins * sizeof(double)));
@@ -1113,7 +1265,8 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   }
   PK(cudaStreamSynchronize(st));
 out:
-  if (dstl) cudaFreeAsync(dstl, st);
+  for (void* q : {(void*)dstl, (void*)src_bm, (void*)tile_off_d, (void*)tile_cnt, (void*)tile_ex, (void*)uend, scan_tmp})
+    if (q) cudaFreeAsync(q, st);
   if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
     cudaStreamSynchronize(st);
@@ -1138,13 +1291,14 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
       const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
       if (plan.item0[w + 1] > i0) {
         pb_gather_kernel<<<pb.p1_grid_overlap, kGatherThreads, 0, pb.aux>>>(
-            pb.src_bm, plan.item_start + i0, plan.item_len + i0, plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
+            pb.usrc, plan.item_start + i0, plan.item_len + i0, plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
       if ((e = cudaEventRecord(pb.ev[w], pb.aux)) != cudaSuccess) return e;
       if ((e = cudaStreamWaitEvent(st, pb.ev[w], 0)) != cudaSuccess) return e;
       pb_accum_kernel<<<pb.p2_grid_overlap, kAccThreads, pb.acc_smem, st>>>(
-          pb.val, pb.iperm, pb.skey, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_k + u0, plan.unit_j + u0,
+          pb.val, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
+          plan.unit_k + u0, plan.unit_j + u0,
           plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur, peers, base,
           damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1155,12 +1309,13 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
   for (int w = 0; w < W; ++w) {
     const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
     if (plan.item0[w + 1] > i0) {
-      pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.src_bm, plan.item_start + i0, plan.item_len + i0,
+      pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.usrc, plan.item_start + i0, plan.item_len + i0,
                                                               plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
-        pb.val, pb.iperm, pb.skey, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_k + u0, plan.unit_j + u0,
+        pb.val, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
+        plan.unit_k + u0, plan.unit_j + u0,
         plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur,
         peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
