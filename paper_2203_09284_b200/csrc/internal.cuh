@@ -207,14 +207,15 @@ struct PbPlan {
   // phase-2 units: whole bins, heavy bins cut into runs of whole tiles
   // (smaller pieces for more waves, so that every wave has a few units per CTA)
   int32_t* unit_bin = nullptr;
-  int64_t* unit_e = nullptr;      // 2 x units: [first, end) storage position of each unit
+  int64_t* unit_e = nullptr;      // 2 x units: [first, end) run position of each unit
   int64_t* unit_t = nullptr;      // units: the unit's first tile
   int32_t* unit_k = nullptr;      // units of the unit's bin (1 = the bin is whole)
   int32_t* unit_j = nullptr;      // index of the unit within its bin
   int32_t* unit_slot = nullptr;   // split bins: the bin's first row-sum slot (-1 otherwise)
   double* slots = nullptr;        // split-bin units' row sums, 2^shift doubles per slot
-  int64_t* item_start = nullptr;  // pieces: first entry and length
+  int64_t* item_start = nullptr;  // pieces: first entry, length and first run
   uint32_t* item_len = nullptr;
+  int64_t* item_ubase = nullptr;
   unsigned long long* ctr = nullptr;  // 2 x nwaves work counters (reset per sweep)
   std::vector<void*> allocs;
 };
@@ -223,19 +224,24 @@ struct PbSet {
   int chunk_shift = 0;   // source chunk = src >> chunk_shift
   int64_t nbins = 0, nchunks = 0, m = 0, mpad = 0;
   // Entries: bin b's (from bin_pos[b]) are the in-CSR's edges of its rows
-  // regrouped by source chunk, sources ascending inside each (bin, chunk)
-  // segment; each distinct (segment, source) is one value.
-  int64_t nvals = 0, ntiles = 0;
-  int32_t* usrc = nullptr;       // nvals: the source of each value (the gather list)
-  double* val = nullptr;         // nvals: per-sweep scratch, the values (contributions) in order
-  uint16_t* vidx = nullptr;      // mpad: per tile, the stage index of the value of each place in row order
-  uint16_t* skey = nullptr;      // mpad: row offset (in the bin) at each sorted place of a tile; 0xFFFF = pad
-  uint64_t* tile_meta = nullptr;  // ntiles: first value << 16 | values of each tile
+  // regrouped by source chunk, in row order inside each (bin, chunk)
+  // segment.  A run = the entries of one row in one segment piece; each run
+  // is one partial sum (the gather pass sums it), numbered bin by bin from
+  // pbin_pos[b].
+  int64_t nps = 0, ntiles = 0, npieces = 0;
+  int32_t* esrc = nullptr;       // mpad: the source of each entry; bit 31 = the entry closes its run
+  double* psum = nullptr;        // nps: per-sweep scratch, the runs' partial sums
+  uint16_t* vidx = nullptr;      // nps: per tile of runs, the tile index of the run at each sorted place
+  uint16_t* skey = nullptr;      // nps: row offset (in the bin) at each sorted place of a tile; 0xFFFF = pad
+  uint64_t* tile_meta = nullptr;  // ntiles: first run << 16 | runs of each tile
   std::vector<int64_t> tile_off;  // nbins + 1: first tile of each bin
-  uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): values of segment (bin, chunk)
-  int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first value of segment (bin, chunk)
+  std::vector<int64_t> pbin_pos;  // nbins + 1: 8-aligned first run of each bin
+  uint32_t* counts = nullptr;    // nchunks x nbins (chunk-major): entries of segment (bin, chunk)
+  int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
+  uint32_t* seg_piece0 = nullptr;  // nchunks x nbins: the segment's first gather piece
+  int64_t* pbase = nullptr;        // npieces: the first run of each piece
   std::vector<int64_t> bin_edge;  // nbins + 1: in-CSR edge offset of each bin's first row (waves)
-  std::vector<int64_t> bin_pos;   // nbins + 1: 4-aligned storage position of each bin
+  std::vector<int64_t> bin_pos;   // nbins + 1: 8-aligned entry position of each bin
   int64_t* bin_pos_d = nullptr;   // device copy
   double* bin_pairs = nullptr;   // nbins x (max, sum) residual of each bin's rows, reduced in bin order
   unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep

@@ -11,32 +11,38 @@
 //
 // Layout, built once from the resident in-CSR:
 //   * rows are cut into bins of 2^shift consecutive rows; a bin's entries are
-//     exactly its rows' in-edges, stored from an 8-aligned position bin_pos[b]
-//     (<= 7 pad entries per bin, so tile copies stay 16-B aligned);
+//     exactly its rows' in-edges, stored from an 8-aligned position bin_pos[b];
 //   * inside a bin, entries are regrouped by source chunk (src >> chunk_shift):
-//     segment (bin b, chunk c) is contiguous and keeps ascending rows;
-//   * entry = source id (gather side) + value slot;
-//   * the bin is cut into tiles of kTile entries; per tile, iperm[] lists the
-//     entries in the tile's (stable) row order, and skey[] holds the row
-//     offset of every sorted place (accumulate side).
+//     segment (bin b, chunk c) is contiguous and keeps the CSR order (rows
+//     ascending, a row's sources ascending);
+//   * a run = the consecutive entries of one row inside one segment piece
+//     (kPieceEntries entries from the segment start); its last entry carries
+//     a close flag (bit 31 of the source).  Each run is ONE partial sum;
+//     runs are numbered bin by bin from an 8-aligned pbin_pos[b];
+//   * a bin's runs are cut into tiles of kTile; per tile, vidx[] lists the
+//     runs in the tile's (stable) row order, and skey[] holds the row offset
+//     of every sorted place (accumulate side).
 // A sweep plan (get_pb_plan, cached per wave count) cuts the bins into waves
 // of consecutive bins: 1 wave for EC, S for lockstep.  Per wave:
-//   * phase 1 (pb_gather_kernel): warps walk the wave's segments chunk by
-//     chunk, so the sources read at any moment span one chunk's
-//     contributions (a 16 MB window at the default chunk of 2^21 sources),
-//     and write val[pos] = prev[src_bm[pos]] contiguously;
+//   * phase 1 (pb_gather_kernel): warps walk the wave's segment pieces chunk
+//     by chunk, so the sources read at any moment span one chunk's
+//     contributions (a 16 MB window at the default chunk of 2^21 sources);
+//     they gather every entry's contribution, sum each run left to right
+//     (a segmented warp scan across lanes) and write its partial sum;
 //   * phase 2 (pb_accum_kernel): a CTA takes a bin (or a run of tiles of a
 //     heavy bin), streams each tile into shared memory (TMA bulk copies),
-//     reads it in row order, sums every row's run and adds it to the bin's
-//     row accumulators with ONE plain add per row and tile -- no atomics, a
-//     fixed order -- then finishes the rows: base + d*sum without FMA,
-//     contribution, residual.
-// Per edge and sweep: 4 B source + 8 B value written + 8 B read + 2 B iperm
-// + 2 B key, all sequential, where a missed pull gather moved ~64 B of DRAM.
-// A row's sum is a fixed regrouping of the reference's left-to-right sum
-// (chunks in order, i.e. ascending sources), so every run gives the same
-// bits, within 1e-12 per iteration of the reference
-// (tests/test_gpu_engines.py test_pb_*).  Measurements and rejected
+//     reads it in row order, sums every row's places and adds them to the
+//     bin's row accumulators with ONE plain add per row and tile -- no
+//     atomics, a fixed order -- then finishes the rows: base + d*sum without
+//     FMA, contribution, residual.
+// Per edge and sweep: 4 B source read; per run: 8 B partial sum written and
+// read back + 2 B vidx + 2 B key, all sequential, where a missed pull gather
+// moved ~64 B of DRAM.  R-MAT puts a row's in-edges from one chunk next to
+// each other often enough that config 5 has ~0.25 runs per edge.  A row's
+// sum is a fixed regrouping of the reference's left-to-right sum (runs in
+// chunk order, i.e. ascending sources), so every run gives the same bits,
+// within 1e-12 per iteration of the reference (tests/test_gpu_engines.py
+// test_pb_*, tests/test_gpu_fullsize.py).  Measurements and rejected
 // variants: DESIGN.md §3.4.
 #include <cub/cub.cuh>
 
@@ -230,127 +236,119 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
   }
 }
 
-// Distinct values.  Inside a segment the sources ascend, so the repeats of a
-// source (parallel edges into the bin's rows: hub sources on skewed graphs)
-// are neighbours; the gather pass fetches each (segment, source) once and
-// the tiles index the shared value.  An entry opens a new value when it is
-// real and its source differs from the previous entry's, or it starts its
-// bin (different chunks never share a source, so segment starts always
-// open one).  Pads open none.
-__device__ __forceinline__ bool pb_opens(const int32_t* src, int64_t q, int64_t p0, int32_t s) {
-  return s >= 0 && (q == p0 || __ldg(src + q - 1) != s);
+// Row partial sums.  A segment lists its entries in row order, so the edges
+// of one row from one source chunk are neighbours: the gather pass sums them
+// as it fetches them and writes ONE partial sum per (segment, row) run
+// instead of one value per edge (R-MAT configs: ~0.25 values per edge).  An
+// entry closes its run when it is the bin's last real entry, the next entry
+// starts another chunk or row, or it ends its piece (pieces are the gather
+// pass's work items: kPieceEntries entries from the segment's start, so no
+// run spans two of them).  Pads close nothing.  The sources are read with
+// the close flag (bit 31) masked: pb_psum_kernel sets it in place.
+__device__ __forceinline__ bool pb_closes(const int32_t* src, const uint16_t* dstl, const int64_t* start, int64_t q,
+                                          int64_t pe, int64_t b, int64_t nbins, int chunk_shift) {
+  if (q + 1 >= pe) return true;
+  const uint32_t c = ((uint32_t)src[q] & 0x7FFFFFFFu) >> chunk_shift;
+  if ((((uint32_t)src[q + 1] & 0x7FFFFFFFu) >> chunk_shift) != c || dstl[q + 1] != dstl[q]) return true;
+  return (q - __ldg(start + (int64_t)c * nbins + b) + 1) % kPieceEntries == 0;
 }
 
-// Pass A: the number of values each tile opens (tiles numbered bin by bin:
-// tile_off[b] is bin b's first).
-__global__ void __launch_bounds__(kAccThreads) pb_tile_count_kernel(const int32_t* src, const int64_t* bin_pos,
-                                                                    const int64_t* tile_off, int64_t nbins,
-                                                                    int64_t* tile_cnt) {
+// Pass A: the number of runs (partial sums) of each bin.
+__global__ void __launch_bounds__(kAccThreads) pb_close_count_kernel(const int32_t* src, const uint16_t* dstl,
+                                                                     const int64_t* row, int32_t n, int shift,
+                                                                     const int64_t* bin_pos, const int64_t* start,
+                                                                     int64_t nbins, int chunk_shift, int64_t* bin_np) {
   using Reduce = cub::BlockReduce<uint32_t, kAccThreads>;
   __shared__ typename Reduce::TempStorage tmp;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
-    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
-    int64_t g = tile_off[b];
-    for (int64_t t0 = p0; t0 < p1; t0 += kTile, ++g) {
-      const int len = (int)min((int64_t)kTile, p1 - t0);
-      uint32_t c = 0;
-#pragma unroll
-      for (int j = 0; j < kAccEpl; ++j) {
-        const int i = threadIdx.x * kAccEpl + j;
-        if (i < len) c += pb_opens(src, t0 + i, p0, __ldg(src + t0 + i)) ? 1u : 0u;
-      }
-      c = Reduce(tmp).Sum(c);
-      if (threadIdx.x == 0) tile_cnt[g] = (int64_t)c;
-      __syncthreads();
-    }
+    const int64_t r0 = b << shift, r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
+    const int64_t p0 = bin_pos[b], pe = p0 + (row[r1] - row[r0]);
+    uint32_t c = 0;
+    for (int64_t q = p0 + threadIdx.x; q < pe; q += kAccThreads)
+      c += pb_closes(src, dstl, start, q, pe, b, nbins, chunk_shift) ? 1u : 0u;
+    c = Reduce(tmp).Sum(c);
+    if (threadIdx.x == 0) bin_np[b] = (int64_t)c;
+    __syncthreads();
   }
 }
 
-// Pass B, per tile (kTile consecutive entries from bin_pos[b]; the bin's last
-// tile is shorter), with tile_ex[g] = values opened before tile g:
-//   * value numbering: entry i's value is u(i) = tile_ex[g] + (values opened
-//     in [t0, i]) - 1; the opening entries write usrc[u] (the gather list);
-//     the tile's values are the contiguous run [u0, u0 + nu), staged from the
-//     even index u0 & ~1 (16-B aligned TMA copies): tile_meta[g] = u0 << 16 | nu;
-//   * segment bounds in value numbers: ustart (over the segment's first
-//     entry offset in `start`) and uend, for the gather plan;
-//   * the stable sort of the tile's entries by row: skey[t0 + j] = row offset
-//     at sorted place j (kPadKey for pads, which sort last); vidx[t0 + j] =
-//     the stage index of sorted place j's value.
-// Built once with the layout.
-__global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(
-    const uint16_t* dstl, const int32_t* src, const int64_t* bin_pos, const int64_t* tile_off, const int64_t* tile_ex,
-    int64_t nbins, int shift, int chunk_shift, uint16_t* vidx, uint16_t* skey, int32_t* usrc, uint64_t* tile_meta,
-    int64_t* ustart, int64_t* uend) {
-  using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t, FPR_PB_TSORT_BITS>;
+// Pass B, per bin (its runs numbered from pbin_pos[b], an 8-aligned position,
+// so that the accumulate's tile copies stay 16-B aligned):
+//   * closing entries get bit 31 of their source set (the gather's flag);
+//   * pkey[u] = the row offset of run u; the bin's pad places get kPadKey;
+//   * every piece start q records the number of its first run in
+//     pbase[seg_piece0[segment] + piece]: the runs closed before q in the
+//     bin, since q's run closes at or after q.
+__global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, const uint16_t* dstl, const int64_t* row,
+                                                              int32_t n, int shift, const int64_t* bin_pos,
+                                                              const int64_t* pbin_pos, const int64_t* start,
+                                                              const uint32_t* seg_piece0, int64_t nbins,
+                                                              int chunk_shift, uint16_t* pkey, int64_t* pbase) {
   using Scan = cub::BlockScan<uint32_t, kAccThreads>;
-  __shared__ union {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
-  } tmp;
-  __shared__ uint16_t loc[kTile];  // stage index of each storage entry's value
-  __shared__ uint32_t s_f0;
+  __shared__ typename Scan::TempStorage tmp;
+  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int64_t r0 = b << shift, r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
+    const int64_t p0 = bin_pos[b], pe = p0 + (row[r1] - row[r0]);
+    int64_t u = pbin_pos[b];
+    for (int64_t t = p0; t < pe; t += kAccThreads) {
+      const int64_t q = t + threadIdx.x;
+      const bool in = q < pe;
+      const bool cl = in && pb_closes(src, dstl, start, q, pe, b, nbins, chunk_shift);
+      uint32_t before, total;
+      Scan(tmp).ExclusiveSum(cl ? 1u : 0u, before, total);
+      __syncthreads();  // every thread of the tile has read its neighbour's flag-free source
+      if (in) {
+        const uint32_t s = (uint32_t)src[q] & 0x7FFFFFFFu;
+        const int64_t seg = (int64_t)(s >> chunk_shift) * nbins + b;
+        const int64_t off = q - __ldg(start + seg);
+        if (off % kPieceEntries == 0) pbase[(int64_t)seg_piece0[seg] + off / kPieceEntries] = u + before;
+        if (cl) {
+          pkey[u + before] = dstl[q];
+          src[q] = (int32_t)(s | 0x80000000u);
+        }
+      }
+      u += total;
+      __syncthreads();
+    }
+    for (int64_t k = u + threadIdx.x; k < pbin_pos[b + 1]; k += kAccThreads) pkey[k] = kPadKey;
+  }
+}
+
+// Pass C, per tile (kTile consecutive runs from pbin_pos[b]; the bin's last
+// tile is shorter): the stable sort of the tile's runs by row --
+// skey[t0 + j] = row offset at sorted place j (kPadKey for pads, which sort
+// last), vidx[t0 + j] = the tile index of sorted place j's run; tile_meta[g]
+// = t0 << 16 | len (the accumulate stages the tile's runs from t0).
+__global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(const uint16_t* pkey, const int64_t* pbin_pos,
+                                                                   const int64_t* tile_off, int64_t nbins, int shift,
+                                                                   uint16_t* vidx, uint16_t* skey,
+                                                                   uint64_t* tile_meta) {
+  using Sort = cub::BlockRadixSort<uint32_t, kAccThreads, kAccEpl, uint32_t, FPR_PB_TSORT_BITS>;
+  __shared__ typename Sort::TempStorage tmp;
   const uint32_t pad_key = 1u << shift;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
-    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
+    const int64_t p0 = pbin_pos[b], p1 = pbin_pos[b + 1];
     int64_t g = tile_off[b];
     for (int64_t t0 = p0; t0 < p1; t0 += kTile, ++g) {
       const int len = (int)min((int64_t)kTile, p1 - t0);
-      int32_t s[kAccEpl];
-      uint32_t f[kAccEpl], cnt = 0;
-#pragma unroll
-      for (int j = 0; j < kAccEpl; ++j) {
-        const int i = threadIdx.x * kAccEpl + j;
-        s[j] = i < len ? __ldg(src + t0 + i) : -1;
-        f[j] = i < len && pb_opens(src, t0 + i, p0, s[j]) ? 1u : 0u;
-        cnt += f[j];
-      }
-      uint32_t before, total;
-      Scan(tmp.scan).ExclusiveSum(cnt, before, total);
-      if (threadIdx.x == 0) s_f0 = f[0];
-      __syncthreads();
-      const uint32_t f0 = s_f0;
-      const int64_t ex = tile_ex[g];
-      const int64_t u0 = ex + f0 - 1;  // the value of the tile's first entry
-      const uint32_t a = (uint32_t)(u0 & 1);
-      if (threadIdx.x == 0) tile_meta[g] = ((uint64_t)u0 << 16) | (uint64_t)(total - f0 + 1);
-      uint32_t L = before;  // values opened in [t0, i]
-#pragma unroll
-      for (int j = 0; j < kAccEpl; ++j) {
-        const int i = threadIdx.x * kAccEpl + j;
-        L += f[j];
-        if (i < len) {
-          const int64_t u = ex + (int64_t)L - 1;
-          loc[i] = (uint16_t)(L - f0 + a);
-          if (f[j]) usrc[u] = s[j];
-          if (s[j] >= 0) {
-            const int64_t q = t0 + i;
-            const uint32_t c = (uint32_t)s[j] >> chunk_shift;
-            const int64_t seg = (int64_t)c * nbins + b;
-            if (q == p0 || ((uint32_t)__ldg(src + q - 1) >> chunk_shift) != c) ustart[seg] = u;
-            const int32_t nx = q + 1 < p1 ? __ldg(src + q + 1) : -1;
-            if (nx < 0 || ((uint32_t)nx >> chunk_shift) != c) uend[seg] = u + 1;
-          }
-        }
-      }
-      __syncthreads();  // loc complete; the scan's storage free for the sort
+      if (threadIdx.x == 0) tile_meta[g] = ((uint64_t)t0 << 16) | (uint64_t)len;
       uint32_t key[kAccEpl], idx[kAccEpl];
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
         const int i = threadIdx.x * kAccEpl + j;
         // rows < 2^shift; pads sort after them, places past the tile last:
         // shift + 1 key bits (radix passes) instead of 17
-        const uint32_t d = i < len ? (uint32_t)dstl[t0 + i] : 0x10000u;
+        const uint32_t d = i < len ? (uint32_t)pkey[t0 + i] : 0x10000u;
         key[j] = d == 0x10000u ? (pad_key + 1) : (d == kPadKey ? pad_key : d);
         idx[j] = (uint32_t)i;
       }
-      Sort(tmp.sort).Sort(key, idx, 0, shift + 1);
+      Sort(tmp).Sort(key, idx, 0, shift + 1);
 #pragma unroll
       for (int j = 0; j < kAccEpl; ++j) {
         const int p = threadIdx.x * kAccEpl + j;
         if (p < len) {
           skey[t0 + p] = key[j] == pad_key ? kPadKey : (uint16_t)key[j];
-          vidx[t0 + p] = loc[idx[j]];
+          vidx[t0 + p] = (uint16_t)idx[j];
         }
       }
       __syncthreads();
@@ -358,12 +356,11 @@ __global__ void __launch_bounds__(kAccThreads) pb_tile_sort_kernel(
   }
 }
 
-// Segment (bin, chunk) in value numbers: start[s] = its first value (written
-// over the entry offset by pass B), counts[s] = its values.
-__global__ void pb_seg_values_kernel(int64_t nseg, const int64_t* uend, int64_t* start, uint32_t* counts) {
+// Pieces of each segment (kPieceEntries entries from its start).
+__global__ void pb_seg_pieces_kernel(const uint32_t* counts, int64_t nseg, uint32_t* np) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride)
-    counts[s] = counts[s] ? (uint32_t)(uend[s] - start[s]) : 0u;
+    np[s] = (counts[s] + kPieceEntries - 1) / kPieceEntries;
 }
 
 // Plan order: position p walks the waves (runs of consecutive bins), chunk-
@@ -391,104 +388,120 @@ __global__ void pb_piece_count_kernel(const uint32_t* counts, int64_t nseg, cons
 }
 
 __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* start, const uint32_t* piece_off,
-                                     int64_t nseg, const int64_t* wave_bin, int nwaves, int64_t nbins,
-                                     int64_t nchunks, int64_t* item_start, uint32_t* item_len) {
+                                     const uint32_t* seg_piece0, const int64_t* pbase, int64_t nseg,
+                                     const int64_t* wave_bin, int nwaves, int64_t nbins, int64_t nchunks,
+                                     int64_t* item_start, uint32_t* item_len, int64_t* item_ubase) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nseg; p += stride) {
     const int64_t s = pb_seg_of(p, wave_bin, nwaves, nbins, nchunks);
     const uint32_t cnt = counts[s];
     const int64_t p0 = start[s];
     uint32_t o = piece_off[p];
+    const int64_t* pb0 = pbase + seg_piece0[s];
     for (uint32_t k = 0; k < cnt; k += kPieceEntries, ++o) {
       item_start[o] = p0 + k;
       item_len[o] = min((uint32_t)kPieceEntries, cnt - k);
+      item_ubase[o] = pb0[k / kPieceEntries];
     }
   }
 }
 
 // Phase 1: warps take pieces in chunk order from a global counter (static
 // striding lets fast warps drift chunks ahead and the concurrently read
-// contribution window outgrow L2); 8 gathers in flight per lane.
-#ifndef FPR_PB_GATHER_VEC
-#define FPR_PB_GATHER_VEC 1
-#endif
-#ifndef FPR_PB_SRC_SORT
-#define FPR_PB_SRC_SORT 1
-#endif
+// contribution window outgrow L2).  A piece is a run of one segment's
+// entries in row order; the pass fetches every entry's contribution and sums
+// each row's run as it goes, writing one partial sum per run (closing
+// entries carry bit 31 of their source) to consecutive places from the
+// piece's first run number.  Lane L owns 4 consecutive entries per step (one
+// 16-B source load, four gathers; two steps = 8 gathers in flight): it sums
+// its entries left to right, a segmented warp scan of the lanes' open tails
+// carries a run across lanes, and lane 31's open tail carries it into the
+// next step.  The grouping is fixed by the layout, so the bits are the same
+// on every run.
 #ifndef FPR_PB_GATHER_MINB
 #define FPR_PB_GATHER_MINB 1
 #endif
-__global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(const int32_t* usrc, const int64_t* item_start,
-                                                                    const uint32_t* item_len, int64_t nitems,
-                                                                    const double* prev, double* val,
-                                                                    unsigned long long* next_item) {
+__global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(
+    const int32_t* esrc, const int64_t* item_start, const uint32_t* item_len, const int64_t* item_ubase,
+    int64_t nitems, const double* prev, double* psum, unsigned long long* next_item) {
   const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
   for (;;) {
     unsigned long long it = 0;
     if (lane == 0) it = atomicAdd(next_item, 1ull);
     it = __shfl_sync(0xffffffffu, it, 0);
     if ((int64_t)it >= nitems) break;
     const int64_t p0 = __ldg(item_start + it);
-    const uint32_t len = __ldg(item_len + it);
-#if FPR_PB_GATHER_VEC
-    // Lane L owns 4 consecutive entries per step (positions from the piece's
-    // 4-aligned base): one 16-B source load and one 32-B value store per 4
-    // entries instead of one instruction per entry each, so the LSU queue
-    // (lg_throttle, 27% of the scalar form's stall samples) carries mostly
-    // the gathers.  Partial vectors at the piece's ends store per entry.
-    constexpr int U = 2;  // steps in flight: 8 gathers per lane
-    const int64_t a0 = p0 & ~int64_t(3), p1 = p0 + len;
-    for (int64_t q0 = a0; q0 < p1; q0 += 128 * U) {
+    const int64_t p1 = p0 + __ldg(item_len + it);
+    int64_t ub = __ldg(item_ubase + it);  // the next run's number (warp-uniform)
+    double carry = 0.0;                   // the run left open by the previous step
+    constexpr int U = 2;
+    for (int64_t q0 = p0 & ~int64_t(3); q0 < p1; q0 += 128 * U) {
       int4 sv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t q = q0 + u * 128 + 4 * lane;
-        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(usrc + q)) : make_int4(-1, -1, -1, -1);
+        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(esrc + q)) : make_int4(0, 0, 0, 0);
       }
       double v[U][4];
+      unsigned cl[U];  // bit j: entry j closes its run
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t q = q0 + u * 128 + 4 * lane;
         const int s4[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+        cl[u] = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const bool ok = q + j >= p0 && q + j < p1 && s4[j] >= 0;
-          v[u][j] = ok ? (FPR_PB_GATHER_L1 ? __ldca(prev + s4[j]) : __ldcg(prev + s4[j])) : 0.0;
+          const bool ok = q + j >= p0 && q + j < p1;
+          const int32_t s = s4[j] & 0x7FFFFFFF;
+          v[u][j] = ok ? (FPR_PB_GATHER_L1 ? __ldca(prev + s) : __ldcg(prev + s)) : 0.0;
+          if (ok && s4[j] < 0) cl[u] |= 1u << j;
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * 128 + 4 * lane;
-        if (q >= p0 && q + 4 <= p1) {
-          asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(val + q), "d"(v[u][0]), "d"(v[u][1]),
-                       "d"(v[u][2]), "d"(v[u][3])
-                       : "memory");
-        } else {
+        // this lane's runs: closed ones in o[], the open tail in T
+        double o[4], run = 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (q + j >= p0 && q + j < p1) __stcs(val + q + j, v[u][j]);
+        for (int j = 0; j < 4; ++j) {
+          run = j == 0 ? v[u][0] : run + v[u][j];
+          o[j] = run;
+          if (cl[u] >> j & 1u) run = 0.0;
         }
+        const bool h = cl[u] != 0u;
+        double T = run;
+        if (lane == 0 && !h) T = carry + T;
+        // segmented inclusive scan of the tails, restarting at closing lanes
+        double S = T;
+        bool f = h;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, S, d);
+          const bool g = __shfl_up_sync(0xffffffffu, f, d);
+          if (lane >= d && !f) {
+            S = t + S;
+            f = g;
+          }
+        }
+        double ci = __shfl_up_sync(0xffffffffu, S, 1);  // the run entering this lane
+        if (lane == 0) ci = carry;
+        carry = __shfl_sync(0xffffffffu, S, 31);
+        // places: runs closed by earlier lanes of this step, then in order
+        const unsigned b0 = __ballot_sync(0xffffffffu, cl[u] & 1u), b1 = __ballot_sync(0xffffffffu, cl[u] & 2u),
+                       b2 = __ballot_sync(0xffffffffu, cl[u] & 4u), b3 = __ballot_sync(0xffffffffu, cl[u] & 8u);
+        int64_t k = ub + __popc(b0 & below) + __popc(b1 & below) + __popc(b2 & below) + __popc(b3 & below);
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (cl[u] >> j & 1u) {
+            __stcs(psum + k, first ? ci + o[j] : o[j]);
+            first = false;
+            ++k;
+          }
+        }
+        ub += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
       }
     }
-#else
-    constexpr int U = 8;
-    for (uint32_t k0 = 0; k0 < len; k0 += 32 * U) {
-      int32_t s[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t k = k0 + u * 32 + lane;
-        s[u] = k < len ? __ldcs(usrc + p0 + k) : -1;
-      }
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = s[u] >= 0 ? (FPR_PB_GATHER_L1 ? __ldca(prev + s[u]) : __ldcg(prev + s[u])) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t k = k0 + u * 32 + lane;
-        if (k < len) __stcs(val + p0 + k, v[u]);
-      }
-    }
-#endif
   }
 }
 
@@ -496,7 +509,7 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
 // run of tiles of a heavy bin (skewed graphs put a large share of the edges
 // in the bins of the hub rows; one CTA per bin left one SM working 7x longer
 // than the average on config 3).  Per tile:
-//   * thread 0 streams the tile's values, inverse permutation and sorted
+//   * thread 0 streams the tile's partial sums, inverse permutation and sorted
 //     keys into a shared-memory stage with three TMA bulk copies completing
 //     on the stage's mbarrier, kStages tiles ahead;
 //   * lane L owns the sorted places [4L, 4L+4): it reads their keys and,
@@ -887,20 +900,6 @@ __global__ void __launch_bounds__(kReduceThreads) pb_reduce_kernel(int64_t nbins
   }
 }
 
-// Segment offsets of bins [b0, b1) relative to base, bin-major (the sort's
-// segment order does not matter; bin-major keeps each group contiguous).
-__global__ void pb_group_offsets_kernel(const uint32_t* counts, const int64_t* start, int64_t nbins, int64_t nchunks,
-                                        int64_t b0, int64_t b1, int64_t base, int64_t* beg, int64_t* end) {
-  const int64_t nseg = (b1 - b0) * nchunks;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nseg; i += stride) {
-    const int64_t b = b0 + i / nchunks, c = i % nchunks;
-    const int64_t st = start[c * nbins + b] - base;
-    beg[i] = st;
-    end[i] = st + counts[c * nbins + b];
-  }
-}
-
 int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1012,9 +1011,11 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     e = alloc((void**)&plan.item_start, off[W] * sizeof(int64_t));
   }
   if (e == cudaSuccess) e = alloc((void**)&plan.item_len, off[W] * sizeof(uint32_t));
+  if (e == cudaSuccess) e = alloc((void**)&plan.item_ubase, off[W] * sizeof(int64_t));
   if (e == cudaSuccess) {
-    pb_piece_fill_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, pb.start, piece_off, nseg, d_wb, W, nbins, nchunks,
-                                                   plan.item_start, plan.item_len);
+    pb_piece_fill_kernel<<<sms * 4, 256, 0, st>>>(pb.counts, pb.start, piece_off, pb.seg_piece0, pb.pbase, nseg,
+                                                   d_wb, W, nbins, nchunks, plan.item_start, plan.item_len,
+                                                   plan.item_ubase);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = alloc((void**)&plan.ctr, 2 * (size_t)W * sizeof(unsigned long long));
@@ -1031,8 +1032,8 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     // `piece` entries: small enough that each wave has several units per
     // CTA, never below twice the average bin (a split bin writes and re-reads
     // a slot of row sums per unit; splitting config 4's even bins cost 5-10%)
-    const int64_t avg_bin = pb.m / std::max<int64_t>(1, pb.nbins);
-    int64_t piece = std::max<int64_t>({int64_t(1) << 16, 2 * avg_bin, pb.m / ((int64_t)pb.p2_grid * 8 * W)});
+    const int64_t avg_bin = pb.nps / std::max<int64_t>(1, pb.nbins);
+    int64_t piece = std::max<int64_t>({int64_t(1) << 16, 2 * avg_bin, pb.nps / ((int64_t)pb.p2_grid * 8 * W)});
     if (const char* v = std::getenv("FPR_B200_PB_PIECE")) piece = std::max<int64_t>(32, std::atoll(v));  // tests
     const int64_t piece_tiles = std::max<int64_t>(1, (piece + kTile - 1) / kTile);
     std::vector<int32_t> ubin, uk, uj, uslot;
@@ -1042,7 +1043,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     for (int w = 0; w < W; ++w) {
       plan.unit0[w] = (int64_t)ubin.size();
       for (int64_t b = plan.wave_bin[w]; b < plan.wave_bin[w + 1]; ++b) {
-        const int64_t p0 = pb.bin_pos[b], p1 = pb.bin_pos[b + 1];
+        const int64_t p0 = pb.pbin_pos[b], p1 = pb.pbin_pos[b + 1];
         const int64_t tiles = std::max<int64_t>(1, (p1 - p0 + kTile - 1) / kTile);
         const int64_t k = (tiles + piece_tiles - 1) / piece_tiles;
         for (int64_t j = 0; j < k; ++j) {
@@ -1060,7 +1061,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
     // unit u ends where unit u + 1 starts, or at its bin's end
     std::vector<int64_t> uend(ubin.size() + 1);
     for (size_t u = 0; u < ubin.size(); ++u)
-      uend[u] = (u + 1 < ubin.size() && ubin[u + 1] == ubin[u]) ? ue[u + 1] : pb.bin_pos[ubin[u] + 1];
+      uend[u] = (u + 1 < ubin.size() && ubin[u + 1] == ubin[u]) ? ue[u + 1] : pb.pbin_pos[ubin[u] + 1];
     // unit_e holds [start, end) pairs flattened: start of u at 2u, end at 2u + 1
     std::vector<int64_t> ue2(2 * ubin.size());
     for (size_t u = 0; u < ubin.size(); ++u) {
@@ -1104,19 +1105,23 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   const int64_t n = g.n;
   const int64_t nbins = n > 0 ? (n + (1ll << shift) - 1) >> shift : 0;
   const int64_t nchunks = std::max<int64_t>(1, (nsrc + (1ll << chunk_shift) - 1) >> chunk_shift);
+  const int64_t nseg = nbins * nchunks;
   // layout kernel: chunk counters + the bin's (2^shift + 1) relative row offsets
   const size_t hist_smem = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t) +
                            (((size_t)1 << std::min(shift, 20)) + 1) * sizeof(uint32_t) +
                            (nchunks <= kSplitMaxChunks ? (size_t)(nchunks + 1) * 32 * sizeof(uint32_t) : 0);
   const size_t acc_smem = ((size_t)sizeof(double) << shift) + (size_t)kStages * sizeof(PbStage);
-  // layout temporaries: per-entry row offsets and sources (storage order),
-  // tile offsets, per-tile value counts and their exclusive scan, segment ends
+  // layout temporaries: per-entry row offsets, tile offsets, per-bin run
+  // counts, per-segment pieces and their scan, per-run row offsets
   uint16_t* dstl = nullptr;
-  int32_t* src_bm = nullptr;
-  int64_t *tile_off_d = nullptr, *tile_cnt = nullptr, *tile_ex = nullptr, *uend = nullptr;
+  uint16_t* pkey = nullptr;
+  int64_t *tile_off_d = nullptr, *bin_np = nullptr, *pbin_pos_d = nullptr;
+  uint32_t* seg_np = nullptr;
   void* scan_tmp = nullptr;
+  const unsigned tgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 4));
+  const unsigned sgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, (int64_t)sms * 32));
   if (n == 0 || shift < 5 || shift > 13 || chunk_shift < 0 || chunk_shift > 31 || hist_smem > 192 * 1024 ||
-      acc_smem + 2048 > 227 * 1024 || nbins * nchunks > (1ll << 31)) {
+      acc_smem + 2048 > 227 * 1024 || nseg > (1ll << 31) || nsrc > 0x7FFFFFFFll) {
     *msg = "bin/chunk geometry out of range";
     return cudaSuccess;
   }
@@ -1132,7 +1137,7 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   pb.m = g.m;
   {
     // bin edge offsets (host copy: wave plans cut waves from them) and the
-    // bins' 8-aligned storage positions (16-B aligned TMA copies of tiles)
+    // bins' 8-aligned entry positions (16-B source loads)
     std::vector<int64_t> be;
     e = pb_bin_edges(g, shift, st, &be);
     if (e != cudaSuccess) goto out;
@@ -1147,20 +1152,12 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     }
   }
   pb.mpad = pb.bin_pos[nbins];
-  pb.tile_off.assign(nbins + 1, 0);
-  for (int64_t b = 0; b < nbins; ++b)
-    pb.tile_off[b + 1] = pb.tile_off[b] + (pb.bin_pos[b + 1] - pb.bin_pos[b] + kTile - 1) / kTile;
-  pb.ntiles = pb.tile_off[nbins];
-  PK(alloc((void**)&pb.counts, nbins * nchunks * sizeof(uint32_t)));
-  PK(alloc((void**)&pb.start, nbins * nchunks * sizeof(int64_t)));
-  PK(alloc((void**)&pb.vidx, pb.mpad * sizeof(uint16_t)));
-  PK(alloc((void**)&pb.skey, pb.mpad * sizeof(uint16_t)));
-  PK(alloc((void**)&pb.tile_meta, pb.ntiles * sizeof(uint64_t)));
+  PK(alloc((void**)&pb.counts, nseg * sizeof(uint32_t)));
+  PK(alloc((void**)&pb.start, nseg * sizeof(int64_t)));
   PK(alloc((void**)&pb.bin_pos_d, (nbins + 1) * sizeof(int64_t)));
   PK(cudaMemcpyAsync(pb.bin_pos_d, pb.bin_pos.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PK(cudaMallocAsync(&tile_off_d, (nbins + 1) * sizeof(int64_t), st));
-  PK(cudaMemcpyAsync(tile_off_d, pb.tile_off.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  PK(cudaMallocAsync(&src_bm, std::max<int64_t>(pb.mpad, 1) * sizeof(int32_t), st));
+  // the gather's 16-B source loads read up to 3 entries past a piece
+  PK(alloc((void**)&pb.esrc, std::max<int64_t>(pb.mpad, 1) * sizeof(int32_t) + 64));
   PK(cudaMallocAsync(&dstl, std::max<int64_t>(pb.mpad, 1) * sizeof(uint16_t), st));
   {
     int key_bits = 1;
@@ -1168,80 +1165,63 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     PK(cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem));
     pb_layout_kernel<<<(unsigned)std::min<int64_t>(nbins, sms), kPbThreads, hist_smem, st>>>(
         g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.bin_pos_d, pb.counts, pb.start,
-        src_bm, dstl);
-    PK(cudaGetLastError());
-    if (FPR_PB_SRC_SORT) {
-      // Sources ascending inside every (bin, chunk) segment: a hub source's
-      // repeats become neighbours and share one value; neighbouring sources
-      // share L2 lines in one gather instruction.  The accumulate's tile sort
-      // restores row order.  CUB segmented sort, in groups of bins of < 2^31
-      // entries (its item count is an int).
-      int64_t b0 = 0;
-      while (b0 < nbins) {
-        int64_t b1 = b0 + 1;
-        while (b1 < nbins && pb.bin_pos[b1 + 1] - pb.bin_pos[b0] < (int64_t(1) << 30)) ++b1;
-        const int64_t base = pb.bin_pos[b0], items = pb.bin_pos[b1] - base, nseg = (b1 - b0) * nchunks;
-        int64_t *beg = nullptr, *end = nullptr;
-        int32_t* ko = nullptr;
-        uint16_t* vo = nullptr;
-        void* temp = nullptr;
-        size_t tb = 0;
-        PK(cudaMallocAsync(&beg, nseg * sizeof(int64_t), st));
-        PK(cudaMallocAsync(&end, nseg * sizeof(int64_t), st));
-        PK(cudaMallocAsync(&ko, std::max<int64_t>(items, 1) * sizeof(int32_t), st));
-        PK(cudaMallocAsync(&vo, std::max<int64_t>(items, 1) * sizeof(uint16_t), st));
-        pb_group_offsets_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, sms * 32)), 256,
-                                  0, st>>>(pb.counts, pb.start, nbins, nchunks, b0, b1, base, beg, end);
-        PK(cudaGetLastError());
-        PK(cudaMemcpyAsync(ko, src_bm + base, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));  // pads
-        PK(cudaMemcpyAsync(vo, dstl + base, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
-        PK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, src_bm + base, ko, dstl + base, vo, (int)items,
-                                                     (int)nseg, beg, end, st));
-        PK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));
-        PK(cub::DeviceSegmentedSort::StableSortPairs(temp, tb, src_bm + base, ko, dstl + base, vo, (int)items,
-                                                     (int)nseg, beg, end, st));
-        PK(cudaMemcpyAsync(src_bm + base, ko, items * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-        PK(cudaMemcpyAsync(dstl + base, vo, items * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
-        for (void* q : {(void*)beg, (void*)end, (void*)ko, (void*)vo, temp}) cudaFreeAsync(q, st);
-        b0 = b1;
-      }
-    }
-    // value numbering: values opened per tile, scanned, then the tile pass
-    const int64_t nt = std::max<int64_t>(pb.ntiles, 1), nseg = nbins * nchunks;
-    const unsigned tgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 2));
-    PK(cudaMallocAsync(&tile_cnt, nt * sizeof(int64_t), st));
-    PK(cudaMallocAsync(&tile_ex, nt * sizeof(int64_t), st));
-    PK(cudaMallocAsync(&uend, nseg * sizeof(int64_t), st));
-    PK(cudaMemsetAsync(tile_cnt, 0, nt * sizeof(int64_t), st));
-    pb_tile_count_kernel<<<tgrid, kAccThreads, 0, st>>>(src_bm, pb.bin_pos_d, tile_off_d, nbins, tile_cnt);
-    PK(cudaGetLastError());
-    {
-      size_t tb = 0;
-      PK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tile_cnt, tile_ex, nt, st));
-      PK(cudaMallocAsync(&scan_tmp, std::max<size_t>(tb, 16), st));
-      PK(cub::DeviceScan::ExclusiveSum(scan_tmp, tb, tile_cnt, tile_ex, nt, st));
-    }
-    {
-      int64_t last_ex = 0, last_cnt = 0;
-      PK(cudaMemcpyAsync(&last_ex, tile_ex + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      PK(cudaMemcpyAsync(&last_cnt, tile_cnt + nt - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      PK(cudaStreamSynchronize(st));
-      pb.nvals = last_ex + last_cnt;
-    }
-    // the gather's 16-B source loads and the stage's pair-rounded value
-    // copies read a few words past the end
-    PK(alloc((void**)&pb.usrc, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(int32_t) + 64));
-    PK(alloc((void**)&pb.val, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(double) + 64));
-    PK(cudaMemsetAsync(pb.val, 0, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(double) + 64, st));
-    PK(cudaMemsetAsync(pb.usrc, 0xFF, ((pb.nvals + 7) & ~int64_t(7)) * sizeof(int32_t) + 64, st));
-    pb_tile_sort_kernel<<<tgrid, kAccThreads, 0, st>>>(dstl, src_bm, pb.bin_pos_d, tile_off_d, tile_ex, nbins, shift,
-                                                       chunk_shift, pb.vidx, pb.skey, pb.usrc, pb.tile_meta,
-                                                       pb.start, uend);
-    PK(cudaGetLastError());
-    pb_seg_values_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, sms * 32)), 256, 0,
-                           st>>>(nseg, uend, pb.start, pb.counts);
+        pb.esrc, dstl);
     PK(cudaGetLastError());
   }
+  // runs per bin -> their 8-aligned positions and the accumulate's tiles
+  PK(cudaMallocAsync(&bin_np, std::max<int64_t>(nbins, 1) * sizeof(int64_t), st));
+  pb_close_count_kernel<<<tgrid, kAccThreads, 0, st>>>(pb.esrc, dstl, g.row, g.n, shift, pb.bin_pos_d, pb.start,
+                                                      nbins, chunk_shift, bin_np);
+  PK(cudaGetLastError());
+  {
+    std::vector<int64_t> np(nbins);
+    PK(cudaMemcpyAsync(np.data(), bin_np, nbins * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PK(cudaStreamSynchronize(st));
+    pb.pbin_pos.assign(nbins + 1, 0);
+    for (int64_t b = 0; b < nbins; ++b) pb.pbin_pos[b + 1] = pb.pbin_pos[b] + ((np[b] + 7) & ~int64_t(7));
+  }
+  pb.nps = pb.pbin_pos[nbins];
+  pb.tile_off.assign(nbins + 1, 0);
+  for (int64_t b = 0; b < nbins; ++b)
+    pb.tile_off[b + 1] = pb.tile_off[b] + (pb.pbin_pos[b + 1] - pb.pbin_pos[b] + kTile - 1) / kTile;
+  pb.ntiles = pb.tile_off[nbins];
+  PK(cudaMallocAsync(&pbin_pos_d, (nbins + 1) * sizeof(int64_t), st));
+  PK(cudaMemcpyAsync(pbin_pos_d, pb.pbin_pos.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PK(cudaMallocAsync(&tile_off_d, (nbins + 1) * sizeof(int64_t), st));
+  PK(cudaMemcpyAsync(tile_off_d, pb.tile_off.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // the gather pieces of every segment (numbered segment by segment,
+  // chunk-major) and the first run of each
+  PK(cudaMallocAsync(&seg_np, std::max<int64_t>(nseg, 1) * sizeof(uint32_t), st));
+  PK(alloc((void**)&pb.seg_piece0, std::max<int64_t>(nseg, 1) * sizeof(uint32_t)));
+  pb_seg_pieces_kernel<<<sgrid, 256, 0, st>>>(pb.counts, nseg, seg_np);
+  PK(cudaGetLastError());
+  {
+    size_t tb = 0;
+    PK(cub::DeviceScan::ExclusiveSum(nullptr, tb, seg_np, pb.seg_piece0, nseg, st));
+    PK(cudaMallocAsync(&scan_tmp, std::max<size_t>(tb, 16), st));
+    PK(cub::DeviceScan::ExclusiveSum(scan_tmp, tb, seg_np, pb.seg_piece0, nseg, st));
+    uint32_t last0 = 0, last1 = 0;
+    PK(cudaMemcpyAsync(&last0, pb.seg_piece0 + nseg - 1, 4, cudaMemcpyDeviceToHost, st));
+    PK(cudaMemcpyAsync(&last1, seg_np + nseg - 1, 4, cudaMemcpyDeviceToHost, st));
+    PK(cudaStreamSynchronize(st));
+    pb.npieces = (int64_t)last0 + last1;
+  }
+  PK(alloc((void**)&pb.pbase, std::max<int64_t>(pb.npieces, 1) * sizeof(int64_t)));
+  PK(cudaMallocAsync(&pkey, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t), st));
+  pb_psum_kernel<<<tgrid, kAccThreads, 0, st>>>(pb.esrc, dstl, g.row, g.n, shift, pb.bin_pos_d, pbin_pos_d, pb.start,
+                                               pb.seg_piece0, nbins, chunk_shift, pkey, pb.pbase);
+  PK(cudaGetLastError());
+  // the accumulate's side: per tile of runs, the row order
+  PK(alloc((void**)&pb.vidx, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.skey, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t)));
+  PK(alloc((void**)&pb.tile_meta, std::max<int64_t>(pb.ntiles, 1) * sizeof(uint64_t)));
+  pb_tile_sort_kernel<<<tgrid, kAccThreads, 0, st>>>(pkey, pbin_pos_d, tile_off_d, nbins, shift, pb.vidx, pb.skey,
+                                                    pb.tile_meta);
+  PK(cudaGetLastError());
+  // per-sweep scratch: the runs' partial sums (the stage's pair-rounded
+  // copies read one past a tile)
+  PK(alloc((void**)&pb.psum, std::max<int64_t>(pb.nps, 1) * sizeof(double) + 64));
+  PK(cudaMemsetAsync(pb.psum, 0, std::max<int64_t>(pb.nps, 1) * sizeof(double) + 64, st));
   PK(alloc((void**)&pb.bin_pairs, 2 * nbins * sizeof(double)));
   PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
   PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
@@ -1265,7 +1245,8 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   }
   PK(cudaStreamSynchronize(st));
 out:
-  for (void* q : {(void*)dstl, (void*)src_bm, (void*)tile_off_d, (void*)tile_cnt, (void*)tile_ex, (void*)uend, scan_tmp})
+  for (void* q : {(void*)dstl, (void*)pkey, (void*)tile_off_d, (void*)bin_np, (void*)pbin_pos_d, (void*)seg_np,
+                  scan_tmp})
     if (q) cudaFreeAsync(q, st);
   if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
@@ -1291,13 +1272,14 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
       const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
       if (plan.item0[w + 1] > i0) {
         pb_gather_kernel<<<pb.p1_grid_overlap, kGatherThreads, 0, pb.aux>>>(
-            pb.usrc, plan.item_start + i0, plan.item_len + i0, plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
+            pb.esrc, plan.item_start + i0, plan.item_len + i0, plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
+            pb.psum, plan.ctr + w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
       if ((e = cudaEventRecord(pb.ev[w], pb.aux)) != cudaSuccess) return e;
       if ((e = cudaStreamWaitEvent(st, pb.ev[w], 0)) != cudaSuccess) return e;
       pb_accum_kernel<<<pb.p2_grid_overlap, kAccThreads, pb.acc_smem, st>>>(
-          pb.val, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
+          pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
           plan.unit_k + u0, plan.unit_j + u0,
           plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur, peers, base,
           damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
@@ -1309,12 +1291,13 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
   for (int w = 0; w < W; ++w) {
     const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
     if (plan.item0[w + 1] > i0) {
-      pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.usrc, plan.item_start + i0, plan.item_len + i0,
-                                                              plan.item0[w + 1] - i0, prev, pb.val, plan.ctr + w);
+      pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.esrc, plan.item_start + i0, plan.item_len + i0,
+                                                              plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
+                                                              pb.psum, plan.ctr + w);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
-        pb.val, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
+        pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
         plan.unit_k + u0, plan.unit_j + u0,
         plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur,
         peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);

@@ -3,7 +3,7 @@
   python scripts/probe.py sweep CONFIGS [--engines ec,fused,lockstep] [--sweep auto|pb|pull]
                                 [--geoms 13:21,12:21] [--reorder degree|sources] [--reps 1]
       per-sweep device times, iterations, GTEPS and the BASELINE roofline
-      fraction; --geoms sets the propagation-blocked bin:chunk shifts; every
+      fraction and a digest of the rank bits (compare variant builds); --geoms sets the propagation-blocked bin:chunk shifts; every
       PB run is repeated and checked bit-for-bit (fixed-order row sums).
   python scripts/probe.py waves CONFIG [--waves 1,2,4,8,16,32] [--sweep auto|pb|pull]
       the lockstep FusEd schedule's sweeps and time against its wave count.
@@ -23,6 +23,7 @@ BFS relabel), 4 (Chung-Lu 2^26), 5 (R-MAT s28).  FPR_B200_LIB=<path> selects a
 variant build (make -C paper_2203_09284_b200/csrc variant / pbvariant).
 """
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -76,10 +77,11 @@ def cmd_sweep(a):
                     r2 = dg.run(ENGINES[e], cfg)
                     same = bool(np.array_equal(r.ranks.values.view(np.uint64), r2.ranks.values.view(np.uint64)))
                     ms = r.solve_ms / r.trace.iterations
+                    dig = hashlib.sha1(r.ranks.values.view(np.uint64).tobytes()).hexdigest()[:16]
                     print(f"cfg{c} {e} sweep={'pb' if r.sweep else 'pull'} geom={':'.join(geom) if geom else '-'}: "
                           f"{r.trace.iterations} it, {ms:.3f} ms/sweep, {dg.m / ms / 1e6:.1f} GTEPS, roofline "
                           f"{(12 * dg.m + 36 * dg.n) / ms / 1e6 / PEAK:.3f}, first run (layout) "
-                          f"{1e3 * (t1 - t0):.0f} ms, rerun bit-equal {same}", flush=True)
+                          f"{1e3 * (t1 - t0):.0f} ms, rerun bit-equal {same}, ranks sha1 {dig}", flush=True)
 
 
 def cmd_waves(a):
