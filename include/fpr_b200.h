@@ -179,6 +179,13 @@ void fpr_b200_graph_destroy(fpr_b200_graph* g);
 /* Lockstep engine: waves per sweep for later runs (0 = auto). */
 int fpr_b200_graph_set_wave_count(fpr_b200_graph* g, uint32_t wave_count);
 int fpr_b200_graph_info(const fpr_b200_graph* g, uint64_t* n, uint64_t* m, uint64_t* ntasks);
+/* The propagation-blocked layout of g (built by its first PB solve): runs
+ * (one partial sum per row and segment piece, incl. pad places), gather
+ * pieces, accumulate tiles; all 0 while no layout exists.  *sweep is the
+ * sweep kind the graph uses (FPR_B200_SWEEP_*).  Instrumentation for the
+ * roofline (bench.py), not part of the reference interface. */
+int fpr_b200_graph_layout_info(const fpr_b200_graph* g, int* sweep, uint64_t* runs, uint64_t* pieces,
+                               uint64_t* tiles);
 /* Downloads the CSR as fpr::Graph arrays (u64).  EINVAL for a graph created
  * with FPR_B200_OPT_REORDER (its resident CSR is in internal ids). */
 int fpr_b200_graph_download_csr(const fpr_b200_graph* g, uint64_t* in_start, uint64_t* in_src,

@@ -108,7 +108,7 @@ EXPORTS = [
     "fpr_b200_ipc_export", "fpr_b200_ipc_import", "fpr_b200_ipc_close", "fpr_b200_graph_set_wave_count",
     "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev", "fpr_b200_part_create",
     "fpr_b200_mgpu_create", "fpr_b200_mgpu_generate", "fpr_b200_mgpu_run", "fpr_b200_mgpu_info",
-    "fpr_b200_mgpu_destroy", "fpr_b200_generate_edges",
+    "fpr_b200_mgpu_destroy", "fpr_b200_generate_edges", "fpr_b200_graph_layout_info",
 ]
 
 _lib = None
@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
         L.fpr_b200_graph_destroy.argtypes = [vp]
         L.fpr_b200_graph_destroy.restype = None
         L.fpr_b200_graph_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
+        L.fpr_b200_graph_layout_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(u64),
+                                                 C.POINTER(u64)]
         L.fpr_b200_graph_download_csr.argtypes = [vp, vp, vp, vp]
         L.fpr_b200_graph_wave_starts.argtypes = [vp, C.c_uint32, vp, u64, C.POINTER(u64)]
         L.fpr_b200_graph_bfs_order.argtypes = [vp, u64, vp]
@@ -444,6 +446,13 @@ class DeviceGraph:
                 raise ValueError("download_into: need C-contiguous u64 arrays of n+1, m and n entries")
         _check(lib().fpr_b200_graph_download_csr(self._h, in_start.ctypes.data, in_src.ctypes.data if self.m else None,
                                                  out_degree.ctypes.data))
+
+    def layout_info(self) -> dict:
+        """Propagation-blocked layout sizes (0 until the first PB solve built it)."""
+        sw, runs, pieces, tiles = C.c_int(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().fpr_b200_graph_layout_info(self._h, C.byref(sw), C.byref(runs), C.byref(pieces),
+                                                C.byref(tiles)))
+        return {"sweep": sw.value, "runs": runs.value, "pieces": pieces.value, "tiles": tiles.value}
 
     def wave_starts(self, wave_count: int = 0) -> np.ndarray:
         nw = C.c_uint64()

@@ -412,20 +412,21 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 // entries in row order; the pass fetches every entry's contribution and sums
 // each row's run as it goes, writing one partial sum per run (closing
 // entries carry bit 31 of their source) to consecutive places from the
-// piece's first run number.  Lane L owns 4 consecutive entries per step (one
-// 16-B source load, four gathers; two steps = 8 gathers in flight): it sums
-// its entries left to right, a segmented warp scan of the lanes' open tails
-// carries a run across lanes, and lane 31's open tail carries it into the
-// next step.  The grouping is fixed by the layout, so the bits are the same
-// on every run.
+// piece's first run number.  Lane L owns 8 consecutive entries per step (one
+// 32-B source load, eight gathers in flight): it sums its entries left to
+// right, one segmented warp scan of the lanes' open tails carries a run
+// across lanes (with the plain prefix of the lanes' closing counts: the
+// output places), and lane 31's open tail carries it into the next step.
+// The grouping is fixed by the layout, so the bits are the same on every run.
 #ifndef FPR_PB_GATHER_MINB
-#define FPR_PB_GATHER_MINB 1
+#define FPR_PB_GATHER_MINB 4
 #endif
 __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(
     const int32_t* esrc, const int64_t* item_start, const uint32_t* item_len, const int64_t* item_ubase,
     int64_t nitems, const double* prev, double* psum, unsigned long long* next_item) {
   const int lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1u;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   for (;;) {
     unsigned long long it = 0;
     if (lane == 0) it = atomicAdd(next_item, 1ull);
@@ -435,72 +436,78 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
     const int64_t p1 = p0 + __ldg(item_len + it);
     int64_t ub = __ldg(item_ubase + it);  // the next run's number (warp-uniform)
     double carry = 0.0;                   // the run left open by the previous step
-    constexpr int U = 2;
-    for (int64_t q0 = p0 & ~int64_t(3); q0 < p1; q0 += 128 * U) {
-      int4 sv[U];
+    for (int64_t q0 = p0 & ~int64_t(7); q0 < p1; q0 += 256) {
+      const int64_t qb = q0 + 8 * lane;
+      // this lane's entries inside the piece: bits [jlo, jhi)
+      const int jlo = (int)max((int64_t)0, min((int64_t)8, p0 - qb));
+      const int jhi = (int)max((int64_t)0, min((int64_t)8, p1 - qb));
+      const unsigned okm = ((1u << jhi) - 1u) & ~((1u << jlo) - 1u);
+      int s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (okm)
+        asm volatile(
+            "ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+            : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]), "=r"(s[7])
+            : "l"(esrc + qb), "l"(pol));
+      double v[8];
+      unsigned clm = 0;  // bit j: entry j closes its run
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * 128 + 4 * lane;
-        sv[u] = q < p1 ? __ldcs(reinterpret_cast<const int4*>(esrc + q)) : make_int4(0, 0, 0, 0);
-      }
-      double v[U][4];
-      unsigned cl[U];  // bit j: entry j closes its run
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * 128 + 4 * lane;
-        const int s4[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
-        cl[u] = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool ok = q + j >= p0 && q + j < p1;
-          const int32_t s = s4[j] & 0x7FFFFFFF;
-          v[u][j] = ok ? (FPR_PB_GATHER_L1 ? __ldca(prev + s) : __ldcg(prev + s)) : 0.0;
-          if (ok && s4[j] < 0) cl[u] |= 1u << j;
+      for (int j = 0; j < 8; ++j) {
+        v[j] = 0.0;
+        if (okm >> j & 1u) {
+          const double* a = prev + (s[j] & 0x7FFFFFFF);
+          v[j] = FPR_PB_GATHER_L1 ? __ldca(a) : __ldcg(a);
+          if (s[j] < 0) clm |= 1u << j;
         }
       }
+      // the partial of the lane's first closed run, and its open tail
+      double run = 0.0, F = 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        // this lane's runs: closed ones in o[], the open tail in T
-        double o[4], run = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          run = j == 0 ? v[u][0] : run + v[u][j];
-          o[j] = run;
-          if (cl[u] >> j & 1u) run = 0.0;
+      for (int j = 0; j < 8; ++j) {
+        run = run + v[j];
+        if (clm >> j & 1u) {
+          if ((clm & ((1u << j) - 1u)) == 0u) F = run;
+          run = 0.0;
         }
-        const bool h = cl[u] != 0u;
-        double T = run;
-        if (lane == 0 && !h) T = carry + T;
-        // segmented inclusive scan of the tails, restarting at closing lanes
-        double S = T;
-        bool f = h;
+      }
+      const bool h = clm != 0u;
+      const int c = __popc(clm);
+      double S = run;
+      if (lane == 0 && !h) S = carry + S;
+      // segmented inclusive scan of the tails (restarting at closing lanes)
+      // and the inclusive prefix of the closing counts
+      bool f = h;
+      int C = c;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, S, d);
-          const bool g = __shfl_up_sync(0xffffffffu, f, d);
-          if (lane >= d && !f) {
+      for (int d = 1; d < 32; d <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, S, d);
+        const bool g = __shfl_up_sync(0xffffffffu, f, d);
+        const int y = __shfl_up_sync(0xffffffffu, C, d);
+        if (lane >= d) {
+          C += y;
+          if (!f) {
             S = t + S;
             f = g;
           }
         }
-        double ci = __shfl_up_sync(0xffffffffu, S, 1);  // the run entering this lane
-        if (lane == 0) ci = carry;
-        carry = __shfl_sync(0xffffffffu, S, 31);
-        // places: runs closed by earlier lanes of this step, then in order
-        const unsigned b0 = __ballot_sync(0xffffffffu, cl[u] & 1u), b1 = __ballot_sync(0xffffffffu, cl[u] & 2u),
-                       b2 = __ballot_sync(0xffffffffu, cl[u] & 4u), b3 = __ballot_sync(0xffffffffu, cl[u] & 8u);
-        int64_t k = ub + __popc(b0 & below) + __popc(b1 & below) + __popc(b2 & below) + __popc(b3 & below);
-        bool first = true;
+      }
+      double ci = __shfl_up_sync(0xffffffffu, S, 1);  // the run entering this lane
+      if (lane == 0) ci = carry;
+      carry = __shfl_sync(0xffffffffu, S, 31);
+      const int total = __shfl_sync(0xffffffffu, C, 31);
+      if (h) {
+        int64_t k = ub + (C - c);
+        run = 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (cl[u] >> j & 1u) {
-            __stcs(psum + k, first ? ci + o[j] : o[j]);
-            first = false;
+        for (int j = 0; j < 8; ++j) {
+          run = run + v[j];
+          if (clm >> j & 1u) {
+            __stcs(psum + k, (clm & ((1u << j) - 1u)) == 0u ? ci + F : run);
             ++k;
+            run = 0.0;
           }
         }
-        ub += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
       }
+      ub += total;
     }
   }
 }

@@ -931,6 +931,16 @@ int fpr_b200_graph_set_wave_count(fpr_b200_graph* h, uint32_t wave_count) {
   return FPR_B200_OK;
 }
 
+int fpr_b200_graph_layout_info(const fpr_b200_graph* h, int* sweep, uint64_t* runs, uint64_t* pieces,
+                               uint64_t* tiles) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_layout_info: null graph");
+  if (sweep) *sweep = h->use_pb ? FPR_B200_SWEEP_PB : FPR_B200_SWEEP_PULL;
+  if (runs) *runs = h->pb ? (uint64_t)h->pb->nps : 0;
+  if (pieces) *pieces = h->pb ? (uint64_t)h->pb->npieces : 0;
+  if (tiles) *tiles = h->pb ? (uint64_t)h->pb->ntiles : 0;
+  return FPR_B200_OK;
+}
+
 int fpr_b200_graph_info(const fpr_b200_graph* h, uint64_t* n, uint64_t* m, uint64_t* ntasks) {
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_info: null graph");
   if (n) *n = (uint64_t)h->g.n;
