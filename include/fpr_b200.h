@@ -98,7 +98,7 @@ typedef struct fpr_config {
  * exceeds twice the device's L2 -- configs 4/5, where the pull gathers miss L2
  * -- and the pull sweep otherwise.  The two flags force one kind. */
 #define FPR_B200_OPT_PB 4u      /* EC and lockstep engines: propagation-blocked sweeps
-                                  (bins of 2^13 rows, source chunks of 2^21;
+                                  (bins of 2^13 rows, source chunks of 2^23;
                                   FPR_B200_PB_SHIFT / FPR_B200_PB_CHUNK_SHIFT override):
                                   two streaming passes instead of the random pull
                                   gather; row sums are exact

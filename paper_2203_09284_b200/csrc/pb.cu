@@ -26,7 +26,7 @@
 // of consecutive bins: 1 wave for EC, S for lockstep.  Per wave:
 //   * phase 1 (pb_gather_kernel): warps walk the wave's segment pieces chunk
 //     by chunk, so the sources read at any moment span one chunk's
-//     contributions (a 16 MB window at the default chunk of 2^21 sources);
+//     contributions (a 64 MB window at the default chunk of 2^23 sources);
 //     they gather every entry's contribution, sum each run left to right
 //     (a segmented warp scan across lanes) and write its partial sum;
 //   * phase 2 (pb_accum_kernel): a CTA takes a bin (or a run of tiles of a

@@ -505,12 +505,14 @@ int validate_config(const fpr_config* cfg) {
 }
 
 // Propagation-blocked geometry: 2^13-row bins (64 KB of shared accumulators,
-// 2 CTAs per SM) and 2^21-source chunks (a 16 MB contribution window)
-// measured best on configs 4/5 with the final kernels; the
-// environment overrides are for tests and probes.
+// 2 CTAs per SM) and 2^23-source chunks (a 64 MB contribution window: the
+// larger the chunk, the longer a row's runs and the fewer partial sums, until
+// the window stops fitting L2 -- 2^24 loses 30% on config 4's unordered
+// ids); measured on configs 4/5.  The environment
+// overrides are for tests and probes.
 void pb_geometry(int* shift, int* chunk_shift) {
   *shift = 13;
-  *chunk_shift = 21;
+  *chunk_shift = 23;
   if (const char* s = std::getenv("FPR_B200_PB_SHIFT")) *shift = std::atoi(s);
   if (const char* s = std::getenv("FPR_B200_PB_CHUNK_SHIFT")) *chunk_shift = std::atoi(s);
 }
