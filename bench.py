@@ -71,11 +71,12 @@ def algorithmic_bytes(n: int, m: int) -> int:
     return 12 * m + 36 * n
 
 
-def pb_stream_bytes(n: int, m: int) -> int:
+def pb_stream_bytes(n: int, m: int, runs: int) -> int:
     """Per propagation-blocked sweep, what the two passes stream besides the
-    random gather: 4 B source + 8 B value written + 8 B value
-    read + 2 B inverse permutation + 2 B row key per edge, + 36 B/vertex."""
-    return 24 * m + 36 * n
+    random gather: 4 B source per edge; per run (one row's
+    edges inside one source chunk, summed by the gather pass) 8 B partial sum
+    written + 8 B read back + 2 B tile index + 2 B row key; + 36 B/vertex."""
+    return 4 * m + 20 * runs + 36 * n
 
 
 # Random 8-B fetches per second against the contribution vector's size,
@@ -83,12 +84,13 @@ def pb_stream_bytes(n: int, m: int) -> int:
 GATHER_CEILING = ((33.6e6, 270e9), (134e6, 113e9), (537e6, 56e9), (2.15e9, 46e9))
 
 
-def ceiling_ms(n: int, m: int, pb: bool, peak: float) -> float:
+def ceiling_ms(n: int, m: int, pb: bool, peak: float, runs: int = 0) -> float:
     """The sweep's own floor: the pull sweep's gathers at the measured random-
     fetch rate for 8 n bytes of contributions; a propagation-blocked sweep's
-    gather requests at ~270 G/s plus its 20 B/edge + 36 B/vertex stream."""
+    gathers at ~270 G/s (one L2 request each, L2-resident window) plus the
+    accumulate's stream (20 B/run + 36 B/vertex) at the copy peak."""
     if pb:
-        return (m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3
+        return (m / 270e9 + (20 * runs + 36 * n) / (peak * 1e9)) * 1e3
     size = 8 * n
     rate = next((r for s, r in GATHER_CEILING if size <= s * 1.05), GATHER_CEILING[-1][1])
     return m / rate * 1e3
@@ -337,8 +339,8 @@ def secondary_legs(fb, device, peak) -> dict:
                 "sweep": "pb" if pb else "pull",
                 # the sweep's own ceiling: pull = the measured random-fetch
                 # rate for a contribution vector of this size; PB = gather requests + stream
-                "ceiling_ms": ceiling_ms(dg.n, dg.m, pb, peak),
-                "ceiling_frac": ceiling_ms(dg.n, dg.m, pb, peak) / ms_it}
+                "ceiling_ms": ceiling_ms(dg.n, dg.m, pb, peak, dg.layout_info()["runs"]),
+                "ceiling_frac": ceiling_ms(dg.n, dg.m, pb, peak, dg.layout_info()["runs"]) / ms_it}
 
     names = {"2": "config2: uniform G(n=2^22, 2^26 draws, seed 2)",
              "3": "config3: RMAT s24 ef16 seed 3, BFS crawl-order relabel",
@@ -435,6 +437,7 @@ def main() -> None:
     sweep_ms = kms / iters
     achieved = algorithmic_bytes(n, m) / (sweep_ms * 1e-3) / 1e9
     pb = r.sweep == fb.SWEEP_PB
+    runs = dg.layout_info()["runs"]
 
     # per-iteration device times and trace of one more solve
     tr = dg.run(fb.ENGINE_EC, cfg, copy_ranks=True, copy_trace=True)
@@ -492,13 +495,14 @@ def main() -> None:
                      "unit_of_work": "one EC sweep (the PB gather + accumulate + reduce launches) = one iteration",
                      "algorithmic_bytes_per_sweep": algorithmic_bytes(n, m),
                      "sweep_ms": sweep_ms,
-                     "pb_stream_bytes_frac": pb_stream_bytes(n, m) / (sweep_ms * 1e-3) / 1e9 / peak if pb else None,
+                     "pb_runs": runs if pb else None,
+                     "pb_stream_bytes_frac": (pb_stream_bytes(n, m, runs) / (sweep_ms * 1e-3) / 1e9 / peak
+                                              if pb else None),
                      # the design's own floor: the gather pass at the measured
                      # random-fetch ceiling (~270 G L2 requests/s, bench_micro/gather_bench.cu)
-                     # plus the accumulate's stream (20 B/edge + 36 B/vertex) at the copy peak
-                     "pb_design_floor_ms": (m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3 if pb else None,
-                     "pb_design_floor_frac": ((m / 270e9 + (20 * m + 36 * n) / (peak * 1e9)) * 1e3 / sweep_ms
-                                              if pb else None),
+                     # plus the accumulate's stream (20 B/run + 36 B/vertex) at the copy peak
+                     "pb_design_floor_ms": ceiling_ms(n, m, True, peak, runs) if pb else None,
+                     "pb_design_floor_frac": ceiling_ms(n, m, True, peak, runs) / sweep_ms if pb else None,
                      "traffic_source": traffic.get("source") if traffic else None,
                      "kernel_shares": traffic.get("kernel_shares") if traffic else None},
         "fused": fused,
