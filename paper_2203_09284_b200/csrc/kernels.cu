@@ -175,6 +175,13 @@ constexpr int kPos = 32 * kLaneItems;  // 256 positions per task
 struct alignas(16) WarpSmem {
   double pacc[kPos];  // per position: lane-local running sum since the last segment start
   double carry[33];   // carry[L] = inclusive segmented scan of lane L-1's tail (0 for L=0)
+  // the head row whose finish is deferred by one task (finish_head)
+  double ph_sum;      // its sum inside the owner task
+  double ph_ov;       // pr[r] before the sweep
+  int ph_od;          // outdeg[r]
+  int ph_r;           // the row
+  int ph_t;           // the owner task, -1 = none
+  int ph_pad;
 };
 // Launch shape per engine: Jacobi/lockstep run 20 warps/SM (160-thread CTAs,
 // <= 102 registers, no spills); the async engine runs 16 warps/SM, which its
@@ -329,6 +336,53 @@ __device__ __forceinline__ double task_sums(const double (&v)[8], unsigned bits8
   return acc;
 }
 
+// A head row split across earlier tasks is finished one task LATER by the
+// warp that holds its end (the owner): the partials of the earlier tasks are
+// written while this warp runs its next task, so the combine rarely waits
+// (waiting at once spun on partials of tasks running in parallel: 26% of
+// config 3's stall samples).  The same warp finishes the row in the same
+// place of its schedule on every run, so ranks and residuals keep their bits.
+#ifndef FPR_DEFER_HEAD
+#define FPR_DEFER_HEAD 1
+#endif
+template <bool ASYNC, int MODE>
+__device__ __forceinline__ void finish_head(const SolveParams& p, WarpSmem& ws, double* cur, int lane,
+                                            double& lmax, double& lsum) {
+  const int t = ws.ph_t;
+  if (t < 0) return;
+  const int ta = __ldg(p.head_first + t);
+  double accp = 0.0;
+  for (int tt = ta + lane; tt < t; tt += 32) {
+    double x = ld_relaxed_f64(p.tail_partial + tt);
+    while (!(x >= 0.0)) {
+      __nanosleep(64);
+      x = ld_relaxed_f64(p.tail_partial + tt);
+    }
+    accp += x;
+    st_relaxed_f64(p.tail_partial + tt, tail_not_ready());  // consumed: re-arm
+  }
+  const double head_extra = warp_sum(accp);
+  if (lane == 0) {
+    const int r = ws.ph_r, od = ws.ph_od;
+    const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, head_extra + ws.ph_sum));
+    p.pr_out[r] = nv;
+    if (od > 0) {
+      const double c = __ddiv_rn(nv, (double)od);
+      if (ASYNC)
+        st_relaxed_f64(cur + r, c);
+      else
+        cur[r] = c;
+      if (MODE == kModePeers)
+        for (int q = 0; q < p.npeers; ++q) p.peer[q][r] = c;
+    }
+    const double d = fabs(nv - ws.ph_ov);
+    lmax = fmax(lmax, d);
+    lsum += d;
+    ws.ph_t = -1;
+  }
+  __syncwarp();
+}
+
 template <bool ASYNC, int MODE>
 __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const TaskMeta& m,
                                             double acc, unsigned bits8, const RowPre& rp,
@@ -374,9 +428,14 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
   }
   __syncwarp();
 
-  // 4. head row split across earlier tasks: combine their partials in task order.
+  // 4. head row split across earlier tasks: combine their partials in task
+  //    order -- deferred (finish_head): the previous task's head row now,
+  //    this task's after the next task.
   double head_extra = 0.0;
   const bool has_head = i0 < i1 && __shfl_sync(FULL_MASK, rp.lo, 0) < 0;
+#if FPR_DEFER_HEAD
+  finish_head<ASYNC, MODE>(p, ws, cur, lane, lmax, lsum);
+#else
   if (has_head) {
     const int ta = __ldg(p.head_first + t);
     double accp = 0.0;
@@ -391,6 +450,7 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
     }
     head_extra = warp_sum(accp);
   }
+#endif
 
   // 5. finalize rows [i0, i1): lane per row.  A row's in-task sum is the
   //    running sum at its last position plus the carry into that lane when
@@ -413,7 +473,18 @@ __device__ __forceinline__ void task_finish(const SolveParams& p, int t, const T
         sum = ws.pacc[e];
         if (lo + off < (e & ~7)) sum = ws.carry[e >> 3] + sum;
       }
+#if FPR_DEFER_HEAD
+      if (r == i0 && has_head) {  // finished after the next task (finish_head)
+        ws.ph_r = r;
+        ws.ph_sum = sum;
+        ws.ph_od = od;
+        ws.ph_ov = ov;
+        ws.ph_t = t;
+        continue;
+      }
+#else
       if (r == i0 && has_head) sum = head_extra + sum;
+#endif
       const double nv = __dadd_rn(p.base, __dmul_rn(p.damping, sum));
       p.pr_out[r] = nv;
       if (od > 0) {
@@ -484,6 +555,8 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
   }
   RowPre rp = load_rowpre<MODE>(p, m, lane);
   unsigned bits = load_bits8(p, t, lane);
+  if (lane == 0) ws.ph_t = -1;
+  __syncwarp();
   TaskMeta mn{0, 0, 0, 0}, mnn{0, 0, 0, 0};
   Src8 sn{{0, 0, 0, 0}, {0, 0, 0, 0}};
   if (t + nwarps < te) {
@@ -518,6 +591,7 @@ __device__ __forceinline__ void run_tasks(const SolveParams& p, int tb, int te, 
     sn = snn;
     mnn = mnnn;
   }
+  finish_head<ASYNC, MODE>(p, ws, cur, lane, lmax, lsum);  // the last task's head row
 }
 
 // ------------------------------------------------------ persistent solver
