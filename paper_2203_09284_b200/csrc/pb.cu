@@ -245,12 +245,45 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
 // pass's work items: kPieceEntries entries from the segment's start, so no
 // run spans two of them).  Pads close nothing.  The sources are read with
 // the close flag (bit 31) masked: pb_psum_kernel sets it in place.
-__device__ __forceinline__ bool pb_closes(const int32_t* src, const uint16_t* dstl, const int64_t* start, int64_t q,
-                                          int64_t pe, int64_t b, int64_t nbins, int chunk_shift) {
-  if (q + 1 >= pe) return true;
-  const uint32_t c = ((uint32_t)src[q] & 0x7FFFFFFFu) >> chunk_shift;
-  if ((((uint32_t)src[q + 1] & 0x7FFFFFFFu) >> chunk_shift) != c || dstl[q + 1] != dstl[q]) return true;
-  return (q - __ldg(start + (int64_t)c * nbins + b) + 1) % kPieceEntries == 0;
+// Close mask of the 8 entries [q, q + 8) (q 8-aligned; entries at or past
+// pe are pads, never closing); s/d receive their sources (flag masked) and
+// row offsets.
+__device__ __forceinline__ unsigned pb_close_mask8(const int32_t* src, const uint16_t* dstl, const int64_t* start,
+                                                   int64_t q, int64_t pe, int64_t b, int64_t nbins,
+                                                   int chunk_shift, uint32_t (&s)[8], uint32_t (&d)[8]) {
+  const int4 a0 = *reinterpret_cast<const int4*>(src + q), a1 = *reinterpret_cast<const int4*>(src + q + 4);
+  const uint4 dv = *reinterpret_cast<const uint4*>(dstl + q);
+  s[0] = (uint32_t)a0.x, s[1] = (uint32_t)a0.y, s[2] = (uint32_t)a0.z, s[3] = (uint32_t)a0.w;
+  s[4] = (uint32_t)a1.x, s[5] = (uint32_t)a1.y, s[6] = (uint32_t)a1.z, s[7] = (uint32_t)a1.w;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    s[j] &= 0x7FFFFFFFu;
+    d[j] = (j & 1) ? ((&dv.x)[j >> 1] >> 16) : ((&dv.x)[j >> 1] & 0xFFFFu);
+  }
+  uint32_t s8 = 0, d8 = 0;
+  if (q + 8 < pe) {
+    s8 = (uint32_t)src[q + 8] & 0x7FFFFFFFu;
+    d8 = dstl[q + 8];
+  }
+  unsigned m = 0;
+  uint32_t cprev = 0xFFFFFFFFu;
+  int64_t ss = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (q + j >= pe) break;
+    const uint32_t c = s[j] >> chunk_shift;
+    if (c != cprev) {
+      ss = __ldg(start + (int64_t)c * nbins + b);
+      cprev = c;
+    }
+    bool cl = q + j + 1 >= pe;
+    if (!cl) {
+      const uint32_t sn = j < 7 ? s[j + 1] : s8, dn = j < 7 ? d[j + 1] : d8;
+      cl = (sn >> chunk_shift) != c || dn != d[j] || (q + j - ss + 1) % kPieceEntries == 0;
+    }
+    if (cl) m |= 1u << j;
+  }
+  return m;
 }
 
 // Pass A: the number of runs (partial sums) of each bin.
@@ -264,8 +297,10 @@ __global__ void __launch_bounds__(kAccThreads) pb_close_count_kernel(const int32
     const int64_t r0 = b << shift, r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
     const int64_t p0 = bin_pos[b], pe = p0 + (row[r1] - row[r0]);
     uint32_t c = 0;
-    for (int64_t q = p0 + threadIdx.x; q < pe; q += kAccThreads)
-      c += pb_closes(src, dstl, start, q, pe, b, nbins, chunk_shift) ? 1u : 0u;
+    for (int64_t q = p0 + 8 * (int64_t)threadIdx.x; q < pe; q += 8 * kAccThreads) {
+      uint32_t sv[8], dv[8];
+      c += __popc(pb_close_mask8(src, dstl, start, q, pe, b, nbins, chunk_shift, sv, dv));
+    }
     c = Reduce(tmp).Sum(c);
     if (threadIdx.x == 0) bin_np[b] = (int64_t)c;
     __syncthreads();
@@ -279,6 +314,7 @@ __global__ void __launch_bounds__(kAccThreads) pb_close_count_kernel(const int32
 //   * every piece start q records the number of its first run in
 //     pbase[seg_piece0[segment] + piece]: the runs closed before q in the
 //     bin, since q's run closes at or after q.
+// Threads take 8 consecutive entries (32-B source words, 16-B row offsets).
 __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, const uint16_t* dstl, const int64_t* row,
                                                               int32_t n, int shift, const int64_t* bin_pos,
                                                               const int64_t* pbin_pos, const int64_t* start,
@@ -290,21 +326,44 @@ __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, cons
     const int64_t r0 = b << shift, r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
     const int64_t p0 = bin_pos[b], pe = p0 + (row[r1] - row[r0]);
     int64_t u = pbin_pos[b];
-    for (int64_t t = p0; t < pe; t += kAccThreads) {
-      const int64_t q = t + threadIdx.x;
-      const bool in = q < pe;
-      const bool cl = in && pb_closes(src, dstl, start, q, pe, b, nbins, chunk_shift);
+    for (int64_t t = p0; t < pe; t += 8 * kAccThreads) {
+      const int64_t q = t + 8 * (int64_t)threadIdx.x;
+      uint32_t sv[8], dv[8];
+      const unsigned m = q < pe ? pb_close_mask8(src, dstl, start, q, pe, b, nbins, chunk_shift, sv, dv) : 0u;
       uint32_t before, total;
-      Scan(tmp).ExclusiveSum(cl ? 1u : 0u, before, total);
-      __syncthreads();  // every thread of the tile has read its neighbour's flag-free source
-      if (in) {
-        const uint32_t s = (uint32_t)src[q] & 0x7FFFFFFFu;
-        const int64_t seg = (int64_t)(s >> chunk_shift) * nbins + b;
-        const int64_t off = q - __ldg(start + seg);
-        if (off % kPieceEntries == 0) pbase[(int64_t)seg_piece0[seg] + off / kPieceEntries] = u + before;
-        if (cl) {
-          pkey[u + before] = dstl[q];
-          src[q] = (int32_t)(s | 0x80000000u);
+      Scan(tmp).ExclusiveSum((uint32_t)__popc(m), before, total);
+      if (q < pe) {
+        uint32_t cprev = 0xFFFFFFFFu;
+        int64_t ss = 0, seg = 0;
+        uint32_t k = before;  // runs closed before entry q + j in the bin
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (q + j >= pe) break;
+          const uint32_t c = sv[j] >> chunk_shift;
+          if (c != cprev) {
+            seg = (int64_t)c * nbins + b;
+            ss = __ldg(start + seg);
+            cprev = c;
+          }
+          const int64_t off = q + j - ss;
+          if (off % kPieceEntries == 0) pbase[(int64_t)__ldg(seg_piece0 + seg) + off / kPieceEntries] = u + k;
+          if (m >> j & 1u) {
+            pkey[u + k] = (uint16_t)dv[j];
+            ++k;
+          }
+        }
+        int4 w0, w1;
+        w0.x = (int)(sv[0] | (m << 31)), w0.y = (int)(sv[1] | ((m >> 1) << 31)), w0.z = (int)(sv[2] | ((m >> 2) << 31));
+        w0.w = (int)(sv[3] | ((m >> 3) << 31)), w1.x = (int)(sv[4] | ((m >> 4) << 31));
+        w1.y = (int)(sv[5] | ((m >> 5) << 31)), w1.z = (int)(sv[6] | ((m >> 6) << 31));
+        w1.w = (int)(sv[7] | ((m >> 7) << 31));
+        // pads past pe keep their -1 (never read by the gather pass)
+        if (q + 8 <= pe) {
+          *reinterpret_cast<int4*>(src + q) = w0;
+          *reinterpret_cast<int4*>(src + q + 4) = w1;
+        } else {
+          const int ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          for (int j = 0; j < 8 && q + j < pe; ++j) src[q + j] = ww[j];
         }
       }
       u += total;
