@@ -579,7 +579,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     dev = f"cuda:{local}"
     solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1,
-                               speculate=ws > 1)
+                               device_stop=ws > 1, batch=8)
     for _ in range(args.warmup):
         r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=False)
     iters = r.iterations
@@ -616,9 +616,10 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "config": config_block(args.workload, n, m),
             "step": "1 full EC solve (time-to-converge)",
             "iterations": iters, "parallelism": f"dst-range partition x{ws}", "exchange": exchange,
-            "sweep": "pull (per part)",
-            "host_loop": ("speculative: sweep k+1 enqueued before iteration k's residual is read"
-                          if ws > 1 else "synchronous"),
+            "sweep": ("propagation-blocked" if part.graph.layout_info()["sweep"] == fb.SWEEP_PB else "pull")
+                     + " (per part, the library's choice for the part's exchange space)",
+            "host_loop": ("device-side stop: batches of 8 iterations (sweep, pair all-gather, gate update) "
+                          "enqueued without a host read; one gate read per batch" if ws > 1 else "synchronous"),
             "exchange_fallback": solver.fallback, "slice": part.slice,
             "time_to_converge_ms": ms_step,
             "fused": {"iterations": fr.iterations},

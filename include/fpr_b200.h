@@ -264,6 +264,31 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* g, int engine, const fpr_config* c
                               const double* exch_read, double* exch_write,
                               double* const* peer_write, uint32_t npeer_bufs, double* pair_out);
 
+/* ---- device-side stop rule (multi-GPU drivers) -------------
+ * The reference's parallel engines reduce the per-thread residuals and apply
+ * `error <= threshold` in the barrier's completion step (pagerank.hpp:209-218,
+ * :276-286).  A multi-GPU driver that does this on the host pays a device ->
+ * host round trip per iteration.  A gate moves the rule onto the device: it
+ * is fpr_b200_gate_bytes(trace_cap) bytes of device memory holding the
+ * iteration count, a stop flag and the (max, sum) residual trace.
+ *   * fpr_b200_part_set_gate binds a part to a gate: its sweeps become
+ *     no-ops (nothing read or written) once the gate is stopped;
+ *   * fpr_b200_gate_update, enqueued after an iteration's residual pairs are
+ *     in place (all parts' pairs: pointers on `device` or peer-mapped), adds
+ *     the iteration to the trace and sets the stop flag when the reference's
+ *     predicate holds or max_iterations is reached;
+ * so a driver enqueues a batch of iterations -- sweep, pair exchange, gate
+ * update -- and reads the gate once per batch (fpr_b200_gate_read).  The
+ * ranks after the stopping iteration k are fpr_b200_part_ranks_after(g, k). */
+uint64_t fpr_b200_gate_bytes(uint64_t trace_cap);
+int fpr_b200_gate_init(void* gate, uint64_t trace_cap, int device, void* stream);
+int fpr_b200_gate_update(void* gate, const double* const* pairs, uint32_t npairs, const fpr_config* cfg, int norm,
+                         int device, void* stream);
+int fpr_b200_gate_read(const void* gate, int device, void* stream, uint64_t* iterations, int* stopped,
+                       double* errors_out, double* l1_errors_out, uint64_t cap);
+int fpr_b200_part_set_gate(fpr_b200_graph* g, const void* gate);
+int fpr_b200_part_ranks_after(fpr_b200_graph* g, uint64_t sweeps, double* ranks_out);
+
 /* CUDA IPC of exchange buffers between the per-GPU processes.  A handle is
  * the cudaIpcMemHandle of the allocation holding dev_ptr plus dev_ptr's
  * offset in it (buffers from caching allocators are sub-allocations). */

@@ -109,6 +109,8 @@ EXPORTS = [
     "fpr_b200_graph_from_edges", "fpr_b200_part_ranks_prev", "fpr_b200_part_create",
     "fpr_b200_mgpu_create", "fpr_b200_mgpu_generate", "fpr_b200_mgpu_run", "fpr_b200_mgpu_info",
     "fpr_b200_mgpu_destroy", "fpr_b200_generate_edges", "fpr_b200_graph_layout_info",
+    "fpr_b200_gate_bytes", "fpr_b200_gate_init", "fpr_b200_gate_update", "fpr_b200_gate_read",
+    "fpr_b200_part_set_gate", "fpr_b200_part_ranks_after",
 ]
 
 _lib = None
@@ -156,6 +158,13 @@ def lib() -> C.CDLL:
         L.fpr_b200_part_sweep_peers.argtypes = [vp, i32, C.POINTER(_Config), vp, vp, vp, u32, vp]
         L.fpr_b200_part_ranks.argtypes = [vp, vp]
         L.fpr_b200_part_ranks_prev.argtypes = [vp, vp]
+        L.fpr_b200_gate_bytes.argtypes = [u64]
+        L.fpr_b200_gate_bytes.restype = u64
+        L.fpr_b200_gate_init.argtypes = [vp, u64, i32, vp]
+        L.fpr_b200_gate_update.argtypes = [vp, vp, u32, C.POINTER(_Config), i32, i32, vp]
+        L.fpr_b200_gate_read.argtypes = [vp, i32, vp, C.POINTER(u64), C.POINTER(C.c_int), vp, vp, u64]
+        L.fpr_b200_part_set_gate.argtypes = [vp, vp]
+        L.fpr_b200_part_ranks_after.argtypes = [vp, u64, vp]
         L.fpr_b200_ipc_export.argtypes = [vp, vp]
         L.fpr_b200_ipc_import.argtypes = [C.c_char_p, i32, C.POINTER(vp)]
         L.fpr_b200_ipc_close.argtypes = [vp]

@@ -106,7 +106,29 @@ struct SolveParams {
   int32_t npeers;
   int32_t peer_skip_empty;  // peers already hold the constant contribution of rows without in-edges
   double* peer[kMaxPeers];
+  // device-side stop (multi-GPU drivers): the sweep is a no-op while *gate
+  // != 0 (the stop flag of a GateHdr); nullptr = ungated
+  const unsigned int* gate;
 };
+
+// Device-side stop rule (fpr_b200_gate_*): header, then 2 x cap doubles of
+// trace (max |delta|, sum |delta| per iteration).
+struct GateHdr {
+  unsigned int stop;
+  unsigned int pad;
+  unsigned long long iters;
+  unsigned long long cap;
+  unsigned long long pad2;
+};
+struct PairPtrs {
+  int n = 0;
+  const double* p[kMaxPeers + 1] = {};
+};
+cudaError_t launch_gate_init(GateHdr* g, uint64_t cap, cudaStream_t s);
+// One iteration's stop decision from the parts' residual pairs, reduced in
+// part order (max, sum) -- the host driver's rule, on the device.
+cudaError_t launch_gate_update(GateHdr* g, const PairPtrs& pp, double threshold, int norm, uint64_t max_iterations,
+                               cudaStream_t s);
 
 enum Engine { kEC = 0, kFused = 1, kLockstep = 2 };
 // Launch-shape id of the async engine on graphs whose contributions exceed
@@ -278,7 +300,8 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
 // multi-GPU part's ping-pong); contributions go to cur (+ peers).
 cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
                             const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
-                            double damping, double* err, double* l1, cudaStream_t st);
+                            double damping, double* err, double* l1, cudaStream_t st,
+                            const unsigned int* gate = nullptr);
 
 // runtime.cu hooks for mgpu.cu (the multi-device driver over the part API)
 int set_error(int code, const std::string& msg);  // thread-local last error; returns code

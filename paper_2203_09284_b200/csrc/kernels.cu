@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(BT, MB) solve_kernel(SolveParams p) {
   const int gwarp = blockIdx.x * kWPB + wib;
   const int nwarps = gridDim.x * kWPB;
   const unsigned long long pol = evict_first_policy();
+  if (p.gate && *reinterpret_cast<const volatile unsigned int*>(p.gate)) return;  // stopped: no-op sweep
   int par = p.parity0;
   if (blockIdx.x == 0 && threadIdx.x == 0) p.iter_ns[0] = globaltimer();
 
@@ -948,6 +949,49 @@ cudaError_t solve_grid(int engine, int num_sms, int* grid_out) {
   if (best < 1) return cudaErrorInvalidConfiguration;
   *grid_out = best * num_sms;
   return cudaSuccess;
+}
+
+// ------------------------------------------------- device-side stop rule
+// One thread: the parts' pairs in part order (max, then sum -- the order the
+// host drivers use), the trace entry, and pagerank.hpp's predicate
+// `error <= threshold` (:141, :216) or the iteration cap.  A stopped gate
+// stays stopped (later updates and gated sweeps are no-ops).
+__global__ void gate_update_kernel(GateHdr* g, PairPtrs pp, double threshold, int norm, uint64_t max_iterations) {
+  if (g->stop) return;
+  double err = 0.0, l1 = 0.0;
+  for (int r = 0; r < pp.n; ++r) {
+    const volatile double* q = pp.p[r];
+    err = fmax(err, q[0]);
+    l1 += q[1];
+  }
+  const unsigned long long it = g->iters;
+  double* trace = reinterpret_cast<double*>(g + 1);
+  if (it < g->cap) {
+    trace[2 * it] = err;
+    trace[2 * it + 1] = l1;
+  }
+  g->iters = it + 1;
+  const double crit = norm ? l1 : err;  // FPR_B200_NORM_L1 = 1
+  if (crit <= threshold || it + 1 >= max_iterations) g->stop = 1u;
+}
+
+__global__ void gate_init_kernel(GateHdr* g, uint64_t cap) {
+  g->stop = 0u;
+  g->pad = 0u;
+  g->iters = 0ull;
+  g->cap = cap;
+  g->pad2 = 0ull;
+}
+
+cudaError_t launch_gate_init(GateHdr* g, uint64_t cap, cudaStream_t s) {
+  gate_init_kernel<<<1, 1, 0, s>>>(g, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_update(GateHdr* g, const PairPtrs& pp, double threshold, int norm, uint64_t max_iterations,
+                               cudaStream_t s) {
+  gate_update_kernel<<<1, 1, 0, s>>>(g, pp, threshold, norm, max_iterations);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_solve(int engine, int grid, const SolveParams& p, cudaStream_t s) {

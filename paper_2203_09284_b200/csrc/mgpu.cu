@@ -16,12 +16,19 @@
 //     (fpr_b200_part_sweep_peers: kernels.cu kModePeers for the pull sweep,
 //     the accumulate's finalize in pb.cu for propagation-blocked parts, which
 //     the library picks when the exchange space far exceeds L2);
-//   * the calling thread waits for the parts' 16-B (max, sum) residual pairs,
-//     reduces them in part order (the on_barrier step, deterministic) and
-//     applies the reference's predicate `error <= threshold` (:141, :216).
+//   * the stop rule runs on the devices: after each iteration every part's
+//     stream waits (CUDA events, no host involvement) for all parts' sweeps,
+//     then a one-thread gate kernel reduces the parts' 16-B (max, sum)
+//     residual pairs in part order -- peer loads -- (the on_barrier step,
+//     deterministic) and applies the reference's predicate
+//     `error <= threshold` (:141, :216); once it holds, the parts' later
+//     sweeps are no-ops (fpr_b200_part_set_gate).  The calling thread
+//     enqueues batches of iterations and reads device 0's gate once per
+//     batch, so no iteration waits on a host round trip.
 // Parts that share a device run on their own streams one after the other;
 // the test suite uses that to check P parts against one GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -37,8 +44,10 @@ struct fpr_b200_mgpu {
   std::vector<fpr_b200_graph*> parts;
   std::vector<uint64_t> bounds;    // P + 1 row bounds
   std::vector<double*> x[2];       // per part: exchange vectors (P * slice doubles, on the part's device)
-  std::vector<double*> dpair;      // per part: its (max, sum) residual pair (device)
-  double* hpairs = nullptr;        // P pairs (pinned host)
+  std::vector<double*> dpair;      // per part: its (max, sum) residual pair, two slots by iteration parity
+  std::vector<void*> gate;         // per part: device-side stop rule (fpr_b200_gate_*) on its device
+  uint64_t gate_cap = 0;           // trace capacity of the gates
+  std::vector<cudaEvent_t> ev[2];  // per part: its sweep of an even / odd iteration finished
 };
 
 namespace {
@@ -102,9 +111,17 @@ int finish(fpr_b200_mgpu* mg) {
     for (auto& v : mg->x) MCK(cudaMalloc(&v[r], (size_t)mg->P * mg->slice * sizeof(double)));
     MCK(cudaMemset(mg->x[0][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
     MCK(cudaMemset(mg->x[1][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
-    MCK(cudaMalloc(&mg->dpair[r], 2 * sizeof(double)));
+    MCK(cudaMalloc(&mg->dpair[r], 4 * sizeof(double)));
+    MCK(cudaMemset(mg->dpair[r], 0, 4 * sizeof(double)));
   }
-  MCK(cudaMallocHost(&mg->hpairs, 2 * (size_t)mg->P * sizeof(double)));
+  mg->gate.assign(mg->P, nullptr);
+  for (auto& v : mg->ev) {
+    v.assign(mg->P, nullptr);
+    for (uint32_t r = 0; r < mg->P; ++r) {
+      MCK(cudaSetDevice(mg->dev[r]));
+      MCK(cudaEventCreateWithFlags(&v[r], cudaEventDisableTiming));
+    }
+  }
   return FPR_B200_OK;
 }
 
@@ -124,9 +141,11 @@ void fpr_b200_mgpu_destroy(fpr_b200_mgpu* mg) {
     for (auto& v : mg->x)
       if (r < v.size() && v[r]) cudaFree(v[r]);
     if (r < mg->dpair.size() && mg->dpair[r]) cudaFree(mg->dpair[r]);
+    if (r < mg->gate.size() && mg->gate[r]) cudaFree(mg->gate[r]);
+    for (auto& v : mg->ev)
+      if (r < v.size() && v[r]) cudaEventDestroy(v[r]);
     fpr_b200_graph_destroy(mg->parts[r]);
   }
-  if (mg->hpairs) cudaFreeHost(mg->hpairs);
   delete mg;
 }
 
@@ -246,56 +265,90 @@ int fpr_b200_mgpu_run(fpr_b200_mgpu* mg, int engine, const fpr_config* cfg, doub
     MCK(cudaSetDevice(mg->dev[r]));
     MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
   }
+  // gates: one per part on its device (every part reaches the same decision
+  // from the same pairs in the same order); trace capacity = the iteration cap
+  const uint64_t cap = std::min<uint64_t>(cfg->max_iterations, uint64_t(1) << 22);
+  if (mg->gate_cap < cap) {
+    for (uint32_t r = 0; r < P; ++r) {
+      MCK(cudaSetDevice(mg->dev[r]));
+      if (mg->gate[r]) MCK(cudaFree(mg->gate[r]));
+      mg->gate[r] = nullptr;
+      MCK(cudaMalloc(&mg->gate[r], fpr_b200_gate_bytes(cap)));
+    }
+    mg->gate_cap = cap;
+  }
+  for (uint32_t r = 0; r < P; ++r) {
+    if ((rc = fpr_b200_gate_init(mg->gate[r], mg->gate_cap, mg->dev[r], fprb::graph_stream(mg->parts[r])))) return rc;
+    if ((rc = fpr_b200_part_set_gate(mg->parts[r], mg->gate[r]))) return rc;
+  }
+  uint64_t batch = 8;
+  if (const char* v = std::getenv("FPR_B200_MGPU_BATCH")) batch = (uint64_t)std::max(1, std::atoi(v));
   MCK(cudaSetDevice(mg->dev[0]));
   MCK(cudaEventRecord(t0, fprb::graph_stream(mg->parts[0])));
   std::vector<double*> peers(P);
-  uint64_t it = 0;
-  int cur = 0;
-  double err = 1.0, l1 = 1.0;
-  bool stop = false;
-  while (it < cfg->max_iterations && !stop) {
-    const int nxt = engine == FPR_B200_ENGINE_EC ? cur ^ 1 : cur;
-    for (uint32_t q = 0; q < P; ++q) peers[q] = mg->x[nxt][q];
-    for (uint32_t r = 0; r < P; ++r) {
-      if ((rc = fpr_b200_part_sweep_peers(mg->parts[r], engine, cfg, mg->x[cur][r], mg->x[nxt][r], peers.data(), P,
-                                          mg->dpair[r])))
-        return rc;
-      MCK(cudaSetDevice(mg->dev[r]));
-      MCK(cudaMemcpyAsync(mg->hpairs + 2 * r, mg->dpair[r], 2 * sizeof(double), cudaMemcpyDeviceToHost,
-                          fprb::graph_stream(mg->parts[r])));
+  std::vector<const double*> pairs(P);
+  uint64_t issued = 0, it = 0;
+  int stopped = 0;
+  while (!stopped && issued < cfg->max_iterations) {
+    for (uint64_t k = 0; k < batch && issued < cfg->max_iterations; ++k, ++issued) {
+      const int par = (int)(issued & 1);
+      const int cur = engine == FPR_B200_ENGINE_EC ? par : 0;
+      const int nxt = engine == FPR_B200_ENGINE_EC ? cur ^ 1 : cur;
+      for (uint32_t q = 0; q < P; ++q) peers[q] = mg->x[nxt][q];
+      for (uint32_t r = 0; r < P; ++r) {
+        // gated: a no-op once the stop rule held
+        if ((rc = fpr_b200_part_sweep_peers(mg->parts[r], engine, cfg, mg->x[cur][r], mg->x[nxt][r], peers.data(), P,
+                                            mg->dpair[r] + 2 * par)))
+          return rc;
+        MCK(cudaSetDevice(mg->dev[r]));
+        MCK(cudaEventRecord(mg->ev[par][r], fprb::graph_stream(mg->parts[r])));
+      }
+      // the barrier (stream waits on every part's sweep: its pair and its
+      // peer stores are in place), then the stop rule on every device
+      for (uint32_t q = 0; q < P; ++q) pairs[q] = mg->dpair[q] + 2 * par;
+      for (uint32_t r = 0; r < P; ++r) {
+        MCK(cudaSetDevice(mg->dev[r]));
+        for (uint32_t q = 0; q < P; ++q)
+          if (q != r) MCK(cudaStreamWaitEvent(fprb::graph_stream(mg->parts[r]), mg->ev[par][q], 0));
+        if ((rc = fpr_b200_gate_update(mg->gate[r], pairs.data(), P, cfg, mg->norm, mg->dev[r],
+                                       fprb::graph_stream(mg->parts[r]))))
+          return rc;
+      }
     }
-    // the barrier: every part's sweep (and its peer stores) has completed
-    for (uint32_t r = 0; r < P; ++r) {
-      MCK(cudaSetDevice(mg->dev[r]));
-      MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
-    }
-    err = 0.0;
-    l1 = 0.0;
-    for (uint32_t r = 0; r < P; ++r) {  // part order: deterministic
-      err = std::max(err, mg->hpairs[2 * r]);
-      l1 += mg->hpairs[2 * r + 1];
-    }
-    if (errors_out) {
-      if (errors_cap < it + 1)
-        return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: errors buffer holds " + std::to_string(errors_cap) +
-                                              " entries, need " + std::to_string(it + 1));
-      errors_out[it] = err;
-    }
-    if (l1_out && errors_cap >= it + 1) l1_out[it] = l1;
-    ++it;
-    cur = nxt;
-    stop = (mg->norm == FPR_B200_NORM_L1 ? l1 : err) <= cfg->threshold;
+    // one read per batch: device 0's gate (its stream has waited for every part)
+    if ((rc = fpr_b200_gate_read(mg->gate[0], mg->dev[0], fprb::graph_stream(mg->parts[0]), &it, &stopped, nullptr,
+                                 nullptr, 0)))
+      return rc;
   }
   MCK(cudaSetDevice(mg->dev[0]));
   MCK(cudaEventRecord(t1, fprb::graph_stream(mg->parts[0])));
   MCK(cudaEventSynchronize(t1));
+  for (uint32_t r = 0; r < P; ++r) {
+    MCK(cudaSetDevice(mg->dev[r]));
+    MCK(cudaStreamSynchronize(fprb::graph_stream(mg->parts[r])));
+  }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, t0, t1);
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
+  std::vector<double> errs(it), l1s(it);
+  if (it > 0 && (rc = fpr_b200_gate_read(mg->gate[0], mg->dev[0], fprb::graph_stream(mg->parts[0]), &it, &stopped,
+                                         errs.data(), l1s.data(), it)))
+    return rc;
+  if (it > mg->gate_cap && (errors_out || l1_out))
+    return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: trace longer than " + std::to_string(mg->gate_cap));
+  if (errors_out) {
+    if (errors_cap < it)
+      return set_error(FPR_B200_EINVAL, "fpr_b200_mgpu_run: errors buffer holds " + std::to_string(errors_cap) +
+                                            " entries, need " + std::to_string(it));
+    std::copy(errs.begin(), errs.end(), errors_out);
+  }
+  if (l1_out && errors_cap >= it) std::copy(l1s.begin(), l1s.end(), l1_out);
+  const double err = it > 0 ? errs[it - 1] : 1.0, l1 = it > 0 ? l1s[it - 1] : 1.0;
   if (ranks_out)
     for (uint32_t r = 0; r < P; ++r)
-      if ((rc = fpr_b200_part_ranks(mg->parts[r], ranks_out + mg->bounds[r]))) return rc;
+      if ((rc = fpr_b200_part_ranks_after(mg->parts[r], it, ranks_out + mg->bounds[r]))) return rc;
+  for (uint32_t r = 0; r < P; ++r) fpr_b200_part_set_gate(mg->parts[r], nullptr);
   if (result) {
     result->iterations = it;
     result->converged = (it > 0 && (mg->norm == FPR_B200_NORM_L1 ? l1 : err) <= cfg->threshold) ? 1 : 0;
@@ -303,7 +356,7 @@ int fpr_b200_mgpu_run(fpr_b200_mgpu* mg, int engine, const fpr_config* cfg, doub
     result->final_error = it > 0 ? err : 1.0;
     result->solve_ms = ms;  // device 0's stream: first sweep issued .. last residual read
     result->setup_ms = 0.0;
-    result->kernel_launches = it * P + P;
+    result->kernel_launches = issued * P * 2 + P;  // sweeps (no-ops after the stop included) + gate updates
   }
   return FPR_B200_OK;
 }

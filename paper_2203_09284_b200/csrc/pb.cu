@@ -482,7 +482,8 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 #endif
 __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(
     const int32_t* esrc, const int64_t* item_start, const uint32_t* item_len, const int64_t* item_ubase,
-    int64_t nitems, const double* prev, double* psum, unsigned long long* next_item) {
+    int64_t nitems, const double* prev, double* psum, unsigned long long* next_item, const unsigned int* gate) {
+  if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   const int lane = threadIdx.x & 31;
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -633,7 +634,9 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
     const int64_t* unit_e, const int64_t* unit_t, const int32_t* unit_k, const int32_t* unit_j,
     const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
     const int32_t* outdeg, const double* pr, double* pr_out, double* cur, PbPeers peers, double base,
-    double damping, double* slots, unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs) {
+    double damping, double* slots, unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs,
+    const unsigned int* gate) {
+  if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   constexpr int NW = kAccThreads / 32;
   constexpr int WE = 32 * kAccEpl;  // sorted places per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -931,7 +934,8 @@ __global__ void pb_bin_edges_kernel(const int64_t* row, int32_t n, int shift, in
 // contiguous run of bins in order, then a fixed shuffle/shared tree.
 constexpr int kReduceThreads = 1024;
 __global__ void __launch_bounds__(kReduceThreads) pb_reduce_kernel(int64_t nbins, const double* bin_pairs,
-                                                                   double* err, double* l1) {
+                                                                   double* err, double* l1, const unsigned int* gate) {
+  if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   const int64_t per = (nbins + kReduceThreads - 1) / kReduceThreads;
   const int64_t b0 = (int64_t)threadIdx.x * per, b1 = min(nbins, b0 + per);
   double mx = 0.0, sm = 0.0;
@@ -1323,7 +1327,7 @@ out:
 
 cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
                             const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
-                            double damping, double* err, double* l1, cudaStream_t st) {
+                            double damping, double* err, double* l1, cudaStream_t st, const unsigned int* gate) {
   const int W = plan.nwaves;
   // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
   cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
@@ -1339,7 +1343,7 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
       if (plan.item0[w + 1] > i0) {
         pb_gather_kernel<<<pb.p1_grid_overlap, kGatherThreads, 0, pb.aux>>>(
             pb.esrc, plan.item_start + i0, plan.item_len + i0, plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
-            pb.psum, plan.ctr + w);
+            pb.psum, plan.ctr + w, gate);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
       if ((e = cudaEventRecord(pb.ev[w], pb.aux)) != cudaSuccess) return e;
@@ -1348,10 +1352,10 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
           pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
           plan.unit_k + u0, plan.unit_j + u0,
           plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur, peers, base,
-          damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
+          damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs, gate);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1);
+    pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1, gate);
     return cudaGetLastError();
   }
   for (int w = 0; w < W; ++w) {
@@ -1359,17 +1363,17 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
     if (plan.item0[w + 1] > i0) {
       pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.esrc, plan.item_start + i0, plan.item_len + i0,
                                                               plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
-                                                              pb.psum, plan.ctr + w);
+                                                              pb.psum, plan.ctr + w, gate);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
         pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
         plan.unit_k + u0, plan.unit_j + u0,
         plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur,
-        peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs);
+        peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs, gate);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1);
+  pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1, gate);
   return cudaGetLastError();
 }
 

@@ -247,6 +247,7 @@ struct fpr_b200_graph {
   uint64_t part_sweeps = 0;       // part sweeps since fpr_b200_part_init
   double* part_pr[2] = {nullptr, nullptr};  // part ranks ping-pong ([0] = pr)
   int part_pr_cur = 0;                       // buffer holding the latest sweep
+  const unsigned int* gate = nullptr;        // device-side stop flag (fpr_b200_part_set_gate)
   double* ranks_tmp = nullptr;    // reordered ranks gathered back to caller order
   uint64_t n_global = 0, row_begin = 0, slice = 0;
 };
@@ -1562,7 +1563,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
       ++h->part_sweeps;
       CK(launch_pb_sweep(*h->pb, *plan, h->g, exch_read, h->part_pr[h->part_pr_cur], h->part_pr[h->part_pr_cur ^ 1],
                          exch_write + off, peers, (1.0 - cfg->damping) / (double)ng, cfg->damping, h->d_errors,
-                         h->d_l1, h->stream));
+                         h->d_l1, h->stream, h->gate));
       h->part_pr_cur ^= 1;
       CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
       CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
@@ -1619,6 +1620,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   // drivers rotate through 2, or 3 when speculating) peers are not sent it
   // again (SURVEY §8(e) exchange compaction).
   p.peer_skip_empty = h->part_sweeps >= 3 ? 1 : 0;
+  p.gate = h->gate;
   ++h->part_sweeps;
   for (uint32_t q = 0; q < npeer_bufs; ++q) {
     if (q == (uint32_t)h->part_id) continue;
@@ -1629,6 +1631,82 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
   h->part_pr_cur ^= 1;
   CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  return FPR_B200_OK;
+}
+
+// ---- device-side stop rule (include/fpr_b200.h fpr_b200_gate_*) ----
+uint64_t fpr_b200_gate_bytes(uint64_t trace_cap) { return sizeof(GateHdr) + 2 * trace_cap * sizeof(double); }
+
+int fpr_b200_gate_init(void* gate, uint64_t trace_cap, int device, void* stream) {
+  if (!gate) return fail(FPR_B200_EINVAL, "fpr_b200_gate_init: null gate");
+  CK(cudaSetDevice(device));
+  CK(launch_gate_init(static_cast<GateHdr*>(gate), trace_cap, static_cast<cudaStream_t>(stream)));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_gate_update(void* gate, const double* const* pairs, uint32_t npairs, const fpr_config* cfg, int norm,
+                         int device, void* stream) {
+  if (!gate || !pairs || !cfg) return fail(FPR_B200_EINVAL, "fpr_b200_gate_update: null argument");
+  if (npairs < 1 || npairs > (uint32_t)kMaxPeers + 1)
+    return fail(FPR_B200_EINVAL, "fpr_b200_gate_update: 1 to " + std::to_string(kMaxPeers + 1) + " residual pairs");
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  PairPtrs pp;
+  pp.n = (int)npairs;
+  for (uint32_t r = 0; r < npairs; ++r) {
+    if (!pairs[r]) return fail(FPR_B200_EINVAL, "fpr_b200_gate_update: null pair pointer");
+    pp.p[r] = pairs[r];
+  }
+  CK(cudaSetDevice(device));
+  CK(launch_gate_update(static_cast<GateHdr*>(gate), pp, cfg->threshold, norm, cfg->max_iterations,
+                        static_cast<cudaStream_t>(stream)));
+  return FPR_B200_OK;
+}
+
+int fpr_b200_gate_read(const void* gate, int device, void* stream, uint64_t* iterations, int* stopped,
+                       double* errors_out, double* l1_out, uint64_t cap) {
+  if (!gate) return fail(FPR_B200_EINVAL, "fpr_b200_gate_read: null gate");
+  CK(cudaSetDevice(device));
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GateHdr hdr{};
+  CK(cudaMemcpyAsync(&hdr, gate, sizeof(hdr), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (iterations) *iterations = hdr.iters;
+  if (stopped) *stopped = hdr.stop ? 1 : 0;
+  const uint64_t k = std::min<uint64_t>(hdr.iters, std::min<uint64_t>(hdr.cap, cap));
+  if ((errors_out || l1_out) && k > 0) {
+    std::vector<double> tr(2 * k);
+    CK(cudaMemcpyAsync(tr.data(), static_cast<const GateHdr*>(gate) + 1, 2 * k * sizeof(double),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < k; ++i) {
+      if (errors_out) errors_out[i] = tr[2 * i];
+      if (l1_out) l1_out[i] = tr[2 * i + 1];
+    }
+  }
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_set_gate(fpr_b200_graph* h, const void* gate) {
+  if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_part_set_gate: null graph");
+  h->gate = static_cast<const unsigned int*>(gate);  // GateHdr::stop is its first word
+  return FPR_B200_OK;
+}
+
+int fpr_b200_part_ranks_after(fpr_b200_graph* h, uint64_t sweeps, double* ranks_out) {
+  if (!h || !ranks_out) return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_after: null argument");
+  if (!h->part_pr[0]) return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_after: call fpr_b200_part_init first");
+  if (sweeps > h->part_sweeps)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_after: " + std::to_string(sweeps) + " sweeps requested, " +
+                                     std::to_string(h->part_sweeps) + " issued");
+  if (sweeps + 1 < h->part_sweeps && !h->gate)
+    return fail(FPR_B200_EINVAL, "fpr_b200_part_ranks_after: only the last two states are kept (no gate)");
+  CK(cudaSetDevice(h->device));
+  // part_init leaves the ranks in part_pr[0]; sweep k writes part_pr[k % 2];
+  // gated no-op sweeps write nothing
+  CK(cudaMemcpyAsync(ranks_out, h->part_pr[sweeps & 1], h->g.n * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   return FPR_B200_OK;
 }
 

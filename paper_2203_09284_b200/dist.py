@@ -141,6 +141,7 @@ class B200Part:
 
             stream = torch_stream_handle()
         self.nparts, self.part = nparts, part
+        self.device, self.stream = device, stream
         bounds = np.empty(nparts + 1, np.uint64)
         sl = C.c_uint64()
         h = C.c_void_p()
@@ -174,6 +175,7 @@ class B200Part:
                                       bounds.ctypes.data, C.byref(sl), C.byref(h)))
         self = cls.__new__(cls)
         self.nparts, self.part = nparts, part
+        self.device, self.stream = device, stream
         self.graph = DeviceGraph(h.value)
         self.bounds = bounds.astype(np.int64)
         self.slice = int(sl.value)
@@ -214,6 +216,51 @@ class B200Part:
         pinned = _pinned_f64(max(self.n_local, 1))
         _check(fn(self.graph._h, pinned.data_ptr()))
         return pinned.numpy()[: self.n_local].copy()
+
+    # -- device-side stop rule (fpr_b200_gate_*): no host round trip per iteration
+    def gate_create(self, cap: int):
+        """A gate (iteration count, stop flag, residual trace of `cap`
+        iterations) in this part's device memory."""
+        import torch
+
+        nbytes = int(lib().fpr_b200_gate_bytes(cap))
+        return {"buf": torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}"), "cap": cap}
+
+    def gate_init(self, gate) -> None:
+        _check(lib().fpr_b200_gate_init(gate["buf"].data_ptr(), gate["cap"], self.device, self.stream))
+
+    def set_gate(self, gate) -> None:
+        """Bind (or with None unbind) the gate: sweeps are no-ops once it stopped."""
+        _check(lib().fpr_b200_part_set_gate(self.graph._h, gate["buf"].data_ptr() if gate else None))
+
+    def gate_update(self, gate, pairs, cfg: PageRankConfig, norm: int) -> None:
+        """Enqueue the stop rule over the all-gathered pairs (2 x world doubles)."""
+        world = pairs.numel() // 2
+        base = pairs.data_ptr()
+        arr = (C.c_void_p * world)(*[base + 16 * r for r in range(world)])
+        c = cfg._c()
+        _check(lib().fpr_b200_gate_update(gate["buf"].data_ptr(), arr, world, C.byref(c), norm, self.device,
+                                          self.stream))
+
+    def gate_read(self, gate, trace: bool = False):
+        """(iterations, stopped, errors, l1_errors); waits for this part's stream."""
+        it, st = C.c_uint64(), C.c_int()
+        cap = gate["cap"] if trace else 0
+        errs, l1s = np.zeros(cap), np.zeros(cap)
+        _check(lib().fpr_b200_gate_read(gate["buf"].data_ptr(), self.device, self.stream, C.byref(it), C.byref(st),
+                                        errs.ctypes.data if trace else None, l1s.ctypes.data if trace else None,
+                                        cap))
+        k = min(it.value, cap)
+        return it.value, bool(st.value), errs[:k].tolist(), l1s[:k].tolist()
+
+    def ranks_after(self, sweeps: int, out: np.ndarray | None = None) -> np.ndarray:
+        """This part's ranks after sweep `sweeps` (later gated sweeps were no-ops)."""
+        if out is None:
+            pinned = _pinned_f64(max(self.n_local, 1))
+            _check(lib().fpr_b200_part_ranks_after(self.graph._h, sweeps, pinned.data_ptr()))
+            return pinned.numpy()[: self.n_local].copy()
+        _check(lib().fpr_b200_part_ranks_after(self.graph._h, sweeps, out.ctypes.data))
+        return out[: self.n_local]
 
     def close(self):
         self.graph.close()
@@ -306,14 +353,24 @@ class PartitionedSolver:
     Triple-buffered exchange vectors keep the extra sweep from touching
     anything iteration k needs; if k was the stopping iteration the part's
     ranks are read one sweep back (fpr_b200_part_ranks_prev), so results and
-    the iteration count are the non-speculative ones."""
+    the iteration count are the non-speculative ones.
+
+    device_stop=True: the stop rule runs on the device (a gate,
+    fpr_b200_gate_*).  Every iteration enqueues the sweep, the pair
+    all-gather and the gate update without reading anything back; the host
+    reads the gate once per `batch` iterations.  Sweeps issued after the
+    stopping iteration are no-ops, and the ranks are those after the stopping
+    sweep (fpr_b200_part_ranks_after), so the iteration count, trace and
+    ranks equal the host-driven loop's."""
 
     def __init__(self, local, exchange: TorchExchange, device="cuda", fused_exchange: bool = False,
-                 pairs_on_host: bool = False, speculate: bool = False):
+                 pairs_on_host: bool = False, speculate: bool = False, device_stop: bool = False,
+                 batch: int = 8):
         import torch
 
         self.local, self.exchange, self.pairs_on_host = local, exchange, pairs_on_host
-        self.speculate = speculate
+        self.speculate = speculate and not device_stop
+        self.device_stop, self.batch, self._gate = device_stop, max(1, int(batch)), None
         P, S = exchange.world, local.slice
         self.bufs = [torch.zeros(P * S, dtype=torch.float64, device=device) for _ in range(3 if speculate else 2)]
         self.pairs = [torch.zeros(2, dtype=torch.float64, device=device) for _ in range(2)]
@@ -367,10 +424,59 @@ class PartitionedSolver:
             ev.synchronize()
         return host.numpy()
 
+    def _solve_device_stop(self, engine: int, cfg: PageRankConfig, norm: int, want_ranks: bool,
+                           ranks_out: np.ndarray | None) -> PartResult:
+        local, exchange = self.local, self.exchange
+        max_it = int(cfg.max_iterations)
+        cap = min(max_it, 1 << 22)
+        if self._gate is None or self._gate["cap"] < cap:
+            self._gate = local.gate_create(cap)
+        gate = self._gate
+        local.init(self.bufs[0])
+        exchange.allgather_slices(self.bufs[0], local.slice)
+        local.gate_init(gate)
+        local.set_gate(gate)
+        res = PartResult(np.empty(0))
+        t0 = time.perf_counter()
+        try:
+            issued, stopped = 0, False
+            while not stopped and issued < max_it:
+                for _ in range(min(self.batch, max_it - issued)):
+                    nb = len(self.bufs)
+                    ri, wi = (issued % nb, (issued + 1) % nb) if engine == ENGINE_EC else (0, 0)
+                    read, write = self.bufs[ri], self.bufs[wi]
+                    pair = self.pairs[issued % 2]
+                    if self.reps is not None:
+                        local.sweep_peers(engine, cfg, read, write, self.reps.ptrs[wi], pair)
+                    else:
+                        local.sweep(engine, cfg, read, write, pair)
+                        exchange.allgather_slices(write, local.slice)
+                    # the pair all-gather is the barrier; the gate update reads
+                    # its result on the device, in rank order
+                    if self.pairs_on_host:  # gloo groups (tests): through host memory
+                        pairs = exchange.allgather_pairs(pair.cpu()).to(pair.device)
+                    else:
+                        pairs = exchange.allgather_pairs(pair)
+                    local.gate_update(gate, pairs, cfg, norm)
+                    issued += 1
+                _, stopped, _, _ = local.gate_read(gate)
+            it, stopped, errs, l1s = local.gate_read(gate, trace=True)
+            if want_ranks:  # while bound: the sweeps past `it` were no-ops
+                res.ranks = local.ranks_after(it, out=ranks_out)
+        finally:
+            local.set_gate(None)
+        res.iterations, res.errors, res.l1_errors = it, errs, l1s
+        res.iter_seconds = [(time.perf_counter() - t0) / max(it, 1)] * it
+        crit = l1s[-1] if norm == NORM_L1 else errs[-1]
+        res.converged = crit <= cfg.threshold
+        return res
+
     def solve(self, engine: int, cfg: PageRankConfig, norm: int = NORM_LINF,
               want_ranks: bool = True, ranks_out: np.ndarray | None = None) -> PartResult:
         if engine not in (ENGINE_EC, ENGINE_FUSED):
             raise ValueError("multi-GPU engines: EC or FUSED")
+        if self.device_stop:
+            return self._solve_device_stop(engine, cfg, norm, want_ranks, ranks_out)
         spec = self.speculate and engine == ENGINE_EC
         local, exchange = self.local, self.exchange
         local.init(self.bufs[0])
@@ -416,14 +522,15 @@ class PartitionedSolver:
 def solve_partitioned(local, exchange: TorchExchange, engine: int, cfg: PageRankConfig,
                       norm: int = NORM_LINF, device="cuda", want_ranks: bool = True,
                       fused_exchange: bool = False, pairs_on_host: bool = False,
-                      speculate: bool = False) -> PartResult:
+                      speculate: bool = False, device_stop: bool = False, batch: int = 8) -> PartResult:
     """Run `engine` to convergence on this rank's part (one process per GPU);
     a one-shot PartitionedSolver.  want_ranks=False leaves the part's ranks on
     the device (benchmarking).  fused_exchange=True replaces the per-iteration
     all-gather of contribution slices by the sweep's own P2P stores into the
     peers' replicas.  pairs_on_host moves the 16-B pair through host memory
-    (gloo groups)."""
-    s = PartitionedSolver(local, exchange, device, fused_exchange, pairs_on_host, speculate)
+    (gloo groups).  device_stop=True applies the stop rule on the device
+    (PartitionedSolver)."""
+    s = PartitionedSolver(local, exchange, device, fused_exchange, pairs_on_host, speculate, device_stop, batch)
     try:
         return s.solve(engine, cfg, norm, want_ranks)
     finally:

@@ -28,14 +28,19 @@ class NumpyPart:
         self.src = remap_sources(g.in_src[start[b0]:start[b1]], bounds, self.slice)
         self.outdeg = g.out_degree[b0:b1].astype(np.float64)
         self.pr = None
+        self.gate = None
+        self.hist = []
 
     def init(self, exch):
         self.pr = np.full(self.n_local, 1.0 / self.n_global)
+        self.hist = [self.pr]
         x = exch.numpy()
         off = self.part * self.slice
         x[off:off + self.n_local] = np.where(self.outdeg > 0, self.pr / np.maximum(self.outdeg, 1), 0.0)
 
     def sweep(self, engine, cfg, read, write, pair):
+        if self.gate is not None and self.gate["stop"]:
+            return  # gated: a stopped gate makes the sweep a no-op (fpr_b200_part_set_gate)
         rd, wr = read.numpy(), write.numpy()
         vals = rd[self.src]
         sums = np.zeros(self.n_local)
@@ -50,6 +55,37 @@ class NumpyPart:
         wr[off:off + self.n_local] = np.where(self.outdeg > 0, nv / np.maximum(self.outdeg, 1), 0.0)
         p = pair.numpy()
         p[0], p[1] = (d.max() if d.size else 0.0), d.sum()
+        self.hist.append(nv)
+
+    # the device-side stop rule's contract (fpr_b200_gate_*), restated
+    def gate_create(self, cap):
+        return {"cap": cap}
+
+    def gate_init(self, gate):
+        gate.update(stop=0, iters=0, errs=[], l1s=[])
+
+    def set_gate(self, gate):
+        self.gate = gate
+
+    def gate_update(self, gate, pairs, cfg, norm):
+        if gate["stop"]:
+            return
+        p = pairs.numpy()
+        err = max([0.0] + [float(p[2 * r]) for r in range(len(p) // 2)])
+        l1 = 0.0
+        for r in range(len(p) // 2):
+            l1 += float(p[2 * r + 1])
+        gate["errs"].append(err)
+        gate["l1s"].append(l1)
+        gate["iters"] += 1
+        if (l1 if norm else err) <= cfg.threshold or gate["iters"] >= cfg.max_iterations:
+            gate["stop"] = 1
+
+    def gate_read(self, gate, trace=False):
+        return gate["iters"], bool(gate["stop"]), list(gate["errs"]), list(gate["l1s"])
+
+    def ranks_after(self, sweeps, out=None):
+        return self.hist[sweeps]
 
     def ranks(self, back=0, out=None):
         r = self.prev if back else self.pr
@@ -59,7 +95,7 @@ class NumpyPart:
         return r
 
 
-def _worker(rank, world, port, engine, threshold, out_dir, speculate=False):
+def _worker(rank, world, port, engine, threshold, out_dir, speculate=False, batch=0):
     import torch.distributed as dist
 
     from oracle import Oracle
@@ -73,7 +109,7 @@ def _worker(rank, world, port, engine, threshold, out_dir, speculate=False):
     bounds = partition_bounds(g.in_start, world)
     local = NumpyPart(g, bounds, rank)
     res = solve_partitioned(local, TorchExchange(), engine, PageRankConfig(threshold=threshold),
-                            device="cpu", speculate=speculate)
+                            device="cpu", speculate=speculate, device_stop=batch > 0, batch=max(batch, 1))
     np.save(os.path.join(out_dir, f"r{rank}.npy"), res.ranks)
     np.save(os.path.join(out_dir, f"e{rank}.npy"), np.array(res.errors))
     dist.destroy_process_group()
@@ -85,8 +121,9 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _run(engine, threshold, tmp_path, speculate=False):
-    mp.spawn(_worker, args=(2, _free_port(), engine, threshold, str(tmp_path), speculate), nprocs=2, join=True)
+def _run(engine, threshold, tmp_path, speculate=False, batch=0):
+    mp.spawn(_worker, args=(2, _free_port(), engine, threshold, str(tmp_path), speculate, batch), nprocs=2,
+             join=True)
     ranks = np.concatenate([np.load(tmp_path / f"r{r}.npy") for r in range(2)])
     errs = [np.load(tmp_path / f"e{r}.npy") for r in range(2)]
     return ranks, errs
@@ -126,3 +163,18 @@ def test_gloo_fused_converges(oracle, tmp_path):
     xstar = oracle.pagerank_ec(g, threshold=1e-16, max_iterations=400).ranks
     assert errs[0][-1] <= 1e-10
     assert oracle.l1_norm(ranks, xstar) <= g.n * 1e-10 * 0.85 / 0.15
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_gloo_device_stop_matches_oracle(oracle, tmp_path, batch):
+    """Device-side stop (PartitionedSolver device_stop): batches of iterations
+    enqueued without a host read, the gate's rule applied after each pair
+    all-gather, sweeps past the stop no-ops, ranks after the stopping sweep.
+    Same iteration count, trace and ranks as the host-driven loop."""
+    ranks, errs = _run(ENGINE_EC, 1e-10, tmp_path, batch=batch)
+    n, s, d = oracle.generate_rmat(11, 16, seed=7)
+    ref = oracle.pagerank_ec(oracle.build_csr(n, s, d), threshold=1e-10)
+    assert len(errs[0]) == len(errs[1]) == ref.iterations
+    assert np.array_equal(errs[0], errs[1])
+    assert np.allclose(errs[0], ref.errors, rtol=0, atol=1e-15)  # numpy sums vs sequential: ~1e-17 apart
+    assert float(np.max(np.abs(ranks - ref.ranks) / ref.ranks)) <= 1e-12

@@ -91,6 +91,12 @@ def _ipc_worker(rank, world, port, path, q):
         cfg = fbw.PageRankConfig(threshold=1e-10)
         res = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, cfg, fused_exchange=True, pairs_on_host=True,
                                 speculate=True)
+        # the same with the stop rule on the device (batches of 3 iterations
+        # enqueued without a host read; sweeps past the stop are no-ops)
+        dres = solve_partitioned(part, HostGather(), fbw.ENGINE_EC, cfg, fused_exchange=True, pairs_on_host=True,
+                                 device_stop=True, batch=3)
+        assert dres.iterations == res.iterations and dres.errors == res.errors
+        assert np.array_equal(dres.ranks, res.ranks)
         # FusEd in place: peers' P2P stores land in the vector this rank is sweeping
         fres = solve_partitioned(part, HostGather(), fbw.ENGINE_FUSED, cfg, fused_exchange=True,
                                  pairs_on_host=True)

@@ -46,6 +46,24 @@ def test_mgpu_ec_matches_oracle(oracle, rmat16, P, pb, monkeypatch):
     assert fu.trace.converged and oracle.l1_norm(fu.ranks.values, xstar) <= g.n * T * 0.85 / 0.15
 
 
+@pytest.mark.parametrize("batch", ["1", "3", "64"])
+def test_mgpu_device_stop_batches(rmat16, batch, monkeypatch):
+    """The driver enqueues `batch` iterations between reads of the device-side
+    gate; sweeps issued past the stopping iteration are no-ops.  Any batch
+    gives the same iteration count, trace and rank bits."""
+    g, hg = rmat16
+    cfg = fb.PageRankConfig(threshold=T)
+    with fb.MultiDeviceGraph.from_graph(hg, [0, 0, 0]) as mg:
+        base = mg.run(fb.ENGINE_EC, cfg)
+        monkeypatch.setenv("FPR_B200_MGPU_BATCH", batch)
+        r = mg.run(fb.ENGINE_EC, cfg)
+        cap = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T, max_iterations=5))
+    assert r.trace.iterations == base.trace.iterations
+    assert np.array_equal(r.trace.errors, base.trace.errors)
+    assert np.array_equal(r.ranks.values, base.ranks.values)
+    assert cap.trace.iterations == 5 and not cap.trace.converged
+
+
 def test_mgpu_generate_equals_host_view(rmat16):
     """Every device generating the graph itself gives the same parts, the
     same iterations and the same bits as the parts uploaded from the host."""
