@@ -109,10 +109,14 @@ int finish(fpr_b200_mgpu* mg) {
   for (uint32_t r = 0; r < mg->P; ++r) {
     MCK(cudaSetDevice(mg->dev[r]));
     for (auto& v : mg->x) MCK(cudaMalloc(&v[r], (size_t)mg->P * mg->slice * sizeof(double)));
-    MCK(cudaMemset(mg->x[0][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
-    MCK(cudaMemset(mg->x[1][r], 0, (size_t)mg->P * mg->slice * sizeof(double)));
+    // on the part's own stream: the library's streams are non-blocking, so a
+    // legacy-stream cudaMemset could land after the first run's part_init
+    const cudaStream_t st = fprb::graph_stream(mg->parts[r]);
+    MCK(cudaMemsetAsync(mg->x[0][r], 0, (size_t)mg->P * mg->slice * sizeof(double), st));
+    MCK(cudaMemsetAsync(mg->x[1][r], 0, (size_t)mg->P * mg->slice * sizeof(double), st));
     MCK(cudaMalloc(&mg->dpair[r], 4 * sizeof(double)));
-    MCK(cudaMemset(mg->dpair[r], 0, 4 * sizeof(double)));
+    MCK(cudaMemsetAsync(mg->dpair[r], 0, 4 * sizeof(double), st));
+    MCK(cudaStreamSynchronize(st));
   }
   mg->gate.assign(mg->P, nullptr);
   for (auto& v : mg->ev) {

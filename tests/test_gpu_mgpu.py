@@ -109,7 +109,7 @@ def test_mgpu_argument_errors(rmat16):
             mg.run(fb.ENGINE_EC, fb.PageRankConfig(damping=1.5))
 
 
-@pytest.mark.parametrize("config,P", [("4", 2), ("4", 3), ("5", 2)])
+@pytest.mark.parametrize("config,P", [("4", 2), ("4", 3), ("4", 8), ("5", 2), ("5", 4), ("5", 8)])
 def test_mgpu_full_size_equals_single_gpu(config, P):
     """Configs 4/5 split into P destination-range parts on this one GPU, each
     part generating the graph on its device and running propagation-blocked
