@@ -268,9 +268,6 @@ struct PbSet {
   double* bin_pairs = nullptr;   // nbins x (max, sum) residual of each bin's rows, reduced in bin order
   unsigned int* bin_done = nullptr;  // nbins: units of a split bin finished this sweep
   int p1_grid = 0, p2_grid = 0, acc_smem = 0;
-  int p1_grid_overlap = 0, p2_grid_overlap = 0;  // EC waves overlapped on two streams
-  cudaStream_t aux = nullptr;                    // the gather passes of overlapped EC waves
-  std::vector<cudaEvent_t> ev;                   // per wave: gather done; [nwaves]: sweep start
   std::map<uint32_t, PbPlan> plans;  // by wave count
   std::vector<void*> allocs;
 };

@@ -986,12 +986,6 @@ int sm_count() {
 }  // namespace
 
 void free_pb(PbSet& pb, cudaStream_t st) {
-  if (pb.aux) {
-    cudaStreamSynchronize(pb.aux);
-    cudaStreamDestroy(pb.aux);
-  }
-  for (cudaEvent_t ev : pb.ev)
-    if (ev) cudaEventDestroy(ev);
   for (auto& kv : pb.plans)
     for (void* p : kv.second.allocs)
       if (p) cudaFreeAsync(p, st);
@@ -1305,13 +1299,6 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     pb.p2_grid = (int)std::min<int64_t>(nbins, (int64_t)sms * per_sm);
     pb.p1_grid = sms * 8;
     pb.acc_smem = (int)acc_smem;
-    // overlapped EC waves: one accumulate CTA + two gather CTAs per SM
-    // (registers: 512 x 64 + 2 x 256 x 48 < 64 K)
-    pb.p2_grid_overlap = (int)std::min<int64_t>(nbins, (int64_t)sms);
-    pb.p1_grid_overlap = sms * 2;
-    PK(cudaStreamCreateWithFlags(&pb.aux, cudaStreamNonBlocking));
-    pb.ev.assign(65, nullptr);
-    for (auto& ev : pb.ev) PK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   PK(cudaStreamSynchronize(st));
 out:
@@ -1332,32 +1319,6 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
   // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
   cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  if (prev != cur && W > 1 && pb.aux && (int)pb.ev.size() > W) {
-    // Jacobi waves are independent (all read prev, write cur), so wave w+1's
-    // gather pass (request-bound) runs on the side stream beside wave w's
-    // accumulate (stream-bound); grids sized so both fit on every SM
-    if ((e = cudaEventRecord(pb.ev[W], st)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(pb.aux, pb.ev[W], 0)) != cudaSuccess) return e;
-    for (int w = 0; w < W; ++w) {
-      const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
-      if (plan.item0[w + 1] > i0) {
-        pb_gather_kernel<<<pb.p1_grid_overlap, kGatherThreads, 0, pb.aux>>>(
-            pb.esrc, plan.item_start + i0, plan.item_len + i0, plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
-            pb.psum, plan.ctr + w, gate);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-      }
-      if ((e = cudaEventRecord(pb.ev[w], pb.aux)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, pb.ev[w], 0)) != cudaSuccess) return e;
-      pb_accum_kernel<<<pb.p2_grid_overlap, kAccThreads, pb.acc_smem, st>>>(
-          pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
-          plan.unit_k + u0, plan.unit_j + u0,
-          plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur, peers, base,
-          damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs, gate);
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1, gate);
-    return cudaGetLastError();
-  }
   for (int w = 0; w < W; ++w) {
     const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
     if (plan.item0[w + 1] > i0) {

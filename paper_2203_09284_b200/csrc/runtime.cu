@@ -523,9 +523,10 @@ void pb_geometry(int* shift, int* chunk_shift) {
 // all chunk windows and drains two launches, so fewer waves pay: one per
 // 128 M merge items, 2-8 (measured optima: config 4 4-8 waves, config 5 8;
 // DESIGN.md §3.4).
-// EC on propagation-blocked sweeps: waves overlapped on two streams (wave
-// w+1's gather beside wave w's accumulate, pb.cu launch_pb_sweep).
-// FPR_B200_PB_EC_WAVES overrides (1 = no overlap).
+// EC on propagation-blocked sweeps: one wave (every bin reads the previous
+// sweep's contributions).  FPR_B200_PB_EC_WAVES splits it for tests: the
+// waves run one after the other (round 1 overlapped them on two streams,
+// wave w+1's gather beside wave w's accumulate: slower).
 uint32_t pb_ec_waves(const fpr_b200_graph* h) {
   (void)h;
   uint32_t w = 1;
