@@ -57,7 +57,10 @@ namespace fprb {
 
 namespace {
 
-constexpr int kPbThreads = 1024;
+#ifndef FPR_PB_LAYOUT_THREADS
+#define FPR_PB_LAYOUT_THREADS 1024
+#endif
+constexpr int kPbThreads = FPR_PB_LAYOUT_THREADS;  // layout kernel CTA (several CTAs per SM when smaller)
 constexpr int64_t kSplitMaxChunks = 256;  // layout: multi-split fast path up to this many source chunks
 #ifndef FPR_PB_TSORT_BITS
 #define FPR_PB_TSORT_BITS 5  // tile sort radix digit: 14-bit keys in 3 passes
@@ -97,61 +100,146 @@ constexpr uint16_t kPadKey = 0xFFFF;  // row offset of a pad entry (bins hold < 
 #define FPR_PB_GATHER_L1 1
 #endif
 
-// One CTA per bin: histogram its edges by source chunk, scan, then a stable
-// scatter (tiles of the bin's CSR edges, block radix-sorted by chunk) so each
-// (bin, chunk) segment lists its entries in ascending row order.  The bin's
-// entries start at bin_pos[b]; its pad entries (up to bin_pos[b + 1]) get
-// source -1 and key kPadKey.  counts/start are chunk-major.
-__global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* row, const int32_t* src, int32_t n,
-                                                                int shift, int chunk_shift, int key_bits,
-                                                                int64_t nbins, int64_t nchunks,
-                                                                const int64_t* bin_pos, uint32_t* counts,
-                                                                int64_t* start, int32_t* src_bm, uint16_t* dstl_bm) {
-  using Sort = cub::BlockRadixSort<uint32_t, kPbThreads, 1, uint64_t>;
-  using ScanU = cub::BlockScan<uint32_t, kPbThreads>;
-  using ScanI = cub::BlockScan<int, kPbThreads>;
-  __shared__ union {
-    typename Sort::TempStorage sort;
-    typename ScanU::TempStorage scanu;
-    typename ScanI::TempStorage scani;
-  } tmp;
-  __shared__ uint32_t skey[kPbThreads];
-  extern __shared__ uint32_t h[];           // nchunks chunk counters, then
-  uint32_t* srow = h + ((nchunks + 3) & ~3ll);  // the bin's row offsets relative to its first edge
+// The layout works on PIECES of a bin's CSR edges (kLayoutPiece edges; a
+// bin's last piece is shorter, an empty bin is one empty piece), so that the
+// few bins holding the hub rows (config 5's first bin: ~70 M edges) spread
+// over many CTAs instead of one CTA walking them alone.
+constexpr int64_t kLayoutPiece = int64_t(1) << 18;
+
+__device__ __forceinline__ int64_t pb_bin_edge_end(const int64_t* row, int32_t n, int shift, int64_t b) {
+  return row[min((int64_t)n, (b + 1) << shift)];
+}
+
+// Pass 1: per piece, the histogram of its edges' source chunks (four loads in
+// flight per thread, one shared atomic per distinct chunk of a warp).
+__global__ void __launch_bounds__(kPbThreads) pb_piece_hist_kernel(const int64_t* row, const int32_t* src, int32_t n,
+                                                                    int shift, int chunk_shift, int64_t nchunks,
+                                                                    const int32_t* piece_bin, const int64_t* piece_e,
+                                                                    int64_t npieces, uint32_t* phist) {
+  extern __shared__ uint32_t h[];
   const int tid = threadIdx.x;
   const uint32_t sentinel = (uint32_t)nchunks;
-  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
-    for (int64_t c = tid; c < nchunks; c += blockDim.x) h[c] = 0;
-    const int64_t r0 = b << shift;
-    const int64_t r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
-    const int64_t e0 = row[r0], e1 = row[r1];
-    const int64_t p0 = bin_pos[b], p1 = bin_pos[b + 1];
-    for (int64_t q = p0 + (e1 - e0) + tid; q < p1; q += blockDim.x) {
-      src_bm[q] = -1;
-      dstl_bm[q] = kPadKey;
+  for (int64_t pc = blockIdx.x; pc < npieces; pc += gridDim.x) {
+    for (int64_t c = tid; c < nchunks; c += kPbThreads) h[c] = 0;
+    __syncthreads();
+    const int64_t b = piece_bin[pc], es = piece_e[pc];
+    const int64_t ee = (pc + 1 < npieces && piece_bin[pc + 1] == b) ? piece_e[pc + 1] : pb_bin_edge_end(row, n, shift, b);
+    for (int64_t eb = es; eb < ee; eb += 4 * (int64_t)kPbThreads) {
+      uint32_t c4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = eb + k * kPbThreads + tid;
+        c4[k] = e < ee ? ((uint32_t)__ldg(src + e) >> chunk_shift) : sentinel;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned peers = __match_any_sync(0xffffffffu, c4[k]);
+        if (c4[k] != sentinel && __ffs(peers) - 1 == (tid & 31)) atomicAdd(&h[c4[k]], (uint32_t)__popc(peers));
+      }
     }
-    for (int64_t r = r0 + tid; r <= r1; r += blockDim.x) srow[r - r0] = (uint32_t)(__ldg(row + r) - e0);
     __syncthreads();
-    for (int64_t e = e0 + tid; e < e1; e += blockDim.x) atomicAdd(&h[(uint32_t)__ldg(src + e) >> chunk_shift], 1u);
+    for (int64_t c = tid; c < nchunks; c += kPbThreads) phist[pc * nchunks + c] = h[c];
     __syncthreads();
+  }
+}
+
+// Pass 2, per bin: its segments' sizes and starts (chunk-major counts/start:
+// an exclusive scan over the chunks from the bin's 8-aligned position), and
+// each piece's starting cursor per chunk (the earlier pieces' counts added).
+__global__ void __launch_bounds__(kPbThreads) pb_bin_scan_kernel(const int64_t* bin_pos, int64_t nbins, int64_t nchunks,
+                                                                  const int64_t* bin_piece0, const uint32_t* phist,
+                                                                  uint32_t* counts, int64_t* start, uint32_t* pcur) {
+  using ScanU = cub::BlockScan<uint32_t, kPbThreads>;
+  __shared__ typename ScanU::TempStorage tmp;
+  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int64_t q0 = bin_piece0[b], q1 = bin_piece0[b + 1];
     uint32_t running = 0;
-    for (int64_t t0 = 0; t0 < nchunks; t0 += blockDim.x) {
-      const int64_t c = t0 + tid;
-      const uint32_t v = c < nchunks ? h[c] : 0u;
+    for (int64_t t0 = 0; t0 < nchunks; t0 += kPbThreads) {
+      const int64_t c = t0 + threadIdx.x;
+      uint32_t tot = 0;
+      if (c < nchunks)
+        for (int64_t pc = q0; pc < q1; ++pc) tot += phist[pc * nchunks + c];
       uint32_t x, tile;
-      ScanU(tmp.scanu).ExclusiveSum(v, x, tile);
+      ScanU(tmp).ExclusiveSum(tot, x, tile);
       if (c < nchunks) {
-        counts[c * nbins + b] = v;
-        start[c * nbins + b] = p0 + running + x;
-        h[c] = running + x;
+        counts[c * nbins + b] = tot;
+        start[c * nbins + b] = bin_pos[b] + running + x;
+        uint32_t cur = running + x;
+        for (int64_t pc = q0; pc < q1; ++pc) {
+          pcur[pc * nchunks + c] = cur;
+          cur += phist[pc * nchunks + c];
+        }
       }
       running += tile;
       __syncthreads();
     }
-    int rcur = -1;  // row holding the current CSR tile's first edge (carried across tiles)
+  }
+}
+
+// Pass 3, per piece: a stable scatter of the piece's edges (tiles of
+// kPbThreads CSR edges, multi-split by chunk) from each chunk's cursor, so
+// every (bin, chunk) segment lists its entries in CSR order (rows ascending,
+// a row's sources ascending) -- the pieces of a bin fill disjoint ranges of
+// each segment in piece order.  The bin's last piece also writes its pad
+// entries (source -1, key kPadKey, up to bin_pos[b + 1]).
+__global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* row, const int32_t* src, int32_t n,
+                                                                int shift, int chunk_shift, int key_bits,
+                                                                int64_t nchunks, const int64_t* bin_pos,
+                                                                const int32_t* piece_bin, const int64_t* piece_e,
+                                                                int64_t npieces, const uint32_t* pcur,
+                                                                int32_t* src_bm, uint16_t* dstl_bm) {
+  using Sort = cub::BlockRadixSort<uint32_t, kPbThreads, 1, uint64_t>;
+  using ScanI = cub::BlockScan<int, kPbThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename ScanI::TempStorage scani;
+  } tmp;
+  __shared__ uint32_t skey[kPbThreads];
+  __shared__ int s_rcur;
+  extern __shared__ uint32_t h[];           // nchunks chunk cursors, then
+  uint32_t* srow = h + ((nchunks + 3) & ~3ll);  // the bin's row offsets relative to its first edge
+  const int tid = threadIdx.x;
+  const uint32_t sentinel = (uint32_t)nchunks;
+  for (int64_t pc = blockIdx.x; pc < npieces; pc += gridDim.x) {
+    const int64_t b = piece_bin[pc];
+    const bool last = !(pc + 1 < npieces && piece_bin[pc + 1] == b);
+    const int64_t r0 = b << shift;
+    const int64_t r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
+    const int64_t e0 = row[r0], e1 = row[r1];
+    const int64_t es = piece_e[pc], ee = last ? e1 : piece_e[pc + 1];
+    const int64_t p0 = bin_pos[b];
+    if (last)
+      for (int64_t q = p0 + (e1 - e0) + tid; q < bin_pos[b + 1]; q += kPbThreads) {
+        src_bm[q] = -1;
+        dstl_bm[q] = kPadKey;
+      }
+    for (int64_t c = tid; c < nchunks; c += kPbThreads) h[c] = pcur[pc * nchunks + c];
     const int nrows = (int)(r1 - r0);
-    for (int64_t t = e0; t < e1; t += kPbThreads) {
+    for (int64_t r = r0 + tid; r <= r1; r += kPbThreads) srow[r - r0] = (uint32_t)(__ldg(row + r) - e0);
+    __syncthreads();
+    // the row holding the piece's first edge: the last row starting at or
+    // before it (-1 at a bin start: the tile's own marks find it)
+    if (tid == 0) {
+      int rc = -1;
+      if (es > e0) {
+        const uint32_t ps = (uint32_t)(es - e0);
+        int lo = 0, hi = nrows - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (srow[mid] <= ps) lo = mid;
+          else hi = mid - 1;
+        }
+        rc = lo;
+      }
+      s_rcur = rc;
+    }
+    __syncthreads();
+    int rcur = s_rcur;  // row holding the current CSR tile's first edge (carried across tiles)
+    uint32_t s_next = es + tid < ee ? (uint32_t)__ldg(src + es + tid) : 0u;  // prefetched one tile ahead
+    for (int64_t t = es; t < ee; t += kPbThreads) {
       const int64_t e = t + tid;
+      const uint32_t s_cur = s_next;
+      if (e + kPbThreads < ee) s_next = (uint32_t)__ldg(src + e + kPbThreads);
       // row of every edge of the tile: each row that starts inside the tile
       // marks its first position (empty rows share the next row's start, so
       // the max wins), then one block max-scan fills the positions between
@@ -179,8 +267,8 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
         // chunk's running cursor h[] -- no radix passes
         const int lane = tid & 31, warp = tid >> 5;
         uint32_t* wcnt = srow + (((int64_t)1 << min(shift, 20)) + 1);  // (nchunks + 1) x 32 counts
-        const uint32_t ck = e < e1 ? ((uint32_t)__ldg(src + e) >> chunk_shift) : sentinel;
-        const uint32_t sv = e < e1 ? (uint32_t)__ldg(src + e) : 0u;
+        const uint32_t ck = e < ee ? (s_cur >> chunk_shift) : sentinel;
+        const uint32_t sv = e < ee ? s_cur : 0u;
         for (int64_t i = tid; i < (nchunks + 1) * 32; i += kPbThreads) wcnt[i] = 0;
         __syncthreads();
         const unsigned peers = __match_any_sync(0xffffffffu, ck);
@@ -212,10 +300,10 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       }
       uint32_t key[1] = {sentinel};
       uint64_t val[1] = {0};
-      if (e < e1) {
-        const uint32_t s = (uint32_t)__ldg(src + e);
-        key[0] = s >> chunk_shift;
-        val[0] = ((uint64_t)s << 16) | (uint64_t)rowp;
+      if (e < ee) {
+        const uint32_t sx = s_cur;
+        key[0] = sx >> chunk_shift;
+        val[0] = ((uint64_t)sx << 16) | (uint64_t)rowp;
       }
       Sort(tmp.sort).Sort(key, val, 0, key_bits);
       __syncthreads();
@@ -233,6 +321,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
       if (real && (tid == kPbThreads - 1 || skey[tid + 1] != key[0])) h[key[0]] += (uint32_t)(tid - hs + 1);
       __syncthreads();
     }
+    __syncthreads();
   }
 }
 
@@ -1226,11 +1315,52 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   {
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
-    PK(cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem));
-    pb_layout_kernel<<<(unsigned)std::min<int64_t>(nbins, sms), kPbThreads, hist_smem, st>>>(
-        g.row, g.src, g.n, shift, chunk_shift, key_bits, nbins, nchunks, pb.bin_pos_d, pb.counts, pb.start,
-        pb.esrc, dstl);
-    PK(cudaGetLastError());
+    // pieces of every bin's edges (hub bins spread over many CTAs)
+    std::vector<int32_t> hb;
+    std::vector<int64_t> he, hp0(nbins + 1, 0);
+    for (int64_t b = 0; b < nbins; ++b) {
+      hp0[b] = (int64_t)hb.size();
+      const int64_t len = pb.bin_edge[b + 1] - pb.bin_edge[b];
+      const int64_t k = std::max<int64_t>(1, (len + kLayoutPiece - 1) / kLayoutPiece);
+      for (int64_t j = 0; j < k; ++j) {
+        hb.push_back((int32_t)b);
+        he.push_back(pb.bin_edge[b] + j * kLayoutPiece);
+      }
+    }
+    hp0[nbins] = (int64_t)hb.size();
+    const int64_t npc = (int64_t)hb.size();
+    int32_t* piece_bin = nullptr;
+    int64_t *piece_e = nullptr, *bin_piece0 = nullptr;
+    uint32_t *phist = nullptr, *pcur = nullptr;
+    e = cudaMallocAsync(&piece_bin, npc * sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&piece_e, npc * sizeof(int64_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&bin_piece0, (nbins + 1) * sizeof(int64_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&phist, npc * nchunks * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pcur, npc * nchunks * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(piece_bin, hb.data(), npc * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(piece_e, he.data(), npc * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(bin_piece0, hp0.data(), (nbins + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    const size_t hsm = ((size_t)(nchunks + 3) & ~(size_t)3) * sizeof(uint32_t);
+    if (e == cudaSuccess && hsm > 48 * 1024)
+      e = cudaFuncSetAttribute(pb_piece_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(pb_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_smem);
+    if (e == cudaSuccess) {
+      const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(npc, (int64_t)sms * 2));
+      pb_piece_hist_kernel<<<pgrid, kPbThreads, hsm, st>>>(g.row, g.src, g.n, shift, chunk_shift, nchunks, piece_bin,
+                                                           piece_e, npc, phist);
+      pb_bin_scan_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 2)), kPbThreads, 0,
+                           st>>>(pb.bin_pos_d, nbins, nchunks, bin_piece0, phist, pb.counts, pb.start, pcur);
+      pb_layout_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(npc, (int64_t)sms)), kPbThreads, hist_smem,
+                         st>>>(g.row, g.src, g.n, shift, chunk_shift, key_bits, nchunks, pb.bin_pos_d, piece_bin, piece_e,
+                               npc, pcur, pb.esrc, dstl);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host piece vectors die here
+    for (void* q : {(void*)piece_bin, (void*)piece_e, (void*)bin_piece0, (void*)phist, (void*)pcur})
+      if (q) cudaFreeAsync(q, st);
+    PK(e);
   }
   // runs per bin -> their 8-aligned positions and the accumulate's tiles
   PK(cudaMallocAsync(&bin_np, std::max<int64_t>(nbins, 1) * sizeof(int64_t), st));
