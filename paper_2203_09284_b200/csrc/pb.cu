@@ -1316,15 +1316,17 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
     int key_bits = 1;
     while ((1ll << key_bits) <= nchunks) ++key_bits;  // chunk ids and the sentinel nchunks
     // pieces of every bin's edges (hub bins spread over many CTAs)
+    int64_t lpiece = kLayoutPiece;
+    if (const char* v = std::getenv("FPR_B200_PB_LAYOUT_PIECE")) lpiece = std::max<int64_t>(1, std::atoll(v));  // tests
     std::vector<int32_t> hb;
     std::vector<int64_t> he, hp0(nbins + 1, 0);
     for (int64_t b = 0; b < nbins; ++b) {
       hp0[b] = (int64_t)hb.size();
       const int64_t len = pb.bin_edge[b + 1] - pb.bin_edge[b];
-      const int64_t k = std::max<int64_t>(1, (len + kLayoutPiece - 1) / kLayoutPiece);
+      const int64_t k = std::max<int64_t>(1, (len + lpiece - 1) / lpiece);
       for (int64_t j = 0; j < k; ++j) {
         hb.push_back((int32_t)b);
-        he.push_back(pb.bin_edge[b] + j * kLayoutPiece);
+        he.push_back(pb.bin_edge[b] + j * lpiece);
       }
     }
     hp0[nbins] = (int64_t)hb.size();

@@ -248,20 +248,25 @@ def test_pinned_upload_split(config1, share, monkeypatch):
             src[pos] = old
 
 
-@pytest.mark.parametrize("shift,chunk_shift,reorder,piece", [(13, 20, False, 0), (5, 4, False, 0),
-                                                             (9, 12, False, 0), (12, 10, True, 0), (7, 6, False, 0),
-                                                             (13, 20, False, 1000), (9, 12, True, 77)])
-def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piece, monkeypatch):
-    """FPR_B200_OPT_PB: propagation-blocked EC sweeps (gather pass into the
-    bin-major value stream + shared-memory bin accumulation) give the
-    reference's per-iteration ranks within 1e-12 relative and its iteration
-    count, from one bin/chunk to thousands of each, with whole bins and with
-    bins split into units finished by their last-arriving CTA."""
+@pytest.mark.parametrize("shift,chunk_shift,reorder,piece,lpiece",
+                         [(13, 20, False, 0, 0), (5, 4, False, 0, 0), (9, 12, False, 0, 0), (12, 10, True, 0, 0),
+                          (7, 6, False, 0, 0), (13, 20, False, 1000, 0), (9, 12, True, 77, 0),
+                          (13, 20, False, 0, 1000), (9, 12, False, 77, 333), (13, 16, False, 0, 1)])
+def test_pb_ec_matches_oracle(config1, oracle, shift, chunk_shift, reorder, piece, lpiece, monkeypatch):
+    """FPR_B200_OPT_PB: propagation-blocked EC sweeps (gather pass summing
+    each row's run into the bin-major partial-sum stream + shared-memory bin
+    accumulation) give the reference's per-iteration ranks within 1e-12
+    relative and its iteration count, from one bin/chunk to thousands of
+    each, with whole bins and with bins split into units finished by their
+    last-arriving CTA, and with the layout built from bins cut into pieces
+    of `lpiece` edges (pieces start mid-row; down to one edge per piece)."""
     rec, g, dg = config1
     monkeypatch.setenv("FPR_B200_PB_SHIFT", str(shift))
     monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", str(chunk_shift))
     if piece:  # heavy bins split into phase-2 units of about `piece` entries
         monkeypatch.setenv("FPR_B200_PB_PIECE", str(piece))
+    if lpiece:  # the layout's pieces (default 2^18 edges: only hub bins split)
+        monkeypatch.setenv("FPR_B200_PB_LAYOUT_PIECE", str(lpiece))
     ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
     with fb.DeviceGraph.from_graph(to_fb(g), pb=True, reorder=reorder) as d2:
         r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=1))
