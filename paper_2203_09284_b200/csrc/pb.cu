@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kPbThreads) pb_layout_kernel(const int64_t* ro
 // Row partial sums.  A segment lists its entries in row order, so the edges
 // of one row from one source chunk are neighbours: the gather pass sums them
 // as it fetches them and writes ONE partial sum per (segment, row) run
-// instead of one value per edge (R-MAT configs: ~0.25 values per edge).  An
+// instead of one value per edge (config 5: 0.137 partial sums per edge).  An
 // entry closes its run when it is the bin's last real entry, the next entry
 // starts another chunk or row, or it ends its piece (pieces are the gather
 // pass's work items: kPieceEntries entries from the segment's start, so no
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
 //     keys into a shared-memory stage with three TMA bulk copies completing
 //     on the stage's mbarrier, kStages tiles ahead;
 //   * lane L owns the sorted places [4L, 4L+4): it reads their keys and,
-//     through the inverse permutation, their values from the stage, folds
+//     through vidx, their partial sums from the stage, folds
 //     runs of equal rows in registers, and one segmented warp scan of the
 //     lane tails carries a run across lanes to the lane where it ends, so
 //     each run inside the warp is summed exactly once, in a fixed order.
@@ -713,7 +713,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 struct alignas(16) PbStage {
-  double v[kTile + 2];   // the tile's distinct values (from an even value index)
+  double v[kTile + 2];   // the tile's partial sums (staged from an even run number)
   uint16_t ip[kTile];    // stage index of each sorted place's value
   uint16_t k[kTile];     // row offset of each sorted place
 };
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
   uint32_t tc = 0;  // tiles this CTA consumed so far: stage tc % kStages, parity (tc / kStages) & 1
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  // tile meta = first value << 16 | values: the values are staged from the
+  // tile meta = first run << 16 | runs: the partial sums are staged from the
   // even index below the first (16-B aligned copy), rounded up to pairs
   auto issue = [&](uint32_t tile_no, uint64_t meta, int64_t t0, int len) {
     PbStage& st = stage[tile_no % kStages];

@@ -159,7 +159,7 @@ def test_one_step_parity_full_size(config, oracle):
     print(f"\nconfig{config}: n={og.n} m={og.m} EC {K} iterations, sweep {'pb' if sweep else 'pull'}")
 
 
-@pytest.mark.parametrize("config", ["2", "4", "5"])
+@pytest.mark.parametrize("config", ["2", "3", "4", "5"])
 def test_fused_within_tail_bound_full_size(config):
     """FusEd (the library's FUSED choice and the lockstep schedule) against x*,
     with the iteration counts beside EC's; on config 2 also the reference's
@@ -179,8 +179,10 @@ def test_fused_within_tail_bound_full_size(config):
     if config == "2":
         ref = load("config2.json")["runs"]["fused_seq@1e-10"]["iterations"]
         print(f"\nconfig2: reference fused_seq {ref} sweeps")
-    print(f"\nconfig{config}: EC {ec.trace.iterations}, FUSED {out[fb.ENGINE_FUSED].trace.iterations}, "
-          f"lockstep {out[fb.ENGINE_FUSED_LOCKSTEP].trace.iterations}")
+    l1s = {e: fb.l1_norm(r.ranks.values, xstar) for e, r in out.items()}
+    print(f"\nconfig{config}: EC {ec.trace.iterations}, FUSED {out[fb.ENGINE_FUSED].trace.iterations} "
+          f"(L1 to x* {l1s[fb.ENGINE_FUSED]:.2e}), lockstep {out[fb.ENGINE_FUSED_LOCKSTEP].trace.iterations} "
+          f"(L1 {l1s[fb.ENGINE_FUSED_LOCKSTEP]:.2e}); tail bound {bound:.2e}")
 
 
 @pytest.mark.parametrize("config", ["4", "5"])
