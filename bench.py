@@ -458,6 +458,23 @@ def main() -> None:
             pull = {"iterations": rp.trace.iterations, "time_to_converge_ms": rp.solve_ms,
                     "ms_per_sweep": rp.solve_ms / rp.trace.iterations,
                     "roofline_frac": algorithmic_bytes(n, m) / (rp.solve_ms / rp.trace.iterations * 1e-3) / 1e9 / peak}
+    # the opt-in renumbering by degree inside each source chunk
+    # (FPR_B200_OPT_REORDER_BLOCKS): faster sweeps, paid by a CSR rebuild at creation
+    reorder = None
+    if not args.no_large and args.workload == "5":
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with make_graph(fb, args.workload, local, stream=sptr, reorder="blocks") as dr:
+            torch.cuda.synchronize()
+            create_s = time.perf_counter() - t0
+            dr.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)  # the layout
+            re_ec = dr.run(fb.ENGINE_EC, cfg, copy_ranks=False, copy_trace=False)
+            re_fu = dr.run(fb.ENGINE_FUSED, cfg, copy_ranks=False, copy_trace=False)
+        reorder = {"option": "FPR_B200_OPT_REORDER_BLOCKS", "iterations": re_ec.trace.iterations,
+                   "time_to_converge_ms": re_ec.solve_ms, "ms_per_sweep": re_ec.solve_ms / re_ec.trace.iterations,
+                   "gteps": m * re_ec.trace.iterations / re_ec.solve_ms / 1e6,
+                   "fused_iterations": re_fu.trace.iterations, "fused_time_to_converge_ms": re_fu.solve_ms,
+                   "create_s_with_generation": create_s}
 
     g_host = None
     e2e = None
@@ -507,6 +524,7 @@ def main() -> None:
                      "kernel_shares": traffic.get("kernel_shares") if traffic else None},
         "fused": fused,
         "ec_pull_sweep": pull,
+        "ec_reorder_blocks": reorder,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "configs_2_4": large,

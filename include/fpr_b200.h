@@ -93,6 +93,15 @@ typedef struct fpr_config {
                                   order's locality; ranks and
                                   traces in the caller's ids.  OPT_REORDER wins if
                                   both are set */
+#define FPR_B200_OPT_REORDER_BLOCKS 32u /* renumber by descending out-degree inside
+                                  each block of 2^23 ids (the propagation-blocked
+                                  sweep's source chunk): a chunk's hub
+                                  contributions share cache lines, so more gathers
+                                  hit L1, while the chunks keep their edges and the
+                                  FusEd waves their order (for
+                                  repeated solves: the renumbering costs a CSR
+                                  rebuild at creation).  Ranks and traces in the
+                                  caller's ids; OPT_REORDER wins if both are set */
 /* Sweep kind.  By default the library picks it when the graph is created:
  * propagation-blocked sweeps (below) when the contribution vector (8 n bytes)
  * exceeds twice the device's L2 -- configs 4/5, where the pull gathers miss L2

@@ -44,6 +44,7 @@ OPT_PB = 4  # FPR_B200_OPT_PB: force propagation-blocked sweeps
 OPT_PULL = 16  # FPR_B200_OPT_PULL: force pull sweeps (default: the library picks, include/fpr_b200.h)
 SWEEP_PULL, SWEEP_PB = 0, 1  # fpr_b200_result.sweep
 OPT_REORDER_SOURCES = 8  # FPR_B200_OPT_REORDER_SOURCES
+OPT_REORDER_BLOCKS = 32  # FPR_B200_OPT_REORDER_BLOCKS
 
 
 class B200Error(RuntimeError):
@@ -313,9 +314,9 @@ def _options(device=-1, norm=NORM_LINF, wave_count=0, stream=None, reorder=False
     o.wave_count = wave_count
     # reorder: False, True / "degree" (FPR_B200_OPT_REORDER) or "sources"
     # (FPR_B200_OPT_REORDER_SOURCES)
-    if reorder not in (False, True, "degree", "sources"):
-        raise ValueError(f"reorder must be False, True, 'degree' or 'sources', not {reorder!r}")
-    ro = OPT_REORDER_SOURCES if reorder == "sources" else (OPT_REORDER if reorder else 0)
+    if reorder not in (False, True, "degree", "sources", "blocks"):
+        raise ValueError(f"reorder must be False, True, 'degree', 'sources' or 'blocks', not {reorder!r}")
+    ro = {"sources": OPT_REORDER_SOURCES, "blocks": OPT_REORDER_BLOCKS}.get(reorder, OPT_REORDER if reorder else 0)
     # pb: None = the library picks the sweep kind, True = propagation-blocked, False = pull
     o.flags = ro | (0 if pb is None else (OPT_PB if pb else OPT_PULL))
     o.stream = stream

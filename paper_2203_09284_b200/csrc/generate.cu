@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -692,18 +693,24 @@ cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_o
 // vector shrinks to them while the caller's (crawl) order is kept inside
 // each class.  Returns the new CSR in `out` and new_of_old (device, n int32)
 // in *perm.
-__global__ void degree_key_kernel(const int32_t* outdeg, int32_t n, bool sources_only, uint64_t* keys,
-                                  int32_t* ids) {
+// block_shift > 0: the order holds inside each block of 2^block_shift ids
+// (block, then the degree key, then the id inside the block: 62 bits).
+__global__ void degree_key_kernel(const int32_t* outdeg, int32_t n, bool sources_only, int block_shift,
+                                  uint64_t* keys, int32_t* ids) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t major = sources_only ? (outdeg[i] == 0 ? 1u : 0u) : (uint32_t)(INT32_MAX - outdeg[i]);
-    keys[i] = ((uint64_t)major << 32) | (uint32_t)i;
+    if (block_shift > 0)
+      keys[i] = ((uint64_t)(i >> block_shift) << 54) | ((uint64_t)major << block_shift) |
+                (uint64_t)(i & ((int64_t(1) << block_shift) - 1));
+    else
+      keys[i] = ((uint64_t)major << 32) | (uint32_t)i;
     ids[i] = (int32_t)i;
   }
 }
 
-cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, DevGraph& out, int32_t** perm, cudaStream_t st,
-                              const char** msg) {
+cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, int block_shift, DevGraph& out, int32_t** perm,
+                              cudaStream_t st, const char** msg) {
   *msg = nullptr;
   *perm = nullptr;
   cudaError_t e = cudaSuccess;
@@ -721,7 +728,7 @@ cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, DevGraph& ou
   GK(cudaMallocAsync(&i1, n * sizeof(int32_t), st));
   GK(cudaMallocAsync(&i2, n * sizeof(int32_t), st));
   GK(cudaMallocAsync(&p, n * sizeof(int32_t), st));
-  degree_key_kernel<<<blocks_for(n), 256, 0, st>>>(g.outdeg, n, sources_only, k1, i1);
+  degree_key_kernel<<<blocks_for(n), 256, 0, st>>>(g.outdeg, n, sources_only, block_shift, k1, i1);
   GK(cudaGetLastError());
   GK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, i1, i2, (int64_t)n, 0, 64, st));
   GK(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));

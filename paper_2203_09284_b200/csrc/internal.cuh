@@ -185,8 +185,8 @@ cudaError_t generate_draws(const GenRequest& req, uint64_t i0, uint64_t count, u
 // Locality reorder by descending out-degree, or (sources_only) the stable
 // partition with the out-degree > 0 vertices first: new CSR in `out`
 // (allocated on stream s), *perm = device new_of_old (n int32, caller frees).
-cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, DevGraph& out, int32_t** perm, cudaStream_t s,
-                              const char** msg);
+cudaError_t reorder_by_degree(const DevGraph& g, bool sources_only, int block_shift, DevGraph& out, int32_t** perm,
+                              cudaStream_t s, const char** msg);
 // BFS discovery order of g (config-3 relabel) into a host buffer of n int32.
 cudaError_t relabel_order_bfs(const DevGraph& g, int32_t root, int32_t* new_id_out,
                               cudaStream_t s, const char** msg);

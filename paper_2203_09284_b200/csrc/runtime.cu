@@ -365,6 +365,8 @@ int64_t source_space(const fpr_b200_graph* h) {
   return h->nparts > 1 ? (int64_t)h->nparts * (int64_t)h->slice : (int64_t)h->g.n;
 }
 
+void pb_geometry(int* shift, int* chunk_shift);
+
 bool pb_wanted(const fpr_b200_graph* h) {
   if (h->flags & FPR_B200_OPT_PULL) return false;
   if (h->flags & FPR_B200_OPT_PB) return true;
@@ -376,12 +378,17 @@ bool pb_wanted(const fpr_b200_graph* h) {
 }
 
 int finish_graph(fpr_b200_graph* h) {
-  if ((h->flags & (FPR_B200_OPT_REORDER | FPR_B200_OPT_REORDER_SOURCES)) && h->g.n > 1) {
+  if ((h->flags & (FPR_B200_OPT_REORDER | FPR_B200_OPT_REORDER_SOURCES | FPR_B200_OPT_REORDER_BLOCKS)) &&
+      h->g.n > 1) {
     DevGraph re;
     int32_t* perm = nullptr;
     const char* msg = nullptr;
-    const bool sources_only = !(h->flags & FPR_B200_OPT_REORDER);
-    CK(reorder_by_degree(h->g, sources_only, re, &perm, h->stream, &msg));
+    const bool by_degree = h->flags & (FPR_B200_OPT_REORDER | FPR_B200_OPT_REORDER_BLOCKS);
+    // degree order inside blocks of the PB source chunk (unless OPT_REORDER)
+    int shift = 0, chunk_shift = 0;
+    pb_geometry(&shift, &chunk_shift);
+    const int block_shift = (h->flags & FPR_B200_OPT_REORDER) ? 0 : std::max(1, std::min(chunk_shift, 23));
+    CK(reorder_by_degree(h->g, !by_degree, by_degree ? block_shift : 0, re, &perm, h->stream, &msg));
     if (msg) return fail(FPR_B200_ENOMEM, std::string("fpr_b200 reorder: ") + msg);
     h->allocs.push_back(re.row);
     h->allocs.push_back(re.src);
@@ -959,7 +966,7 @@ int fpr_b200_graph_download_csr(const fpr_b200_graph* hc, uint64_t* in_start, ui
   if (!h) return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: null graph");
   if (h->new_of_old)
     return fail(FPR_B200_EINVAL, "fpr_b200_graph_download_csr: graph was created with "
-                                 "FPR_B200_OPT_REORDER or OPT_REORDER_SOURCES (resident CSR uses internal ids)");
+                                 "FPR_B200_OPT_REORDER / _SOURCES / _BLOCKS (resident CSR uses internal ids)");
   CK(cudaSetDevice(h->device));
   const DevGraph& g = h->g;
   const int64_t chunk = 1 << 24;

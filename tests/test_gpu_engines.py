@@ -194,15 +194,19 @@ def test_upload_download_roundtrip(config1):
     np.testing.assert_array_equal(back.out_degree, g.out_degree)
 
 
-@pytest.mark.parametrize("reorder", [True, "sources"])
-def test_reorder_option_preserves_results(config1, oracle, reorder):
+@pytest.mark.parametrize("reorder,pb", [(True, None), ("sources", None), ("blocks", None), ("blocks", True),
+                                        (True, True)])
+def test_reorder_option_preserves_results(config1, oracle, reorder, pb, monkeypatch):
     """FPR_B200_OPT_REORDER renumbers vertices internally by out-degree,
-    FPR_B200_OPT_REORDER_SOURCES puts the vertices with out-edges first; EC
+    FPR_B200_OPT_REORDER_SOURCES puts the vertices with out-edges first,
+    FPR_B200_OPT_REORDER_BLOCKS orders by degree inside each source-chunk
+    block (small chunks here, so that the blocks matter); EC
     results come back in the caller's ids, per-iteration within 1e-12, with
     the same iteration count (Jacobi is relabel-invariant)."""
     rec, g, dg = config1
+    monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", "12")
     ref = oracle.pagerank_ec(g, threshold=1e-10, history_cap=3)
-    with fb.DeviceGraph.from_graph(to_fb(g), reorder=reorder) as d2:
+    with fb.DeviceGraph.from_graph(to_fb(g), reorder=reorder, pb=pb) as d2:
         r1 = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10, max_iterations=3))
         assert rel(r1.ranks.values, ref.history[2]) <= EC_RTOL
         r = d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
