@@ -262,6 +262,11 @@ struct PbSet {
   int64_t* start = nullptr;      // nchunks x nbins (chunk-major): first entry of segment (bin, chunk)
   uint32_t* seg_piece0 = nullptr;  // nchunks x nbins: the segment's first gather piece
   int64_t* pbase = nullptr;        // npieces: the first run of each piece
+  // hot sources: per chunk up to kHot frequent sources whose entries read a
+  // dense copy (hot_val[slot] = contribution of hot_src[slot], refreshed per wave)
+  int64_t nhot = 0;
+  int32_t* hot_src = nullptr;
+  double* hot_val = nullptr;
   std::vector<int64_t> bin_edge;  // nbins + 1: in-CSR edge offset of each bin's first row (waves)
   std::vector<int64_t> bin_pos;   // nbins + 1: 8-aligned entry position of each bin
   int64_t* bin_pos_d = nullptr;   // device copy

@@ -94,6 +94,9 @@ static_assert(kAccEpl == 4 || kAccEpl == 8, "kAccEpl is 4 or 8");
 
 static_assert(kTile <= 65536, "perm is uint16");
 constexpr uint16_t kPadKey = 0xFFFF;  // row offset of a pad entry (bins hold < 2^16 rows)
+// gather-pass source words: bit 31 closes a run, bit 30 marks a hot source
+// (the low 30 bits then name its slot in the dense hot copy)
+constexpr uint32_t kHotBit = 0x40000000u, kIdMask = 0x3FFFFFFFu;
 // phase 1 gathers: L1-allocating (default: hub sources recur across the bins a
 // CTA walks in one chunk, 4-6% faster on configs 4/5) or L2-only (0)
 #ifndef FPR_PB_GATHER_L1
@@ -408,7 +411,8 @@ __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, cons
                                                               int32_t n, int shift, const int64_t* bin_pos,
                                                               const int64_t* pbin_pos, const int64_t* start,
                                                               const uint32_t* seg_piece0, int64_t nbins,
-                                                              int chunk_shift, uint16_t* pkey, int64_t* pbase) {
+                                                              int chunk_shift, uint16_t* pkey, int64_t* pbase,
+                                                              const int32_t* hot_slot) {
   using Scan = cub::BlockScan<uint32_t, kAccThreads>;
   __shared__ typename Scan::TempStorage tmp;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
@@ -441,18 +445,28 @@ __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, cons
             ++k;
           }
         }
+        // the gather's word: close flag (bit 31); a hot source (bit 30) names
+        // its slot in the dense copy instead (the threads of this tile have
+        // all read their neighbours' sources: the scan above synchronised)
+        uint32_t ww[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          ww[j] = sv[j];
+          if (hot_slot && q + j < pe) {
+            const int32_t sl = __ldg(hot_slot + sv[j]);
+            if (sl >= 0) ww[j] = kHotBit | (uint32_t)sl;
+          }
+          ww[j] |= ((m >> j) & 1u) << 31;
+        }
         int4 w0, w1;
-        w0.x = (int)(sv[0] | (m << 31)), w0.y = (int)(sv[1] | ((m >> 1) << 31)), w0.z = (int)(sv[2] | ((m >> 2) << 31));
-        w0.w = (int)(sv[3] | ((m >> 3) << 31)), w1.x = (int)(sv[4] | ((m >> 4) << 31));
-        w1.y = (int)(sv[5] | ((m >> 5) << 31)), w1.z = (int)(sv[6] | ((m >> 6) << 31));
-        w1.w = (int)(sv[7] | ((m >> 7) << 31));
+        w0.x = (int)ww[0], w0.y = (int)ww[1], w0.z = (int)ww[2], w0.w = (int)ww[3];
+        w1.x = (int)ww[4], w1.y = (int)ww[5], w1.z = (int)ww[6], w1.w = (int)ww[7];
         // pads past pe keep their -1 (never read by the gather pass)
         if (q + 8 <= pe) {
           *reinterpret_cast<int4*>(src + q) = w0;
           *reinterpret_cast<int4*>(src + q + 4) = w1;
         } else {
-          const int ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-          for (int j = 0; j < 8 && q + j < pe; ++j) src[q + j] = ww[j];
+          for (int j = 0; j < 8 && q + j < pe; ++j) src[q + j] = (int32_t)ww[j];
         }
       }
       u += total;
@@ -569,9 +583,14 @@ __global__ void pb_piece_fill_kernel(const uint32_t* counts, const int64_t* star
 #ifndef FPR_PB_GATHER_MINB
 #define FPR_PB_GATHER_MINB 4
 #endif
+#ifndef FPR_PB_HOT
+#define FPR_PB_HOT 8192  // hot sources per chunk with a dense copy (0 = none)
+#endif
+constexpr int64_t kHot = FPR_PB_HOT;
 __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_kernel(
     const int32_t* esrc, const int64_t* item_start, const uint32_t* item_len, const int64_t* item_ubase,
-    int64_t nitems, const double* prev, double* psum, unsigned long long* next_item, const unsigned int* gate) {
+    int64_t nitems, const double* prev, const double* hot, double* psum, unsigned long long* next_item,
+    const unsigned int* gate) {
   if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   const int lane = threadIdx.x & 31;
   uint64_t pol;
@@ -603,7 +622,9 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
       for (int j = 0; j < 8; ++j) {
         v[j] = 0.0;
         if (okm >> j & 1u) {
-          const double* a = prev + (s[j] & 0x7FFFFFFF);
+          // a hot source (bit 30) is read from the dense per-sweep copy of its
+          // chunk's hot contributions: its L1 lines hold only hub values
+          const double* a = (s[j] & kHotBit) ? hot + (s[j] & kIdMask) : prev + (s[j] & kIdMask);
           v[j] = FPR_PB_GATHER_L1 ? __ldca(a) : __ldcg(a);
           if (s[j] < 0) clm |= 1u << j;
         }
@@ -658,6 +679,75 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
       }
       ub += total;
     }
+  }
+}
+
+// Hot sources (layout): each source's frequency among the entries, a
+// threshold per chunk so that about kc = min(kHot, chunk size) of its sources
+// reach it (and at least 2 entries each), and slots for up to kc of them;
+// their entries get bit 30 and the slot (chunk * kc + k) in place of the
+// source.  Any choice
+// is exact: a hot copy holds the same double as the vector.
+__global__ void pb_src_hist_kernel(const int32_t* esrc, int64_t mpad, uint32_t* cnt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < mpad; q += stride) {
+    const int32_t e = __ldg(esrc + q);
+    if (e != -1) atomicAdd(cnt + ((uint32_t)e & 0x7FFFFFFFu), 1u);
+  }
+}
+
+constexpr int kHotBins = 4096;
+__global__ void __launch_bounds__(1024) pb_hot_threshold_kernel(const uint32_t* cnt, int64_t nsrc, int chunk_shift,
+                                                                int64_t kc, uint32_t* thr) {
+  __shared__ uint32_t hist[kHotBins];
+  const int64_t c = blockIdx.x;
+  for (int i = threadIdx.x; i < kHotBins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int64_t s0 = c << chunk_shift, s1 = min(nsrc, (c + 1) << chunk_shift);
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    const uint32_t k = __ldg(cnt + s);
+    if (k >= 2) atomicAdd(&hist[min(k, (uint32_t)kHotBins - 1)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the smallest t >= 2 whose sources (count >= t) fit kc slots, else the top bin
+    uint32_t above = 0, t = kHotBins - 1;
+    for (int v = kHotBins - 1; v >= 2; --v) {
+      if (above + hist[v] > (uint32_t)kc) break;
+      above += hist[v];
+      t = (uint32_t)v;
+    }
+    thr[c] = t;
+  }
+}
+
+__global__ void pb_hot_assign_kernel(const uint32_t* cnt, int64_t nsrc, int chunk_shift, int64_t kc,
+                                     const uint32_t* thr, uint32_t* hot_n, int32_t* hot_slot, int32_t* hot_src) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsrc; s += stride) {
+    const int64_t c = s >> chunk_shift;
+    int32_t slot = -1;
+    if (__ldg(cnt + s) >= __ldg(thr + c)) {
+      const uint32_t k = atomicAdd(hot_n + c, 1u);
+      if (k < (uint32_t)kc) {
+        slot = (int32_t)(c * kc + k);
+        hot_src[slot] = (int32_t)s;
+      }
+    }
+    hot_slot[s] = slot;
+  }
+}
+
+// Per wave, before its gather pass: the dense copy of every hot source's
+// current contribution (in place for the lockstep schedule, so the copy sees
+// the earlier waves' updates, as the vector does).
+__global__ void pb_hot_refresh_kernel(const int32_t* hot_src, int64_t nslots, const double* prev, double* hot,
+                                      const unsigned int* gate) {
+  if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += stride) {
+    const int32_t s = __ldg(hot_src + i);
+    if (s >= 0) hot[i] = __ldcg(prev + s);
   }
 }
 
@@ -1270,6 +1360,7 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   uint16_t* pkey = nullptr;
   int64_t *tile_off_d = nullptr, *bin_np = nullptr, *pbin_pos_d = nullptr;
   uint32_t* seg_np = nullptr;
+  int32_t* hot_slot = nullptr;  // source -> hot slot (-1: cold), until the run-numbering pass
   void* scan_tmp = nullptr;
   const unsigned tgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 4));
   const unsigned sgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, (int64_t)sms * 32));
@@ -1404,9 +1495,41 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   }
   PK(alloc((void**)&pb.pbase, std::max<int64_t>(pb.npieces, 1) * sizeof(int64_t)));
   PK(cudaMallocAsync(&pkey, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t), st));
+  // hot sources per chunk, with a dense copy refreshed before every gather pass
+  if (kHot > 0 && nsrc <= (int64_t)kIdMask + 1 && g.m > 0) {
+    uint32_t *cnt = nullptr, *thr = nullptr, *hot_n = nullptr;
+    const int64_t kc = std::min<int64_t>(kHot, int64_t(1) << chunk_shift);  // slots per chunk
+    pb.nhot = nchunks * kc;
+    e = alloc((void**)&pb.hot_src, pb.nhot * sizeof(int32_t));
+    if (e == cudaSuccess) e = alloc((void**)&pb.hot_val, pb.nhot * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(pb.hot_src, 0xFF, pb.nhot * sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(pb.hot_val, 0, pb.nhot * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&cnt, nsrc * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&thr, nchunks * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&hot_n, nchunks * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&hot_slot, nsrc * sizeof(int32_t), st);
+    // a source's frequency among the entries is its out-degree on a whole
+    // graph; a multi-GPU part counts its own entries
+    const bool whole = nsrc == (int64_t)g.n;
+    if (e == cudaSuccess && whole)
+      e = cudaMemcpyAsync(cnt, g.outdeg, nsrc * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && !whole) e = cudaMemsetAsync(cnt, 0, nsrc * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(hot_n, 0, nchunks * sizeof(uint32_t), st);
+    if (e == cudaSuccess) {
+      const unsigned grid = (unsigned)sms * 8;
+      if (!whole) pb_src_hist_kernel<<<grid, 256, 0, st>>>(pb.esrc, pb.mpad, cnt);
+      pb_hot_threshold_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(cnt, nsrc, chunk_shift, kc, thr);
+      pb_hot_assign_kernel<<<grid, 256, 0, st>>>(cnt, nsrc, chunk_shift, kc, thr, hot_n, hot_slot, pb.hot_src);
+      e = cudaGetLastError();
+    }
+    for (void* q : {(void*)cnt, (void*)thr, (void*)hot_n})
+      if (q) cudaFreeAsync(q, st);
+    PK(e);
+  }
   pb_psum_kernel<<<tgrid, kAccThreads, 0, st>>>(pb.esrc, dstl, g.row, g.n, shift, pb.bin_pos_d, pbin_pos_d, pb.start,
-                                               pb.seg_piece0, nbins, chunk_shift, pkey, pb.pbase);
+                                               pb.seg_piece0, nbins, chunk_shift, pkey, pb.pbase, hot_slot);
   PK(cudaGetLastError());
+
   // the accumulate's side: per tile of runs, the row order
   PK(alloc((void**)&pb.vidx, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t)));
   PK(alloc((void**)&pb.skey, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t)));
@@ -1435,7 +1558,7 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   PK(cudaStreamSynchronize(st));
 out:
   for (void* q : {(void*)dstl, (void*)pkey, (void*)tile_off_d, (void*)bin_np, (void*)pbin_pos_d, (void*)seg_np,
-                  scan_tmp})
+                  (void*)hot_slot, scan_tmp})
     if (q) cudaFreeAsync(q, st);
   if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
@@ -1454,9 +1577,14 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
   for (int w = 0; w < W; ++w) {
     const int64_t i0 = plan.item0[w], u0 = plan.unit0[w];
     if (plan.item0[w + 1] > i0) {
+      if (pb.nhot > 0) {
+        pb_hot_refresh_kernel<<<(unsigned)std::min<int64_t>((pb.nhot + 255) / 256, (int64_t)pb.p1_grid), 256, 0,
+                                st>>>(pb.hot_src, pb.nhot, prev, pb.hot_val, gate);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      }
       pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.esrc, plan.item_start + i0, plan.item_len + i0,
                                                               plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
-                                                              pb.psum, plan.ctr + w, gate);
+                                                              pb.hot_val, pb.psum, plan.ctr + w, gate);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
