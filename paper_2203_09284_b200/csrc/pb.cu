@@ -399,6 +399,17 @@ __global__ void __launch_bounds__(kAccThreads) pb_close_count_kernel(const int32
   }
 }
 
+// The slot of source s (chunk * kc + rank) if it is hot, else -1.
+__device__ __forceinline__ int32_t pb_hot_slot(const uint32_t* bits, const uint32_t* wpre, uint32_t s,
+                                               int chunk_shift, int64_t kc) {
+  const uint32_t word = __ldg(bits + (s >> 5));
+  const uint32_t bit = 1u << (s & 31u);
+  if (!(word & bit)) return -1;
+  const uint32_t rank = __ldg(wpre + (s >> 5)) + (uint32_t)__popc(word & (bit - 1u));
+  if (rank >= (uint64_t)kc) return -1;
+  return (int32_t)((int64_t)(s >> chunk_shift) * kc + rank);
+}
+
 // Pass B, per bin (its runs numbered from pbin_pos[b], an 8-aligned position,
 // so that the accumulate's tile copies stay 16-B aligned):
 //   * closing entries get bit 31 of their source set (the gather's flag);
@@ -411,8 +422,7 @@ __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, cons
                                                               int32_t n, int shift, const int64_t* bin_pos,
                                                               const int64_t* pbin_pos, const int64_t* start,
                                                               const uint32_t* seg_piece0, int64_t nbins,
-                                                              int chunk_shift, uint16_t* pkey, int64_t* pbase,
-                                                              const int32_t* hot_slot) {
+                                                              int chunk_shift, uint16_t* pkey, int64_t* pbase) {
   using Scan = cub::BlockScan<uint32_t, kAccThreads>;
   __shared__ typename Scan::TempStorage tmp;
   for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
@@ -445,19 +455,12 @@ __global__ void __launch_bounds__(kAccThreads) pb_psum_kernel(int32_t* src, cons
             ++k;
           }
         }
-        // the gather's word: close flag (bit 31); a hot source (bit 30) names
-        // its slot in the dense copy instead (the threads of this tile have
-        // all read their neighbours' sources: the scan above synchronised)
+        // the gather's word: the source with the close flag in bit 31 (the
+        // threads of this tile have all read their neighbours' sources: the
+        // scan above synchronised)
         uint32_t ww[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          ww[j] = sv[j];
-          if (hot_slot && q + j < pe) {
-            const int32_t sl = __ldg(hot_slot + sv[j]);
-            if (sl >= 0) ww[j] = kHotBit | (uint32_t)sl;
-          }
-          ww[j] |= ((m >> j) & 1u) << 31;
-        }
+        for (int j = 0; j < 8; ++j) ww[j] = sv[j] | (((m >> j) & 1u) << 31);
         int4 w0, w1;
         w0.x = (int)ww[0], w0.y = (int)ww[1], w0.z = (int)ww[2], w0.w = (int)ww[3];
         w1.x = (int)ww[4], w1.y = (int)ww[5], w1.z = (int)ww[6], w1.w = (int)ww[7];
@@ -721,20 +724,71 @@ __global__ void __launch_bounds__(1024) pb_hot_threshold_kernel(const uint32_t* 
   }
 }
 
-__global__ void pb_hot_assign_kernel(const uint32_t* cnt, int64_t nsrc, int chunk_shift, int64_t kc,
-                                     const uint32_t* thr, uint32_t* hot_n, int32_t* hot_slot, int32_t* hot_src) {
+// The hot set as a bitmap (1 bit per source: 32 MB at config 5, L2-resident
+// while the run-numbering pass looks it up per entry) plus, per 32-bit word,
+// the hot sources before it in its chunk: a source's slot is its rank among
+// its chunk's hot sources (ascending ids), the first kc of them are hot.
+__global__ void pb_hot_bits_kernel(const uint32_t* cnt, int64_t nsrc, int chunk_shift, const uint32_t* thr,
+                                   uint32_t* bits) {
+  const int64_t nw = (nsrc + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw; w += wstride) {
+    const int64_t s = (w << 5) + lane;
+    const bool hot = s < nsrc && __ldg(cnt + s) >= __ldg(thr + (s >> chunk_shift));
+    const unsigned word = __ballot_sync(0xffffffffu, hot);
+    if (lane == 0) bits[w] = word;
+  }
+}
+
+// One CTA per chunk: exclusive prefix of the hot counts over the chunk's words.
+__global__ void __launch_bounds__(1024) pb_hot_rank_kernel(const uint32_t* bits, int64_t nsrc, int chunk_shift,
+                                                           uint32_t* wpre) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t w0 = ((int64_t)blockIdx.x << chunk_shift) >> 5;
+  const int64_t w1 = min((nsrc + 31) >> 5, (((int64_t)blockIdx.x + 1) << chunk_shift) >> 5);
+  uint32_t running = 0;
+  for (int64_t t = w0; t < w1; t += 1024) {
+    const int64_t w = t + threadIdx.x;
+    const uint32_t c = w < w1 ? (uint32_t)__popc(__ldg(bits + w)) : 0u;
+    uint32_t x, tot;
+    Scan(tmp).ExclusiveSum(c, x, tot);
+    if (w < w1) wpre[w] = running + x;
+    running += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void pb_hot_src_kernel(const uint32_t* bits, const uint32_t* wpre, int64_t nsrc, int chunk_shift,
+                                  int64_t kc, int32_t* hot_src) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsrc; s += stride) {
-    const int64_t c = s >> chunk_shift;
-    int32_t slot = -1;
-    if (__ldg(cnt + s) >= __ldg(thr + c)) {
-      const uint32_t k = atomicAdd(hot_n + c, 1u);
-      if (k < (uint32_t)kc) {
-        slot = (int32_t)(c * kc + k);
-        hot_src[slot] = (int32_t)s;
+    const int32_t sl = pb_hot_slot(bits, wpre, (uint32_t)s, chunk_shift, kc);
+    if (sl >= 0) hot_src[sl] = (int32_t)s;
+  }
+}
+
+// Entries of hot sources: bit 30 + the slot in place of the source (the
+// close flag kept); four words per thread, many lookups in flight.
+__global__ void pb_hot_rewrite_kernel(int32_t* esrc, int64_t mpad, const uint32_t* bits, const uint32_t* wpre,
+                                      int chunk_shift, int64_t kc) {
+  const int64_t n4 = mpad >> 2;  // mpad is a multiple of 8
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    int4 w = reinterpret_cast<const int4*>(esrc)[i];
+    int* x = &w.x;
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (x[j] == -1) continue;  // pad
+      const int32_t sl = pb_hot_slot(bits, wpre, (uint32_t)x[j] & 0x7FFFFFFFu, chunk_shift, kc);
+      if (sl >= 0) {
+        x[j] = (int32_t)(((uint32_t)x[j] & 0x80000000u) | kHotBit | (uint32_t)sl);
+        any = true;
       }
     }
-    hot_slot[s] = slot;
+    if (any) reinterpret_cast<int4*>(esrc)[i] = w;
   }
 }
 
@@ -1360,7 +1414,8 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   uint16_t* pkey = nullptr;
   int64_t *tile_off_d = nullptr, *bin_np = nullptr, *pbin_pos_d = nullptr;
   uint32_t* seg_np = nullptr;
-  int32_t* hot_slot = nullptr;  // source -> hot slot (-1: cold), until the run-numbering pass
+  uint32_t *hot_bits = nullptr, *hot_wpre = nullptr;  // hot-source bitmap + rank prefix (layout only)
+  int64_t hot_kc = 0;
   void* scan_tmp = nullptr;
   const unsigned tgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nbins, (int64_t)sms * 4));
   const unsigned sgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nseg + 255) / 256, (int64_t)sms * 32));
@@ -1496,39 +1551,46 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   PK(alloc((void**)&pb.pbase, std::max<int64_t>(pb.npieces, 1) * sizeof(int64_t)));
   PK(cudaMallocAsync(&pkey, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t), st));
   // hot sources per chunk, with a dense copy refreshed before every gather pass
-  if (kHot > 0 && nsrc <= (int64_t)kIdMask + 1 && g.m > 0) {
-    uint32_t *cnt = nullptr, *thr = nullptr, *hot_n = nullptr;
-    const int64_t kc = std::min<int64_t>(kHot, int64_t(1) << chunk_shift);  // slots per chunk
-    pb.nhot = nchunks * kc;
+  if (kHot > 0 && chunk_shift >= 5 && nsrc <= (int64_t)kIdMask + 1 && g.m > 0) {
+    uint32_t *cnt = nullptr, *thr = nullptr;
+    hot_kc = std::min<int64_t>(kHot, int64_t(1) << chunk_shift);  // slots per chunk
+    pb.nhot = nchunks * hot_kc;
+    const int64_t nw = (nsrc + 31) >> 5;
     e = alloc((void**)&pb.hot_src, pb.nhot * sizeof(int32_t));
     if (e == cudaSuccess) e = alloc((void**)&pb.hot_val, pb.nhot * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(pb.hot_src, 0xFF, pb.nhot * sizeof(int32_t), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(pb.hot_val, 0, pb.nhot * sizeof(double), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&cnt, nsrc * sizeof(uint32_t), st);
     if (e == cudaSuccess) e = cudaMallocAsync(&thr, nchunks * sizeof(uint32_t), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&hot_n, nchunks * sizeof(uint32_t), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&hot_slot, nsrc * sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&hot_bits, nw * sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&hot_wpre, nw * sizeof(uint32_t), st);
     // a source's frequency among the entries is its out-degree on a whole
     // graph; a multi-GPU part counts its own entries
     const bool whole = nsrc == (int64_t)g.n;
     if (e == cudaSuccess && whole)
       e = cudaMemcpyAsync(cnt, g.outdeg, nsrc * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess && !whole) e = cudaMemsetAsync(cnt, 0, nsrc * sizeof(uint32_t), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(hot_n, 0, nchunks * sizeof(uint32_t), st);
     if (e == cudaSuccess) {
       const unsigned grid = (unsigned)sms * 8;
       if (!whole) pb_src_hist_kernel<<<grid, 256, 0, st>>>(pb.esrc, pb.mpad, cnt);
-      pb_hot_threshold_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(cnt, nsrc, chunk_shift, kc, thr);
-      pb_hot_assign_kernel<<<grid, 256, 0, st>>>(cnt, nsrc, chunk_shift, kc, thr, hot_n, hot_slot, pb.hot_src);
+      pb_hot_threshold_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(cnt, nsrc, chunk_shift, hot_kc, thr);
+      pb_hot_bits_kernel<<<grid, 256, 0, st>>>(cnt, nsrc, chunk_shift, thr, hot_bits);
+      pb_hot_rank_kernel<<<(unsigned)nchunks, 1024, 0, st>>>(hot_bits, nsrc, chunk_shift, hot_wpre);
+      pb_hot_src_kernel<<<grid, 256, 0, st>>>(hot_bits, hot_wpre, nsrc, chunk_shift, hot_kc, pb.hot_src);
       e = cudaGetLastError();
     }
-    for (void* q : {(void*)cnt, (void*)thr, (void*)hot_n})
+    for (void* q : {(void*)cnt, (void*)thr})
       if (q) cudaFreeAsync(q, st);
     PK(e);
   }
   pb_psum_kernel<<<tgrid, kAccThreads, 0, st>>>(pb.esrc, dstl, g.row, g.n, shift, pb.bin_pos_d, pbin_pos_d, pb.start,
-                                               pb.seg_piece0, nbins, chunk_shift, pkey, pb.pbase, hot_slot);
+                                               pb.seg_piece0, nbins, chunk_shift, pkey, pb.pbase);
   PK(cudaGetLastError());
+  if (hot_bits) {
+    pb_hot_rewrite_kernel<<<(unsigned)sms * 8, 256, 0, st>>>(pb.esrc, pb.mpad, hot_bits, hot_wpre, chunk_shift,
+                                                             hot_kc);
+    PK(cudaGetLastError());
+  }
 
   // the accumulate's side: per tile of runs, the row order
   PK(alloc((void**)&pb.vidx, std::max<int64_t>(pb.nps, 1) * sizeof(uint16_t)));
@@ -1558,7 +1620,7 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   PK(cudaStreamSynchronize(st));
 out:
   for (void* q : {(void*)dstl, (void*)pkey, (void*)tile_off_d, (void*)bin_np, (void*)pbin_pos_d, (void*)seg_np,
-                  (void*)hot_slot, scan_tmp})
+                  (void*)hot_bits, (void*)hot_wpre, scan_tmp})
     if (q) cudaFreeAsync(q, st);
   if (e != cudaSuccess || *msg) {
     free_pb(pb, st);
