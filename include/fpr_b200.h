@@ -104,8 +104,8 @@ typedef struct fpr_config {
                                   caller's ids; OPT_REORDER wins if both are set */
 /* Sweep kind.  By default the library picks it when the graph is created:
  * propagation-blocked sweeps (below) when the contribution vector (8 n bytes)
- * exceeds twice the device's L2 -- configs 4/5, where the pull gathers miss L2
- * -- and the pull sweep otherwise.  The two flags force one kind. */
+ * exceeds half the device's L2 -- configs 3-5, where the pull gathers start
+ * missing L2 -- and the pull sweep otherwise.  The two flags force one kind. */
 #define FPR_B200_OPT_PB 4u      /* EC and lockstep engines: propagation-blocked sweeps
                                   (bins of 2^13 rows, source chunks of 2^23;
                                   FPR_B200_PB_SHIFT / FPR_B200_PB_CHUNK_SHIFT override):

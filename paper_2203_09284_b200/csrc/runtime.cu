@@ -355,10 +355,11 @@ constexpr int64_t kTraceWarps = 0;
 #endif
 
 // Sweep kind, fixed at creation: OPT_PULL / OPT_PB force it; by default
-// propagation blocking when the contribution vector (8 n bytes) exceeds twice
-// the L2 -- there the pull gathers miss L2 and each miss moves ~64 B of DRAM
-// for 8 useful bytes (configs 4/5: PB 2.1-2.2x faster per sweep), while on
-// L2-resident vectors (configs 1-3) the pull sweep wins.
+// propagation blocking when the contribution vector (8 n bytes) exceeds half
+// the L2 -- past it the pull gathers start missing L2 (each miss moves ~64 B
+// of DRAM for 8 useful bytes) and the run-sum PB sweep wins: config 3 (134 MB)
+// 1.04 vs 1.61 ms, configs 4/5 3x; on config 2 (33.5 MB, L2-resident) the
+// pull sweep wins, 0.32 vs 0.36 ms.
 // A multi-GPU part gathers from the whole exchange space (nparts x slice
 // contributions), so the rule uses that size.
 int64_t source_space(const fpr_b200_graph* h) {
@@ -374,7 +375,7 @@ bool pb_wanted(const fpr_b200_graph* h) {
   if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
   const int64_t bytes = source_space(h) * (int64_t)sizeof(double);
   if (const char* v = std::getenv("FPR_B200_PB_AUTO_BYTES")) return bytes > std::atoll(v);  // tests
-  return bytes > 2 * (int64_t)l2;
+  return bytes > (int64_t)l2 / 2;
 }
 
 int finish_graph(fpr_b200_graph* h) {
@@ -544,7 +545,7 @@ uint32_t pb_ec_waves(const fpr_b200_graph* h) {
 uint32_t lockstep_waves(const fpr_b200_graph* h) {
   if (h->wave_count) return h->wave_count;
   const int64_t items = (int64_t)h->g.n + h->g.m;
-  if (h->use_pb) return (uint32_t)std::min<int64_t>(8, std::max<int64_t>(2, items >> 27));
+  if (h->use_pb) return (uint32_t)std::min<int64_t>(8, std::max<int64_t>(2, items >> 26));
   return (uint32_t)std::min<int64_t>(32, std::max<int64_t>(2, items >> 25));
 }
 
