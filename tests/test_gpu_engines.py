@@ -346,9 +346,17 @@ def test_sweep_kind_auto_and_forced(config1, oracle, monkeypatch):
     assert r.sweep == fb.SWEEP_PULL
     monkeypatch.setenv("FPR_B200_PB_AUTO_BYTES", "1024")
     with fb.DeviceGraph.from_graph(to_fb(g)) as d, fb.DeviceGraph.from_graph(to_fb(g), pb=False) as dp:
+        before = d.layout_info()
         ra, rp = d.run(fb.ENGINE_EC, cfg), dp.run(fb.ENGINE_EC, cfg)
         fa = d.run(fb.ENGINE_FUSED, cfg)
+        after, pull = d.layout_info(), dp.layout_info()
     assert ra.sweep == fb.SWEEP_PB and fa.sweep == fb.SWEEP_PB and rp.sweep == fb.SWEEP_PULL
+    # fpr_b200_graph_layout_info: the PB layout exists after the first PB run;
+    # one partial sum per run: at most one per entry (+ up to 7 pad places per bin)
+    assert before["sweep"] == fb.SWEEP_PB and before["runs"] == 0
+    assert after["runs"] > 0 and after["pieces"] > 0 and after["tiles"] > 0
+    assert after["runs"] <= g.m + 8 * (g.n // 8192 + 1)
+    assert pull["sweep"] == fb.SWEEP_PULL and pull["runs"] == 0
     for x in (ra, rp):
         assert x.trace.iterations == ref.iterations
         assert rel(x.ranks.values, ref.ranks) <= EC_RTOL
