@@ -596,6 +596,7 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
     const unsigned int* gate) {
   if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   const int lane = threadIdx.x & 31;
+  const int32_t idmask = hot ? (int32_t)kIdMask : 0x7FFFFFFF;
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   for (;;) {
@@ -626,8 +627,9 @@ __global__ void __launch_bounds__(kGatherThreads, FPR_PB_GATHER_MINB) pb_gather_
         v[j] = 0.0;
         if (okm >> j & 1u) {
           // a hot source (bit 30) is read from the dense per-sweep copy of its
-          // chunk's hot contributions: its L1 lines hold only hub values
-          const double* a = (s[j] & kHotBit) ? hot + (s[j] & kIdMask) : prev + (s[j] & kIdMask);
+          // chunk's hot contributions: its L1 lines hold only hub values.
+          // Without a hot copy (source spaces past 2^30) bit 30 is an id bit.
+          const double* a = (hot && (s[j] & kHotBit)) ? hot + (s[j] & kIdMask) : prev + (s[j] & idmask);
           v[j] = FPR_PB_GATHER_L1 ? __ldca(a) : __ldcg(a);
           if (s[j] < 0) clm |= 1u << j;
         }
@@ -1646,7 +1648,8 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
       }
       pb_gather_kernel<<<pb.p1_grid, kGatherThreads, 0, st>>>(pb.esrc, plan.item_start + i0, plan.item_len + i0,
                                                               plan.item_ubase + i0, plan.item0[w + 1] - i0, prev,
-                                                              pb.hot_val, pb.psum, plan.ctr + w, gate);
+                                                              pb.nhot > 0 ? pb.hot_val : nullptr, pb.psum,
+                                                              plan.ctr + w, gate);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     pb_accum_kernel<<<pb.p2_grid, kAccThreads, pb.acc_smem, st>>>(
