@@ -81,3 +81,38 @@ def test_from_edges_length_mismatch_and_range():
         fb.DeviceGraph.from_edges(3, [0, 1], [1])
     with pytest.raises(ValueError, match="n >= 2"):
         fb.DeviceGraph.from_edges(1 << 31, [0], [1])
+
+
+def test_gate_misuse():
+    """Device-side stop rule (fpr_b200_gate_*, fpr_b200_part_ranks_after):
+    null gates, pair counts outside 1..8 and sweeps beyond those issued are
+    EINVAL; a gate reads back 0 iterations after init."""
+    import torch
+
+    L = fb.lib()
+    cfg = fb.PageRankConfig()._c()
+    assert L.fpr_b200_gate_init(None, 4, 0, None) == fb.EINVAL
+    gate = torch.zeros(int(L.fpr_b200_gate_bytes(4)), dtype=torch.uint8, device="cuda")
+    assert L.fpr_b200_gate_init(gate.data_ptr(), 4, 0, None) == fb.OK
+    pairs = torch.zeros(18, dtype=torch.float64, device="cuda")
+    arr = (C.c_void_p * 9)(*[pairs.data_ptr() + 16 * r for r in range(9)])
+    assert L.fpr_b200_gate_update(gate.data_ptr(), arr, 0, C.byref(cfg), 0, 0, None) == fb.EINVAL
+    assert L.fpr_b200_gate_update(gate.data_ptr(), arr, 9, C.byref(cfg), 0, 0, None) == fb.EINVAL
+    it, st = C.c_uint64(7), C.c_int(7)
+    assert L.fpr_b200_gate_read(gate.data_ptr(), 0, None, C.byref(it), C.byref(st), None, None, 0) == fb.OK
+    assert it.value == 0 and st.value == 0
+    # one update with a zero residual: the rule holds, the gate stops and stays stopped
+    assert L.fpr_b200_gate_update(gate.data_ptr(), arr, 2, C.byref(cfg), 0, 0, None) == fb.OK
+    assert L.fpr_b200_gate_update(gate.data_ptr(), arr, 2, C.byref(cfg), 0, 0, None) == fb.OK
+    assert L.fpr_b200_gate_read(gate.data_ptr(), 0, None, C.byref(it), C.byref(st), None, None, 0) == fb.OK
+    assert it.value == 1 and st.value == 1
+    with fb.DeviceGraph.from_graph(_small()) as full:
+        part = B200Part(full, 1, 0)
+        out = np.empty(part.n_local)
+        assert L.fpr_b200_part_ranks_after(part.graph._h, 0, out.ctypes.data) == fb.EINVAL  # before part_init
+        ex = torch.zeros(part.slice, dtype=torch.float64, device="cuda")
+        part.init(ex)
+        assert L.fpr_b200_part_ranks_after(part.graph._h, 1, out.ctypes.data) == fb.EINVAL  # none issued
+        assert L.fpr_b200_part_ranks_after(part.graph._h, 0, out.ctypes.data) == fb.OK
+        assert np.allclose(out, 1.0 / 5)
+        part.close()
