@@ -371,3 +371,40 @@ def test_pb_rejects_bad_geometry(config1, monkeypatch):
     with fb.DeviceGraph.from_graph(to_fb(g), pb=True) as d2:
         with pytest.raises(ValueError, match="propagation-blocked"):
             d2.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+
+
+def test_pb_random_geometries(oracle, monkeypatch):
+    """Randomised propagation-blocked layouts against the oracle: R-MAT and
+    uniform graphs of random size and degree, random bin / chunk shifts,
+    layout pieces, accumulate units and wave counts (hot copy on and off:
+    chunks below 32 sources have none).  EC: the reference's iteration count
+    and ranks within 1e-12; lockstep: converged; reruns bit-equal."""
+    import os
+
+    rng = np.random.default_rng(int(os.environ.get("FPR_TEST_SEED", "2026")))
+    for case in range(int(os.environ.get("FPR_TEST_CASES", "16"))):
+        if case % 2:
+            n, s, d = oracle.generate_rmat(int(rng.integers(5, 15)), int(rng.integers(1, 24)),
+                                           seed=int(rng.integers(1 << 30)))
+        else:
+            n0 = int(rng.integers(1, 40000))
+            n, s, d = oracle.random_sparse(n0, int(rng.integers(1, 20)), int(rng.integers(1 << 30)))
+        g = oracle.build_csr(n, s, d)
+        if g.n == 0:
+            continue
+        env = {"FPR_B200_PB_SHIFT": str(int(rng.integers(5, 14))),
+               "FPR_B200_PB_CHUNK_SHIFT": str(int(rng.integers(3, 16))),
+               "FPR_B200_PB_LAYOUT_PIECE": str(int(rng.choice([1, 17, 500, 1 << 18]))),
+               "FPR_B200_PB_PIECE": str(int(rng.choice([32, 300, 1 << 16])))}
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ref = oracle.pagerank_ec(g, threshold=1e-10)
+        with fb.DeviceGraph.from_graph(to_fb(g), pb=True, wave_count=int(rng.integers(0, 9))) as dg:
+            r = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+            r2 = dg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=1e-10))
+            lk = dg.run(fb.ENGINE_FUSED_LOCKSTEP, fb.PageRankConfig(threshold=1e-10))
+        assert r.sweep == fb.SWEEP_PB, (case, env)
+        assert r.trace.iterations == ref.iterations, (case, env)
+        assert rel(r.ranks.values, ref.ranks) <= EC_RTOL, (case, env)
+        assert np.array_equal(r.ranks.values.view(np.uint64), r2.ranks.values.view(np.uint64)), (case, env)
+        assert lk.trace.converged, (case, env)

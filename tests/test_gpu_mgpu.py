@@ -137,3 +137,31 @@ def test_mgpu_full_size_equals_single_gpu(config, P):
     assert float(np.max(np.abs(r.ranks.values - ref.ranks.values) / ref.ranks.values)) <= 1e-12
     print(f"\nconfig{config} x{P} parts: {r.trace.iterations} iterations, {r.solve_ms:.0f} ms "
           f"(one GPU, parts in turn; single-part {ref.solve_ms:.0f} ms)")
+
+
+def test_mgpu_random_parts(oracle, monkeypatch):
+    """Randomised multi-part solves on one GPU: random graphs, 2-6 parts,
+    pull or propagation-blocked parts with random geometries, random batch
+    sizes of the device-side stop.  EC equals the oracle (iterations, 1e-12)."""
+    import os
+
+    rng = np.random.default_rng(int(os.environ.get("FPR_TEST_SEED", "7")))
+    for case in range(int(os.environ.get("FPR_TEST_CASES", "8"))):
+        if case % 2:
+            n, s, d = oracle.generate_rmat(int(rng.integers(6, 14)), int(rng.integers(2, 20)),
+                                           seed=int(rng.integers(1 << 30)))
+        else:
+            n, s, d = oracle.random_sparse(int(rng.integers(50, 30000)), int(rng.integers(1, 16)),
+                                           int(rng.integers(1 << 30)))
+        g = oracle.build_csr(n, s, d)
+        P = int(rng.integers(2, 7))
+        pb = bool(rng.integers(0, 2))
+        monkeypatch.setenv("FPR_B200_PB_SHIFT", str(int(rng.integers(5, 14))))
+        monkeypatch.setenv("FPR_B200_PB_CHUNK_SHIFT", str(int(rng.integers(4, 16))))
+        monkeypatch.setenv("FPR_B200_MGPU_BATCH", str(int(rng.integers(1, 12))))
+        ref = oracle.pagerank_ec(g, threshold=T)
+        hg = fb.Graph(g.n, g.m, g.in_start, g.in_src, g.out_degree)
+        with fb.MultiDeviceGraph.from_graph(hg, [0] * P, pb=pb) as mg:
+            r = mg.run(fb.ENGINE_EC, fb.PageRankConfig(threshold=T))
+        assert r.trace.iterations == ref.iterations, (case, P, pb)
+        assert float(np.max(np.abs(r.ranks.values - ref.ranks) / ref.ranks)) <= 1e-12, (case, P, pb)
