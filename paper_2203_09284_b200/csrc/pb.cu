@@ -44,6 +44,15 @@
 // within 1e-12 per iteration of the reference (tests/test_gpu_engines.py
 // test_pb_*, tests/test_gpu_fullsize.py).  Measurements and rejected
 // variants: DESIGN.md §3.4.
+//
+// Kernels, in the order they run:
+//   layout  pb_piece_hist_kernel, pb_bin_scan_kernel, pb_layout_kernel
+//           (segments), pb_close_count_kernel, pb_psum_kernel (runs),
+//           pb_hot_threshold/bits/rank/src/rewrite_kernel (hot copy),
+//           pb_tile_sort_kernel (accumulate tiles); per wave count:
+//           pb_piece_count/fill_kernel (gather plan);
+//   sweep   pb_hot_refresh_kernel, pb_gather_kernel, pb_accum_kernel per
+//           wave, then pb_reduce_kernel.
 #include <cub/cub.cuh>
 
 #include <algorithm>
