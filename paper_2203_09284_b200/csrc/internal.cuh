@@ -264,6 +264,8 @@ struct PbSet {
   int64_t* pbase = nullptr;        // npieces: the first run of each piece
   // hot sources: per chunk up to kHot frequent sources whose entries read a
   // dense copy (hot_val[slot] = contribution of hot_src[slot], refreshed per wave)
+  uint16_t* live_rows = nullptr;  // nbins << shift: per bin, its rows with in-edges (offsets)
+  int32_t* live_cnt = nullptr;    // nbins
   int64_t nhot = 0;
   int32_t* hot_src = nullptr;
   double* hot_val = nullptr;
@@ -303,7 +305,7 @@ cudaError_t get_pb_plan(PbSet& pb, uint32_t S, cudaStream_t st, const PbPlan** o
 cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
                             const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
                             double damping, double* err, double* l1, cudaStream_t st,
-                            const unsigned int* gate = nullptr);
+                            const unsigned int* gate = nullptr, bool skip_empty = false);
 
 // runtime.cu hooks for mgpu.cu (the multi-device driver over the part API)
 int set_error(int code, const std::string& msg);  // thread-local last error; returns code

@@ -816,6 +816,28 @@ __global__ void pb_hot_refresh_kernel(const int32_t* hot_src, int64_t nslots, co
   }
 }
 
+// Per bin, its rows with in-edges (row offsets, ascending) for the
+// accumulate's finalize once rows without in-edges are settled.
+__global__ void __launch_bounds__(1024) pb_live_rows_kernel(const int64_t* row, int32_t n, int shift, int64_t nbins,
+                                                            uint16_t* live_rows, int32_t* live_cnt) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  for (int64_t b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int64_t r0 = b << shift, r1 = min((int64_t)n, r0 + ((int64_t)1 << shift));
+    int base = 0;
+    for (int64_t t = r0; t < r1; t += 1024) {
+      const int64_t r = t + threadIdx.x;
+      const int live = (r < r1 && __ldg(row + r + 1) > __ldg(row + r)) ? 1 : 0;
+      int x, tot;
+      Scan(tmp).ExclusiveSum(live, x, tot);
+      if (live) live_rows[(b << shift) + base + x] = (uint16_t)(r - r0);
+      base += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) live_cnt[b] = base;
+  }
+}
+
 // Phase 2: CTAs take work units from a counter: a unit is a whole bin, or a
 // run of tiles of a heavy bin (skewed graphs put a large share of the edges
 // in the bins of the hub rows; one CTA per bin left one SM working 7x longer
@@ -879,7 +901,7 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
     const int32_t* unit_slot, int64_t nunits, int shift, int32_t n,
     const int32_t* outdeg, const double* pr, double* pr_out, double* cur, PbPeers peers, double base,
     double damping, double* slots, unsigned int* bin_done, unsigned long long* next_unit, double* bin_pairs,
-    const unsigned int* gate) {
+    const unsigned int* gate, const uint16_t* live_rows, const int32_t* live_cnt) {
   if (gate && *reinterpret_cast<const volatile unsigned int*>(gate)) return;  // stopped: no-op sweep
   constexpr int NW = kAccThreads / 32;
   constexpr int WE = 32 * kAccEpl;  // sorted places per warp
@@ -1099,13 +1121,27 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
       double lmax = 0.0, lsum = 0.0;
       // rows in batches of 4 per thread: the pr / outdeg loads of a batch are
       // issued together (one latency per batch, not per row)
+      //
+      // Rows without in-edges keep rank base and a constant contribution
+      // from the first sweep on: once every buffer holds those (live_rows
+      // set by the caller), only the bin's rows with in-edges are finished
+      // (their list: live_rows[b << shift ..], live_cnt[b]) -- the same
+      // values, and a zero |delta| left out of the residual.
       constexpr int RB = 4;
-      for (int64_t rb = r0 + threadIdx.x; rb < r1; rb += (int64_t)RB * kAccThreads) {
+      const int nfin = live_rows ? __ldg(live_cnt + b) : (int)(r1 - r0);
+      const uint16_t* lv = live_rows ? live_rows + (b << shift) : nullptr;
+      for (int ib = threadIdx.x; ib < nfin; ib += RB * kAccThreads) {
         double old[RB], sum[RB];
         int od[RB];
+        int64_t rr[RB];
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-          const int64_t r = rb + (int64_t)q * kAccThreads;
+          const int i = ib + q * kAccThreads;
+          rr[q] = i < nfin ? r0 + (lv ? (int64_t)__ldg(lv + i) : (int64_t)i) : r1;
+        }
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          const int64_t r = rr[q];
           old[q] = 0.0;
           od[q] = 0;
           sum[q] = 0.0;
@@ -1122,7 +1158,7 @@ __global__ void __launch_bounds__(kAccThreads, kAccCtas) pb_accum_kernel(
         }
 #pragma unroll
         for (int q = 0; q < RB; ++q) {
-          const int64_t r = rb + (int64_t)q * kAccThreads;
+          const int64_t r = rr[q];
           if (r < r1) {
             const double nv = __dadd_rn(base, __dmul_rn(damping, sum[q]));
             const double dd = fabs(nv - old[q]);
@@ -1615,6 +1651,10 @@ cudaError_t build_pb(const DevGraph& g, int64_t nsrc, int shift, int chunk_shift
   PK(alloc((void**)&pb.psum, std::max<int64_t>(pb.nps, 1) * sizeof(double) + 64));
   PK(cudaMemsetAsync(pb.psum, 0, std::max<int64_t>(pb.nps, 1) * sizeof(double) + 64, st));
   PK(alloc((void**)&pb.bin_pairs, 2 * nbins * sizeof(double)));
+  PK(alloc((void**)&pb.live_rows, (size_t)nbins * sizeof(uint16_t) << shift));
+  PK(alloc((void**)&pb.live_cnt, nbins * sizeof(int32_t)));
+  pb_live_rows_kernel<<<tgrid, 1024, 0, st>>>(g.row, g.n, shift, nbins, pb.live_rows, pb.live_cnt);
+  PK(cudaGetLastError());
   PK(alloc((void**)&pb.bin_done, nbins * sizeof(unsigned int)));
   PK(cudaMemsetAsync(pb.bin_done, 0, nbins * sizeof(unsigned int), st));
   PK(cudaFuncSetAttribute(pb_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
@@ -1642,7 +1682,9 @@ out:
 
 cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph& g, const double* prev,
                             const double* pr, double* pr_out, double* cur, const PbPeers& peers, double base,
-                            double damping, double* err, double* l1, cudaStream_t st, const unsigned int* gate) {
+                            double damping, double* err, double* l1, cudaStream_t st, const unsigned int* gate,
+                            bool skip_empty) {
+  const uint16_t* lrows = skip_empty && pb.live_rows ? pb.live_rows : nullptr;
   const int W = plan.nwaves;
   // work counters: [0, W) phase-1 pieces, [W, 2W) phase-2 units
   cudaError_t e = cudaMemsetAsync(plan.ctr, 0, 2 * (size_t)W * sizeof(unsigned long long), st);
@@ -1665,7 +1707,7 @@ cudaError_t launch_pb_sweep(const PbSet& pb, const PbPlan& plan, const DevGraph&
         pb.psum, pb.vidx, pb.skey, pb.tile_meta, plan.unit_bin + u0, plan.unit_e + 2 * u0, plan.unit_t + u0,
         plan.unit_k + u0, plan.unit_j + u0,
         plan.unit_slot + u0, plan.unit0[w + 1] - u0, pb.shift, g.n, g.outdeg, pr, pr_out, cur,
-        peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs, gate);
+        peers, base, damping, plan.slots, pb.bin_done, plan.ctr + W + w, pb.bin_pairs, gate, lrows, pb.live_cnt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   pb_reduce_kernel<<<1, kReduceThreads, 0, st>>>(pb.nbins, pb.bin_pairs, err, l1, gate);

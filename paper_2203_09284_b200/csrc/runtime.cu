@@ -1131,8 +1131,10 @@ int run_pb(fpr_b200_graph* h, bool lockstep, const fpr_config* cfg, double* rank
     CK(cudaEventRecord(h->ev[1], h->stream));
     double* prev = h->contrib[lockstep ? 0 : par];
     double* next = h->contrib[lockstep ? 0 : par ^ 1];
+    // rows without in-edges are settled once both contribution buffers hold
+    // their constant (after two sweeps of this run; lockstep after one)
     CK(launch_pb_sweep(*h->pb, *plan, g, prev, h->pr, h->pr, next, PbPeers{}, base, cfg->damping, h->d_errors,
-                       h->d_l1, h->stream));
+                       h->d_l1, h->stream, nullptr, total >= 2));
     launches += (uint64_t)plan->nwaves + (uint64_t)(plan->item0.back() > 0 ? plan->nwaves : 0) + 1;
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(cudaMemcpyAsync(h->h_errors, h->d_errors, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1572,7 +1574,7 @@ int fpr_b200_part_sweep_peers(fpr_b200_graph* h, int engine, const fpr_config* c
       ++h->part_sweeps;
       CK(launch_pb_sweep(*h->pb, *plan, h->g, exch_read, h->part_pr[h->part_pr_cur], h->part_pr[h->part_pr_cur ^ 1],
                          exch_write + off, peers, (1.0 - cfg->damping) / (double)ng, cfg->damping, h->d_errors,
-                         h->d_l1, h->stream, h->gate));
+                         h->d_l1, h->stream, h->gate, h->part_sweeps > 3));  // rows without in-edges: as the peer rule
       h->part_pr_cur ^= 1;
       CK(cudaMemcpyAsync(pair_out, h->d_errors, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
       CK(cudaMemcpyAsync(pair_out + 1, h->d_l1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
