@@ -597,7 +597,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
     cfg = fb.PageRankConfig(damping=DAMPING, threshold=THRESHOLD)
     dev = f"cuda:{local}"
     solver = PartitionedSolver(part, ex, device=dev, fused_exchange=not args.copy_exchange and ws > 1,
-                               device_stop=ws > 1, batch=8)
+                               device_stop=True, batch=8)
     for _ in range(args.warmup):
         r = solver.solve(fb.ENGINE_EC, cfg, want_ranks=False)
     iters = r.iterations
@@ -637,7 +637,7 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
             "sweep": ("propagation-blocked" if part.graph.layout_info()["sweep"] == fb.SWEEP_PB else "pull")
                      + " (per part, the library's choice for the part's exchange space)",
             "host_loop": ("device-side stop: batches of 8 iterations (sweep, pair all-gather, gate update) "
-                          "enqueued without a host read; one gate read per batch" if ws > 1 else "synchronous"),
+                          "enqueued without a host read; one gate read per batch"),
             "exchange_fallback": solver.fallback, "slice": part.slice,
             "time_to_converge_ms": ms_step,
             "fused": {"iterations": fr.iterations},
@@ -645,7 +645,12 @@ def run_multi(args, fb, dist, ws, rank, local) -> None:
                          "peak": peak, "unit": "GB/s (per GPU)",
                          "frac": algorithmic_bytes(n, m) / ws / (sweep_ms * 1e-3) / 1e9 / peak, "traffic": None},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": int(args.steps * iters), "clocks": clk.summary(),
+            # per issued sweep (batches of 8, the ones past the stop are no-ops): the PB
+            # sweep's hot-copy refresh, gather, accumulate and reduce (or the pull
+            # solve kernel) + the gate update
+            "gpu_launches": int(args.steps * ((iters + 7) // 8 * 8) *
+                                ((5 if part.graph.layout_info()["sweep"] == fb.SWEEP_PB else 2))),
+            "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     solver.close()
